@@ -1,0 +1,203 @@
+/*
+ * fsx.h -- C ABI of the B200-native sidecar data plane (libfsx.so).
+ *
+ * Drop-in boundary for the reference's sidecar hot path (fissim,
+ * /root/reference/proj/include/fissim/sidecar.hpp).  The reference is
+ * header-only C++ with no FFI of its own; these are the entry points its
+ * C++ SidecarFabric would bind to move bytes on B200s.  Every
+ * function cites the reference interface it replaces as file:line relative to
+ * /root/reference/proj.  The C++ SidecarFabric-compatible engine
+ * (include/fsx/fabric.hpp) and the Python bindings sit on top of this header.
+ *
+ * Conventions
+ *  - All functions return int status: 0 = OK, otherwise 1 + the ordinal of
+ *    fissim::ErrorCode (include/fissim/common.hpp:29-47); the message is in
+ *    fsx_last_error() (thread-local).  The C++ shim rethrows fissim::Error.
+ *  - "gpu" is the fabric's logical GPU id (the keys of the reference's
+ *    gpu_to_node map, sidecar.hpp:242-248).  Each logical GPU is bound to a
+ *    CUDA device ordinal at fsx_open().
+ *  - Pointers named d_* are device pointers, h_* host pointers.  `stream` is a
+ *    cudaStream_t passed as void* (NULL = the fabric's own stream for that
+ *    device).  Calls that take a stream are asynchronous on it.
+ *  - There is NO CPU fallback: without a CUDA device fsx_open fails with
+ *    FSX_E_CONFIG and every data-moving call fails.
+ */
+#ifndef FSX_H
+#define FSX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1 + fissim::ErrorCode ordinal (common.hpp:29-47) ---- */
+#define FSX_OK 0
+#define FSX_E_VALIDATION 1
+#define FSX_E_NOT_FOUND 3
+#define FSX_E_OOM 5
+#define FSX_E_INTEGRITY 10
+#define FSX_E_PROTOCOL 11
+#define FSX_E_TIMEOUT 12
+#define FSX_E_CONFIG 14
+#define FSX_E_CANCELLED 16
+#define FSX_E_INTERNAL 17
+
+/* Transport, sidecar.hpp:32 (enum class Transport { LocalBuffer, NetworkStream }) */
+#define FSX_TRANSPORT_LOCAL_BUFFER 0
+#define FSX_TRANSPORT_NETWORK_STREAM 1
+
+typedef struct fsx_fabric fsx_fabric;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* fsx_last_error(void);
+/* Library version string and the CUDA arch it was built for. */
+const char* fsx_version(void);
+/* Number of visible CUDA devices (0 on a GPU-less host; never a fallback). */
+int fsx_device_count(int* n);
+
+/* ---- fabric lifetime ------------------------------------------------------
+ * Replaces SidecarFabric(SimKernel&, std::map<int,int> gpu_to_node, SidecarConfig)
+ * (sidecar.hpp:242-248).  gpu_ids[i] lives on node node_ids[i] and is bound to
+ * CUDA device devices[i] (devices == NULL or devices[i] < 0 -> gpu_id % count).
+ * Peer access is enabled between every pair of distinct bound devices. */
+int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* devices,
+             fsx_fabric** out);
+int fsx_close(fsx_fabric* f);
+
+/* SidecarFabric::node_of (sidecar.hpp:255-260): FSX_E_NOT_FOUND for an unknown gpu. */
+int fsx_node_of(fsx_fabric* f, int gpu, int* node);
+/* SidecarFabric::route (sidecar.hpp:250-253). */
+int fsx_route(fsx_fabric* f, int src_gpu, int dst_gpu, int* transport);
+/* CUDA device ordinal bound to a logical gpu. */
+int fsx_device_of(fsx_fabric* f, int gpu, int* device);
+
+/* ---- receive slabs --------------------------------------------------------
+ * The reference keeps one shm NodeArena per node (sidecar.hpp:106-135,
+ * 244-247).  Here every consumer GPU owns a device-memory receive slab with the
+ * same allocation policy: first fit in offset order, 64 B alignment, zero-byte
+ * requests take one 64 B unit, coalescing free (sidecar.hpp:149-186). */
+int fsx_slab_register(fsx_fabric* f, int gpu, int64_t bytes);
+/* NodeArena::alloc (sidecar.hpp:149-163).  *off = -1 when nothing fits (the
+ * caller backlogs, sidecar.hpp:329-334); that is not an error. */
+int fsx_slab_alloc(fsx_fabric* f, int gpu, int64_t len, int64_t* off);
+/* NodeArena::free_seg (sidecar.hpp:165-186): FSX_E_INTERNAL on double free. */
+int fsx_slab_free(fsx_fabric* f, int gpu, int64_t off);
+/* NodeArena::data (sidecar.hpp:188), as a device pointer into the slab. */
+int fsx_slab_ptr(fsx_fabric* f, int gpu, int64_t off, void** d_ptr);
+/* NodeArena::segments_in_use / bytes_in_use / peak_bytes / capacity
+ * (sidecar.hpp:147, 190-192). */
+int fsx_slab_usage(fsx_fabric* f, int gpu, int64_t* segments, int64_t* bytes_in_use,
+                   int64_t* peak_bytes, int64_t* capacity);
+/* Copy n bytes of a slab segment into host memory and wait for them: the
+ * owned-vector delivery of the reference ChunkCallback path
+ * (sidecar.hpp:543-544).  Zero-copy consumers use fsx_slab_ptr instead. */
+int fsx_slab_read(fsx_fabric* f, int gpu, int64_t off, void* h_dst, int64_t n, void* stream);
+/* Cross-process slabs (executor_worker.hpp:63-87 shm-name handshake ->
+ * cudaIpcMemHandle).  export writes 64 handle bytes; import maps a slab owned
+ * by another process as logical `gpu` (chunk flags included). */
+int fsx_slab_export(fsx_fabric* f, int gpu, void* handle64, int64_t* bytes);
+int fsx_slab_import(fsx_fabric* f, int gpu, const void* handle64, int64_t bytes);
+
+/* ---- chunk flags ----------------------------------------------------------
+ * Per-consumer-GPU ring of 64-bit completion flags, mirrored in device memory
+ * (for consumer kernels that start early) and in mapped pinned host memory
+ * (for the host progress thread).  A flag holds the token of the transfer
+ * chunk that last completed there; tokens are unique per fsx_forward call, so
+ * slots never need resetting. */
+int fsx_flags_alloc(fsx_fabric* f, int dst_gpu, int32_t n, int64_t* flag_base);
+int fsx_flag_ptr(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t** d_flag);
+
+/* ---- forwarding (K1) --------------------------------------------------------
+ * Replaces the payload placement of SidecarFabric::send / try_place_local
+ * (sidecar.hpp:302-347, 465-483: checksum + copy into PendingSend + memcpy into
+ * the arena).  An sm_100a kernel on src_gpu's device pushes `bytes` from d_src
+ * into dst_gpu's slab at dst_off with 16-byte stores (NVLink/NVSwitch P2P when
+ * the devices differ, HBM copy when they are the same), chunk by chunk; when
+ * chunk c is fully stored its flag flag_base + c is set to the returned token
+ * (release, system scope).  n_chunks = ceil(bytes / chunk_bytes) (1 when
+ * chunk_bytes <= 0 or >= bytes); chunk_bytes must be a multiple of 16. */
+int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
+                int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                void* stream);
+/* Same contract for a HOST source span (the reference send(span) path,
+ * sidecar.hpp:302): host->device copy straight into the consumer slab on
+ * dst_gpu's device, then the chunk flags.  Pageable or pinned h_src. */
+int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
+                     int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                     void* stream);
+/* Non-blocking readiness of one chunk (host mirror of the flag). */
+int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token, int* ready);
+/* Host wait until flags [flag_base, flag_base + n) all equal token;
+ * FSX_E_TIMEOUT after timeout_us (< 0 = forever). */
+int fsx_wait(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, uint64_t token,
+             int64_t timeout_us);
+/* Device-side wait: enqueue on `stream` (a stream of dst_gpu's device) a tiny
+ * kernel that spins on the device flags (acquire, system scope) so that work
+ * queued after it starts exactly when the chunks have landed. */
+int fsx_stream_wait_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n,
+                          uint64_t token, void* stream);
+
+/* ---- merge (K3) -------------------------------------------------------------
+ * New on this path: the reference consumer discards the bytes
+ * (executor_sim.hpp:382-392).  Contract: request r
+ * owns rows [req_row_off[r], req_row_off[r+1]) of d_embeds / d_token_ids and
+ * items [req_item_off[r], req_item_off[r+1]) in input-slot order
+ * (record_replay.hpp:404-416).  The k-th row of request r whose token id equals
+ * placeholder_id receives row k of concat(item rows).  Text rows are never
+ * touched.  If the placeholder count of request r differs from the sum of its
+ * item rows, request r is left untouched and d_status[r] = FSX_E_VALIDATION
+ * (0 otherwise).  Rows are moved as opaque bytes (bf16 NaN/Inf patterns
+ * survive).  All arrays are DEVICE arrays on gpu's device.  Optional early
+ * start: when d_item_flag is non-NULL, row j of item i is copied only after
+ * d_item_flag[i][j / d_item_chunk_rows[i]] == d_item_token[i]. */
+typedef struct fsx_merge_batch {
+  int32_t num_requests;
+  int32_t num_items;
+  int64_t row_bytes;                 /* hidden_dim * embed_elem_bytes (profiles.hpp:278-283) */
+  int32_t placeholder_id;
+  int32_t _pad;
+  void* d_embeds;                    /* [sum T, row_bytes] */
+  const int32_t* d_token_ids;        /* [sum T] */
+  const int64_t* d_req_row_off;      /* [R + 1] */
+  const int64_t* d_req_item_off;     /* [R + 1] */
+  const void* const* d_item_src;     /* [M] device pointers (slab views) */
+  const int64_t* d_item_row_off;     /* [M + 1] prefix sums of item rows */
+  int32_t* d_scratch;                /* [sum item rows] scratch */
+  int32_t* d_status;                 /* [R] out */
+  const uint64_t* const* d_item_flag; /* optional [M] */
+  const uint64_t* d_item_token;      /* optional [M] */
+  const int64_t* d_item_chunk_rows;  /* optional [M] */
+  int64_t total_rows;                /* sum T (== d_req_row_off[R]) */
+  int64_t total_item_rows;           /* == d_item_row_off[M] */
+} fsx_merge_batch;
+int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream);
+
+/* ---- synthesis (K0) ---------------------------------------------------------
+ * synth_payload_into (common.hpp:247-259) on the device: byte-identical to the
+ * reference stream.  Used by producers/tests/bench to create inputs. */
+int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_t n,
+                      void* stream);
+
+/* ---- stats ----------------------------------------------------------------
+ * SidecarStats (sidecar.hpp:209-217, 403-415) device-side counterparts plus
+ * the number of fsx kernels launched (bench "gpu_launches"). */
+typedef struct fsx_stats {
+  int64_t forwards;        /* fsx_forward / fsx_forward_host calls */
+  int64_t bytes_forwarded; /* payload bytes moved into slabs */
+  int64_t merges;
+  int64_t merged_rows;
+  int64_t segments_in_use; /* over all slabs */
+  int64_t bytes_in_use;
+  int64_t kernel_launches;
+} fsx_stats;
+int fsx_get_stats(fsx_fabric* f, fsx_stats* out);
+
+/* Synchronize every stream the fabric owns. */
+int fsx_synchronize(fsx_fabric* f);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSX_H */

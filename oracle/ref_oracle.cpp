@@ -1,0 +1,260 @@
+// ref_oracle.cpp -- C-ABI shim over the UNMODIFIED reference headers.
+// TEST INFRASTRUCTURE ONLY: built by oracle/Makefile from
+// $(FISSIM_REF_INCLUDE)/fissim/*.hpp (default /root/reference/proj/include)
+// into oracle/_ref/libref_oracle.so.  No reference source is copied: the
+// headers are only #included.  Used to
+//   * pin the C restatement (oracle/fsx_oracle.c) and generate tests/golden/,
+//   * time the reference CPU forwarding path (bench.py --impl reference and
+//     the cpu_baseline leg), which is SidecarFabric::send_payload ->
+//     SimKernel::run_until_idle (sidecar.hpp:302-347, 465-563) on 1 core.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fissim/executor_sim.hpp"
+#include "fissim/profiles.hpp"
+#include "fissim/sidecar.hpp"
+#include "fissim/workload.hpp"
+
+extern "C" {
+#include "fsx_oracle.h"
+}
+
+using namespace fissim;
+
+namespace {
+
+// ExecutorBase::payload_seed is protected (executor_sim.hpp:231-233); expose
+// the reference's own implementation through a do-nothing subclass.
+struct SeedProbe : ExecutorBase {
+  SeedProbe() : ExecutorBase(ExecutorEnv{}, ReplicaSpec{}) {}
+  void on_invocation(InvocationMessage) override {}
+  uint64_t seed(const std::string& ref, int64_t seq) const { return payload_seed(ref, seq); }
+};
+
+std::map<int, int> topo_8x2() {
+  std::map<int, int> t;
+  for (int g = 0; g < 8; ++g) t[g] = g < 4 ? 0 : 1;  // tests/test_sidecar.cpp:15-20
+  return t;
+}
+
+thread_local std::string g_err;
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_checksum64(const uint8_t* p, size_t n) { return checksum64(p, n); }
+void ref_synth_payload_into(uint64_t seed, uint8_t* out, size_t n) {
+  if (n) synth_payload_into(seed, out, n);
+}
+uint64_t ref_fnv1a64(const char* s, size_t n) { return fnv1a64(std::string_view(s, n)); }
+uint64_t ref_splitmix64(uint64_t* st) { return splitmix64(*st); }
+uint64_t ref_payload_seed(const char* s, size_t n, int64_t seq) {
+  static SeedProbe probe;
+  return probe.seed(std::string(s, n), seq);
+}
+
+// ShapeRules::item_tokens / embed_desc (profiles.hpp:256-283) on JSON inputs.
+int64_t ref_item_tokens(const char* rules_json, const char* item_json) {
+  try {
+    ShapeRules r = ShapeRules::from_json(json::parse(rules_json));
+    return r.item_tokens(json::parse(item_json));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+int64_t ref_embed_bytes(const char* rules_json, const char* item_json) {
+  try {
+    ShapeRules r = ShapeRules::from_json(json::parse(rules_json));
+    return r.embed_desc(json::parse(item_json)).total_bytes();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// NodeArena (sidecar.hpp:106-205), the reference allocator itself.
+void* ref_arena_new(int64_t cap) {
+  try {
+    return new NodeArena(0, cap);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_arena_delete(void* a) { delete static_cast<NodeArena*>(a); }
+int64_t ref_arena_alloc(void* a, int64_t len) {
+  auto off = static_cast<NodeArena*>(a)->alloc(len);
+  return off ? *off : -1;
+}
+int ref_arena_free(void* a, int64_t off) {
+  try {
+    static_cast<NodeArena*>(a)->free_seg(off);
+    return 0;
+  } catch (const Error&) {
+    return -2;
+  }
+}
+int64_t ref_arena_segments_in_use(void* a) {
+  return (int64_t) static_cast<NodeArena*>(a)->segments_in_use();
+}
+int64_t ref_arena_bytes_in_use(void* a) { return static_cast<NodeArena*>(a)->bytes_in_use(); }
+
+// One single-shot transfer through the reference SidecarFabric on the 8-GPU
+// two-node topology; the delivered bytes (the vector handed to the
+// ChunkCallback, sidecar.hpp:543-561) are copied to `out`.
+// stats_out[7] = {transfers, bytes_forwarded, integrity_errors, orphan_reclaims,
+//                 segments_in_use, bytes_in_use, delivered_chunks}.
+int ref_forward(int src_gpu, int dst_gpu, const char* ref_id, const uint8_t* payload, size_t n,
+                uint8_t* out, int64_t* stats_out) {
+  try {
+    SimKernel k(ClockMode::Virtual);
+    SidecarConfig cfg;
+    cfg.arena_bytes = std::max<int64_t>(int64_t{64} << 20, 2 * static_cast<int64_t>(n) + 4096);
+    SidecarFabric fabric(k, topo_8x2(), cfg);
+    DataRef ref;
+    ref.ref_id = ref_id;
+    ref.producer = "p";
+    ref.desc = {{static_cast<int64_t>(n)}, 1};
+    int64_t chunks = 0;
+    fabric.register_interest(dst_gpu, ref.ref_id,
+                             [&](const ForwardEnvelope&, std::vector<uint8_t> bytes) {
+                               if (bytes.size() == n && n) std::memcpy(out, bytes.data(), n);
+                               ++chunks;
+                             });
+    k.post("send", [&] {
+      fabric.send_payload("req", ref, src_gpu, dst_gpu, std::span<const uint8_t>(payload, n));
+    });
+    k.run_until_idle();
+    auto s = fabric.stats();
+    int64_t v[7] = {s.transfers,          s.bytes_forwarded,   s.integrity_errors,
+                    s.orphan_reclaims,    (int64_t)s.segments_in_use, s.bytes_in_use, chunks};
+    std::memcpy(stats_out, v, sizeof(v));
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return 1 + static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1 + static_cast<int>(ErrorCode::Internal);
+  }
+}
+
+// Reference CPU forwarding throughput: `iters` single-shot sends of `bytes`
+// from gpu 0 to `dst_gpu` (1 = LocalBuffer, 4 = NetworkStream), each drained
+// with run_until_idle (Virtual clock: modeled latency costs no wall time).
+// Returns wall seconds for the timed iterations (2 warm-ups excluded).
+double ref_forward_bench(size_t bytes, int iters, int dst_gpu) {
+  SimKernel k(ClockMode::Virtual);
+  SidecarConfig cfg;
+  cfg.arena_bytes = std::max<int64_t>(int64_t{64} << 20, 2 * static_cast<int64_t>(bytes) + 4096);
+  SidecarFabric fabric(k, topo_8x2(), cfg);
+  auto payload = synth_payload(fnv1a64("req/r0"), bytes);
+  size_t sink = 0;
+  auto one = [&](int i) {
+    DataRef ref;
+    ref.ref_id = "bench/r" + std::to_string(i);
+    ref.producer = "p";
+    ref.desc = {{static_cast<int64_t>(bytes)}, 1};
+    fabric.register_interest(dst_gpu, ref.ref_id,
+                             [&](const ForwardEnvelope&, std::vector<uint8_t> b) { sink += b.size(); });
+    k.post("send", [&, ref] { fabric.send_payload("bench", ref, 0, dst_gpu, payload); });
+    k.run_until_idle();
+  };
+  for (int i = 0; i < 2; ++i) one(-1 - i);
+  auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < iters; ++i) one(i);
+  auto t1 = std::chrono::steady_clock::now();
+  if (sink == 0 && bytes) return -1;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// One pass of the reference data plane over a batch: every item payload is
+// forwarded producer gpu -> consumer gpu through SidecarFabric (single shot,
+// as executor_sim.hpp:321-336 emits it), the consumer callback keeps the
+// delivered bytes, then the derived merge (or_merge, the reference has none)
+// writes them into the placeholder rows.  ref_ids[i] names item i.
+// Returns wall seconds of the pass, or a negative value on error.
+double ref_dataplane_pass(int32_t num_requests, int32_t num_items, int64_t row_bytes,
+                          int32_t placeholder_id, uint8_t* embeds, const int32_t* token_ids,
+                          const int64_t* req_row_off, const int64_t* req_item_off,
+                          const uint8_t* const* item_payload, const int64_t* item_rows,
+                          const char* const* ref_ids, int src_gpu, int dst_gpu, int merge_threads,
+                          int32_t* status) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    SimKernel k(ClockMode::Virtual);
+    int64_t total = 0, biggest = 0;
+    for (int32_t i = 0; i < num_items; ++i) {
+      total += item_rows[i] * row_bytes;
+      biggest = std::max(biggest, item_rows[i] * row_bytes);
+    }
+    SidecarConfig cfg;  // default 1 GiB arena, grown if the batch needs more
+    cfg.arena_bytes = std::max<int64_t>(cfg.arena_bytes, total + 64 * (num_items + 1));
+    SidecarFabric fabric(k, topo_8x2(), cfg);
+    std::vector<std::vector<uint8_t>> got(num_items);
+    for (int32_t i = 0; i < num_items; ++i) {
+      fabric.register_interest(dst_gpu, ref_ids[i],
+                               [&got, i](const ForwardEnvelope&, std::vector<uint8_t> b) {
+                                 got[i] = std::move(b);
+                               });
+    }
+    k.post("send", [&] {
+      for (int32_t i = 0; i < num_items; ++i) {
+        DataRef ref;
+        ref.ref_id = ref_ids[i];
+        ref.producer = "encoder";
+        ref.desc = {{item_rows[i], row_bytes / 2}, 2};
+        std::string rid(ref.ref_id.substr(0, ref.ref_id.find('/')));
+        fabric.send_payload(rid, ref, src_gpu, dst_gpu,
+                            std::span<const uint8_t>(item_payload[i], item_rows[i] * row_bytes));
+      }
+    });
+    k.run_until_idle();
+    std::vector<const uint8_t*> src(num_items);
+    for (int32_t i = 0; i < num_items; ++i) {
+      if (static_cast<int64_t>(got[i].size()) != item_rows[i] * row_bytes) {
+        g_err = "item " + std::to_string(i) + " not delivered";
+        return -2;
+      }
+      src[i] = got[i].data();
+    }
+    or_merge(num_requests, row_bytes, placeholder_id, embeds, token_ids, req_row_off, req_item_off,
+             src.data(), item_rows, status, merge_threads);
+    auto t1 = std::chrono::steady_clock::now();
+    (void)biggest;
+    return std::chrono::duration<double>(t1 - t0).count();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// generate_workload (workload.hpp:196-242) on a mix file: the reference's own
+// seeded sampler, returned as a JSON array of {arrival_ms, class, request}.
+// The returned pointer stays valid until the next call on this thread.
+const char* ref_generate_workload(const char* mix_path, double rate_per_s, double duration_s,
+                                  uint64_t seed) {
+  static thread_local std::string out;
+  try {
+    auto mix = WorkloadMix::load(mix_path);
+    auto reqs = generate_workload(mix, rate_per_s, duration_s, seed);
+    json arr = json::array();
+    for (const auto& r : reqs)
+      arr.push_back(json{{"arrival_ms", r.arrival_ms}, {"class", r.class_name}, {"request", r.request}});
+    out = arr.dump();
+    return out.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,372 @@
+// fsx_kernels.cu -- sm_100a kernels of the sidecar data plane.
+//
+//   K0 synth_kernel      synth_payload_into (common.hpp:247-259) on the device
+//   K1 forward_kernel    payload placement of SidecarFabric::send/try_place_local
+//                        (sidecar.hpp:302-347, 465-483) as a chunked 16-byte push
+//                        into the consumer slab with per-chunk completion flags
+//   K3 merge_scan_kernel + merge_copy_kernel
+//                        the consumer-side multimodal merge (derived contract,
+//                        SURVEY.md 8a-8; record_replay.hpp:404-416 slot order)
+//   flag kernels         set / wait on chunk flags (release/acquire, sys scope)
+//
+// Everything here is integer byte movement: rows are opaque 16-byte vectors,
+// never converted through a floating-point type, so bf16 NaN/Inf patterns in the
+// synthetic payloads survive bit for bit.  No tensor cores: nothing is a
+// contraction.  All kernels are HBM- or NVLink-bound; see DESIGN.md.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fsx_kernels.cuh"
+
+namespace fsx {
+namespace kern {
+
+constexpr int kFwdThreads = 512;
+constexpr int kFwdUnroll = 8;  // 512 threads x 8 x 16 B = 64 KiB per round
+constexpr int kMergeThreads = 256;
+constexpr int kMergeUnroll = 16;  // 32 lanes x 16 x 16 B = 8 KiB of a row per batch
+constexpr int kScanThreads = 1024;
+constexpr int kScanPerThread = 16;
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Coherent streaming load: used where the data may have been written by a
+// peer GPU during this kernel's lifetime (early-start merge).
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t token) {
+  while (ld_acquire_sys(flag) != token) __nanosleep(64);
+}
+
+// splitmix64 finaliser (common.hpp:203-208): output k (1-based) of a stream
+// with state s0 is mix(s0 + k * gamma), which makes every word independent.
+__device__ __forceinline__ uint64_t splitmix_word(uint64_t s0, uint64_t k) {
+  uint64_t z = s0 + k * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// K1 forward
+
+// Copy [beg, end) of src into dst with the whole CTA.  `vec` means src and dst
+// are 16-byte aligned, so every 16-byte-aligned offset is a legal vector.
+__device__ __forceinline__ void cta_copy_range(const uint8_t* __restrict__ src,
+                                               uint8_t* __restrict__ dst, int64_t beg,
+                                               int64_t end, bool vec) {
+  if (vec) {
+    const int64_t vbeg = (beg + 15) & ~int64_t{15};
+    const int64_t vend = end & ~int64_t{15};
+    if (vbeg < vend) {
+      const uint4* s = reinterpret_cast<const uint4*>(src + vbeg);
+      uint4* d = reinterpret_cast<uint4*>(dst + vbeg);
+      const int64_t nv = (vend - vbeg) >> 4;
+      for (int64_t base = 0; base < nv; base += int64_t{kFwdThreads} * kFwdUnroll) {
+        uint4 r[kFwdUnroll];
+#pragma unroll
+        for (int k = 0; k < kFwdUnroll; ++k) {
+          const int64_t i = base + k * kFwdThreads + threadIdx.x;
+          if (i < nv) r[k] = ld_nc_v4(s + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kFwdUnroll; ++k) {
+          const int64_t i = base + k * kFwdThreads + threadIdx.x;
+          if (i < nv) st_v4(d + i, r[k]);
+        }
+      }
+      for (int64_t i = beg + threadIdx.x; i < vbeg && i < end; i += blockDim.x) dst[i] = src[i];
+      for (int64_t i = (vend > vbeg ? vend : vbeg) + threadIdx.x; i < end; i += blockDim.x)
+        dst[i] = src[i];
+      return;
+    }
+  }
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) dst[i] = src[i];
+}
+
+// Work unit u covers slice s of chunk c (units are chunk-major, so chunks
+// complete roughly in order and the consumer can start on chunk 0 early).
+// After its slice, a CTA fences at system scope and counts itself into the
+// chunk's counter; the CTA completing the chunk publishes the token to the
+// consumer-device flag and to the host-mapped flag with release semantics.
+__global__ void __launch_bounds__(kFwdThreads) forward_kernel(FwdArgs a) {
+  for (int64_t u = blockIdx.x; u < a.total_units; u += gridDim.x) {
+    const int64_t c = u / a.chunk_units;
+    const int64_t s = u - c * a.chunk_units;
+    const int64_t cbeg = c * a.chunk_bytes;
+    const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
+    const int64_t beg = cbeg + s * a.slice;
+    const int64_t end = min(beg + a.slice, cend);
+    cta_copy_range(a.src, a.dst, beg, end, a.vec != 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
+      const uint32_t prev = atomicAdd(&a.counters[c], 1u);
+      if (prev == units - 1) {
+        a.counters[c] = 0u;  // slot is clean for the next transfer that draws it
+        __threadfence_system();
+        st_release_sys(&a.dflags[c], a.token);
+        if (a.hflags) st_release_sys(&a.hflags[c], a.token);
+      }
+    }
+  }
+}
+
+__global__ void set_flags_kernel(FlagSetArgs a) {
+  for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+    st_release_sys(&a.dflags[i], a.token);
+    if (a.hflags) st_release_sys(&a.hflags[i], a.token);
+  }
+}
+
+__global__ void wait_flags_kernel(const uint64_t* dflags, int32_t n, uint64_t token) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(&dflags[i], token);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K3 merge, phase 1: per-request placeholder positions.
+//
+// One CTA per request.  Each thread owns kScanPerThread consecutive token ids
+// per round; the CTA computes an exclusive prefix sum of the per-thread
+// placeholder counts (warp shuffles + one shared-memory pass over warp totals)
+// and writes, for the k-th placeholder row of the request, its row offset
+// inside the request into scratch[item_row_off[first item] + k].
+__global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batch b) {
+  __shared__ int32_t warp_tot[kScanThreads / 32];
+  __shared__ int64_t running;
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = b.d_req_row_off[r], t1 = b.d_req_row_off[r + 1];
+  const int64_t i0 = b.d_req_item_off[r], i1 = b.d_req_item_off[r + 1];
+  const int64_t kbase = b.d_item_row_off[i0];
+  const int64_t want = b.d_item_row_off[i1] - kbase;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  for (int64_t t = t0; t < t1; t += int64_t{kScanThreads} * kScanPerThread) {
+    const int64_t mine = t + int64_t{threadIdx.x} * kScanPerThread;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPerThread; ++k) {
+      const int64_t tt = mine + k;
+      if (tt < t1 && b.d_token_ids[tt] == b.placeholder_id) mask |= 1u << k;
+    }
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int v = warp_tot[lane];
+      int wi = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, wi, off);
+        if (lane >= off) wi += x;
+      }
+      warp_tot[lane] = wi - v;  // exclusive over warps
+    }
+    __syncthreads();
+    int64_t k = running + warp_tot[warp] + (incl - cnt);
+    while (mask) {
+      const int bit = __ffs(mask) - 1;
+      mask &= mask - 1;
+      if (k < want) b.d_scratch[kbase + k] = (int32_t)(mine + bit - t0);
+      ++k;
+    }
+    __syncthreads();
+    if (threadIdx.x == kScanThreads - 1) running += warp_tot[kScanThreads / 32 - 1] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) b.d_status[r] = (running == want) ? 0 : FSX_E_VALIDATION;
+}
+
+__device__ __forceinline__ int64_t upper_index(const int64_t* off, int64_t n, int64_t x) {
+  // largest i in [0, n) with off[i] <= x  (off is non-decreasing, off[0] == 0)
+  int64_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// K3 merge, phase 2: one warp per placeholder row.  Lane 0 resolves the row's
+// item (binary search over item row offsets) and request, then the warp moves
+// the row as 16-byte vectors, all loads of a batch issued before its stores.
+__global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_batch b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
+  const int64_t rb = b.row_bytes;
+  const bool vec_rows = (rb & 15) == 0;
+  for (int64_t g = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
+       g < b.total_item_rows; g += warps) {
+    int64_t item = 0, req = 0;
+    if (lane == 0) {
+      item = upper_index(b.d_item_row_off, b.num_items + 1, g);
+      // skip zero-row items sharing the same offset
+      while (b.d_item_row_off[item + 1] <= g) ++item;
+      req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+      while (b.d_req_item_off[req + 1] <= item) ++req;
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    req = __shfl_sync(0xffffffffu, req, 0);
+    if (b.d_status[req] != 0) continue;  // validation failed: request untouched
+    const int64_t j = g - b.d_item_row_off[item];
+    if (b.d_item_flag) {
+      if (lane == 0) {
+        const int64_t cr = b.d_item_chunk_rows[item];
+        spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
+      }
+      __syncwarp();
+    }
+    const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
+    const int64_t t = b.d_req_row_off[req] + b.d_scratch[g];
+    uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + t * rb;
+    if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      const int64_t nv = rb >> 4;
+      const uint4* s = reinterpret_cast<const uint4*>(src);
+      uint4* d = reinterpret_cast<uint4*>(dst);
+      for (int64_t base = 0; base < nv; base += 32 * kMergeUnroll) {
+        uint4 r[kMergeUnroll];
+#pragma unroll
+        for (int k = 0; k < kMergeUnroll; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) r[k] = ld_v4(s + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kMergeUnroll; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) st_v4(d + i, r[k]);
+        }
+      }
+    } else {
+      for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K0 synth: each thread emits word pairs as one 16-byte store.
+__global__ void synth_kernel(uint64_t s0, uint8_t* __restrict__ dst, int64_t n) {
+  const int64_t nwords = n >> 3;
+  const int64_t npairs = nwords >> 1;
+  const bool al16 = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += stride) {
+    const uint64_t w0 = splitmix_word(s0, 2 * p + 1);
+    const uint64_t w1 = splitmix_word(s0, 2 * p + 2);
+    if (al16) {
+      *reinterpret_cast<ulonglong2*>(dst + 16 * p) = make_ulonglong2(w0, w1);
+    } else {
+      for (int bt = 0; bt < 8; ++bt) dst[16 * p + bt] = (uint8_t)(w0 >> (8 * bt));
+      for (int bt = 0; bt < 8; ++bt) dst[16 * p + 8 + bt] = (uint8_t)(w1 >> (8 * bt));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int64_t w = 2 * npairs; w * 8 < n; ++w) {  // odd last word and the truncated tail
+      const uint64_t v = splitmix_word(s0, (uint64_t)w + 1);
+      for (int bt = 0; bt < 8 && w * 8 + bt < n; ++bt) dst[w * 8 + bt] = (uint8_t)(v >> (8 * bt));
+    }
+  }
+}
+
+}  // namespace kern
+
+using namespace kern;
+
+// ---------------------------------------------------------------------------
+// Launchers
+
+int forward_block_threads() { return kFwdThreads; }
+int merge_copy_block_threads() { return kMergeThreads; }
+
+int forward_blocks_per_sm() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, forward_kernel, kFwdThreads, 0) != cudaSuccess)
+    return 1;
+  return n > 0 ? n : 1;
+}
+
+int merge_copy_blocks_per_sm() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_copy_kernel, kMergeThreads, 0) !=
+      cudaSuccess)
+    return 1;
+  return n > 0 ? n : 1;
+}
+
+cudaError_t launch_forward(const FwdArgs& a, int grid, int block, cudaStream_t s) {
+  forward_kernel<<<grid, block, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s) {
+  set_flags_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s) {
+  wait_flags_kernel<<<1, 32, 0, s>>>(dflags, n, token);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
+  *launches = 0;
+  if (b.num_requests <= 0) return cudaSuccess;
+  merge_scan_kernel<<<b.num_requests, kScanThreads, 0, s>>>(b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  *launches = 1;
+  if (b.total_item_rows <= 0) return cudaSuccess;
+  const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
+  const int grid = (int)(need < copy_grid ? need : copy_grid);
+  merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) *launches = 2;
+  return e;
+}
+
+cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s) {
+  synth_kernel<<<grid, 256, 0, s>>>(seed ^ 0xd6e8feb86659fd93ull, dst, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fsx

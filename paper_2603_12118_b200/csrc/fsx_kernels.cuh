@@ -1,0 +1,50 @@
+// fsx_kernels.cuh -- kernel argument blocks and host launchers (internal to
+// libfsx).  The kernels live in fsx_kernels.cu; the C ABI in fsx_runtime.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fsx.h"
+
+namespace fsx {
+
+// K1: chunked push copy with per-chunk completion flags.
+struct FwdArgs {
+  const uint8_t* src;
+  uint8_t* dst;        // slab view (local or peer-mapped)
+  int64_t bytes;
+  int64_t chunk_bytes; // > 0
+  int64_t slice;       // bytes per work unit (multiple of 16)
+  int64_t chunk_units; // units per full chunk
+  int64_t last_units;  // units of the last chunk
+  int64_t total_units;
+  int32_t n_chunks;
+  int32_t vec;         // 16-byte path usable
+  uint32_t* counters;  // [n_chunks] on the source device, zero on entry, self-resetting
+  uint64_t* dflags;    // [n_chunks] consumer-device flags (may be peer memory)
+  uint64_t* hflags;    // [n_chunks] mapped pinned host flags, or nullptr
+  uint64_t token;
+};
+
+struct FlagSetArgs {
+  uint64_t* dflags;
+  uint64_t* hflags;
+  int32_t n;
+  uint64_t token;
+};
+
+// Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
+cudaError_t launch_forward(const FwdArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
+cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);
+cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s);
+
+// Occupancy helpers.
+int forward_block_threads();
+int forward_blocks_per_sm();
+int merge_copy_block_threads();
+int merge_copy_blocks_per_sm();
+
+}  // namespace fsx

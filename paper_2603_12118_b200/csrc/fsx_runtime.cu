@@ -1,0 +1,669 @@
+// fsx_runtime.cu -- the C ABI of libfsx (include/fsx.h): logical GPU map,
+// per-consumer-GPU device receive slabs with the reference allocation policy,
+// chunk-flag rings, and the launch paths of K0/K1/K3.
+//
+// Threading: every entry point is safe to call from any host thread (one mutex
+// guards the bookkeeping; launches happen outside of it where possible).  The
+// C++ fabric engine (include/fsx/fabric.hpp) calls in from the SimKernel
+// thread and from its progress thread.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fsx.h"
+#include "fsx_kernels.cuh"
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+#define FSX_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(FSX_E_INTERNAL, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+constexpr int64_t kAlign = 64;             // sidecar.hpp:195
+constexpr int64_t kFlagRing = 1 << 18;     // flags per consumer slab (2 MiB)
+constexpr int64_t kCounterRing = 1 << 16;  // chunk counters per source device
+constexpr int64_t kSlice = 64 * 1024;      // K1 work unit
+
+// Address-ordered block list over [0, capacity).  First fit in offset order,
+// 64-byte units, coalescing on free: the allocation policy of the reference
+// NodeArena (sidecar.hpp:149-186), re-homed to a device slab.
+class BlockList {
+ public:
+  void reset(int64_t capacity) {
+    blocks_.clear();
+    blocks_[0] = Block{capacity, true};
+    used_segments_ = 0;
+    used_bytes_ = 0;
+    peak_ = 0;
+  }
+
+  int64_t alloc(int64_t len) {
+    const int64_t need = (std::max<int64_t>(len, 1) + kAlign - 1) & ~(kAlign - 1);
+    for (auto it = blocks_.begin(); it != blocks_.end(); ++it) {
+      if (!it->second.free || it->second.len < need) continue;
+      const int64_t off = it->first;
+      const int64_t rest = it->second.len - need;
+      it->second = Block{need, false};
+      if (rest > 0) blocks_.emplace_hint(std::next(it), off + need, Block{rest, true});
+      ++used_segments_;
+      used_bytes_ += need;
+      peak_ = std::max(peak_, used_bytes_);
+      return off;
+    }
+    return -1;
+  }
+
+  bool release(int64_t off) {
+    auto it = blocks_.find(off);
+    if (it == blocks_.end() || it->second.free) return false;
+    --used_segments_;
+    used_bytes_ -= it->second.len;
+    it->second.free = true;
+    auto nx = std::next(it);
+    if (nx != blocks_.end() && nx->second.free) {
+      it->second.len += nx->second.len;
+      blocks_.erase(nx);
+    }
+    if (it != blocks_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->second.free) {
+        pv->second.len += it->second.len;
+        blocks_.erase(it);
+      }
+    }
+    return true;
+  }
+
+  int64_t segments() const { return used_segments_; }
+  int64_t bytes() const { return used_bytes_; }
+  int64_t peak() const { return peak_; }
+
+ private:
+  struct Block {
+    int64_t len;
+    bool free;
+  };
+  std::map<int64_t, Block> blocks_;
+  int64_t used_segments_ = 0, used_bytes_ = 0, peak_ = 0;
+};
+
+// Bump ring of contiguous index ranges (flags / counters).  Reuse is safe
+// because flag values are unique tokens and counters reset themselves.
+struct Ring {
+  int64_t size = 0, next = 0;
+  int64_t take(int64_t n) {
+    if (next + n > size) next = 0;
+    const int64_t at = next;
+    next += n;
+    return at;
+  }
+};
+
+struct Slab {
+  int gpu = -1;
+  int device = -1;
+  bool imported = false;
+  uint8_t* base = nullptr;      // data region [0, capacity)
+  int64_t capacity = 0;
+  uint64_t* dflags = nullptr;   // kFlagRing device flags (right after the data region)
+  uint64_t* hflags = nullptr;   // kFlagRing mapped pinned host flags (owner process only)
+  BlockList blocks;
+  Ring flags;
+};
+
+struct Device {
+  int ordinal = -1;
+  cudaStream_t stream = nullptr;
+  uint32_t* counters = nullptr;
+  Ring counter_ring;
+  int sms = 0;
+  int fwd_grid = 0;
+  int merge_grid = 0;
+};
+
+}  // namespace
+
+struct fsx_fabric {
+  std::mutex mu;
+  std::map<int, int> node_of;
+  std::map<int, int> device_of;
+  std::map<int, std::unique_ptr<Slab>> slabs;
+  std::map<int, std::unique_ptr<Device>> devices;
+  std::atomic<uint64_t> next_token{1};
+  std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
+};
+
+namespace {
+
+int find_gpu(fsx_fabric* f, int gpu, int* device) {
+  auto it = f->device_of.find(gpu);
+  if (it == f->device_of.end())
+    return fail(FSX_E_NOT_FOUND, "gpu " + std::to_string(gpu) + " not in topology map");
+  if (device) *device = it->second;
+  return FSX_OK;
+}
+
+Slab* slab_of(fsx_fabric* f, int gpu) {
+  auto it = f->slabs.find(gpu);
+  return it == f->slabs.end() ? nullptr : it->second.get();
+}
+
+// Lazily create per-device state (stream, counter ring, grid sizes).
+int device_state(fsx_fabric* f, int ordinal, Device** out) {
+  auto it = f->devices.find(ordinal);
+  if (it != f->devices.end()) {
+    *out = it->second.get();
+    return FSX_OK;
+  }
+  auto d = std::make_unique<Device>();
+  d->ordinal = ordinal;
+  FSX_CUDA(cudaSetDevice(ordinal));
+  FSX_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  FSX_CUDA(cudaMalloc(&d->counters, kCounterRing * sizeof(uint32_t)));
+  FSX_CUDA(cudaMemset(d->counters, 0, kCounterRing * sizeof(uint32_t)));
+  d->counter_ring.size = kCounterRing;
+  FSX_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, ordinal));
+  d->fwd_grid = d->sms * fsx::forward_blocks_per_sm();
+  d->merge_grid = d->sms * fsx::merge_copy_blocks_per_sm();
+  *out = d.get();
+  f->devices.emplace(ordinal, std::move(d));
+  return FSX_OK;
+}
+
+cudaStream_t pick_stream(Device* d, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : d->stream;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fsx_last_error(void) { return t_err.c_str(); }
+
+const char* fsx_version(void) { return "fsx 0.1 (sm_100a)"; }
+
+int fsx_device_count(int* n) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  *n = c;
+  return FSX_OK;
+}
+
+int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* devices,
+             fsx_fabric** out) {
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(FSX_E_CONFIG, "no CUDA device visible: libfsx has no CPU fallback");
+  if (n_gpus <= 0) return fail(FSX_E_CONFIG, "empty topology map");
+  auto f = std::make_unique<fsx_fabric>();
+  for (int i = 0; i < n_gpus; ++i) {
+    const int dev = (devices && devices[i] >= 0) ? devices[i] : gpu_ids[i] % count;
+    if (dev >= count) return fail(FSX_E_CONFIG, "device ordinal out of range");
+    f->node_of[gpu_ids[i]] = node_ids[i];
+    f->device_of[gpu_ids[i]] = dev;
+  }
+  // Peer access between every pair of distinct bound devices (NVLink/NVSwitch).
+  std::vector<int> devs;
+  for (auto& [g, d] : f->device_of) devs.push_back(d);
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  for (int a : devs) {
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      FSX_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return fail(FSX_E_CONFIG, "no peer access between devices");
+      FSX_CUDA(cudaSetDevice(a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(FSX_E_CONFIG, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  }
+  for (int d : devs) {
+    Device* st = nullptr;
+    int rc = device_state(f.get(), d, &st);
+    if (rc) return rc;
+  }
+  *out = f.release();
+  return FSX_OK;
+}
+
+int fsx_close(fsx_fabric* f) {
+  if (!f) return FSX_OK;
+  for (auto& [o, d] : f->devices) {
+    cudaSetDevice(o);
+    cudaStreamSynchronize(d->stream);
+  }
+  for (auto& [g, s] : f->slabs) {
+    cudaSetDevice(s->device);
+    if (s->imported) {
+      if (s->base) cudaIpcCloseMemHandle(s->base);
+    } else {
+      if (s->base) cudaFree(s->base);
+      if (s->hflags) cudaFreeHost(s->hflags);
+    }
+  }
+  for (auto& [o, d] : f->devices) {
+    cudaSetDevice(o);
+    if (d->counters) cudaFree(d->counters);
+    if (d->stream) cudaStreamDestroy(d->stream);
+  }
+  delete f;
+  return FSX_OK;
+}
+
+int fsx_node_of(fsx_fabric* f, int gpu, int* node) {
+  auto it = f->node_of.find(gpu);
+  if (it == f->node_of.end())
+    return fail(FSX_E_NOT_FOUND, "gpu " + std::to_string(gpu) + " not in topology map");
+  *node = it->second;
+  return FSX_OK;
+}
+
+int fsx_route(fsx_fabric* f, int src_gpu, int dst_gpu, int* transport) {
+  int a = 0, b = 0;
+  int rc = fsx_node_of(f, src_gpu, &a);
+  if (rc) return rc;
+  rc = fsx_node_of(f, dst_gpu, &b);
+  if (rc) return rc;
+  *transport = a == b ? FSX_TRANSPORT_LOCAL_BUFFER : FSX_TRANSPORT_NETWORK_STREAM;
+  return FSX_OK;
+}
+
+int fsx_device_of(fsx_fabric* f, int gpu, int* device) { return find_gpu(f, gpu, device); }
+
+// ---------------------------------------------------------------------------
+// Slabs
+
+int fsx_slab_register(fsx_fabric* f, int gpu, int64_t bytes) {
+  int dev = 0;
+  int rc = find_gpu(f, gpu, &dev);
+  if (rc) return rc;
+  if (bytes <= 0) return fail(FSX_E_CONFIG, "slab size must be positive");
+  std::lock_guard<std::mutex> lk(f->mu);
+  if (f->slabs.count(gpu)) return fail(FSX_E_CONFIG, "slab already registered for gpu");
+  auto s = std::make_unique<Slab>();
+  s->gpu = gpu;
+  s->device = dev;
+  s->capacity = (bytes + kAlign - 1) & ~(kAlign - 1);
+  FSX_CUDA(cudaSetDevice(dev));
+  // One allocation: data region followed by the device flag ring, so a single
+  // IPC handle exports both.
+  cudaError_t e = cudaMalloc(&s->base, s->capacity + kFlagRing * sizeof(uint64_t));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FSX_E_OOM, std::string("slab cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  s->dflags = reinterpret_cast<uint64_t*>(s->base + s->capacity);
+  FSX_CUDA(cudaMemset(s->dflags, 0, kFlagRing * sizeof(uint64_t)));
+  FSX_CUDA(cudaHostAlloc(&s->hflags, kFlagRing * sizeof(uint64_t),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(s->hflags, 0, kFlagRing * sizeof(uint64_t));
+  FSX_CUDA(cudaDeviceSynchronize());
+  s->blocks.reset(s->capacity);
+  s->flags.size = kFlagRing;
+  f->slabs.emplace(gpu, std::move(s));
+  return FSX_OK;
+}
+
+int fsx_slab_alloc(fsx_fabric* f, int gpu, int64_t len, int64_t* off) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  if (s->imported) return fail(FSX_E_CONFIG, "imported slabs are allocated by their owner");
+  *off = s->blocks.alloc(len);
+  return FSX_OK;
+}
+
+int fsx_slab_free(fsx_fabric* f, int gpu, int64_t off) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  if (!s->blocks.release(off)) return fail(FSX_E_INTERNAL, "double free in slab");
+  return FSX_OK;
+}
+
+int fsx_slab_ptr(fsx_fabric* f, int gpu, int64_t off, void** d_ptr) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  if (off < 0 || off > s->capacity) return fail(FSX_E_VALIDATION, "slab offset out of range");
+  *d_ptr = s->base + off;
+  return FSX_OK;
+}
+
+int fsx_slab_usage(fsx_fabric* f, int gpu, int64_t* segments, int64_t* bytes_in_use,
+                   int64_t* peak_bytes, int64_t* capacity) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  if (segments) *segments = s->blocks.segments();
+  if (bytes_in_use) *bytes_in_use = s->blocks.bytes();
+  if (peak_bytes) *peak_bytes = s->blocks.peak();
+  if (capacity) *capacity = s->capacity;
+  return FSX_OK;
+}
+
+int fsx_slab_read(fsx_fabric* f, int gpu, int64_t off, void* h_dst, int64_t n, void* stream) {
+  Slab* s = nullptr;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+    if (off < 0 || n < 0 || off + n > s->capacity)
+      return fail(FSX_E_VALIDATION, "slab read out of range");
+    int rc = device_state(f, s->device, &dev);
+    if (rc) return rc;
+  }
+  if (n == 0) return FSX_OK;
+  FSX_CUDA(cudaSetDevice(s->device));
+  cudaStream_t st = pick_stream(dev, stream);
+  FSX_CUDA(cudaMemcpyAsync(h_dst, s->base + off, n, cudaMemcpyDeviceToHost, st));
+  FSX_CUDA(cudaStreamSynchronize(st));
+  return FSX_OK;
+}
+
+int fsx_slab_export(fsx_fabric* f, int gpu, void* handle64, int64_t* bytes) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s || s->imported) return fail(FSX_E_NOT_FOUND, "no owned slab for gpu");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  FSX_CUDA(cudaSetDevice(s->device));
+  FSX_CUDA(cudaIpcGetMemHandle(&h, s->base));
+  std::memcpy(handle64, &h, sizeof(h));
+  *bytes = s->capacity;
+  return FSX_OK;
+}
+
+int fsx_slab_import(fsx_fabric* f, int gpu, const void* handle64, int64_t bytes) {
+  int dev = 0;
+  int rc = find_gpu(f, gpu, &dev);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(f->mu);
+  if (f->slabs.count(gpu)) return fail(FSX_E_CONFIG, "slab already registered for gpu");
+  auto s = std::make_unique<Slab>();
+  s->gpu = gpu;
+  s->device = dev;  // device of THIS process the mapping is opened on
+  s->imported = true;
+  s->capacity = bytes;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  FSX_CUDA(cudaSetDevice(dev));
+  void* p = nullptr;
+  FSX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  s->base = static_cast<uint8_t*>(p);
+  s->dflags = reinterpret_cast<uint64_t*>(s->base + s->capacity);
+  s->flags.size = kFlagRing;
+  f->slabs.emplace(gpu, std::move(s));
+  return FSX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Flags
+
+int fsx_flags_alloc(fsx_fabric* f, int dst_gpu, int32_t n, int64_t* flag_base) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, dst_gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (n <= 0 || n > kFlagRing / 4) return fail(FSX_E_VALIDATION, "bad flag count");
+  *flag_base = s->flags.take(n);
+  return FSX_OK;
+}
+
+int fsx_flag_ptr(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t** d_flag) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, dst_gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (flag_idx < 0 || flag_idx >= kFlagRing) return fail(FSX_E_VALIDATION, "flag index out of range");
+  *d_flag = s->dflags + flag_idx;
+  return FSX_OK;
+}
+
+int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
+                int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                void* stream) {
+  int src_dev = 0;
+  int rc = find_gpu(f, src_gpu, &src_dev);
+  if (rc) return rc;
+  if (bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+  if (chunk_bytes <= 0 || chunk_bytes >= bytes) chunk_bytes = std::max<int64_t>(bytes, 1);
+  else if (chunk_bytes % 16) return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
+  const int64_t n_chunks = bytes == 0 ? 1 : (bytes + chunk_bytes - 1) / chunk_bytes;
+  fsx::FwdArgs a{};
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    Slab* s = slab_of(f, dst_gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+    if (dst_off < 0 || dst_off + bytes > s->capacity)
+      return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
+    if (flag_base < 0 || flag_base + n_chunks > kFlagRing)
+      return fail(FSX_E_VALIDATION, "flag range out of the ring");
+    rc = device_state(f, src_dev, &dev);
+    if (rc) return rc;
+    a.counters = dev->counters + dev->counter_ring.take(n_chunks);
+    a.dst = s->base + dst_off;
+    a.dflags = s->dflags + flag_base;
+    a.hflags = s->hflags ? s->hflags + flag_base : nullptr;
+  }
+  a.src = static_cast<const uint8_t*>(d_src);
+  a.bytes = bytes;
+  a.chunk_bytes = chunk_bytes;
+  a.slice = std::min<int64_t>(kSlice, std::max<int64_t>(16, chunk_bytes));
+  a.slice = (a.slice + 15) & ~int64_t{15};
+  a.chunk_units = (chunk_bytes + a.slice - 1) / a.slice;
+  const int64_t last_len = bytes - (n_chunks - 1) * chunk_bytes;
+  a.last_units = std::max<int64_t>(1, (last_len + a.slice - 1) / a.slice);
+  a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
+  a.n_chunks = (int32_t)n_chunks;
+  a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
+  a.token = f->next_token.fetch_add(1);
+  FSX_CUDA(cudaSetDevice(src_dev));
+  const int grid = (int)std::min<int64_t>(a.total_units, dev->fwd_grid);
+  FSX_CUDA(fsx::launch_forward(a, grid, fsx::forward_block_threads(), pick_stream(dev, stream)));
+  f->launches++;
+  f->forwards++;
+  f->bytes_forwarded += bytes;
+  if (token) *token = a.token;
+  return FSX_OK;
+}
+
+int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
+                     int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                     void* stream) {
+  if (bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+  if (chunk_bytes <= 0 || chunk_bytes >= bytes) chunk_bytes = std::max<int64_t>(bytes, 1);
+  else if (chunk_bytes % 16) return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
+  const int64_t n_chunks = bytes == 0 ? 1 : (bytes + chunk_bytes - 1) / chunk_bytes;
+  Slab* s = nullptr;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, dst_gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+    if (dst_off < 0 || dst_off + bytes > s->capacity)
+      return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
+    if (flag_base < 0 || flag_base + n_chunks > kFlagRing)
+      return fail(FSX_E_VALIDATION, "flag range out of the ring");
+    int rc = device_state(f, s->device, &dev);
+    if (rc) return rc;
+  }
+  const uint64_t tok = f->next_token.fetch_add(1);
+  cudaStream_t st = pick_stream(dev, stream);
+  FSX_CUDA(cudaSetDevice(s->device));
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t beg = c * chunk_bytes, len = std::min(chunk_bytes, bytes - beg);
+    if (len > 0)
+      FSX_CUDA(cudaMemcpyAsync(s->base + dst_off + beg, static_cast<const uint8_t*>(h_src) + beg,
+                               len, cudaMemcpyHostToDevice, st));
+    fsx::FlagSetArgs fa{s->dflags + flag_base + c, s->hflags ? s->hflags + flag_base + c : nullptr,
+                        1, tok};
+    FSX_CUDA(fsx::launch_set_flags(fa, st));
+    f->launches++;
+  }
+  f->forwards++;
+  f->bytes_forwarded += bytes;
+  if (token) *token = tok;
+  return FSX_OK;
+}
+
+int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token, int* ready) {
+  Slab* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, dst_gpu);
+  }
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (!s->hflags) return fail(FSX_E_CONFIG, "host flags are only mapped in the slab owner");
+  if (flag_idx < 0 || flag_idx >= kFlagRing) return fail(FSX_E_VALIDATION, "flag index out of range");
+  const uint64_t v = __atomic_load_n(&s->hflags[flag_idx], __ATOMIC_ACQUIRE);
+  *ready = v == token;
+  return FSX_OK;
+}
+
+int fsx_wait(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, uint64_t token,
+             int64_t timeout_us) {
+  Slab* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, dst_gpu);
+  }
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (!s->hflags) return fail(FSX_E_CONFIG, "host flags are only mapped in the slab owner");
+  if (flag_base < 0 || n < 0 || flag_base + n > kFlagRing)
+    return fail(FSX_E_VALIDATION, "flag range out of the ring");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int32_t i = 0; i < n; ++i) {
+    int spins = 0;
+    while (__atomic_load_n(&s->hflags[flag_base + i], __ATOMIC_ACQUIRE) != token) {
+      if (++spins > 1024) {
+        std::this_thread::yield();
+        if (timeout_us >= 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(timeout_us))
+          return fail(FSX_E_TIMEOUT, "chunk flags not set before the timeout");
+      }
+    }
+  }
+  return FSX_OK;
+}
+
+int fsx_stream_wait_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n,
+                          uint64_t token, void* stream) {
+  Slab* s = nullptr;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, dst_gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+    int rc = device_state(f, s->device, &dev);
+    if (rc) return rc;
+  }
+  if (flag_base < 0 || n < 0 || flag_base + n > kFlagRing)
+    return fail(FSX_E_VALIDATION, "flag range out of the ring");
+  FSX_CUDA(cudaSetDevice(s->device));
+  FSX_CUDA(fsx::launch_wait_flags(s->dflags + flag_base, n, token, pick_stream(dev, stream)));
+  f->launches++;
+  return FSX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Merge / synth / stats
+
+int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, gpu, &ordinal);
+  if (rc) return rc;
+  if (!b || b->num_requests < 0 || b->num_items < 0 || b->row_bytes <= 0)
+    return fail(FSX_E_VALIDATION, "bad merge batch");
+  if (b->num_requests > 0 &&
+      (!b->d_embeds || !b->d_token_ids || !b->d_req_row_off || !b->d_req_item_off ||
+       !b->d_item_row_off || !b->d_status || (b->total_item_rows > 0 && (!b->d_item_src || !b->d_scratch))))
+    return fail(FSX_E_VALIDATION, "merge batch is missing a device array");
+  if (b->d_item_flag && (!b->d_item_token || !b->d_item_chunk_rows))
+    return fail(FSX_E_VALIDATION, "early-start merge needs tokens and chunk rows");
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  int launched = 0;
+  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched);
+  f->launches += launched;
+  if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge launch: ") + cudaGetErrorString(e));
+  f->merges++;
+  f->merged_rows += b->total_item_rows;
+  return FSX_OK;
+}
+
+int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_t n,
+                      void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, gpu, &ordinal);
+  if (rc) return rc;
+  if (n < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+  if (n == 0) return FSX_OK;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  const int64_t pairs = (n / 16) + 1;
+  const int grid = (int)std::min<int64_t>((pairs + 255) / 256, (int64_t)dev->sms * 8);
+  FSX_CUDA(fsx::launch_synth(seed, static_cast<uint8_t*>(d_dst), n, std::max(grid, 1),
+                             pick_stream(dev, stream)));
+  f->launches++;
+  return FSX_OK;
+}
+
+int fsx_get_stats(fsx_fabric* f, fsx_stats* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->forwards = f->forwards.load();
+  out->bytes_forwarded = f->bytes_forwarded.load();
+  out->merges = f->merges.load();
+  out->merged_rows = f->merged_rows.load();
+  out->kernel_launches = f->launches.load();
+  std::lock_guard<std::mutex> lk(f->mu);
+  for (auto& [g, s] : f->slabs) {
+    out->segments_in_use += s->blocks.segments();
+    out->bytes_in_use += s->blocks.bytes();
+  }
+  return FSX_OK;
+}
+
+int fsx_synchronize(fsx_fabric* f) {
+  for (auto& [o, d] : f->devices) {
+    FSX_CUDA(cudaSetDevice(o));
+    FSX_CUDA(cudaStreamSynchronize(d->stream));
+  }
+  return FSX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""One data-plane pass over a request batch on the device fabric.
+
+A pass is what the reference does per request between the encoder's
+``emit_output`` (executor_sim.hpp:221-229, 321-336) and the LLM's admission
+(executor_sim.hpp:382-392), plus the merge the reference leaves out:
+
+  1. the producer's embeddings live on the producer GPU (K0 synthesises them
+     as ``synth_payload(payload_seed(ref_id, 0))``, executor_sim.hpp:330-331);
+  2. each item gets a segment of the consumer GPU's slab (fsx_slab_alloc,
+     NodeArena policy sidecar.hpp:149-163) and a run of chunk flags;
+  3. K1 pushes each item into its segment chunk by chunk (fsx_forward);
+  4. K3 merges all items of the batch into the prompt embedding (fsx_merge);
+  5. the segments are released (the ack, sidecar.hpp:287-290, 547).
+
+torch provides device memory and streams only.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .fabric import DeviceFabric
+from .trace import (PLACEHOLDER_ID, BatchLayout, Request, ShapeRules, layout, payload_seed,
+                    prompt_tokens, text_seed)
+
+ALIGN = 256
+
+
+def _align(n: int, a: int = ALIGN) -> int:
+    return (n + a - 1) // a * a
+
+
+class DataPlaneBatch:
+    def __init__(self, fab: DeviceFabric, requests: List[Request], rules: ShapeRules,
+                 src_gpu: int, dst_gpu: int, placeholder_id: int = PLACEHOLDER_ID,
+                 chunk_rows: Optional[int] = None):
+        self.fab = fab
+        self.rules = rules
+        self.rb = rules.row_bytes
+        self.lay: BatchLayout = layout(requests, self.rb)
+        self.src_gpu, self.dst_gpu = src_gpu, dst_gpu
+        self.pid = placeholder_id
+        self.chunk_rows = chunk_rows
+        self.src_dev = torch.device("cuda", fab.device_of(src_gpu))
+        self.dst_dev = torch.device("cuda", fab.device_of(dst_gpu))
+        lay = self.lay
+        M = len(lay.items)
+        # Producer side: one buffer, each item at a 256 B aligned offset.
+        self.src_off = np.zeros(M, dtype=np.int64)
+        at = 0
+        for i, it in enumerate(lay.items):
+            self.src_off[i] = at
+            at += _align(it.rows * self.rb)
+        self.src_buf = torch.empty(max(at, ALIGN), dtype=torch.uint8, device=self.src_dev)
+        # Consumer side: prompt embedding, token ids, merge descriptors.
+        self.embeds = torch.empty(max(lay.total_rows * self.rb, 16), dtype=torch.uint8,
+                                  device=self.dst_dev)
+        tok = np.concatenate([prompt_tokens(q, placeholder_id) for q in requests]) \
+            if requests else np.zeros(0, np.int32)
+        self.tok_host = tok
+        self.tok = torch.from_numpy(tok).to(self.dst_dev) if len(tok) else \
+            torch.zeros(1, dtype=torch.int32, device=self.dst_dev)
+        self.req_row_off = torch.from_numpy(lay.req_row_off).to(self.dst_dev)
+        self.req_item_off = torch.from_numpy(lay.req_item_off).to(self.dst_dev)
+        self.item_row_off = torch.from_numpy(lay.item_row_off).to(self.dst_dev)
+        self.scratch = torch.empty(max(lay.total_item_rows, 1), dtype=torch.int32,
+                                   device=self.dst_dev)
+        self.status = torch.full((max(len(requests), 1),), -1, dtype=torch.int32,
+                                 device=self.dst_dev)
+        self.item_src = torch.zeros(max(M, 1), dtype=torch.int64, device=self.dst_dev)
+        self.item_flag = torch.zeros(max(M, 1), dtype=torch.int64, device=self.dst_dev)
+        self.item_token = torch.zeros(max(M, 1), dtype=torch.int64, device=self.dst_dev)
+        self.item_chunk_rows = torch.zeros(max(M, 1), dtype=torch.int64, device=self.dst_dev)
+        self.slab_off: Optional[np.ndarray] = None
+        self.flag_base = np.zeros(M, dtype=np.int64)
+        self.n_chunks = np.ones(M, dtype=np.int64)
+        self.tokens = np.zeros(M, dtype=np.uint64)
+
+    # -- inputs ---------------------------------------------------------------
+    def synth_inputs(self, stream=None) -> None:
+        """K0: producer payloads and the pre-filled prompt embeddings."""
+        base = self.src_buf.data_ptr()
+        for i, it in enumerate(self.lay.items):
+            self.fab.synth(self.src_gpu, payload_seed(it.ref_id, 0), base + int(self.src_off[i]),
+                           it.rows * self.rb, stream)
+        eb = self.embeds.data_ptr()
+        for r, q in enumerate(self.lay.requests):
+            self.fab.synth(self.dst_gpu, text_seed(q), eb + int(self.lay.req_row_off[r]) * self.rb,
+                           q.total_rows * self.rb, stream)
+
+    # -- slab -------------------------------------------------------------------
+    def alloc(self) -> bool:
+        """One slab segment per item; False (nothing held) if the slab is full."""
+        offs = []
+        for it in self.lay.items:
+            off = self.fab.slab_alloc(self.dst_gpu, it.rows * self.rb)
+            if off is None:
+                for o in offs:
+                    self.fab.slab_free(self.dst_gpu, o)
+                return False
+            offs.append(off)
+        self.slab_off = np.array(offs, dtype=np.int64)
+        ptrs = [self.fab.slab_ptr(self.dst_gpu, o) for o in offs]
+        if ptrs:
+            self.item_src.copy_(torch.tensor(ptrs, dtype=torch.int64))
+        return True
+
+    def release(self) -> None:
+        if self.slab_off is not None:
+            for o in self.slab_off:
+                self.fab.slab_free(self.dst_gpu, int(o))
+            self.slab_off = None
+
+    # -- K1 ---------------------------------------------------------------------
+    def chunk_bytes(self, it) -> int:
+        if not self.chunk_rows:
+            return 0
+        return self.chunk_rows * self.rb
+
+    def forward(self, stream=None) -> int:
+        """Push every item into its slab segment; returns kernels launched."""
+        assert self.slab_off is not None, "alloc() first"
+        base = self.src_buf.data_ptr()
+        for i, it in enumerate(self.lay.items):
+            nb = it.rows * self.rb
+            cb = self.chunk_bytes(it)
+            n = 1 if (cb <= 0 or cb >= nb) else -(-nb // cb)
+            self.n_chunks[i] = n
+            self.flag_base[i] = self.fab.flags_alloc(self.dst_gpu, n)
+            self.tokens[i] = self.fab.forward(self.src_gpu, base + int(self.src_off[i]),
+                                              self.dst_gpu, int(self.slab_off[i]), nb, cb,
+                                              int(self.flag_base[i]), stream)
+        return len(self.lay.items)
+
+    def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
+        """The host-span send path (sidecar.hpp:302): payload bytes from host
+        memory straight into the consumer slab."""
+        assert self.slab_off is not None, "alloc() first"
+        for i, it in enumerate(self.lay.items):
+            nb = it.rows * self.rb
+            cb = self.chunk_bytes(it)
+            n = 1 if (cb <= 0 or cb >= nb) else -(-nb // cb)
+            self.n_chunks[i] = n
+            self.flag_base[i] = self.fab.flags_alloc(self.dst_gpu, n)
+            self.tokens[i] = self.fab.forward_host(host_payload[i].ctypes.data, self.dst_gpu,
+                                                   int(self.slab_off[i]), nb, cb,
+                                                   int(self.flag_base[i]), stream)
+
+    def wait_host(self, timeout_us: int = 30_000_000) -> None:
+        for i in range(len(self.lay.items)):
+            self.fab.wait(self.dst_gpu, int(self.flag_base[i]), int(self.n_chunks[i]),
+                          int(self.tokens[i]), timeout_us)
+
+    # -- K3 ---------------------------------------------------------------------
+    def merge_batch(self, early_start: bool = False) -> N.MergeBatch:
+        lay = self.lay
+        b = N.MergeBatch()
+        b.num_requests = len(lay.requests)
+        b.num_items = len(lay.items)
+        b.row_bytes = self.rb
+        b.placeholder_id = self.pid
+        b.d_embeds = self.embeds.data_ptr()
+        b.d_token_ids = self.tok.data_ptr()
+        b.d_req_row_off = self.req_row_off.data_ptr()
+        b.d_req_item_off = self.req_item_off.data_ptr()
+        b.d_item_src = self.item_src.data_ptr()
+        b.d_item_row_off = self.item_row_off.data_ptr()
+        b.d_scratch = self.scratch.data_ptr()
+        b.d_status = self.status.data_ptr()
+        b.total_rows = lay.total_rows
+        b.total_item_rows = lay.total_item_rows
+        if early_start and len(lay.items):
+            flags = [self.fab.flag_ptr(self.dst_gpu, int(fb)) for fb in self.flag_base]
+            self.item_flag.copy_(torch.tensor(flags, dtype=torch.int64))
+            self.item_token.copy_(torch.from_numpy(self.tokens.astype(np.int64)))
+            cr = [self.chunk_rows or it.rows for it in lay.items]
+            self.item_chunk_rows.copy_(torch.tensor(cr, dtype=torch.int64))
+            b.d_item_flag = self.item_flag.data_ptr()
+            b.d_item_token = self.item_token.data_ptr()
+            b.d_item_chunk_rows = self.item_chunk_rows.data_ptr()
+        return b
+
+    def merge(self, stream=None, early_start: bool = False) -> None:
+        self.fab.merge(self.dst_gpu, self.merge_batch(early_start), stream)
+
+    # -- readback -----------------------------------------------------------------
+    def embeds_host(self) -> np.ndarray:
+        return self.embeds[: self.lay.total_rows * self.rb].cpu().numpy()
+
+    def status_host(self) -> np.ndarray:
+        return self.status[: len(self.lay.requests)].cpu().numpy()
+
+    def slab_item_host(self, i: int) -> np.ndarray:
+        it = self.lay.items[i]
+        raw = self.fab.slab_read(self.dst_gpu, int(self.slab_off[i]), it.rows * self.rb)
+        return np.frombuffer(raw, dtype=np.uint8)

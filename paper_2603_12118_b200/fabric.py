@@ -1,0 +1,159 @@
+"""Python handle over the libfsx C ABI (include/fsx.h).
+
+``DeviceFabric`` is the device layer the reference's SidecarFabric would sit
+on: the logical GPU map (sidecar.hpp:242-260), per-consumer-GPU
+receive slabs with the NodeArena allocation policy (sidecar.hpp:106-205),
+chunk flags, the K1 forward, the K3 merge and K0 synthesis.  The C++
+SidecarFabric-compatible engine is include/fsx/fabric.hpp; this class exists
+so the Python tests and bench.py can drive the same C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, Optional
+
+from . import _native as N
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)  # torch.cuda.Stream
+
+
+class DeviceFabric:
+    def __init__(self, gpu_to_node: Dict[int, int], devices: Optional[Dict[int, int]] = None):
+        gpus = sorted(gpu_to_node)
+        n = len(gpus)
+        ids = (C.c_int * n)(*gpus)
+        nodes = (C.c_int * n)(*[gpu_to_node[g] for g in gpus])
+        devs = (C.c_int * n)(*[(devices or {}).get(g, -1) for g in gpus])
+        h = C.c_void_p()
+        N.call("fsx_open", n, ids, nodes, devs, C.byref(h))
+        self._h = h
+        self.gpus = gpus
+
+    # -- lifetime -----------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            N.call("fsx_close", self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- topology (sidecar.hpp:250-260) ---------------------------------------
+    def node_of(self, gpu: int) -> int:
+        v = C.c_int()
+        N.call("fsx_node_of", self._h, gpu, C.byref(v))
+        return v.value
+
+    def route(self, src: int, dst: int) -> int:
+        v = C.c_int()
+        N.call("fsx_route", self._h, src, dst, C.byref(v))
+        return v.value
+
+    def device_of(self, gpu: int) -> int:
+        v = C.c_int()
+        N.call("fsx_device_of", self._h, gpu, C.byref(v))
+        return v.value
+
+    # -- slabs ----------------------------------------------------------------
+    def slab_register(self, gpu: int, nbytes: int) -> None:
+        N.call("fsx_slab_register", self._h, gpu, nbytes)
+
+    def slab_alloc(self, gpu: int, nbytes: int) -> Optional[int]:
+        off = C.c_int64()
+        N.call("fsx_slab_alloc", self._h, gpu, nbytes, C.byref(off))
+        return None if off.value < 0 else off.value
+
+    def slab_free(self, gpu: int, off: int) -> None:
+        N.call("fsx_slab_free", self._h, gpu, off)
+
+    def slab_ptr(self, gpu: int, off: int = 0) -> int:
+        p = C.c_void_p()
+        N.call("fsx_slab_ptr", self._h, gpu, off, C.byref(p))
+        return p.value or 0
+
+    def slab_usage(self, gpu: int) -> dict:
+        v = [C.c_int64() for _ in range(4)]
+        N.call("fsx_slab_usage", self._h, gpu, *[C.byref(x) for x in v])
+        return dict(zip(["segments_in_use", "bytes_in_use", "peak_bytes", "capacity"],
+                        [x.value for x in v]))
+
+    def slab_read(self, gpu: int, off: int, nbytes: int, stream=None) -> bytes:
+        buf = (C.c_uint8 * max(nbytes, 1))()
+        N.call("fsx_slab_read", self._h, gpu, off, buf, nbytes, _stream_ptr(stream))
+        return bytes(buf)[:nbytes]
+
+    def slab_export(self, gpu: int) -> tuple:
+        buf = (C.c_uint8 * 64)()
+        nb = C.c_int64()
+        N.call("fsx_slab_export", self._h, gpu, buf, C.byref(nb))
+        return bytes(buf), nb.value
+
+    def slab_import(self, gpu: int, handle: bytes, nbytes: int) -> None:
+        buf = (C.c_uint8 * 64)(*handle)
+        N.call("fsx_slab_import", self._h, gpu, buf, nbytes)
+
+    # -- flags ------------------------------------------------------------------
+    def flags_alloc(self, gpu: int, n: int) -> int:
+        v = C.c_int64()
+        N.call("fsx_flags_alloc", self._h, gpu, n, C.byref(v))
+        return v.value
+
+    def flag_ptr(self, gpu: int, idx: int) -> int:
+        p = C.c_void_p()
+        N.call("fsx_flag_ptr", self._h, gpu, idx, C.byref(p))
+        return p.value or 0
+
+    def chunk_ready(self, gpu: int, idx: int, token: int) -> bool:
+        v = C.c_int()
+        N.call("fsx_chunk_ready", self._h, gpu, idx, token, C.byref(v))
+        return bool(v.value)
+
+    def wait(self, gpu: int, flag_base: int, n: int, token: int, timeout_us: int = -1) -> None:
+        N.call("fsx_wait", self._h, gpu, flag_base, n, token, timeout_us)
+
+    def stream_wait_flags(self, gpu: int, flag_base: int, n: int, token: int, stream=None) -> None:
+        N.call("fsx_stream_wait_flags", self._h, gpu, flag_base, n, token, _stream_ptr(stream))
+
+    # -- data movement ----------------------------------------------------------
+    def forward(self, src_gpu: int, src_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
+                chunk_bytes: int, flag_base: int, stream=None) -> int:
+        tok = C.c_uint64()
+        N.call("fsx_forward", self._h, src_gpu, src_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
+               flag_base, C.byref(tok), _stream_ptr(stream))
+        return tok.value
+
+    def forward_host(self, host_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
+                     chunk_bytes: int, flag_base: int, stream=None) -> int:
+        tok = C.c_uint64()
+        N.call("fsx_forward_host", self._h, host_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
+               flag_base, C.byref(tok), _stream_ptr(stream))
+        return tok.value
+
+    def merge(self, gpu: int, batch: N.MergeBatch, stream=None) -> None:
+        N.call("fsx_merge", self._h, gpu, C.byref(batch), _stream_ptr(stream))
+
+    def synth(self, gpu: int, seed: int, dst_ptr: int, nbytes: int, stream=None) -> None:
+        N.call("fsx_synth_payload", self._h, gpu, seed, dst_ptr, nbytes, _stream_ptr(stream))
+
+    def stats(self) -> dict:
+        s = N.Stats()
+        N.call("fsx_get_stats", self._h, C.byref(s))
+        return {k: getattr(s, k) for k, _ in N.Stats._fields_}
+
+    def synchronize(self) -> None:
+        N.call("fsx_synchronize", self._h)
