@@ -28,6 +28,34 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle all
 
+# C++ fabric tests (run on the GPU by tests/test_cpp_fabric.py).
+FISSIM_REF_INCLUDE ?= /root/reference/proj/include
+FISSIM_REF_TESTS ?= /root/reference/proj/tests
+NLOHMANN_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+CXXTEST := $(CXX) -std=c++20 -O2 -Wall -Wno-unused-parameter -Iinclude -Itests/cpp/catch2_shim \
+           -I/usr/local/cuda/include
+LINKFSX := -L$(PKG) -lfsx -L/usr/local/cuda/lib64 -lcudart -lpthread \
+           -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
+
+build/fsx_oracle_test.o: oracle/fsx_oracle.c oracle/fsx_oracle.h | build
+	$(CC) -std=c11 -O2 -fPIC -c $< -o $@
+
+build/test_fabric: tests/cpp/test_fabric.cpp tests/cpp/shim_main.cpp include/fsx/fabric.hpp \
+                   build/fsx_oracle_test.o $(LIB) | build
+	$(CXXTEST) -Ioracle -o $@ tests/cpp/test_fabric.cpp tests/cpp/shim_main.cpp \
+	    build/fsx_oracle_test.o $(LINKFSX)
+
+# The REFERENCE's own unit tests for the sidecar, compiled unmodified against
+# the drop-in header (needs the reference tree: built here, run on the box).
+build/ref_test_sidecar: $(FISSIM_REF_TESTS)/test_sidecar.cpp tests/cpp/shim_main.cpp \
+                        include/fsx/fabric.hpp include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ $(FISSIM_REF_TESTS)/test_sidecar.cpp \
+	    tests/cpp/shim_main.cpp $(LINKFSX)
+
+cpptests: build/test_fabric
+	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then $(MAKE) -s build/ref_test_sidecar; fi
+
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt
 

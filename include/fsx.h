@@ -115,9 +115,11 @@ int fsx_flag_ptr(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t** d_flag
  * the arena).  An sm_100a kernel on src_gpu's device pushes `bytes` from d_src
  * into dst_gpu's slab at dst_off with 16-byte stores (NVLink/NVSwitch P2P when
  * the devices differ, HBM copy when they are the same), chunk by chunk; when
- * chunk c is fully stored its flag flag_base + c is set to the returned token
+ * chunk c is fully stored its flag flag_base + c is set to the token
  * (release, system scope).  n_chunks = ceil(bytes / chunk_bytes) (1 when
- * chunk_bytes <= 0 or >= bytes); chunk_bytes must be a multiple of 16. */
+ * chunk_bytes <= 0 or >= bytes); chunk_bytes must be a multiple of 16.
+ * token is in/out: a non-zero *token on entry is used as given (tokens agreed
+ * out of band, e.g. across processes); otherwise a fresh one is drawn. */
 int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                 int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                 void* stream);
@@ -138,6 +140,12 @@ int fsx_wait(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, uint64_t 
  * queued after it starts exactly when the chunks have landed. */
 int fsx_stream_wait_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n,
                           uint64_t token, void* stream);
+/* Enqueue on `stream` (any device of this process) a store of token into
+ * flags [flag_base, flag_base + n) of dst_gpu's slab (release, system scope):
+ * the cross-process acknowledgement (ack_raw, sidecar.hpp:287-290) and any
+ * consumer->producer signal ride on it. */
+int fsx_signal_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, uint64_t token,
+                     int src_gpu, void* stream);
 
 /* ---- merge (K3) -------------------------------------------------------------
  * New on this path: the reference consumer discards the bytes
@@ -151,13 +159,20 @@ int fsx_stream_wait_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t
  * (0 otherwise).  Rows are moved as opaque bytes (bf16 NaN/Inf patterns
  * survive).  All arrays are DEVICE arrays on gpu's device.  Optional early
  * start: when d_item_flag is non-NULL, row j of item i is copied only after
- * d_item_flag[i][j / d_item_chunk_rows[i]] == d_item_token[i]. */
+ * d_item_flag[i][j / d_item_chunk_rows[i]] == d_item_token[i].
+ * Two phases: a placeholder scan (needs only token ids, so it can run while
+ * the payload is still in flight) and the row copy.  mode selects both
+ * (FULL), the scan alone (SCAN_ONLY) or the copy of an already-scanned batch
+ * (COPY_ONLY, same d_scratch / d_status). */
+#define FSX_MERGE_FULL 0
+#define FSX_MERGE_SCAN_ONLY 1
+#define FSX_MERGE_COPY_ONLY 2
 typedef struct fsx_merge_batch {
   int32_t num_requests;
   int32_t num_items;
   int64_t row_bytes;                 /* hidden_dim * embed_elem_bytes (profiles.hpp:278-283) */
   int32_t placeholder_id;
-  int32_t _pad;
+  int32_t mode;                      /* FSX_MERGE_FULL / _SCAN_ONLY / _COPY_ONLY */
   void* d_embeds;                    /* [sum T, row_bytes] */
   const int32_t* d_token_ids;        /* [sum T] */
   const int64_t* d_req_row_off;      /* [R + 1] */
@@ -179,6 +194,15 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream);
  * reference stream.  Used by producers/tests/bench to create inputs. */
 int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_t n,
                       void* stream);
+
+/* ---- host helpers -----------------------------------------------------------
+ * Device ordinal owning p, or -1 for host / unregistered memory (never fails).
+ * Lets the send(span) entry point (sidecar.hpp:302) take a producer tensor that
+ * already lives on the GPU down the K1 path instead of the host copy path. */
+int fsx_pointer_device(const void* p, int* device);
+/* Synchronous device->host copy (owning a device payload that must outlive a
+ * borrowed span, e.g. backlogged sends, sidecar.hpp:327). */
+int fsx_copy_to_host(void* h_dst, const void* d_src, int64_t n);
 
 /* ---- stats ----------------------------------------------------------------
  * SidecarStats (sidecar.hpp:209-217, 403-415) device-side counterparts plus

@@ -1,0 +1,662 @@
+// fsx/fabric.hpp -- C++ SidecarFabric engine over the libfsx C ABI.
+//
+// Re-implements the behaviour of the reference sidecar fabric
+// (/root/reference/proj/include/fissim/sidecar.hpp:240-616) on B200 receive
+// slabs:
+//   * routing and topology            sidecar.hpp:250-260
+//   * producer send + placement       sidecar.hpp:302-347, 465-483
+//   * ordered per-ref delivery        sidecar.hpp:498-563
+//   * raw (notify-then-read) interest sidecar.hpp:276-290
+//   * backpressure backlog + timeout  sidecar.hpp:329-334, 571-602
+//   * orphan reclaim                  sidecar.hpp:511-524
+//   * fail_ref / purge / cancel       sidecar.hpp:292-297, 373-401
+//   * stats                           sidecar.hpp:403-415
+// The bytes never go through host arenas: every destination GPU owns a device
+// slab (fsx_slab_*), payloads land there through K1 (device source, NVLink or
+// HBM) or a host->device copy (host span), chunk flags gate delivery, and
+// ChunkCallback consumers get an owned host vector (fsx_slab_read) while raw
+// consumers read the slab in place (slab_ptr) and ack_raw() it.
+//
+// The engine is a template over a Traits policy so the same code runs
+//   * standalone (fsx::StandaloneTraits below: fsx::EventLoop, fsx::Error,
+//     fsx::DataRef) for this repo's own C++ tests, and
+//   * as a drop-in for the reference (include/fsx/dropin/fissim/sidecar.hpp:
+//     fissim::SimKernel, fissim::Error, fissim::DataRef, fissim::ForwardEnvelope).
+//
+// Threading: like the reference (sidecar.hpp:299-301, 604-615) every method
+// runs on the event-kernel thread; the engine holds no locks of its own.
+#pragma once
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <queue>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fsx.h"
+
+namespace fsx {
+
+enum class Transport { LocalBuffer, NetworkStream };
+
+inline const char* transport_name(Transport t) {
+  return t == Transport::LocalBuffer ? "local_buffer" : "network_stream";
+}
+
+// Same knobs as the reference SidecarConfig (sidecar.hpp:38-57); the modeled
+// latency keeps event timestamps identical to the reference in Virtual mode.
+struct SidecarConfig {
+  int64_t arena_bytes = int64_t{1} << 30;  // per destination GPU slab
+  double local_base_ms = 0.5;
+  double local_per_mb_ms = 0.8125;
+  double net_base_ms = 1.0;
+  double net_per_mb_ms = 0.8125;
+  double send_timeout_ms = 10000;
+  double orphan_timeout_ms = 30000;
+  int64_t stream_chunk_bytes = 256 * 1024;
+  // fsx additions
+  int64_t device_chunk_bytes = int64_t{8} << 20;  // flag granularity of K1 pushes
+  int64_t wait_timeout_us = 30'000'000;            // GPU completion watchdog
+
+  double latency_ms(Transport t, int64_t bytes) const {
+    const double mb = static_cast<double>(bytes) / (1024.0 * 1024.0);
+    return t == Transport::LocalBuffer ? local_base_ms + local_per_mb_ms * mb
+                                       : net_base_ms + net_per_mb_ms * mb;
+  }
+};
+
+struct SidecarStats {
+  int64_t transfers = 0;
+  int64_t bytes_forwarded = 0;
+  int64_t integrity_errors = 0;
+  int64_t orphan_reclaims = 0;
+  double added_latency_ms = 0;
+  size_t segments_in_use = 0;
+  int64_t bytes_in_use = 0;
+};
+
+// Wire checksum of the envelope (common.hpp:221-241), needed bit-for-bit for
+// interop with reference peers on the network transport.
+inline uint64_t checksum64(const uint8_t* p, size_t n) {
+  constexpr uint64_t kMul = 0x2545f4914f6cdd1dull;
+  uint64_t h = 0x9e3779b97f4a7c15ull ^ (static_cast<uint64_t>(n) * 0xff51afd7ed558ccdull);
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, p + i, 8);
+    h = (h ^ w) * kMul;
+    h ^= h >> 29;
+  }
+  uint64_t tail = 0;
+  for (unsigned sh = 0; i < n; ++i, sh += 8) tail |= static_cast<uint64_t>(p[i]) << sh;
+  h = (h ^ tail) * kMul;
+  return h ^ (h >> 32);
+}
+
+// Status codes of the C ABI are 1 + fissim::ErrorCode ordinal.
+namespace status {
+constexpr int kValidation = FSX_E_VALIDATION;
+constexpr int kNotFound = FSX_E_NOT_FOUND;
+constexpr int kIntegrity = FSX_E_INTEGRITY;
+constexpr int kProtocol = FSX_E_PROTOCOL;
+constexpr int kTimeout = FSX_E_TIMEOUT;
+constexpr int kConfig = FSX_E_CONFIG;
+constexpr int kInternal = FSX_E_INTERNAL;
+}  // namespace status
+
+template <class Traits>
+class Fabric {
+ public:
+  using Kernel = typename Traits::Kernel;
+  using Envelope = typename Traits::Envelope;
+  using Error = typename Traits::Error;
+  using Ref = typename Traits::DataRef;
+  using ChunkCallback = std::function<void(const Envelope&, std::vector<uint8_t>)>;
+  using RefErrorCallback = std::function<void(const Error&)>;
+  using RawChunkCallback = std::function<void(const Envelope&, int64_t)>;
+  using FailureHandler = std::function<void(const std::string&, const std::string&, const Error&)>;
+
+  // devices: logical gpu -> CUDA ordinal (missing -> gpu % device_count).
+  Fabric(Kernel& kernel, std::map<int, int> gpu_to_node, SidecarConfig config = {},
+         std::map<int, int> devices = {})
+      : kernel_(kernel), topo_(std::move(gpu_to_node)), config_(config) {
+    std::vector<int> ids, nodes, devs;
+    for (const auto& [g, n] : topo_) {
+      ids.push_back(g);
+      nodes.push_back(n);
+      auto it = devices.find(g);
+      devs.push_back(it == devices.end() ? -1 : it->second);
+    }
+    fsx_fabric* h = nullptr;
+    check(fsx_open(static_cast<int>(ids.size()), ids.data(), nodes.data(), devs.data(), &h));
+    h_ = h;
+  }
+
+  Fabric(const Fabric&) = delete;
+  Fabric& operator=(const Fabric&) = delete;
+
+  ~Fabric() {
+    if (h_) fsx_close(h_);
+  }
+
+  // -- topology (sidecar.hpp:250-260) -----------------------------------------
+  Transport route(int src_gpu, int dst_gpu) const {
+    return node_of(src_gpu) == node_of(dst_gpu) ? Transport::LocalBuffer : Transport::NetworkStream;
+  }
+
+  int node_of(int gpu) const {
+    auto it = topo_.find(gpu);
+    if (it == topo_.end())
+      Traits::raise(status::kNotFound, "gpu " + std::to_string(gpu) + " not in topology map");
+    return it->second;
+  }
+
+  // -- consumer side (sidecar.hpp:263-297) -----------------------------------
+  void register_interest(int gpu, const std::string& ref_id, ChunkCallback on_chunk,
+                         RefErrorCallback on_error = {}) {
+    node_of(gpu);
+    RefState& st = refs_[key_of(ref_id, gpu)];
+    st.dst_gpu = gpu;
+    st.on_chunk = std::move(on_chunk);
+    st.raw_cb = nullptr;
+    st.on_error = std::move(on_error);
+    st.has_interest = true;
+    drain(st);
+  }
+
+  void register_interest_raw(int gpu, const std::string& ref_id, RawChunkCallback on_chunk,
+                             RefErrorCallback on_error = {}) {
+    node_of(gpu);
+    RefState& st = refs_[key_of(ref_id, gpu)];
+    st.dst_gpu = gpu;
+    st.raw_cb = std::move(on_chunk);
+    st.on_error = std::move(on_error);
+    st.has_interest = true;
+    drain(st);
+  }
+
+  // Raw consumers release their segment.  `slab_gpu` is the destination GPU
+  // whose slab holds it (the envelope location reads "gpu<G>:off<K>").
+  void ack_raw(int slab_gpu, int64_t offset) {
+    release_segment(slab_gpu, offset);
+    place_backlog(slab_gpu);
+  }
+
+  void cancel_interest(const std::string& ref_id, int gpu) {
+    auto it = refs_.find(key_of(ref_id, gpu));
+    if (it == refs_.end()) return;
+    drop_parked(it->second);
+    refs_.erase(it);
+  }
+
+  // Device view of a delivered segment (zero-copy read for raw consumers).
+  void* slab_ptr(int gpu, int64_t offset) {
+    void* p = nullptr;
+    check(fsx_slab_ptr(h_, gpu, offset, &p));
+    return p;
+  }
+
+  // -- producer side (sidecar.hpp:302-347, 367-370) --------------------------
+  // `payload` may point to host memory (copied host->device into the consumer
+  // slab) or to device memory of src_gpu's device (pushed by K1 over NVLink or
+  // HBM).  The span is borrowed for the duration of the call only.
+  void send(const std::string& request_id, const Ref& ref, int src_gpu, int dst_gpu,
+            std::span<const uint8_t> payload, int64_t seq, bool final_chunk) {
+    const int64_t n = static_cast<int64_t>(payload.size());
+    if (!Traits::streaming(ref) && n != Traits::total_bytes(ref))
+      Traits::raise(status::kProtocol, "payload length " + std::to_string(n) +
+                                           " does not match descriptor total_bytes " +
+                                           std::to_string(Traits::total_bytes(ref)) + " for ref " +
+                                           Traits::ref_id(ref));
+    const Transport t = route(src_gpu, dst_gpu);
+    Pending ps;
+    ps.env.request_id = request_id;
+    ps.env.ref_id = Traits::ref_id(ref);
+    ps.env.seq = seq;
+    ps.env.chunk_bytes = n;
+    ps.env.total_bytes = Traits::total_bytes(ref);
+    Traits::set_transport(ps.env, t == Transport::LocalBuffer);
+    ps.env.final = final_chunk;
+    ps.env.send_time = Traits::now(kernel_);
+    ps.env.src_gpu = src_gpu;
+    ps.env.dst_gpu = dst_gpu;
+    ps.deadline = Traits::now(kernel_) + config_.send_timeout_ms;
+    ps.src = payload.data();
+    ps.src_is_device = n > 0 && device_of_pointer(payload.data()) >= 0;
+
+    if (t == Transport::NetworkStream) {
+      // Cross-node: envelope and bytes travel together (sidecar.hpp:337-346),
+      // staged into the destination slab on arrival.
+      ps.env.checksum = checksum64_any(ps);
+      own_bytes(ps);
+      const double lat = config_.latency_ms(t, n);
+      added_latency_ms_ += lat;
+      auto shared = std::make_shared<Pending>(std::move(ps));
+      Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.net_deliver",
+                       [this, shared] { handle_network(shared->env, std::move(shared->bytes)); });
+      return;
+    }
+    ps.env.checksum = 0;  // local: NVLink/HBM hop, no serial host checksum
+    if (!place_local(ps)) {
+      own_bytes(ps);  // borrowed span dies with the call: keep the bytes for the backlog
+      const int slab = ps.env.dst_gpu;
+      backlog_[slab].push_back(std::move(ps));
+      arm_timeout(slab);
+    }
+  }
+
+  void send_payload(const std::string& request_id, const Ref& ref, int src_gpu, int dst_gpu,
+                    std::span<const uint8_t> payload) {
+    send(request_id, ref, src_gpu, dst_gpu, payload, 0, true);
+  }
+
+  // Network arrival (sidecar.hpp:351-364, 487-496): verify, stage, deliver now.
+  void handle_network(Envelope env, std::vector<uint8_t> bytes) {
+    if (env.chunk_bytes != static_cast<int64_t>(bytes.size()))
+      Traits::raise(status::kProtocol, "network envelope chunk_bytes mismatch for ref " + env.ref_id);
+    Pending ps;
+    ps.env = std::move(env);
+    ps.bytes = std::move(bytes);
+    ps.owned = true;
+    ps.src = ps.bytes.data();
+    ps.deadline = Traits::now(kernel_) + config_.send_timeout_ms;
+    ps.network = true;
+    if (!stage_network(ps)) {
+      const int slab = ps.env.dst_gpu;
+      backlog_[slab].push_back(std::move(ps));
+      arm_timeout(slab);
+    }
+  }
+
+  // -- failure and cleanup (sidecar.hpp:373-401) ------------------------------
+  void fail_ref(const std::string& ref_id, const Error& err) {
+    const std::string prefix = ref_id + "@";
+    for (auto it = refs_.lower_bound(prefix); it != refs_.end(); ++it) {
+      if (it->first.compare(0, prefix.size(), prefix) != 0) break;
+      it->second.failed = std::make_shared<Error>(err);
+      if (it->second.on_error) it->second.on_error(err);
+    }
+  }
+
+  void purge_request(const std::string& request_id) {
+    const std::string prefix = request_id + "/";
+    for (auto it = refs_.begin(); it != refs_.end();) {
+      const bool mine = it->second.request_id == request_id ||
+                        (it->first.size() > prefix.size() && it->first.compare(0, prefix.size(), prefix) == 0);
+      if (mine) {
+        drop_parked(it->second);
+        it = refs_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    for (auto& [slab, q] : backlog_) {
+      q.erase(std::remove_if(q.begin(), q.end(),
+                             [&](const Pending& p) { return p.env.request_id == request_id; }),
+              q.end());
+    }
+  }
+
+  SidecarStats stats() const {
+    SidecarStats s;
+    s.transfers = transfers_;
+    s.bytes_forwarded = bytes_forwarded_;
+    s.integrity_errors = integrity_errors_;
+    s.orphan_reclaims = orphan_reclaims_;
+    s.added_latency_ms = added_latency_ms_;
+    for (int g : slabs_) {
+      int64_t segs = 0, used = 0;
+      if (fsx_slab_usage(h_, g, &segs, &used, nullptr, nullptr) == FSX_OK) {
+        s.segments_in_use += static_cast<size_t>(segs);
+        s.bytes_in_use += used;
+      }
+    }
+    return s;
+  }
+
+  const SidecarConfig& config() const { return config_; }
+  void set_failure_handler(FailureHandler fn) { failure_handler_ = std::move(fn); }
+  fsx_fabric* handle() const { return h_; }
+
+ private:
+  struct RefState {
+    std::string request_id;
+    int dst_gpu = -1;
+    bool has_interest = false;
+    ChunkCallback on_chunk;
+    RawChunkCallback raw_cb;
+    RefErrorCallback on_error;
+    int64_t next_seq = 0;
+    std::map<int64_t, std::pair<Envelope, int64_t>> parked;  // seq -> (env, slab offset)
+    std::shared_ptr<Error> failed;
+  };
+
+  struct Pending {
+    Envelope env;
+    std::vector<uint8_t> bytes;  // owned copy (backlog / network)
+    const uint8_t* src = nullptr;
+    bool owned = false;
+    bool src_is_device = false;
+    bool network = false;
+    double deadline = 0;
+  };
+
+  void check(int rc) const {
+    if (rc != FSX_OK) Traits::raise(rc, fsx_last_error());
+  }
+
+  static std::string key_of(const std::string& ref_id, int gpu) {
+    return ref_id + "@" + std::to_string(gpu);
+  }
+
+  static int device_of_pointer(const void* p) {
+    int dev = -1;
+    if (fsx_pointer_device(p, &dev) != FSX_OK) return -1;
+    return dev;
+  }
+
+  // Bytes of a pending send on the host (network checksum / backlog copies).
+  void own_bytes(Pending& ps) {
+    if (ps.owned) return;
+    const int64_t n = ps.env.chunk_bytes;
+    ps.bytes.resize(static_cast<size_t>(n));
+    if (n > 0) {
+      if (ps.src_is_device) check(fsx_copy_to_host(ps.bytes.data(), ps.src, n));
+      else std::memcpy(ps.bytes.data(), ps.src, static_cast<size_t>(n));
+    }
+    ps.owned = true;
+    ps.src_is_device = false;
+    ps.src = ps.bytes.data();
+  }
+
+  uint64_t checksum64_any(Pending& ps) {
+    if (ps.src_is_device) own_bytes(ps);
+    return checksum64(ps.src, static_cast<size_t>(ps.env.chunk_bytes));
+  }
+
+  void ensure_slab(int gpu) {
+    if (std::find(slabs_.begin(), slabs_.end(), gpu) != slabs_.end()) return;
+    check(fsx_slab_register(h_, gpu, config_.arena_bytes));
+    slabs_.push_back(gpu);
+  }
+
+  // Allocate a segment and start moving the bytes; false when the slab is full.
+  bool start_copy(Pending& ps, int64_t* off, uint64_t* token, int64_t* flag_base, int32_t* n_chunks) {
+    const int dst = ps.env.dst_gpu;
+    ensure_slab(dst);
+    check(fsx_slab_alloc(h_, dst, std::max<int64_t>(ps.env.chunk_bytes, 1), off));
+    if (*off < 0) return false;
+    const int64_t n = ps.env.chunk_bytes;
+    int64_t cb = config_.device_chunk_bytes;
+    if (cb <= 0 || cb >= n) cb = 0;
+    *n_chunks = cb ? static_cast<int32_t>((n + cb - 1) / cb) : 1;
+    check(fsx_flags_alloc(h_, dst, *n_chunks, flag_base));
+    *token = 0;
+    if (ps.src_is_device)
+      check(fsx_forward(h_, ps.env.src_gpu, ps.src, dst, *off, n, cb, *flag_base, token, nullptr));
+    else
+      check(fsx_forward_host(h_, ps.src, dst, *off, n, cb, *flag_base, token, nullptr));
+    return true;
+  }
+
+  void wait_landed(int dst, int64_t flag_base, int32_t n_chunks, uint64_t token) {
+    check(fsx_wait(h_, dst, flag_base, n_chunks, token, config_.wait_timeout_us));
+  }
+
+  // sidecar.hpp:465-483: place now, notify after the modeled latency.
+  bool place_local(Pending& ps) {
+    int64_t off = -1, flag_base = 0;
+    uint64_t token = 0;
+    int32_t n_chunks = 1;
+    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks)) return false;
+    // The source is borrowed (caller span) or owned by a Pending about to be
+    // dropped, so the copy completes before we return, exactly like the
+    // reference's memcpy into the arena (sidecar.hpp:470).  The batched C ABI
+    // (fsx_forward on a stream) is the asynchronous path.
+    wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
+    const double lat = config_.latency_ms(Transport::LocalBuffer, ps.env.chunk_bytes);
+    added_latency_ms_ += lat;
+    auto env = std::make_shared<Envelope>(ps.env);
+    Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.deliver",
+                     [this, env, off] { deliver(*env, off); });
+    return true;
+  }
+
+  // sidecar.hpp:487-496: stage a network arrival into the slab, deliver now.
+  bool stage_network(Pending& ps) {
+    int64_t off = -1, flag_base = 0;
+    uint64_t token = 0;
+    int32_t n_chunks = 1;
+    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks)) return false;
+    ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
+    wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    deliver(ps.env, off);
+    return true;
+  }
+
+  // sidecar.hpp:498-525
+  void deliver(const Envelope& env, int64_t off) {
+    const std::string key = key_of(env.ref_id, env.dst_gpu);
+    RefState& st = refs_[key];
+    if (st.request_id.empty()) st.request_id = env.request_id;
+    if (st.failed) {
+      release_segment(env.dst_gpu, off);
+      place_backlog(env.dst_gpu);
+      return;
+    }
+    st.parked.emplace(env.seq, std::make_pair(env, off));
+    if (st.has_interest) {
+      drain(st);
+      return;
+    }
+    const int64_t seq = env.seq;
+    Traits::schedule(kernel_, Traits::now(kernel_) + config_.orphan_timeout_ms, "sidecar.orphan",
+                     [this, key, seq] { reclaim_orphan(key, seq); });
+  }
+
+  void reclaim_orphan(const std::string& key, int64_t seq) {
+    auto it = refs_.find(key);
+    if (it == refs_.end() || it->second.has_interest) return;
+    auto p = it->second.parked.find(seq);
+    if (p == it->second.parked.end()) return;
+    const int slab = p->second.first.dst_gpu;
+    release_segment(slab, p->second.second);
+    it->second.parked.erase(p);
+    ++orphan_reclaims_;
+    place_backlog(slab);
+  }
+
+  // sidecar.hpp:527-563: in-order delivery of parked chunks.
+  void drain(RefState& st) {
+    for (auto it = st.parked.find(st.next_seq); it != st.parked.end();
+         it = st.parked.find(st.next_seq)) {
+      Envelope env = it->second.first;
+      const int64_t off = it->second.second;
+      st.parked.erase(it);
+      if (st.raw_cb) {
+        ++transfers_;
+        bytes_forwarded_ += env.chunk_bytes;
+        ++st.next_seq;
+        st.raw_cb(env, off);
+        continue;
+      }
+      std::vector<uint8_t> bytes(static_cast<size_t>(env.chunk_bytes));
+      if (env.chunk_bytes > 0)
+        check(fsx_slab_read(h_, env.dst_gpu, off, bytes.data(), env.chunk_bytes, nullptr));
+      const bool verify = !Traits::is_local(env);
+      const bool ok = !verify || checksum64(bytes.data(), bytes.size()) == env.checksum;
+      release_segment(env.dst_gpu, off);
+      place_backlog(env.dst_gpu);
+      if (!ok) {
+        ++integrity_errors_;
+        Error err = Traits::make_error(status::kIntegrity, "checksum mismatch on ref " + env.ref_id +
+                                                               " seq " + std::to_string(env.seq));
+        st.failed = std::make_shared<Error>(err);
+        if (st.on_error) st.on_error(err);
+        if (failure_handler_) failure_handler_(env.request_id, env.ref_id, err);
+        return;
+      }
+      ++transfers_;
+      bytes_forwarded_ += env.chunk_bytes;
+      ++st.next_seq;
+      if (st.on_chunk) st.on_chunk(env, std::move(bytes));
+    }
+  }
+
+  void release_segment(int slab, int64_t off) { check(fsx_slab_free(h_, slab, off)); }
+
+  void drop_parked(RefState& st) {
+    for (auto& [seq, e] : st.parked) release_segment(e.first.dst_gpu, e.second);
+    st.parked.clear();
+  }
+
+  // sidecar.hpp:571-582
+  void place_backlog(int slab) {
+    auto it = backlog_.find(slab);
+    if (it == backlog_.end()) return;
+    auto& q = it->second;
+    while (!q.empty()) {
+      Pending& front = q.front();
+      const bool placed = front.network ? stage_network(front) : place_local(front);
+      if (!placed) break;
+      q.pop_front();
+    }
+  }
+
+  // sidecar.hpp:584-602
+  void arm_timeout(int slab) {
+    Traits::schedule(kernel_, Traits::now(kernel_) + config_.send_timeout_ms, "sidecar.timeout",
+                     [this, slab] {
+                       auto it = backlog_.find(slab);
+                       if (it == backlog_.end()) return;
+                       const double now = Traits::now(kernel_);
+                       auto& q = it->second;
+                       for (auto qit = q.begin(); qit != q.end();) {
+                         if (qit->deadline <= now) {
+                           Error err = Traits::make_error(
+                               status::kTimeout,
+                               "sidecar send timed out under backpressure for ref " + qit->env.ref_id);
+                           const std::string req = qit->env.request_id, ref = qit->env.ref_id;
+                           qit = q.erase(qit);
+                           if (failure_handler_) failure_handler_(req, ref, err);
+                           fail_ref(ref, err);
+                         } else {
+                           ++qit;
+                         }
+                       }
+                     });
+  }
+
+  Kernel& kernel_;
+  std::map<int, int> topo_;
+  SidecarConfig config_;
+  fsx_fabric* h_ = nullptr;
+  std::vector<int> slabs_;
+  std::map<std::string, RefState> refs_;
+  std::map<int, std::deque<Pending>> backlog_;
+  FailureHandler failure_handler_;
+  int64_t transfers_ = 0, bytes_forwarded_ = 0, integrity_errors_ = 0, orphan_reclaims_ = 0;
+  double added_latency_ms_ = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Standalone host types (no reference headers needed).
+
+class Error : public std::runtime_error {
+ public:
+  Error(int status, const std::string& msg) : std::runtime_error(msg), status_(status) {}
+  int status() const { return status_; }  // 1 + fissim::ErrorCode ordinal
+
+ private:
+  int status_;
+};
+
+struct DataRef {
+  std::string ref_id;
+  int64_t total_bytes = 0;
+  bool streaming = false;
+};
+
+struct ForwardEnvelope {
+  std::string request_id;
+  std::string ref_id;
+  int64_t seq = 0;
+  int64_t chunk_bytes = 0;
+  int64_t total_bytes = 0;
+  uint64_t checksum = 0;
+  Transport transport = Transport::LocalBuffer;
+  std::string location;
+  bool final = false;
+  double send_time = 0;
+  int src_gpu = 0;
+  int dst_gpu = 0;
+};
+
+// Minimal discrete-event loop ordered by (time, insertion), Virtual clock:
+// the role SimKernel plays for the reference fabric (sim_kernel.hpp:36-125).
+class EventLoop {
+ public:
+  double now() const { return now_; }
+  void schedule(double at, std::string label, std::function<void()> fn) {
+    heap_.push(Ev{std::max(at, now_), next_++, std::move(label), std::move(fn)});
+  }
+  void post(std::string label, std::function<void()> fn) { schedule(now_, std::move(label), std::move(fn)); }
+  size_t run_until_idle() {
+    size_t n = 0;
+    while (!heap_.empty()) {
+      Ev ev = heap_.top();
+      heap_.pop();
+      now_ = std::max(now_, ev.at);
+      ev.fn();
+      ++n;
+    }
+    return n;
+  }
+
+ private:
+  struct Ev {
+    double at;
+    uint64_t id;
+    std::string label;
+    std::function<void()> fn;
+    bool operator<(const Ev& o) const { return at != o.at ? at > o.at : id > o.id; }
+  };
+  std::priority_queue<Ev> heap_;
+  double now_ = 0;
+  uint64_t next_ = 0;
+};
+
+struct StandaloneTraits {
+  using Kernel = EventLoop;
+  using Envelope = ForwardEnvelope;
+  using Error = fsx::Error;
+  using DataRef = fsx::DataRef;
+  [[noreturn]] static void raise(int st, const std::string& msg) { throw Error(st, msg); }
+  static Error make_error(int st, const std::string& msg) { return Error(st, msg); }
+  static double now(Kernel& k) { return k.now(); }
+  static void schedule(Kernel& k, double at, const char* label, std::function<void()> fn) {
+    k.schedule(at, label, std::move(fn));
+  }
+  static const std::string& ref_id(const DataRef& r) { return r.ref_id; }
+  static int64_t total_bytes(const DataRef& r) { return r.total_bytes; }
+  static bool streaming(const DataRef& r) { return r.streaming; }
+  static void set_transport(Envelope& e, bool local) {
+    e.transport = local ? Transport::LocalBuffer : Transport::NetworkStream;
+  }
+  static bool is_local(const Envelope& e) { return e.transport == Transport::LocalBuffer; }
+};
+
+using SidecarFabric = Fabric<StandaloneTraits>;
+
+}  // namespace fsx

@@ -34,6 +34,10 @@ E_INTERNAL = 17
 LOCAL_BUFFER = 0
 NETWORK_STREAM = 1
 
+MERGE_FULL = 0
+MERGE_SCAN_ONLY = 1
+MERGE_COPY_ONLY = 2
+
 
 class FsxError(RuntimeError):
     """Mirror of fissim::Error: carries the stable code name."""
@@ -50,7 +54,7 @@ class MergeBatch(C.Structure):
         ("num_items", C.c_int32),
         ("row_bytes", C.c_int64),
         ("placeholder_id", C.c_int32),
-        ("_pad", C.c_int32),
+        ("mode", C.c_int32),
         ("d_embeds", C.c_void_p),
         ("d_token_ids", C.c_void_p),
         ("d_req_row_off", C.c_void_p),
@@ -105,8 +109,12 @@ _SIGS = {
     "fsx_chunk_ready": [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.POINTER(C.c_int)],
     "fsx_wait": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_int64],
     "fsx_stream_wait_flags": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_void_p],
+    "fsx_signal_flags": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_int,
+                         C.c_void_p],
     "fsx_merge": [C.c_void_p, C.c_int, C.POINTER(MergeBatch), C.c_void_p],
     "fsx_synth_payload": [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_pointer_device": [C.c_void_p, C.POINTER(C.c_int)],
+    "fsx_copy_to_host": [C.c_void_p, C.c_void_p, C.c_int64],
     "fsx_get_stats": [C.c_void_p, C.POINTER(Stats)],
     "fsx_synchronize": [C.c_void_p],
 }

@@ -21,12 +21,13 @@
 namespace fsx {
 namespace kern {
 
-constexpr int kFwdThreads = 512;
-constexpr int kFwdUnroll = 8;  // 512 threads x 8 x 16 B = 64 KiB per round
+constexpr int kFwdThreads = 256;
+// K1 variants: <vectors per lane per batch, min CTAs per SM>.  0: 16 x 16 B
+// (8 KiB per warp batch, 2 CTAs/SM), 1: 8 x 16 B at 4 CTAs/SM (register cap 64).
 constexpr int kMergeThreads = 256;
 constexpr int kMergeUnroll = 16;  // 32 lanes x 16 x 16 B = 8 KiB of a row per batch
 constexpr int kScanThreads = 1024;
-constexpr int kScanPerThread = 16;
+constexpr int kScanRounds = 16;  // 1024 threads x 16 = 16384 token ids per round
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -59,6 +60,14 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -81,11 +90,14 @@ __device__ __forceinline__ uint64_t splitmix_word(uint64_t s0, uint64_t k) {
 // ---------------------------------------------------------------------------
 // K1 forward
 
-// Copy [beg, end) of src into dst with the whole CTA.  `vec` means src and dst
-// are 16-byte aligned, so every 16-byte-aligned offset is a legal vector.
-__device__ __forceinline__ void cta_copy_range(const uint8_t* __restrict__ src,
-                                               uint8_t* __restrict__ dst, int64_t beg,
-                                               int64_t end, bool vec) {
+// Copy [beg, end) of src into dst with one warp.  `vec` means src and dst are
+// 16-byte aligned, so every 16-byte-aligned offset is a legal vector.  All
+// loads of a batch are issued before its stores (kFwdUnroll x 16 B per lane in
+// flight).
+template <int U>
+__device__ __forceinline__ void warp_copy_range(const uint8_t* __restrict__ src,
+                                                uint8_t* __restrict__ dst, int64_t beg,
+                                                int64_t end, bool vec, int lane) {
   if (vec) {
     const int64_t vbeg = (beg + 15) & ~int64_t{15};
     const int64_t vend = end & ~int64_t{15};
@@ -93,52 +105,76 @@ __device__ __forceinline__ void cta_copy_range(const uint8_t* __restrict__ src,
       const uint4* s = reinterpret_cast<const uint4*>(src + vbeg);
       uint4* d = reinterpret_cast<uint4*>(dst + vbeg);
       const int64_t nv = (vend - vbeg) >> 4;
-      for (int64_t base = 0; base < nv; base += int64_t{kFwdThreads} * kFwdUnroll) {
-        uint4 r[kFwdUnroll];
+      for (int64_t base = 0; base < nv; base += 32 * U) {
+        uint4 r[U];
 #pragma unroll
-        for (int k = 0; k < kFwdUnroll; ++k) {
-          const int64_t i = base + k * kFwdThreads + threadIdx.x;
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
           if (i < nv) r[k] = ld_nc_v4(s + i);
         }
 #pragma unroll
-        for (int k = 0; k < kFwdUnroll; ++k) {
-          const int64_t i = base + k * kFwdThreads + threadIdx.x;
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
           if (i < nv) st_v4(d + i, r[k]);
         }
       }
-      for (int64_t i = beg + threadIdx.x; i < vbeg && i < end; i += blockDim.x) dst[i] = src[i];
-      for (int64_t i = (vend > vbeg ? vend : vbeg) + threadIdx.x; i < end; i += blockDim.x)
-        dst[i] = src[i];
+      for (int64_t i = beg + lane; i < vbeg && i < end; i += 32) dst[i] = src[i];
+      for (int64_t i = vend + lane; i < end; i += 32) dst[i] = src[i];
       return;
     }
   }
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) dst[i] = src[i];
+  for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
 }
 
-// Work unit u covers slice s of chunk c (units are chunk-major, so chunks
-// complete roughly in order and the consumer can start on chunk 0 early).
-// After its slice, a CTA fences at system scope and counts itself into the
-// chunk's counter; the CTA completing the chunk publishes the token to the
-// consumer-device flag and to the host-mapped flag with release semantics.
-__global__ void __launch_bounds__(kFwdThreads) forward_kernel(FwdArgs a) {
-  for (int64_t u = blockIdx.x; u < a.total_units; u += gridDim.x) {
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bool sys) {
+  uint32_t old;
+  if (sys)
+    asm volatile("atom.add.acq_rel.sys.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  else
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Work unit u (kFwdUnitBytes, one warp) covers slice s of chunk c; units are
+// chunk-major so chunks complete roughly in order and a consumer can start on
+// chunk 0 while later chunks are still in flight.  Warps stream independently
+// (no CTA barrier): after its unit a warp counts itself into the chunk counter
+// with an acq_rel atomic (release covers the warp's stores via __syncwarp; gpu
+// scope for a local slab, system scope when the slab is peer memory), and the
+// warp that completes the chunk fences at system scope and publishes the token
+// to the consumer-device flag and the host-mapped flag.
+template <int U, int MINB>
+__global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(FwdArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kFwdThreads / 32);
+  for (int64_t u = (int64_t)blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5); u < a.total_units;
+       u += warps) {
     const int64_t c = u / a.chunk_units;
     const int64_t s = u - c * a.chunk_units;
     const int64_t cbeg = c * a.chunk_bytes;
     const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
     const int64_t beg = cbeg + s * a.slice;
     const int64_t end = min(beg + a.slice, cend);
-    cta_copy_range(a.src, a.dst, beg, end, a.vec != 0);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
+    warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, lane);
+    __syncwarp();
+    if (lane == 0) {
       const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
-      const uint32_t prev = atomicAdd(&a.counters[c], 1u);
+      const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
       if (prev == units - 1) {
         a.counters[c] = 0u;  // slot is clean for the next transfer that draws it
-        __threadfence_system();
-        st_release_sys(&a.dflags[c], a.token);
-        if (a.hflags) st_release_sys(&a.hflags[c], a.token);
+        if (a.peer) {
+          // data sits in peer memory: publish at system scope
+          __threadfence_system();
+          st_release_sys(&a.dflags[c], a.token);
+          if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
+        } else {
+          // data sits in this GPU's memory: every counted warp released at gpu
+          // scope and the acq_rel bump acquired them, so a gpu-scope release
+          // publishes the chunk to device consumers; the host mirror is a
+          // posted store that can only be observed after it.
+          st_release_gpu(&a.dflags[c], a.token);
+          if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
+        }
       }
     }
   }
@@ -159,13 +195,15 @@ __global__ void wait_flags_kernel(const uint64_t* dflags, int32_t n, uint64_t to
 // ---------------------------------------------------------------------------
 // K3 merge, phase 1: per-request placeholder positions.
 //
-// One CTA per request.  Each thread owns kScanPerThread consecutive token ids
-// per round; the CTA computes an exclusive prefix sum of the per-thread
-// placeholder counts (warp shuffles + one shared-memory pass over warp totals)
-// and writes, for the k-th placeholder row of the request, its row offset
-// inside the request into scratch[item_row_off[first item] + k].
+// One CTA per request.  Per round, warp w reads kScanRounds x 32 consecutive
+// token ids with coalesced loads (round j, lane l -> token base_w + 32 j + l),
+// ballots the placeholder mask of each round, and the CTA scans the per-warp
+// totals once in shared memory.  The k-th placeholder row of the request gets
+// its row offset inside the request written to
+// scratch[item_row_off[first item] + k].
 __global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batch b) {
-  __shared__ int32_t warp_tot[kScanThreads / 32];
+  __shared__ int32_t warp_excl[kScanThreads / 32];
+  __shared__ int32_t tile_total;
   __shared__ int64_t running;
   const int r = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -173,45 +211,46 @@ __global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batc
   const int64_t i0 = b.d_req_item_off[r], i1 = b.d_req_item_off[r + 1];
   const int64_t kbase = b.d_item_row_off[i0];
   const int64_t want = b.d_item_row_off[i1] - kbase;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   if (threadIdx.x == 0) running = 0;
   __syncthreads();
-  for (int64_t t = t0; t < t1; t += int64_t{kScanThreads} * kScanPerThread) {
-    const int64_t mine = t + int64_t{threadIdx.x} * kScanPerThread;
-    uint32_t mask = 0;
+  constexpr int64_t kTile = int64_t{kScanThreads} * kScanRounds;
+  for (int64_t t = t0; t < t1; t += kTile) {
+    const int64_t wbase = t + int64_t{warp} * 32 * kScanRounds + lane;
+    uint32_t m[kScanRounds];
+    int wcount = 0;
 #pragma unroll
-    for (int k = 0; k < kScanPerThread; ++k) {
-      const int64_t tt = mine + k;
-      if (tt < t1 && b.d_token_ids[tt] == b.placeholder_id) mask |= 1u << k;
+    for (int j = 0; j < kScanRounds; ++j) {
+      const int64_t tt = wbase + 32 * j;
+      const bool p = tt < t1 && b.d_token_ids[tt] == b.placeholder_id;
+      m[j] = __ballot_sync(0xffffffffu, p);
+      wcount += __popc(m[j]);
     }
-    const int cnt = __popc(mask);
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += v;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
+    if (lane == 0) warp_excl[warp] = wcount;
     __syncthreads();
     if (warp == 0) {
-      const int v = warp_tot[lane];
-      int wi = v;
+      const int v = warp_excl[lane];
+      int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, wi, off);
-        if (lane >= off) wi += x;
+        const int x = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += x;
       }
-      warp_tot[lane] = wi - v;  // exclusive over warps
+      warp_excl[lane] = incl - v;
+      if (lane == 31) tile_total = incl;
     }
     __syncthreads();
-    int64_t k = running + warp_tot[warp] + (incl - cnt);
-    while (mask) {
-      const int bit = __ffs(mask) - 1;
-      mask &= mask - 1;
-      if (k < want) b.d_scratch[kbase + k] = (int32_t)(mine + bit - t0);
-      ++k;
+    int64_t k = running + warp_excl[warp];
+#pragma unroll
+    for (int j = 0; j < kScanRounds; ++j) {
+      if ((m[j] >> lane) & 1u) {
+        const int64_t kk = k + __popc(m[j] & lt_mask);
+        if (kk < want) b.d_scratch[kbase + kk] = (int32_t)(wbase + 32 * j - t0);
+      }
+      k += __popc(m[j]);
     }
     __syncthreads();
-    if (threadIdx.x == kScanThreads - 1) running += warp_tot[kScanThreads / 32 - 1] + incl;
+    if (threadIdx.x == 0) running += tile_total;
     __syncthreads();
   }
   if (threadIdx.x == 0) b.d_status[r] = (running == want) ? 0 : FSX_E_VALIDATION;
@@ -318,9 +357,20 @@ using namespace kern;
 int forward_block_threads() { return kFwdThreads; }
 int merge_copy_block_threads() { return kMergeThreads; }
 
-int forward_blocks_per_sm() {
+namespace {
+using FwdFn = void (*)(FwdArgs);
+FwdFn forward_variant(int v) {
+  switch (v) {
+    case 1: return forward_kernel<8, 4>;
+    default: return forward_kernel<16, 2>;
+  }
+}
+}  // namespace
+
+int forward_blocks_per_sm(int variant) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, forward_kernel, kFwdThreads, 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, forward_variant(variant), kFwdThreads, 0) !=
+      cudaSuccess)
     return 1;
   return n > 0 ? n : 1;
 }
@@ -333,8 +383,8 @@ int merge_copy_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
-cudaError_t launch_forward(const FwdArgs& a, int grid, int block, cudaStream_t s) {
-  forward_kernel<<<grid, block, 0, s>>>(a);
+cudaError_t launch_forward(const FwdArgs& a, int variant, int grid, cudaStream_t s) {
+  forward_variant(variant)<<<grid, kFwdThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -351,16 +401,19 @@ cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token,
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
   *launches = 0;
   if (b.num_requests <= 0) return cudaSuccess;
-  merge_scan_kernel<<<b.num_requests, kScanThreads, 0, s>>>(b);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  *launches = 1;
-  if (b.total_item_rows <= 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (b.mode != FSX_MERGE_COPY_ONLY) {
+    merge_scan_kernel<<<b.num_requests, kScanThreads, 0, s>>>(b);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *launches = 1;
+  }
+  if (b.mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
   const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
   const int grid = (int)(need < copy_grid ? need : copy_grid);
   merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
   e = cudaGetLastError();
-  if (e == cudaSuccess) *launches = 2;
+  if (e == cudaSuccess) ++*launches;
   return e;
 }
 

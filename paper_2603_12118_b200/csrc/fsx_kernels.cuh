@@ -21,6 +21,7 @@ struct FwdArgs {
   int64_t total_units;
   int32_t n_chunks;
   int32_t vec;         // 16-byte path usable
+  int32_t peer;        // dst is peer (NVLink) memory: system-scope release per unit
   uint32_t* counters;  // [n_chunks] on the source device, zero on entry, self-resetting
   uint64_t* dflags;    // [n_chunks] consumer-device flags (may be peer memory)
   uint64_t* hflags;    // [n_chunks] mapped pinned host flags, or nullptr
@@ -35,7 +36,7 @@ struct FlagSetArgs {
 };
 
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
-cudaError_t launch_forward(const FwdArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_forward(const FwdArgs& a, int variant, int grid, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);
@@ -43,7 +44,7 @@ cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaS
 
 // Occupancy helpers.
 int forward_block_threads();
-int forward_blocks_per_sm();
+int forward_blocks_per_sm(int variant);
 int merge_copy_block_threads();
 int merge_copy_blocks_per_sm();
 

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -42,7 +43,25 @@ int fail(int code, const std::string& msg) {
 constexpr int64_t kAlign = 64;             // sidecar.hpp:195
 constexpr int64_t kFlagRing = 1 << 18;     // flags per consumer slab (2 MiB)
 constexpr int64_t kCounterRing = 1 << 16;  // chunk counters per source device
-constexpr int64_t kSlice = 64 * 1024;      // K1 work unit
+// K1 tuning: bytes per warp work unit (one release + counter bump per unit)
+// and the kernel variant (fsx_kernels.cu).  Overridable for sweeps with
+// FSX_FWD_UNIT / FSX_FWD_VARIANT.
+int64_t fwd_unit_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("FSX_FWD_UNIT");
+    const int64_t x = e ? std::atoll(e) : 32 * 1024;
+    return std::max<int64_t>(512, (x + 511) & ~int64_t{511});
+  }();
+  return v;
+}
+
+int fwd_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("FSX_FWD_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 
 // Address-ordered block list over [0, capacity).  First fit in offset order,
 // 64-byte units, coalescing on free: the allocation policy of the reference
@@ -183,7 +202,7 @@ int device_state(fsx_fabric* f, int ordinal, Device** out) {
   FSX_CUDA(cudaMemset(d->counters, 0, kCounterRing * sizeof(uint32_t)));
   d->counter_ring.size = kCounterRing;
   FSX_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, ordinal));
-  d->fwd_grid = d->sms * fsx::forward_blocks_per_sm();
+  d->fwd_grid = d->sms * fsx::forward_blocks_per_sm(fwd_variant());
   d->merge_grid = d->sms * fsx::merge_copy_blocks_per_sm();
   *out = d.get();
   f->devices.emplace(ordinal, std::move(d));
@@ -468,12 +487,14 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
     a.counters = dev->counters + dev->counter_ring.take(n_chunks);
     a.dst = s->base + dst_off;
     a.dflags = s->dflags + flag_base;
-    a.hflags = s->hflags ? s->hflags + flag_base : nullptr;
+    static const bool no_host_mirror = std::getenv("FSX_FWD_NO_HOST_FLAGS") != nullptr;  // sweeps
+    a.hflags = (s->hflags && !no_host_mirror) ? s->hflags + flag_base : nullptr;
+    a.peer = (s->imported || s->device != src_dev) ? 1 : 0;
   }
   a.src = static_cast<const uint8_t*>(d_src);
   a.bytes = bytes;
   a.chunk_bytes = chunk_bytes;
-  a.slice = std::min<int64_t>(kSlice, std::max<int64_t>(16, chunk_bytes));
+  a.slice = std::min<int64_t>(fwd_unit_bytes(), std::max<int64_t>(16, chunk_bytes));
   a.slice = (a.slice + 15) & ~int64_t{15};
   a.chunk_units = (chunk_bytes + a.slice - 1) / a.slice;
   const int64_t last_len = bytes - (n_chunks - 1) * chunk_bytes;
@@ -481,10 +502,12 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
   a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
   a.n_chunks = (int32_t)n_chunks;
   a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
-  a.token = f->next_token.fetch_add(1);
+  a.token = (token && *token) ? *token : f->next_token.fetch_add(1);
   FSX_CUDA(cudaSetDevice(src_dev));
-  const int grid = (int)std::min<int64_t>(a.total_units, dev->fwd_grid);
-  FSX_CUDA(fsx::launch_forward(a, grid, fsx::forward_block_threads(), pick_stream(dev, stream)));
+  const int warps_per_cta = fsx::forward_block_threads() / 32;
+  const int grid = (int)std::min<int64_t>((a.total_units + warps_per_cta - 1) / warps_per_cta,
+                                          dev->fwd_grid);
+  FSX_CUDA(fsx::launch_forward(a, fwd_variant(), grid, pick_stream(dev, stream)));
   f->launches++;
   f->forwards++;
   f->bytes_forwarded += bytes;
@@ -512,7 +535,7 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
     int rc = device_state(f, s->device, &dev);
     if (rc) return rc;
   }
-  const uint64_t tok = f->next_token.fetch_add(1);
+  const uint64_t tok = (token && *token) ? *token : f->next_token.fetch_add(1);
   cudaStream_t st = pick_stream(dev, stream);
   FSX_CUDA(cudaSetDevice(s->device));
   for (int64_t c = 0; c < n_chunks; ++c) {
@@ -590,6 +613,30 @@ int fsx_stream_wait_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t
   return FSX_OK;
 }
 
+int fsx_signal_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, uint64_t token,
+                     int src_gpu, void* stream) {
+  int src_dev = 0;
+  int rc = find_gpu(f, src_gpu, &src_dev);
+  if (rc) return rc;
+  fsx::FlagSetArgs fa{};
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    Slab* s = slab_of(f, dst_gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+    if (flag_base < 0 || n <= 0 || flag_base + n > kFlagRing)
+      return fail(FSX_E_VALIDATION, "flag range out of the ring");
+    rc = device_state(f, src_dev, &dev);
+    if (rc) return rc;
+    fa = fsx::FlagSetArgs{s->dflags + flag_base, s->hflags ? s->hflags + flag_base : nullptr, n,
+                          token};
+  }
+  FSX_CUDA(cudaSetDevice(src_dev));
+  FSX_CUDA(fsx::launch_set_flags(fa, pick_stream(dev, stream)));
+  f->launches++;
+  return FSX_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Merge / synth / stats
 
@@ -605,6 +652,8 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
     return fail(FSX_E_VALIDATION, "merge batch is missing a device array");
   if (b->d_item_flag && (!b->d_item_token || !b->d_item_chunk_rows))
     return fail(FSX_E_VALIDATION, "early-start merge needs tokens and chunk rows");
+  if (b->mode < FSX_MERGE_FULL || b->mode > FSX_MERGE_COPY_ONLY)
+    return fail(FSX_E_VALIDATION, "unknown merge mode");
   Device* dev = nullptr;
   {
     std::lock_guard<std::mutex> lk(f->mu);
@@ -616,8 +665,10 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
   cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched);
   f->launches += launched;
   if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge launch: ") + cudaGetErrorString(e));
-  f->merges++;
-  f->merged_rows += b->total_item_rows;
+  if (b->mode != FSX_MERGE_SCAN_ONLY) {
+    f->merges++;
+    f->merged_rows += b->total_item_rows;
+  }
   return FSX_OK;
 }
 
@@ -640,6 +691,25 @@ int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_
   FSX_CUDA(fsx::launch_synth(seed, static_cast<uint8_t*>(d_dst), n, std::max(grid, 1),
                              pick_stream(dev, stream)));
   f->launches++;
+  return FSX_OK;
+}
+
+int fsx_pointer_device(const void* p, int* device) {
+  *device = -1;
+  if (!p) return FSX_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return FSX_OK;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) *device = a.device;
+  return FSX_OK;
+}
+
+int fsx_copy_to_host(void* h_dst, const void* d_src, int64_t n) {
+  if (n < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+  if (n == 0) return FSX_OK;
+  FSX_CUDA(cudaMemcpy(h_dst, d_src, n, cudaMemcpyDefault));
   return FSX_OK;
 }
 

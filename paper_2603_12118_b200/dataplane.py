@@ -155,9 +155,10 @@ class DataPlaneBatch:
                           int(self.tokens[i]), timeout_us)
 
     # -- K3 ---------------------------------------------------------------------
-    def merge_batch(self, early_start: bool = False) -> N.MergeBatch:
+    def merge_batch(self, early_start: bool = False, mode: int = N.MERGE_FULL) -> N.MergeBatch:
         lay = self.lay
         b = N.MergeBatch()
+        b.mode = mode
         b.num_requests = len(lay.requests)
         b.num_items = len(lay.items)
         b.row_bytes = self.rb
@@ -183,8 +184,13 @@ class DataPlaneBatch:
             b.d_item_chunk_rows = self.item_chunk_rows.data_ptr()
         return b
 
-    def merge(self, stream=None, early_start: bool = False) -> None:
-        self.fab.merge(self.dst_gpu, self.merge_batch(early_start), stream)
+    def merge(self, stream=None, early_start: bool = False, mode: int = N.MERGE_FULL) -> None:
+        self.fab.merge(self.dst_gpu, self.merge_batch(early_start, mode), stream)
+
+    def scan(self, stream=None) -> None:
+        """Phase 1 of K3 only: needs just the token ids, so it can run while
+        the payload is still being forwarded."""
+        self.merge(stream, mode=N.MERGE_SCAN_ONLY)
 
     # -- readback -----------------------------------------------------------------
     def embeds_host(self) -> np.ndarray:

@@ -129,17 +129,22 @@ class DeviceFabric:
     def stream_wait_flags(self, gpu: int, flag_base: int, n: int, token: int, stream=None) -> None:
         N.call("fsx_stream_wait_flags", self._h, gpu, flag_base, n, token, _stream_ptr(stream))
 
+    def signal_flags(self, dst_gpu: int, flag_base: int, n: int, token: int, src_gpu: int,
+                     stream=None) -> None:
+        N.call("fsx_signal_flags", self._h, dst_gpu, flag_base, n, token, src_gpu,
+               _stream_ptr(stream))
+
     # -- data movement ----------------------------------------------------------
     def forward(self, src_gpu: int, src_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
-                chunk_bytes: int, flag_base: int, stream=None) -> int:
-        tok = C.c_uint64()
+                chunk_bytes: int, flag_base: int, stream=None, token: int = 0) -> int:
+        tok = C.c_uint64(token)
         N.call("fsx_forward", self._h, src_gpu, src_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
                flag_base, C.byref(tok), _stream_ptr(stream))
         return tok.value
 
     def forward_host(self, host_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
-                     chunk_bytes: int, flag_base: int, stream=None) -> int:
-        tok = C.c_uint64()
+                     chunk_bytes: int, flag_base: int, stream=None, token: int = 0) -> int:
+        tok = C.c_uint64(token)
         N.call("fsx_forward_host", self._h, host_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
                flag_base, C.byref(tok), _stream_ptr(stream))
         return tok.value

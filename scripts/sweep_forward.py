@@ -1,0 +1,65 @@
+#!/usr/bin/env python
+"""K1 sweep on one B200 (intra-device forward, HBM-bound, 2 x payload bytes):
+chunk-size sweep of BASELINE config E plus the config-B video item, timed with
+CUDA events on the launching stream.  Tuning knobs come from the environment
+(FSX_FWD_VARIANT, FSX_FWD_UNIT).  Prints one JSON line per size; compares with
+cudaMemcpyAsync D2D (torch copy_) of the same bytes."""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    from paper_2603_12118_b200.fabric import DeviceFabric
+
+    sizes = [64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20]
+    fab = DeviceFabric({0: 0, 1: 0}, {0: 0, 1: 0})
+    fab.slab_register(1, 1 << 30)
+    s = torch.cuda.Stream()
+    src = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    fab.synth(0, 1234, src.data_ptr(), src.numel())
+    ref = torch.empty_like(src)
+    variant = os.environ.get("FSX_FWD_VARIANT", "0")
+    unit = os.environ.get("FSX_FWD_UNIT", "32768")
+    cases = [(n, 0) for n in sizes] + [(117_440_512, 7_340_032), (256 << 20, 1 << 20),
+                                       (256 << 20, 64 << 10)]
+    for n, chunk in cases:
+        # enough repetitions that each measurement moves >= 2 GiB
+        reps = max(8, (2 << 30) // n)
+        off = fab.slab_alloc(1, n)
+        nch = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+            e1.record(s)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(s)
+            for _ in range(reps):
+                ref[:n].copy_(src[:n])
+            c1.record(s)
+            c1.synchronize()
+            cms = c0.elapsed_time(c1) / reps
+        fab.slab_free(1, off)
+        print(json.dumps({"variant": variant, "unit": unit, "bytes": n, "chunk_bytes": chunk,
+                          "chunks": nch, "us": round(ms * 1e3, 2),
+                          "hbm_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),
+                          "memcpy_us": round(cms * 1e3, 2),
+                          "memcpy_hbm_gbs": round(2 * n / (cms * 1e-3) / 1e9, 1)}), flush=True)
+    fab.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,379 @@
+// GPU tests of the standalone C++ engine (include/fsx/fabric.hpp) in the style
+// of the reference's tests/test_sidecar.cpp and acceptance criterion 4
+// (tests/acceptance_test.cpp:229-334).  Expected bytes come from the oracle
+// restatement (oracle/fsx_oracle.c, test infrastructure).  The reference's own
+// test_sidecar.cpp runs unmodified against the drop-in header separately
+// (build/ref_test_sidecar).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <optional>
+#include <random>
+
+#include "catch_amalgamated.hpp"
+#include "fsx/fabric.hpp"
+
+extern "C" {
+#include "fsx_oracle.h"
+}
+
+using fsx::DataRef;
+using fsx::EventLoop;
+using fsx::ForwardEnvelope;
+using fsx::SidecarConfig;
+using fsx::SidecarFabric;
+using fsx::Transport;
+
+namespace {
+
+std::map<int, int> two_nodes() {
+  std::map<int, int> t;
+  for (int g = 0; g < 8; ++g) t[g] = g < 4 ? 0 : 1;
+  return t;
+}
+
+std::vector<uint8_t> synth(uint64_t seed, size_t n) {
+  std::vector<uint8_t> v(n);
+  if (n) or_synth_payload_into(seed, v.data(), n);
+  return v;
+}
+
+uint64_t seed_of(const std::string& s) { return or_fnv1a64(s.data(), s.size()); }
+
+DataRef ref_of(const std::string& id, int64_t bytes, bool streaming = false) {
+  return DataRef{id, bytes, streaming};
+}
+
+struct Got {
+  std::vector<std::vector<uint8_t>> chunks;
+  std::vector<int64_t> seqs;
+  std::vector<ForwardEnvelope> envs;
+  bool final_seen = false;
+  std::optional<fsx::Error> error;
+};
+
+void collect(SidecarFabric& f, int gpu, const std::string& ref, Got& g) {
+  f.register_interest(
+      gpu, ref,
+      [&g](const ForwardEnvelope& env, std::vector<uint8_t> b) {
+        g.chunks.push_back(std::move(b));
+        g.seqs.push_back(env.seq);
+        g.envs.push_back(env);
+        if (env.final) g.final_seen = true;
+      },
+      [&g](const fsx::Error& e) { g.error = e; });
+}
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  explicit DeviceBuffer(size_t n) { cudaMalloc(&p, std::max<size_t>(n, 1)); }
+  ~DeviceBuffer() { cudaFree(p); }
+};
+
+}  // namespace
+
+TEST_CASE("route, node_of and unknown gpus") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  CHECK(f.route(0, 3) == Transport::LocalBuffer);
+  CHECK(f.route(2, 2) == Transport::LocalBuffer);
+  CHECK(f.route(1, 5) == Transport::NetworkStream);
+  bool threw = false;
+  try {
+    f.node_of(42);
+  } catch (const fsx::Error& e) {
+    threw = e.status() == FSX_E_NOT_FOUND;
+  }
+  CHECK(threw);
+}
+
+TEST_CASE("host spans land byte-exact in device slabs on both transports") {
+  EventLoop k;
+  SidecarConfig cfg;
+  cfg.arena_bytes = 192 << 20;
+  SidecarFabric f(k, two_nodes(), cfg);
+  int idx = 0;
+  for (size_t n : {size_t{1}, size_t{7}, size_t{256}, size_t{4096}, size_t{65536}, size_t{1} << 20,
+                   size_t{8} << 20, size_t{64} << 20}) {
+    for (int dst : {2, 6}) {
+      const std::string id = "req-x/r" + std::to_string(idx++);
+      auto payload = synth(seed_of(id), n);
+      Got g;
+      collect(f, dst, id, g);
+      k.post("send", [&, id, dst] { f.send_payload("req-x", ref_of(id, n), 0, dst, payload); });
+      k.run_until_idle();
+      REQUIRE(g.chunks.size() == 1);
+      CHECK(g.chunks[0] == payload);
+      CHECK(g.final_seen);
+      CHECK(!g.error);
+      CHECK(g.envs[0].location.rfind("gpu" + std::to_string(dst) + ":off", 0) == 0);
+    }
+  }
+  auto s = f.stats();
+  CHECK(s.integrity_errors == 0);
+  CHECK(s.segments_in_use == 0);
+  CHECK(s.bytes_in_use == 0);
+  CHECK(s.transfers == 16);
+}
+
+TEST_CASE("device payloads take the K1 path and land byte-exact") {
+  EventLoop k;
+  SidecarConfig cfg;
+  cfg.arena_bytes = 256 << 20;
+  cfg.device_chunk_bytes = 7340032;  // one Qwen2.5-VL frame per flag
+  SidecarFabric f(k, two_nodes(), cfg);
+  for (size_t n : {size_t{16}, size_t{4099}, size_t{2097152}, size_t{117440512}}) {
+    const std::string id = "req-000000/r" + std::to_string(n);
+    auto payload = synth(or_payload_seed(id.data(), id.size(), 0), n);
+    DeviceBuffer d(n);
+    REQUIRE(cudaMemcpy(d.p, payload.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
+    Got g;
+    collect(f, 1, id, g);
+    k.post("send", [&, id] {
+      f.send_payload("req-000000", ref_of(id, n), 0, 1,
+                     std::span<const uint8_t>(static_cast<const uint8_t*>(d.p), n));
+    });
+    k.run_until_idle();
+    REQUIRE(g.chunks.size() == 1);
+    CHECK(g.chunks[0] == payload);
+  }
+  CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("raw interest reads the slab in place and frees on ack") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  const size_t n = 3 << 20;
+  auto payload = synth(77, n);
+  int64_t off = -1;
+  ForwardEnvelope seen;
+  f.register_interest_raw(3, "req-r/r0", [&](const ForwardEnvelope& env, int64_t o) {
+    off = o;
+    seen = env;
+  });
+  k.post("send", [&] { f.send_payload("req-r", ref_of("req-r/r0", n), 0, 3, payload); });
+  k.run_until_idle();
+  REQUIRE(off >= 0);
+  CHECK(off % 64 == 0);
+  CHECK(f.stats().segments_in_use == 1);
+  std::vector<uint8_t> back(n);
+  REQUIRE(cudaMemcpy(back.data(), f.slab_ptr(3, off), n, cudaMemcpyDeviceToHost) == cudaSuccess);
+  CHECK(back == payload);
+  f.ack_raw(3, off);
+  CHECK(f.stats().segments_in_use == 0);
+  CHECK(seen.chunk_bytes == static_cast<int64_t>(n));
+}
+
+TEST_CASE("zero-byte send, protocol error, and late interest") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  Got z;
+  collect(f, 1, "req-z/r0", z);
+  k.post("send", [&] { f.send_payload("req-z", ref_of("req-z/r0", 0), 0, 1, {}); });
+  k.run_until_idle();
+  REQUIRE(z.chunks.size() == 1);
+  CHECK(z.chunks[0].empty());
+  CHECK(z.final_seen);
+
+  auto small = synth(1, 50);
+  bool threw = false;
+  k.post("send", [&] {
+    try {
+      f.send_payload("req-m", ref_of("req-m/r0", 100), 0, 1, small);
+    } catch (const fsx::Error& e) {
+      threw = e.status() == FSX_E_PROTOCOL;
+    }
+  });
+  k.run_until_idle();
+  CHECK(threw);
+
+  auto p = synth(5, 1024);
+  Got late;
+  k.post("send", [&] { f.send_payload("req-o", ref_of("req-o/r1", 1024), 0, 1, p); });
+  k.schedule(50, "late", [&] { collect(f, 1, "req-o/r1", late); });
+  k.run_until_idle();
+  REQUIRE(late.chunks.size() == 1);
+  CHECK(late.chunks[0] == p);
+  CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("streamed chunks arrive in seq order and corrupt ones fail") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  auto c0 = synth(10, 64), c1 = synth(11, 64);
+  auto env_for = [](int64_t seq, const std::vector<uint8_t>& b, bool fin, uint64_t sum) {
+    ForwardEnvelope e;
+    e.request_id = "req-s";
+    e.ref_id = "req-s/r0";
+    e.seq = seq;
+    e.chunk_bytes = static_cast<int64_t>(b.size());
+    e.total_bytes = 128;
+    e.checksum = sum;
+    e.transport = Transport::NetworkStream;
+    e.final = fin;
+    e.dst_gpu = 4;
+    return e;
+  };
+  Got g;
+  collect(f, 4, "req-s/r0", g);
+  k.post("inject", [&] {
+    f.handle_network(env_for(1, c1, true, fsx::checksum64(c1.data(), c1.size())), c1);
+    f.handle_network(env_for(0, c0, false, fsx::checksum64(c0.data(), c0.size())), c0);
+  });
+  k.run_until_idle();
+  REQUIRE(g.seqs == std::vector<int64_t>({0, 1}));
+  CHECK(g.chunks[0] == c0);
+  CHECK(g.chunks[1] == c1);
+
+  std::vector<std::string> failures;
+  f.set_failure_handler([&](const std::string& req, const std::string&, const fsx::Error&) {
+    failures.push_back(req);
+  });
+  Got bad;
+  collect(f, 5, "req-i/r0", bad);
+  auto b = synth(3, 512);
+  auto e = env_for(0, b, true, fsx::checksum64(b.data(), b.size()) ^ 0xdeadbeef);
+  e.request_id = "req-i";
+  e.ref_id = "req-i/r0";
+  e.dst_gpu = 5;
+  k.post("inject", [&] { f.handle_network(e, b); });
+  k.run_until_idle();
+  CHECK(bad.chunks.empty());
+  REQUIRE(bad.error.has_value());
+  CHECK(bad.error->status() == FSX_E_INTEGRITY);
+  CHECK(failures == std::vector<std::string>({"req-i"}));
+  CHECK(f.stats().integrity_errors == 1);
+  CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("backpressure drains, times out, purge and orphans reclaim") {
+  {
+    EventLoop k;
+    SidecarConfig cfg;
+    cfg.arena_bytes = 2 * 1024 * 1024 + 1024;
+    SidecarFabric f(k, two_nodes(), cfg);
+    int delivered = 0;
+    for (int i = 0; i < 24; ++i)
+      f.register_interest(1, "req-b/r" + std::to_string(i),
+                          [&](const ForwardEnvelope&, std::vector<uint8_t> b) {
+                            delivered += b.size() == (1u << 20);
+                          });
+    k.post("send-all", [&] {
+      for (int i = 0; i < 24; ++i) {
+        auto p = synth(i, 1 << 20);
+        f.send_payload("req-b", ref_of("req-b/r" + std::to_string(i), 1 << 20), 0, 1, p);
+      }
+    });
+    k.run_until_idle();
+    CHECK(delivered == 24);
+    CHECK(f.stats().segments_in_use == 0);
+  }
+  {
+    EventLoop k;
+    SidecarConfig cfg;
+    cfg.arena_bytes = 1024;
+    cfg.send_timeout_ms = 50;
+    SidecarFabric f(k, two_nodes(), cfg);
+    std::vector<std::string> failed;
+    f.set_failure_handler([&](const std::string&, const std::string& ref, const fsx::Error& e) {
+      if (e.status() == FSX_E_TIMEOUT) failed.push_back(ref);
+    });
+    auto p = synth(9, 4096);
+    k.post("send", [&] { f.send_payload("req-t", ref_of("req-t/r0", 4096), 0, 1, p); });
+    k.run_until_idle();
+    CHECK(failed == std::vector<std::string>({"req-t/r0"}));
+  }
+  {
+    EventLoop k;
+    SidecarFabric f(k, two_nodes());
+    auto p = synth(2, 2048);
+    k.post("send", [&] { f.send_payload("req-p", ref_of("req-p/r0", 2048), 0, 1, p); });
+    size_t at100 = 99, after = 99;
+    k.schedule(100, "check", [&] {
+      at100 = f.stats().segments_in_use;
+      f.purge_request("req-p");
+      after = f.stats().segments_in_use;
+    });
+    k.run_until_idle();
+    CHECK(at100 == 1);
+    CHECK(after == 0);
+    CHECK(f.stats().orphan_reclaims == 0);
+  }
+  {
+    EventLoop k;
+    SidecarConfig cfg;
+    cfg.orphan_timeout_ms = 100;
+    SidecarFabric f(k, two_nodes(), cfg);
+    auto p = synth(1, 4096);
+    k.post("send", [&] { f.send_payload("req-orphan", ref_of("req-orphan/r0", 4096), 0, 1, p); });
+    k.run_until_idle();
+    CHECK(f.stats().segments_in_use == 0);
+    CHECK(f.stats().orphan_reclaims == 1);
+  }
+}
+
+TEST_CASE("fail_ref reaches every consumer of the ref and cancel_interest frees") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  int errs = 0;
+  for (int gpu : {1, 2, 5})
+    f.register_interest(gpu, "req-f/r0", [](const ForwardEnvelope&, std::vector<uint8_t>) {},
+                        [&](const fsx::Error&) { ++errs; });
+  f.register_interest(1, "req-f/r1", [](const ForwardEnvelope&, std::vector<uint8_t>) {},
+                      [&](const fsx::Error&) { errs += 100; });
+  f.fail_ref("req-f/r0", fsx::Error(FSX_E_INTERNAL, "injected"));
+  CHECK(errs == 3);
+  auto p = synth(4, 4096);
+  k.post("send", [&] { f.send_payload("req-c", ref_of("req-c/r0", 4096), 0, 2, p); });
+  k.run_until_idle();  // parked (no interest), orphan timer pending far away
+  f.cancel_interest("req-c/r0", 2);
+  CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("criterion 4 sweep: 24 random sizes up to 64 MiB, byte-exact, no leaks") {
+  EventLoop k;
+  SidecarConfig cfg;
+  cfg.arena_bytes = 192 << 20;
+  SidecarFabric f(k, two_nodes(), cfg);
+  std::mt19937_64 rng(4040);  // tests/acceptance_test.cpp:239
+  for (int i = 0; i < 24; ++i) {
+    size_t size = i < 2 ? (i + 1) : size_t(1) << (rng() % 27);
+    if (i % 5 == 0) size = (size_t(1) << 26) - (rng() % 1000);
+    const int dst = (i % 2 == 0) ? 2 : 6;
+    const std::string id = "acc4/r" + std::to_string(i);
+    auto payload = synth(rng(), size);
+    std::vector<uint8_t> got;
+    bool fin = false;
+    f.register_interest(dst, id, [&](const ForwardEnvelope& env, std::vector<uint8_t> b) {
+      got = std::move(b);
+      fin = env.final;
+    });
+    k.post("send", [&, id, dst] { f.send_payload("acc4", ref_of(id, size), 0, dst, payload); });
+    k.run_until_idle();
+    CHECK(fin);
+    CHECK(got == payload);
+  }
+  CHECK(f.stats().integrity_errors == 0);
+  CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("8 MiB forward wall-clock envelope (acceptance <= 50 ms)") {
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  auto payload = synth(7, 8 << 20);
+  std::vector<double> ms;
+  for (int i = 0; i < 7; ++i) {
+    const std::string id = "lat/r" + std::to_string(i);
+    bool done = false;
+    f.register_interest(1, id, [&](const ForwardEnvelope&, std::vector<uint8_t>) { done = true; });
+    const auto t0 = std::chrono::steady_clock::now();
+    k.post("send", [&, id] { f.send_payload("lat", ref_of(id, 8 << 20), 0, 1, payload); });
+    k.run_until_idle();
+    ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    CHECK(done);
+  }
+  std::sort(ms.begin(), ms.end());
+  std::fprintf(stderr, "  8 MiB host-span forward median %.3f ms\n", ms[ms.size() / 2]);
+  CHECK(ms[ms.size() / 2] <= 50.0);
+}

@@ -1,0 +1,39 @@
+"""C++ fabric engine on the GPU:
+
+* build/test_fabric       -- this repo's tests of include/fsx/fabric.hpp
+  (test_sidecar-style cases, device-pointer K1 sends, raw zero-copy reads,
+  acceptance criterion 4 sweep and the 8 MiB latency envelope);
+* build/ref_test_sidecar  -- the REFERENCE's own tests/test_sidecar.cpp,
+  compiled unmodified against include/fsx/dropin/fissim/sidecar.hpp (the
+  drop-in) and a Catch2 shim.  Built where the reference tree exists; the
+  prebuilt binary travels to the GPU box.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _run(binary: str, timeout: int = 600):
+    path = os.path.join(ROOT, "build", binary)
+    assert os.path.exists(path), f"{path} not built: run `make cpptests` (part of build())"
+    p = subprocess.run([path], capture_output=True, text=True, timeout=timeout)
+    return p.returncode, p.stdout + p.stderr
+
+
+def test_standalone_engine(gpu):
+    rc, out = _run("test_fabric")
+    assert rc == 0, out[-4000:]
+    assert " 0 failed" in out
+
+
+def test_reference_test_sidecar_against_dropin(gpu):
+    path = os.path.join(ROOT, "build", "ref_test_sidecar")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/test_sidecar.cpp"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_test_sidecar")
+    rc, out = _run("ref_test_sidecar")
+    assert rc == 0, out[-4000:]
+    assert "13 test cases, 0 failed" in out
