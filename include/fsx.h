@@ -123,6 +123,30 @@ int fsx_flag_ptr(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t** d_flag
 int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                 int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                 void* stream);
+/* fsx_forward with options.  FSX_FWD_HOST_NOTIFY (set by fsx_forward) also
+ * mirrors each chunk flag into mapped host memory for fsx_wait /
+ * fsx_chunk_ready; leave it out when only device consumers (a merge with
+ * early start, fsx_stream_wait_flags, or plain stream order) wait on the chunks,
+ * which saves the posted PCIe store at the kernel tail. */
+#define FSX_FWD_HOST_NOTIFY 1u
+int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
+                   int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                   uint32_t options, void* stream);
+/* Several transfers of one source device in one K1 launch (ExecutorBase::
+ * emit_output fans one output out to every dest gpu, executor_sim.hpp:223-226;
+ * an encoder batch emits several items at once, :321-336).  token is in/out
+ * per transfer as above.  All t[i].src_gpu must be bound to the same device. */
+typedef struct fsx_transfer {
+  int32_t src_gpu;
+  int32_t dst_gpu;
+  const void* d_src;
+  int64_t dst_off;
+  int64_t bytes;
+  int64_t chunk_bytes;
+  int64_t flag_base;
+  uint64_t token;
+} fsx_transfer;
+int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t options, void* stream);
 /* Same contract for a HOST source span (the reference send(span) path,
  * sidecar.hpp:302): host->device copy straight into the consumer slab on
  * dst_gpu's device, then the chunk flags.  Pageable or pinned h_src. */

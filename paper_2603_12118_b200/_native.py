@@ -34,6 +34,8 @@ E_INTERNAL = 17
 LOCAL_BUFFER = 0
 NETWORK_STREAM = 1
 
+FWD_HOST_NOTIFY = 1
+
 MERGE_FULL = 0
 MERGE_SCAN_ONLY = 1
 MERGE_COPY_ONLY = 2
@@ -71,6 +73,19 @@ class MergeBatch(C.Structure):
     ]
 
 
+class Transfer(C.Structure):
+    _fields_ = [
+        ("src_gpu", C.c_int32),
+        ("dst_gpu", C.c_int32),
+        ("d_src", C.c_void_p),
+        ("dst_off", C.c_int64),
+        ("bytes", C.c_int64),
+        ("chunk_bytes", C.c_int64),
+        ("flag_base", C.c_int64),
+        ("token", C.c_uint64),
+    ]
+
+
 class Stats(C.Structure):
     _fields_ = [
         ("forwards", C.c_int64),
@@ -104,6 +119,9 @@ _SIGS = {
     "fsx_flag_ptr": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_void_p)],
     "fsx_forward": [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                     C.c_int64, C.POINTER(C.c_uint64), C.c_void_p],
+    "fsx_forward_ex": [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                       C.c_int64, C.POINTER(C.c_uint64), C.c_uint32, C.c_void_p],
+    "fsx_forward_batch": [C.c_void_p, C.c_int32, C.POINTER(Transfer), C.c_uint32, C.c_void_p],
     "fsx_forward_host": [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                          C.c_int64, C.POINTER(C.c_uint64), C.c_void_p],
     "fsx_chunk_ready": [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.POINTER(C.c_int)],

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "fsx_kernels.cuh"
 
 namespace fsx {
@@ -144,11 +146,16 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bo
 // warp that completes the chunk fences at system scope and publishes the token
 // to the consumer-device flag and the host-mapped flag.
 template <int U, int MINB>
-__global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid_constant__ FwdBatch b) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kFwdThreads / 32);
-  for (int64_t u = (int64_t)blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5); u < a.total_units;
-       u += warps) {
+  const int64_t total = b.unit_off[b.n];
+  int i = 0;  // transfer of the current unit; units only grow per warp
+  for (int64_t gu = (int64_t)blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5); gu < total;
+       gu += warps) {
+    while (gu >= b.unit_off[i + 1]) ++i;
+    const FwdArgs& a = b.t[i];
+    const int64_t u = gu - b.unit_off[i];
     const int64_t c = u / a.chunk_units;
     const int64_t s = u - c * a.chunk_units;
     const int64_t cbeg = c * a.chunk_bytes;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(FwdArgs a) {
           // data sits in this GPU's memory: every counted warp released at gpu
           // scope and the acq_rel bump acquired them, so a gpu-scope release
           // publishes the chunk to device consumers; the host mirror is a
-          // posted store that can only be observed after it.
+          // posted store issued only after every unit of the chunk is in L2.
           st_release_gpu(&a.dflags[c], a.token);
           if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
         }
@@ -358,10 +365,11 @@ int forward_block_threads() { return kFwdThreads; }
 int merge_copy_block_threads() { return kMergeThreads; }
 
 namespace {
-using FwdFn = void (*)(FwdArgs);
+using FwdFn = void (*)(FwdBatch);
 FwdFn forward_variant(int v) {
   switch (v) {
     case 1: return forward_kernel<8, 4>;
+    case 2: return forward_kernel<8, 3>;
     default: return forward_kernel<16, 2>;
   }
 }
@@ -383,8 +391,8 @@ int merge_copy_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
-cudaError_t launch_forward(const FwdArgs& a, int variant, int grid, cudaStream_t s) {
-  forward_variant(variant)<<<grid, kFwdThreads, 0, s>>>(a);
+cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s) {
+  forward_variant(variant)<<<grid, kFwdThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 
@@ -398,6 +406,134 @@ cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// K3 merge, phase 2, TMA variant: rows staged through shared memory by the
+// bulk-copy engine (cp.async.bulk global->shared with mbarrier completion,
+// shared->global bulk_group stores).  One elected thread per CTA runs an
+// S-stage ring: loads run S-1 rows ahead, each row's store is committed as
+// its own bulk group, and a stage is refilled once `wait_group.read 1` says the
+// store that last used it has finished reading shared memory.  No register
+// staging, no per-lane address math: the copy engine moves the 7-8 KiB rows.
+
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "FSX_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra FSX_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(src_smem), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+}  // namespace tma
+
+struct RowRef {
+  const uint8_t* src;
+  uint8_t* dst;
+};
+
+// Resolve placeholder row g: source row in its item, destination prompt row;
+// src == nullptr when its request failed validation.
+__device__ __forceinline__ RowRef resolve_row(const fsx_merge_batch& b, int64_t g) {
+  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g);
+  while (b.d_item_row_off[item + 1] <= g) ++item;
+  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+  while (b.d_req_item_off[req + 1] <= item) ++req;
+  if (b.d_status[req] != 0) return RowRef{nullptr, nullptr};
+  const int64_t j = g - b.d_item_row_off[item];
+  if (b.d_item_flag) {
+    const int64_t cr = b.d_item_chunk_rows[item];
+    spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
+  }
+  const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * b.row_bytes;
+  uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * b.row_bytes;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) {
+    for (int64_t i = 0; i < b.row_bytes; ++i) dst[i] = src[i];  // bulk copies need 16 B alignment
+    return RowRef{nullptr, nullptr};
+  }
+  return RowRef{src, dst};
+}
+
+template <int S>
+__global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  __shared__ __align__(8) uint64_t bars[S];
+  if (threadIdx.x != 0) return;
+  const uint32_t sbase = tma::smem_u32(stage_mem);
+  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
+  tma::mbar_fence_init();
+  const uint32_t rb = (uint32_t)b.row_bytes;
+  const int64_t first = blockIdx.x, stride = gridDim.x, n = b.total_item_rows;
+  uint8_t* dst_of[S];
+  uint32_t parity = 0;  // bit s = phase parity expected next on stage s
+  auto issue = [&](int64_t k) {  // load this CTA's k-th row into stage k % S
+    const int s = (int)(k % S);
+    const RowRef r = resolve_row(b, first + k * stride);
+    dst_of[s] = r.dst;
+    if (!r.src) return;
+    const uint32_t bar = tma::smem_u32(&bars[s]);
+    tma::mbar_expect_tx(bar, rb);
+    tma::bulk_load(sbase + s * stage_bytes, r.src, rb, bar);
+  };
+  for (int64_t k = 0; k < S - 1 && first + k * stride < n; ++k) issue(k);
+  for (int64_t k = 0; first + k * stride < n; ++k) {
+    const int s = (int)(k % S);
+    if (dst_of[s]) {
+      tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
+      parity ^= 1u << s;
+      tma::bulk_store(dst_of[s], sbase + s * stage_bytes, rb);
+    }
+    tma::bulk_commit();  // one group per row (possibly empty) keeps the count exact
+    tma::bulk_wait_read1();  // the store issued one row ago has left shared memory
+    if (first + (k + S - 1) * stride < n) issue(k + S - 1);
+  }
+  tma::bulk_wait_all();
+}
+
+constexpr int kTmaStages = 4;
+
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
   *launches = 0;
   if (b.num_requests <= 0) return cudaSuccess;
@@ -409,6 +545,26 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     *launches = 1;
   }
   if (b.mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
+  static const bool use_tma = [] {
+    const char* e = std::getenv("FSX_MERGE_TMA");
+    return !(e && e[0] == '0');
+  }();
+  const uint32_t stage = (uint32_t)((b.row_bytes + 127) & ~int64_t{127});
+  if (use_tma && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)stage * kTmaStages;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_copy_tma_kernel<kTmaStages>, 32,
+                                                      smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    const int64_t cap = (int64_t)sms * per_sm;
+    const int grid = (int)(b.total_item_rows < cap ? b.total_item_rows : cap);
+    merge_copy_tma_kernel<kTmaStages><<<grid, 32, smem, s>>>(b, stage);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) ++*launches;
+    return e;
+  }
   const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
   const int grid = (int)(need < copy_grid ? need : copy_grid);
   merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);

@@ -28,6 +28,16 @@ struct FwdArgs {
   uint64_t token;
 };
 
+// Up to kFwdMaxBatch transfers of one source device in one K1 launch (kernel
+// parameter space, ~2 KB): units are laid out transfer-major, chunk-major.
+constexpr int kFwdMaxBatch = 16;
+struct FwdBatch {
+  int32_t n;
+  int32_t _pad;
+  int64_t unit_off[kFwdMaxBatch + 1];
+  FwdArgs t[kFwdMaxBatch];
+};
+
 struct FlagSetArgs {
   uint64_t* dflags;
   uint64_t* hflags;
@@ -36,7 +46,7 @@ struct FlagSetArgs {
 };
 
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
-cudaError_t launch_forward(const FwdArgs& a, int variant, int grid, cudaStream_t s);
+cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);

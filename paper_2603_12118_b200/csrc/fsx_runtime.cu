@@ -49,8 +49,8 @@ constexpr int64_t kCounterRing = 1 << 16;  // chunk counters per source device
 int64_t fwd_unit_bytes() {
   static const int64_t v = [] {
     const char* e = std::getenv("FSX_FWD_UNIT");
-    const int64_t x = e ? std::atoll(e) : 32 * 1024;
-    return std::max<int64_t>(512, (x + 511) & ~int64_t{511});
+    if (!e) return int64_t{0};  // adaptive (see fsx_forward_ex)
+    return std::max<int64_t>(512, (std::atoll(e) + 511) & ~int64_t{511});
   }();
   return v;
 }
@@ -58,7 +58,7 @@ int64_t fwd_unit_bytes() {
 int fwd_variant() {
   static const int v = [] {
     const char* e = std::getenv("FSX_FWD_VARIANT");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;  // 8 x 16 B per lane, 4 CTAs/SM (sweep2)
   }();
   return v;
 }
@@ -465,53 +465,101 @@ int fsx_flag_ptr(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t** d_flag
 int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                 int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                 void* stream) {
+  return fsx_forward_ex(f, src_gpu, d_src, dst_gpu, dst_off, bytes, chunk_bytes, flag_base, token,
+                        FSX_FWD_HOST_NOTIFY, stream);
+}
+
+int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
+                   int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                   uint32_t options, void* stream) {
+  fsx_transfer t{src_gpu, dst_gpu, d_src, dst_off, bytes, chunk_bytes, flag_base,
+                 token ? *token : 0};
+  const int rc = fsx_forward_batch(f, 1, &t, options, stream);
+  if (rc == FSX_OK && token) *token = t.token;
+  return rc;
+}
+
+int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t options, void* stream) {
+  if (n <= 0) return n == 0 ? FSX_OK : fail(FSX_E_VALIDATION, "negative transfer count");
   int src_dev = 0;
-  int rc = find_gpu(f, src_gpu, &src_dev);
+  int rc = find_gpu(f, t[0].src_gpu, &src_dev);
   if (rc) return rc;
-  if (bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
-  if (chunk_bytes <= 0 || chunk_bytes >= bytes) chunk_bytes = std::max<int64_t>(bytes, 1);
-  else if (chunk_bytes % 16) return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
-  const int64_t n_chunks = bytes == 0 ? 1 : (bytes + chunk_bytes - 1) / chunk_bytes;
-  fsx::FwdArgs a{};
+  int64_t batch_bytes = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int d = 0;
+    rc = find_gpu(f, t[i].src_gpu, &d);
+    if (rc) return rc;
+    if (d != src_dev) return fail(FSX_E_VALIDATION, "a forward batch must share one source device");
+    if (t[i].bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+    if (t[i].chunk_bytes > 0 && t[i].chunk_bytes < t[i].bytes && t[i].chunk_bytes % 16)
+      return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
+    batch_bytes += t[i].bytes;
+  }
   Device* dev = nullptr;
   {
     std::lock_guard<std::mutex> lk(f->mu);
-    Slab* s = slab_of(f, dst_gpu);
-    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
-    if (dst_off < 0 || dst_off + bytes > s->capacity)
-      return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
-    if (flag_base < 0 || flag_base + n_chunks > kFlagRing)
-      return fail(FSX_E_VALIDATION, "flag range out of the ring");
     rc = device_state(f, src_dev, &dev);
     if (rc) return rc;
-    a.counters = dev->counters + dev->counter_ring.take(n_chunks);
-    a.dst = s->base + dst_off;
-    a.dflags = s->dflags + flag_base;
-    static const bool no_host_mirror = std::getenv("FSX_FWD_NO_HOST_FLAGS") != nullptr;  // sweeps
-    a.hflags = (s->hflags && !no_host_mirror) ? s->hflags + flag_base : nullptr;
-    a.peer = (s->imported || s->device != src_dev) ? 1 : 0;
   }
-  a.src = static_cast<const uint8_t*>(d_src);
-  a.bytes = bytes;
-  a.chunk_bytes = chunk_bytes;
-  a.slice = std::min<int64_t>(fwd_unit_bytes(), std::max<int64_t>(16, chunk_bytes));
-  a.slice = (a.slice + 15) & ~int64_t{15};
-  a.chunk_units = (chunk_bytes + a.slice - 1) / a.slice;
-  const int64_t last_len = bytes - (n_chunks - 1) * chunk_bytes;
-  a.last_units = std::max<int64_t>(1, (last_len + a.slice - 1) / a.slice);
-  a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
-  a.n_chunks = (int32_t)n_chunks;
-  a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
-  a.token = (token && *token) ? *token : f->next_token.fetch_add(1);
+  // Work unit: one warp, one release + counter bump.  Large enough to
+  // amortise the release, small enough that mid-size batches still spread
+  // over every resident warp (sweep3: 16 KiB >= 64 MiB, down to 4 KiB).
+  int64_t unit = fwd_unit_bytes();
+  if (unit == 0) {
+    const int64_t warps =
+        std::max<int64_t>(1, (int64_t)dev->fwd_grid * (fsx::forward_block_threads() / 32));
+    unit = 16384;
+    while (unit > 4096 && batch_bytes / unit < warps / 2) unit /= 2;
+  }
   FSX_CUDA(cudaSetDevice(src_dev));
-  const int warps_per_cta = fsx::forward_block_threads() / 32;
-  const int grid = (int)std::min<int64_t>((a.total_units + warps_per_cta - 1) / warps_per_cta,
-                                          dev->fwd_grid);
-  FSX_CUDA(fsx::launch_forward(a, fwd_variant(), grid, pick_stream(dev, stream)));
-  f->launches++;
-  f->forwards++;
-  f->bytes_forwarded += bytes;
-  if (token) *token = a.token;
+  cudaStream_t st = pick_stream(dev, stream);
+  for (int32_t first = 0; first < n; first += fsx::kFwdMaxBatch) {
+    const int32_t cnt = std::min<int32_t>(n - first, fsx::kFwdMaxBatch);
+    fsx::FwdBatch b{};
+    b.n = cnt;
+    for (int32_t k = 0; k < cnt; ++k) {
+      fsx_transfer& x = t[first + k];
+      fsx::FwdArgs& a = b.t[k];
+      int64_t chunk = x.chunk_bytes;
+      if (chunk <= 0 || chunk >= x.bytes) chunk = std::max<int64_t>(x.bytes, 1);
+      const int64_t n_chunks = x.bytes == 0 ? 1 : (x.bytes + chunk - 1) / chunk;
+      {
+        std::lock_guard<std::mutex> lk(f->mu);
+        Slab* s = slab_of(f, x.dst_gpu);
+        if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(x.dst_gpu));
+        if (x.dst_off < 0 || x.dst_off + x.bytes > s->capacity)
+          return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
+        if (x.flag_base < 0 || x.flag_base + n_chunks > kFlagRing)
+          return fail(FSX_E_VALIDATION, "flag range out of the ring");
+        a.counters = dev->counters + dev->counter_ring.take(n_chunks);
+        a.dst = s->base + x.dst_off;
+        a.dflags = s->dflags + x.flag_base;
+        a.hflags = (s->hflags && (options & FSX_FWD_HOST_NOTIFY)) ? s->hflags + x.flag_base : nullptr;
+        a.peer = (s->imported || s->device != src_dev) ? 1 : 0;
+      }
+      a.src = static_cast<const uint8_t*>(x.d_src);
+      a.bytes = x.bytes;
+      a.chunk_bytes = chunk;
+      a.slice = std::min<int64_t>(unit, std::max<int64_t>(16, chunk));
+      a.slice = (a.slice + 15) & ~int64_t{15};
+      a.chunk_units = (chunk + a.slice - 1) / a.slice;
+      const int64_t last_len = x.bytes - (n_chunks - 1) * chunk;
+      a.last_units = std::max<int64_t>(1, (last_len + a.slice - 1) / a.slice);
+      a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
+      a.n_chunks = (int32_t)n_chunks;
+      a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
+      if (x.token == 0) x.token = f->next_token.fetch_add(1);
+      a.token = x.token;
+      b.unit_off[k + 1] = b.unit_off[k] + a.total_units;
+      f->bytes_forwarded += x.bytes;
+      f->forwards++;
+    }
+    const int warps_per_cta = fsx::forward_block_threads() / 32;
+    const int grid = (int)std::min<int64_t>((b.unit_off[cnt] + warps_per_cta - 1) / warps_per_cta,
+                                            dev->fwd_grid);
+    FSX_CUDA(fsx::launch_forward(b, fwd_variant(), grid, st));
+    f->launches++;
+  }
   return FSX_OK;
 }
 

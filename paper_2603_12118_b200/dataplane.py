@@ -103,9 +103,12 @@ class DataPlaneBatch:
                 return False
             offs.append(off)
         self.slab_off = np.array(offs, dtype=np.int64)
-        ptrs = [self.fab.slab_ptr(self.dst_gpu, o) for o in offs]
-        if ptrs:
+        # first fit hands back the same offsets step after step: upload the
+        # slab views only when they change
+        if offs and offs != getattr(self, "_uploaded_offs", None):
+            ptrs = [self.fab.slab_ptr(self.dst_gpu, o) for o in offs]
             self.item_src.copy_(torch.tensor(ptrs, dtype=torch.int64))
+            self._uploaded_offs = offs
         return True
 
     def release(self) -> None:
@@ -120,20 +123,24 @@ class DataPlaneBatch:
             return 0
         return self.chunk_rows * self.rb
 
-    def forward(self, stream=None) -> int:
-        """Push every item into its slab segment; returns kernels launched."""
+    def forward(self, stream=None, host_notify: bool = True) -> int:
+        """Push every item into its slab segment; returns kernels launched.
+        host_notify=False when only device work (stream order / early-start
+        merge) waits on the chunk flags."""
         assert self.slab_off is not None, "alloc() first"
         base = self.src_buf.data_ptr()
+        xfers = []
         for i, it in enumerate(self.lay.items):
             nb = it.rows * self.rb
             cb = self.chunk_bytes(it)
             n = 1 if (cb <= 0 or cb >= nb) else -(-nb // cb)
             self.n_chunks[i] = n
             self.flag_base[i] = self.fab.flags_alloc(self.dst_gpu, n)
-            self.tokens[i] = self.fab.forward(self.src_gpu, base + int(self.src_off[i]),
-                                              self.dst_gpu, int(self.slab_off[i]), nb, cb,
-                                              int(self.flag_base[i]), stream)
-        return len(self.lay.items)
+            xfers.append((self.src_gpu, base + int(self.src_off[i]), self.dst_gpu,
+                          int(self.slab_off[i]), nb, cb, int(self.flag_base[i]), 0))
+        if xfers:  # one K1 launch per 16 items
+            self.tokens[:] = self.fab.forward_batch(xfers, stream, host_notify=host_notify)
+        return (len(xfers) + 15) // 16
 
     def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
         """The host-span send path (sidecar.hpp:302): payload bytes from host

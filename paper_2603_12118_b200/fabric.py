@@ -136,11 +136,27 @@ class DeviceFabric:
 
     # -- data movement ----------------------------------------------------------
     def forward(self, src_gpu: int, src_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
-                chunk_bytes: int, flag_base: int, stream=None, token: int = 0) -> int:
+                chunk_bytes: int, flag_base: int, stream=None, token: int = 0,
+                host_notify: bool = True) -> int:
+        """K1.  host_notify mirrors chunk flags to host memory (fsx_wait);
+        device-only consumers (stream order, early-start merge) skip it."""
         tok = C.c_uint64(token)
-        N.call("fsx_forward", self._h, src_gpu, src_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
-               flag_base, C.byref(tok), _stream_ptr(stream))
+        N.call("fsx_forward_ex", self._h, src_gpu, src_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
+               flag_base, C.byref(tok), N.FWD_HOST_NOTIFY if host_notify else 0,
+               _stream_ptr(stream))
         return tok.value
+
+    def forward_batch(self, transfers, stream=None, host_notify: bool = True):
+        """K1 over several transfers of one source device in one launch.
+        `transfers`: sequence of (src_gpu, src_ptr, dst_gpu, dst_off, nbytes,
+        chunk_bytes, flag_base, token); returns the tokens used."""
+        n = len(transfers)
+        arr = (N.Transfer * max(n, 1))()
+        for i, (sg, sp, dg, do, nb, cb, fb, tok) in enumerate(transfers):
+            arr[i] = N.Transfer(sg, dg, sp, do, nb, cb, fb, tok)
+        N.call("fsx_forward_batch", self._h, n, arr, N.FWD_HOST_NOTIFY if host_notify else 0,
+               _stream_ptr(stream))
+        return [arr[i].token for i in range(n)]
 
     def forward_host(self, host_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
                      chunk_bytes: int, flag_base: int, stream=None, token: int = 0) -> int:

@@ -119,6 +119,32 @@ def test_forward_rejects_bad_chunk_and_overrun(fab):
     assert e.value.code == "validation"
 
 
+def test_forward_batch_mixed(fab, oracle_mod):
+    """One K1 launch over transfers of different sizes, chunkings, alignments
+    and destination slabs (and more than 16, so two launches)."""
+    torch = _torch()
+    specs = [(n, ch, sh, dst) for n, ch, sh, dst in
+             [(0, 0, 0, 1), (1, 0, 0, 2), (4099, 0, 3, 1), (1 << 20, 65536, 0, 2),
+              (7_340_032 * 2 + 32, 7_340_032, 0, 1), (65536 * 3, 4096, 0, 2)] * 3]
+    srcs, xfers, offs = [], [], []
+    for k, (n, ch, sh, dst) in enumerate(specs):
+        buf = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
+        fab.synth(0, 1000 + k, buf.data_ptr() + sh, n)
+        off = fab.slab_alloc(dst, n)
+        nch = 1 if ch <= 0 or ch >= n else -(-n // ch)
+        fb = fab.flags_alloc(dst, nch)
+        srcs.append(buf)
+        offs.append((dst, off, fb, nch))
+        xfers.append((0, buf.data_ptr() + sh, dst, off, n, ch, fb, 0))
+    toks = fab.forward_batch(xfers)
+    assert len(set(toks)) == len(toks)
+    for k, (n, ch, sh, dst) in enumerate(specs):
+        d, off, fb, nch = offs[k]
+        fab.wait(d, fb, nch, toks[k], timeout_us=20_000_000)
+        assert fab.slab_read(d, off, n) == oracle_mod.synth_payload(1000 + k, n), specs[k]
+        fab.slab_free(d, off)
+
+
 def test_forward_host_span_path(fab, oracle_mod):
     for n, chunk in [(0, 0), (1, 0), (4097, 0), (3 << 20, 1 << 20)]:
         payload = np.frombuffer(oracle_mod.synth_payload(n + 11, n), np.uint8).copy()
