@@ -213,6 +213,30 @@ typedef struct fsx_merge_batch {
 } fsx_merge_batch;
 int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream);
 
+/* ---- streaming channels (config C) ------------------------------------------
+ * The small-message streams of the reference: thinker hidden states, one
+ * [hidden_dim] row per decoded token and request (executor_sim.hpp:556-562),
+ * and talker codes, 4 B per chunk (:543-549), each a streaming DataRef sent
+ * with seq = token index and delivered strictly in seq order
+ * (sidecar.hpp:527-531).  Per-message send()+envelope+event is replaced by one
+ * launch per decode step for all active requests: a channel is one stream
+ * (one request's streaming ref) with a ring of `slots` rows in the consumer's
+ * slab, per-slot flags and device-resident head/tail counters.
+ *   push: row i of d_rows (row_stride apart) -> next slot of channels[i]; waits
+ *         (in kernel) while the ring is full; flag = tag(seq), release.
+ *   pull: for each channels[i], waits for its next seq (acquire), copies it to
+ *         row i of d_out and frees the slot (tail = seq + 1).
+ * All channels of one push share a source device, of one pull a consumer
+ * device.  fsx_channel_progress reads (produced, consumed) for tests. */
+int fsx_channel_open(fsx_fabric* f, int src_gpu, int dst_gpu, int64_t row_bytes, int32_t slots,
+                     int32_t* channel);
+int fsx_channel_close(fsx_fabric* f, int32_t channel);
+int fsx_channel_push(fsx_fabric* f, int32_t n, const int32_t* channels, const void* d_rows,
+                     int64_t row_stride, void* stream);
+int fsx_channel_pull(fsx_fabric* f, int32_t n, const int32_t* channels, void* d_out,
+                     int64_t out_stride, void* stream);
+int fsx_channel_progress(fsx_fabric* f, int32_t channel, uint64_t* produced, uint64_t* consumed);
+
 /* ---- synthesis (K0) ---------------------------------------------------------
  * synth_payload_into (common.hpp:247-259) on the device: byte-identical to the
  * reference stream.  Used by producers/tests/bench to create inputs. */

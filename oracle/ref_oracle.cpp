@@ -237,6 +237,56 @@ double ref_dataplane_pass(int32_t num_requests, int32_t num_items, int64_t row_b
   }
 }
 
+// Reference small-message streaming (config C): `streams` streaming refs (one
+// per request) each receive one `row_bytes` chunk per decode step with
+// seq = step, final on the last step, exactly as LlmEngineExecutor::emit_token
+// sends hidden states (executor_sim.hpp:540-564).  Every step's sends are
+// posted and drained with run_until_idle (Virtual clock).  Returns wall
+// seconds for all steps; delivered chunks are checked for count and order.
+double ref_stream_bench(int64_t row_bytes, int streams, int steps) {
+  try {
+    SimKernel k(ClockMode::Virtual);
+    SidecarFabric fabric(k, topo_8x2());
+    std::vector<int64_t> next(streams, 0);
+    int64_t bad = 0;
+    std::vector<DataRef> refs(streams);
+    std::vector<std::vector<uint8_t>> rows(streams);
+    for (int s = 0; s < streams; ++s) {
+      char id[64];
+      std::snprintf(id, sizeof(id), "req-%06d/r0001", s);
+      refs[s].ref_id = id;
+      refs[s].producer = "thinker";
+      refs[s].desc = {{steps, row_bytes / 2}, 2};
+      refs[s].streaming = true;
+      fabric.register_interest(1, id, [&, s](const ForwardEnvelope& env, std::vector<uint8_t> b) {
+        if (env.seq != next[s]++ || static_cast<int64_t>(b.size()) != row_bytes) ++bad;
+      });
+    }
+    // payload synthesis is the producer's work, not forwarding: outside the timer
+    for (int s = 0; s < streams; ++s)
+      rows[s] = synth_payload(fnv1a64(refs[s].ref_id), static_cast<size_t>(row_bytes));
+    auto t0 = std::chrono::steady_clock::now();
+    for (int step = 0; step < steps; ++step) {
+      k.post("llm.step", [&, step] {
+        for (int s = 0; s < streams; ++s)
+          fabric.send("req", refs[s], 0, 1, rows[s], step, step + 1 == steps);
+      });
+      k.run_until_idle();
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    for (int s = 0; s < streams; ++s)
+      if (next[s] != steps) ++bad;
+    if (bad) {
+      g_err = "stream delivery out of order or incomplete";
+      return -1;
+    }
+    return std::chrono::duration<double>(t1 - t0).count();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // generate_workload (workload.hpp:196-242) on a mix file: the reference's own
 // seeded sampler, returned as a JSON array of {arrival_ms, class, request}.
 // The returned pointer stays valid until the next call on this thread.

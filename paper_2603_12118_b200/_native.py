@@ -130,6 +130,11 @@ _SIGS = {
     "fsx_signal_flags": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_int,
                          C.c_void_p],
     "fsx_merge": [C.c_void_p, C.c_int, C.POINTER(MergeBatch), C.c_void_p],
+    "fsx_channel_open": [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int32, C.POINTER(C.c_int32)],
+    "fsx_channel_close": [C.c_void_p, C.c_int32],
+    "fsx_channel_push": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_channel_pull": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_channel_progress": [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "fsx_synth_payload": [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_pointer_device": [C.c_void_p, C.POINTER(C.c_int)],
     "fsx_copy_to_host": [C.c_void_p, C.c_void_p, C.c_int64],

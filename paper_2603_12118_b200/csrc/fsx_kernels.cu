@@ -407,6 +407,75 @@ cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token,
 }
 
 // ---------------------------------------------------------------------------
+// Streaming channels (config C: thinker hidden states per decode step, talker
+// codes per chunk; executor_sim.hpp:540-564).  One push launch per decode step
+// moves every active request's row (one CTA-warp per row) into slot
+// seq % slots of that request's ring in the consumer slab and publishes
+// flag = tag(seq) with release semantics; one pull launch on the consumer
+// waits per row (acquire), gathers the rows in seq order into the consumer's
+// input and releases the slot back to the producer (tail = seq + 1).  Device
+// counters carry seq, so a step needs no host round trip.
+
+__device__ __forceinline__ void warp_copy_row(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                              uint32_t n, int lane) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | n) & 15) == 0) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint32_t nv = n >> 4;
+    for (uint32_t base = 0; base < nv; base += 32 * 16) {
+      uint4 r[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t i = base + k * 32 + lane;
+        if (i < nv) r[k] = ld_v4(s + i);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t i = base + k * 32 + lane;
+        if (i < nv) st_v4(d + i, r[k]);
+      }
+    }
+  } else {
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+  }
+}
+
+__global__ void __launch_bounds__(32) chan_push_kernel(const __grid_constant__ ChanStep s) {
+  const ChanRow& c = s.c[blockIdx.x];
+  const int lane = threadIdx.x;
+  const uint64_t seq = *c.head;
+  if (lane == 0) {  // backpressure: the slot's previous message was consumed
+    while (seq - ld_acquire_sys(c.tail) >= c.slots) __nanosleep(64);
+  }
+  __syncwarp();
+  uint8_t* dst = c.ring + (seq % c.slots) * (uint64_t)c.row_bytes;
+  warp_copy_row(s.rows + blockIdx.x * s.stride, dst, c.row_bytes, lane);
+  __syncwarp();
+  if (lane == 0) {
+    const uint64_t tag = c.salt | (seq + 1);
+    if (c.peer) {
+      st_release_sys(&c.flags[seq % c.slots], tag);
+    } else {
+      st_release_gpu(&c.flags[seq % c.slots], tag);
+    }
+    *c.head = seq + 1;
+  }
+}
+
+__global__ void __launch_bounds__(32) chan_pull_kernel(const __grid_constant__ ChanStep s) {
+  const ChanRow& c = s.c[blockIdx.x];
+  const int lane = threadIdx.x;
+  const uint64_t seq = *c.tail;
+  const uint64_t slot = seq % c.slots;
+  if (lane == 0) spin_until(&c.flags[slot], c.salt | (seq + 1));
+  __syncwarp();
+  uint8_t* out = const_cast<uint8_t*>(s.rows) + blockIdx.x * s.stride;
+  warp_copy_row(c.ring + slot * (uint64_t)c.row_bytes, out, c.row_bytes, lane);
+  __syncwarp();
+  if (lane == 0) st_release_sys(c.tail, seq + 1);  // slot free for the producer
+}
+
+// ---------------------------------------------------------------------------
 // K3 merge, phase 2, TMA variant: rows staged through shared memory by the
 // bulk-copy engine (cp.async.bulk global->shared with mbarrier completion,
 // shared->global bulk_group stores).  One elected thread per CTA runs an
@@ -533,6 +602,18 @@ __global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, u
 }
 
 constexpr int kTmaStages = 4;
+
+cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st) {
+  if (s.n <= 0) return cudaSuccess;
+  chan_push_kernel<<<s.n, 32, 0, st>>>(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st) {
+  if (s.n <= 0) return cudaSuccess;
+  chan_pull_kernel<<<s.n, 32, 0, st>>>(s);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
   *launches = 0;

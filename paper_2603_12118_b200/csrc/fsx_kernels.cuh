@@ -45,7 +45,30 @@ struct FlagSetArgs {
   uint64_t token;
 };
 
+// Streaming channels (config C): per-token rows pushed into a consumer ring.
+struct ChanRow {
+  uint8_t* ring;        // consumer slab region: slots * row_bytes
+  uint64_t* flags;      // consumer flags: slots (value = tag(seq))
+  uint64_t* head;       // producer state (next seq to write), producer device
+  uint64_t* tail;       // consumer state (next seq to read), consumer device
+  uint64_t salt;        // tag(seq) = salt | (seq + 1)
+  uint32_t slots;
+  uint32_t row_bytes;
+  int32_t peer;         // ring is peer memory
+  int32_t _pad;
+};
+constexpr int kChanMaxRows = 48;
+struct ChanStep {
+  int32_t n;
+  int32_t _pad;
+  const uint8_t* rows;  // producer rows (push) / consumer output rows (pull)
+  int64_t stride;
+  ChanRow c[kChanMaxRows];
+};
+
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
+cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
+cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);

@@ -158,6 +158,23 @@ struct Device {
   int sms = 0;
   int fwd_grid = 0;
   int merge_grid = 0;
+  uint64_t* state = nullptr;  // channel head/tail counters (kStatePool u64)
+  int64_t state_next = 0;
+};
+
+constexpr int64_t kStatePool = 1 << 16;
+
+// A streaming channel: one producer->consumer stream (a streaming DataRef,
+// e.g. one request's thinker hidden states) delivered in seq order through a
+// ring of `slots` rows in the consumer slab.
+struct Channel {
+  bool open = false;
+  int src_gpu = -1, dst_gpu = -1, src_dev = -1, dst_dev = -1;
+  int64_t ring_off = -1, flag_base = -1;
+  uint32_t slots = 0, row_bytes = 0;
+  uint64_t* head = nullptr;  // producer device
+  uint64_t* tail = nullptr;  // consumer device
+  uint64_t salt = 0;
 };
 
 }  // namespace
@@ -168,6 +185,7 @@ struct fsx_fabric {
   std::map<int, int> device_of;
   std::map<int, std::unique_ptr<Slab>> slabs;
   std::map<int, std::unique_ptr<Device>> devices;
+  std::vector<Channel> channels;
   std::atomic<uint64_t> next_token{1};
   std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
 };
@@ -287,6 +305,7 @@ int fsx_close(fsx_fabric* f) {
   for (auto& [o, d] : f->devices) {
     cudaSetDevice(o);
     if (d->counters) cudaFree(d->counters);
+    if (d->state) cudaFree(d->state);
     if (d->stream) cudaStreamDestroy(d->stream);
   }
   delete f;
@@ -758,6 +777,155 @@ int fsx_copy_to_host(void* h_dst, const void* d_src, int64_t n) {
   if (n < 0) return fail(FSX_E_VALIDATION, "negative byte count");
   if (n == 0) return FSX_OK;
   FSX_CUDA(cudaMemcpy(h_dst, d_src, n, cudaMemcpyDefault));
+  return FSX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Streaming channels
+
+namespace {
+
+int state_slot(fsx_fabric* f, Device* d, uint64_t** out) {
+  if (!d->state) {
+    FSX_CUDA(cudaSetDevice(d->ordinal));
+    FSX_CUDA(cudaMalloc(&d->state, kStatePool * sizeof(uint64_t)));
+    FSX_CUDA(cudaMemset(d->state, 0, kStatePool * sizeof(uint64_t)));
+  }
+  if (d->state_next >= kStatePool) return fail(FSX_E_OOM, "channel state pool exhausted");
+  *out = d->state + d->state_next++;
+  FSX_CUDA(cudaSetDevice(d->ordinal));
+  FSX_CUDA(cudaMemset(*out, 0, sizeof(uint64_t)));
+  (void)f;
+  return FSX_OK;
+}
+
+int build_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, int64_t stride,
+               bool push, fsx::ChanStep* st, int* device) {
+  st->n = n;
+  st->rows = static_cast<const uint8_t*>(rows);
+  st->stride = stride;
+  for (int32_t i = 0; i < n; ++i) {
+    if (chs[i] < 0 || chs[i] >= (int32_t)f->channels.size() || !f->channels[chs[i]].open)
+      return fail(FSX_E_NOT_FOUND, "unknown or closed channel " + std::to_string(chs[i]));
+    const Channel& c = f->channels[chs[i]];
+    const int dev = push ? c.src_dev : c.dst_dev;
+    if (i == 0) *device = dev;
+    else if (dev != *device) return fail(FSX_E_VALIDATION, "channels of one step must share a device");
+    if (stride < (int64_t)c.row_bytes) return fail(FSX_E_VALIDATION, "row stride below row size");
+    Slab* s = slab_of(f, c.dst_gpu);
+    fsx::ChanRow& r = st->c[i];
+    r.ring = s->base + c.ring_off;
+    r.flags = s->dflags + c.flag_base;
+    r.head = c.head;
+    r.tail = c.tail;
+    r.salt = c.salt;
+    r.slots = c.slots;
+    r.row_bytes = c.row_bytes;
+    r.peer = (s->imported || c.src_dev != c.dst_dev) ? 1 : 0;
+  }
+  return FSX_OK;
+}
+
+int chan_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, int64_t stride,
+              bool push, void* stream) {
+  if (n < 0) return fail(FSX_E_VALIDATION, "negative channel count");
+  for (int32_t first = 0; first < n; first += fsx::kChanMaxRows) {
+    const int32_t cnt = std::min<int32_t>(n - first, fsx::kChanMaxRows);
+    fsx::ChanStep st{};
+    int device = 0;
+    Device* dev = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(f->mu);
+      int rc = build_step(f, cnt, chs + first, static_cast<const uint8_t*>(rows) + first * stride,
+                          stride, push, &st, &device);
+      if (rc) return rc;
+      rc = device_state(f, device, &dev);
+      if (rc) return rc;
+    }
+    FSX_CUDA(cudaSetDevice(device));
+    cudaStream_t s = pick_stream(dev, stream);
+    FSX_CUDA(push ? fsx::launch_chan_push(st, s) : fsx::launch_chan_pull(st, s));
+    f->launches++;
+    if (push) {
+      f->forwards += cnt;
+      for (int32_t i = 0; i < cnt; ++i) f->bytes_forwarded += st.c[i].row_bytes;
+    }
+  }
+  return FSX_OK;
+}
+
+}  // namespace
+
+int fsx_channel_open(fsx_fabric* f, int src_gpu, int dst_gpu, int64_t row_bytes, int32_t slots,
+                     int32_t* channel) {
+  int src_dev = 0, dst_dev = 0;
+  int rc = find_gpu(f, src_gpu, &src_dev);
+  if (rc) return rc;
+  rc = find_gpu(f, dst_gpu, &dst_dev);
+  if (rc) return rc;
+  if (row_bytes <= 0 || row_bytes > (int64_t{1} << 30) || slots <= 0 || slots > 4096)
+    return fail(FSX_E_VALIDATION, "bad channel geometry");
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, dst_gpu);
+  if (!s || s->imported) return fail(FSX_E_NOT_FOUND, "no owned slab for the consumer gpu");
+  Channel c;
+  c.src_gpu = src_gpu;
+  c.dst_gpu = dst_gpu;
+  c.src_dev = src_dev;
+  c.dst_dev = dst_dev;
+  c.slots = (uint32_t)slots;
+  c.row_bytes = (uint32_t)row_bytes;
+  c.ring_off = s->blocks.alloc(row_bytes * slots);
+  if (c.ring_off < 0) return fail(FSX_E_OOM, "consumer slab cannot hold the channel ring");
+  c.flag_base = s->flags.take(slots);
+  Device *ps = nullptr, *cs = nullptr;
+  rc = device_state(f, src_dev, &ps);
+  if (!rc) rc = device_state(f, dst_dev, &cs);
+  if (!rc) rc = state_slot(f, ps, &c.head);
+  if (!rc) rc = state_slot(f, cs, &c.tail);
+  if (rc) {
+    s->blocks.release(c.ring_off);
+    return rc;
+  }
+  c.salt = (uint64_t)(f->channels.size() + 1) << 40;
+  c.open = true;
+  *channel = (int32_t)f->channels.size();
+  f->channels.push_back(c);
+  return FSX_OK;
+}
+
+int fsx_channel_close(fsx_fabric* f, int32_t channel) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  if (channel < 0 || channel >= (int32_t)f->channels.size() || !f->channels[channel].open)
+    return fail(FSX_E_NOT_FOUND, "unknown or closed channel");
+  Channel& c = f->channels[channel];
+  Slab* s = slab_of(f, c.dst_gpu);
+  if (s) s->blocks.release(c.ring_off);
+  c.open = false;
+  return FSX_OK;
+}
+
+int fsx_channel_push(fsx_fabric* f, int32_t n, const int32_t* channels, const void* d_rows,
+                     int64_t row_stride, void* stream) {
+  return chan_step(f, n, channels, d_rows, row_stride, true, stream);
+}
+
+int fsx_channel_pull(fsx_fabric* f, int32_t n, const int32_t* channels, void* d_out,
+                     int64_t out_stride, void* stream) {
+  return chan_step(f, n, channels, d_out, out_stride, false, stream);
+}
+
+int fsx_channel_progress(fsx_fabric* f, int32_t channel, uint64_t* produced, uint64_t* consumed) {
+  uint64_t *h = nullptr, *t = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (channel < 0 || channel >= (int32_t)f->channels.size())
+      return fail(FSX_E_NOT_FOUND, "unknown channel");
+    h = f->channels[channel].head;
+    t = f->channels[channel].tail;
+  }
+  FSX_CUDA(cudaMemcpy(produced, h, sizeof(uint64_t), cudaMemcpyDefault));
+  FSX_CUDA(cudaMemcpy(consumed, t, sizeof(uint64_t), cudaMemcpyDefault));
   return FSX_OK;
 }
 

@@ -165,6 +165,32 @@ class DeviceFabric:
                flag_base, C.byref(tok), _stream_ptr(stream))
         return tok.value
 
+    # -- streaming channels (config C) ---------------------------------------
+    def channel_open(self, src_gpu: int, dst_gpu: int, row_bytes: int, slots: int = 64) -> int:
+        ch = C.c_int32()
+        N.call("fsx_channel_open", self._h, src_gpu, dst_gpu, row_bytes, slots, C.byref(ch))
+        return ch.value
+
+    def channel_close(self, ch: int) -> None:
+        N.call("fsx_channel_close", self._h, ch)
+
+    @staticmethod
+    def _chs(chs):
+        return (C.c_int32 * max(len(chs), 1))(*chs)
+
+    def channel_push(self, chs, rows_ptr: int, stride: int, stream=None) -> None:
+        N.call("fsx_channel_push", self._h, len(chs), self._chs(chs), rows_ptr, stride,
+               _stream_ptr(stream))
+
+    def channel_pull(self, chs, out_ptr: int, stride: int, stream=None) -> None:
+        N.call("fsx_channel_pull", self._h, len(chs), self._chs(chs), out_ptr, stride,
+               _stream_ptr(stream))
+
+    def channel_progress(self, ch: int):
+        p, c = C.c_uint64(), C.c_uint64()
+        N.call("fsx_channel_progress", self._h, ch, C.byref(p), C.byref(c))
+        return p.value, c.value
+
     def merge(self, gpu: int, batch: N.MergeBatch, stream=None) -> None:
         N.call("fsx_merge", self._h, gpu, C.byref(batch), _stream_ptr(stream))
 
