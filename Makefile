@@ -53,8 +53,14 @@ build/ref_test_sidecar: $(FISSIM_REF_TESTS)/test_sidecar.cpp tests/cpp/shim_main
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ $(FISSIM_REF_TESTS)/test_sidecar.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 
+build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp \
+                         include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	    -o $@ tests/cpp/dropin_criterion4.cpp $(LINKFSX)
+
 cpptests: build/test_fabric
-	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then $(MAKE) -s build/ref_test_sidecar; fi
+	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
+	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -36,6 +36,16 @@ sys.path.insert(0, ROOT)
 CONFIG = "B"
 REQUESTS = 4
 CHUNK_ROWS = 1024  # one video frame = 7,340,032 B
+# --config selects another BASELINE.json merge workload (parity/extra lines; the
+# driver's default line is config B).
+CONFIGS = {
+    "A": {"requests": 64, "chunk_rows": None,
+          "workload": "A: InternVL3 image->text, mllm-chat trace (seed 42), 256 x 4096-d bf16 per image"},
+    "B": {"requests": 4, "chunk_rows": 1024,
+          "workload": "B: Qwen2.5-VL video->text, 16 frames x 1024 tokens x 3584-d bf16 per request"},
+    "D": {"requests": 32, "chunk_rows": 1024,
+          "workload": "D: servegen-like mixed image/video/audio trace (seed 42), 3584-d bf16"},
+}
 METRIC = "forwarded GB/s per producer->consumer pair vs 900 GB/s NVLink; merged req/s"
 
 
@@ -45,9 +55,12 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["fsx", "reference"], default="fsx")
-    p.add_argument("--requests", type=int, default=REQUESTS)
+    p.add_argument("--config", choices=sorted(CONFIGS), default="B")
+    p.add_argument("--requests", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--verify", action="store_true",
+                   help="N>1: consumers check the merged embeddings against a local pass")
     p.add_argument("--profile", action="store_true",
                    help="short run for ncu: no clocks, no cpu baseline, no e2e")
     return p.parse_args()
@@ -168,7 +181,8 @@ def cpu_baseline(min_seconds=10.0, max_passes=40):
     from paper_2603_12118_b200 import trace as T
 
     rules = T.RULES[CONFIG]
-    reqs = T.config_requests(CONFIG, 1)
+    reqs = cpu_sample(T)
+    payload = T.layout(reqs, rules.row_bytes).payload_bytes
     threads = os.cpu_count() or 1
     total_s, total_b, n, kind = 0.0, 0, 0, "reference"
     while total_s < min_seconds and n < max_passes:
@@ -178,11 +192,25 @@ def cpu_baseline(min_seconds=10.0, max_passes=40):
         n += 1
     return {"value": round(total_b / total_s / 1e9, 4), "unit": "GB/s", "cores": threads,
             "kind": kind,
-            "sample": (f"{n} passes of 1 config-B request (117,440,512 B video embedding): "
-                       "SidecarFabric::send_payload -> run_until_idle (reference, compiled unmodified, "
-                       f"single-threaded by construction) + CPU merge on {threads} threads; "
-                       f"{total_s:.1f} s of CPU work"),
-            "merged_req_per_s": round(n / total_s, 3)}
+            "sample": (f"{n} passes of {len(reqs)} config-{CONFIG} request(s) ({payload:,} B of "
+                       "embeddings per pass): SidecarFabric::send_payload -> run_until_idle "
+                       "(reference, compiled unmodified, single-threaded by construction) + CPU "
+                       f"merge on {threads} threads; {total_s:.1f} s of CPU work"),
+            "merged_req_per_s": round(n * len(reqs) / total_s, 3)}
+
+
+def cpu_sample(T):
+    """Bounded CPU sample of the workload: the first requests of the batch
+    whose embeddings add up to >= 100 MiB (one request for config B)."""
+    rules = T.RULES[CONFIG]
+    full = T.config_requests(CONFIG, REQUESTS)
+    out, acc = [], 0
+    for q in full:
+        out.append(q)
+        acc += q.placeholder_rows * rules.row_bytes
+        if acc >= 100 << 20:
+            break
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -195,7 +223,7 @@ def run_reference(args, rank):
 
     rules = T.RULES[CONFIG]
     threads = os.cpu_count() or 1
-    reqs = T.config_requests(CONFIG, 1)  # bounded sample per step: one request
+    reqs = cpu_sample(T)  # bounded sample per step (one request for config B)
     for _ in range(args.warmup):
         cpu_reference_pass(reqs, rules, threads)
     secs, nbytes, kind = 0.0, 0, "reference"
@@ -209,13 +237,15 @@ def run_reference(args, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "merged_req_per_s": round(args.steps / secs, 4),
-        "config": {"workload": "B: Qwen2.5-VL video->text, 16x1024x3584 bf16 per request",
-                   "requests_per_step": 1, "chunk_bytes": "single shot (reference has no chunking)",
+        "merged_req_per_s": round(args.steps * len(reqs) / secs, 4),
+        "config": {"workload": CONFIGS[CONFIG]["workload"],
+                   "requests_per_step": len(reqs),
+                   "chunk_bytes": "single shot (reference has no chunking)",
                    "parallelism": "reference CPU path, 1 process"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": kind,
-                         "sample": "each step: 1 config-B request forwarded through the reference "
-                                   "SidecarFabric (1 thread) + CPU merge on all host threads"},
+                         "sample": f"each step: {len(reqs)} config-{CONFIG} request(s) forwarded "
+                                   "through the reference SidecarFabric (1 thread) + CPU merge on "
+                                   "all host threads"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -338,10 +368,11 @@ def run_single(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (reference synth_payload bytes, K0 on device)",
         "merged_req_per_s": round(len(reqs) / (ms_step * 1e-3), 1),
-        "config": {"workload": "B: Qwen2.5-VL video->text, 16 frames x 1024 tokens x 3584-d bf16 "
-                               "per request, intra-device forward (producer == consumer GPU) + merge",
+        "config": {"workload": CONFIGS[CONFIG]["workload"] +
+                               ", intra-device forward (producer == consumer GPU) + merge",
                    "requests_per_step": len(reqs), "payload_bytes_per_step": payload,
-                   "chunk_bytes": CHUNK_ROWS * rules.row_bytes, "prompt_rows_per_step": lay.total_rows,
+                   "chunk_bytes": (CHUNK_ROWS or 0) * rules.row_bytes or "single shot",
+                   "prompt_rows_per_step": lay.total_rows,
                    "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush needed)"},
         "roofline": roofline,
         "kernels": kernels,
@@ -426,8 +457,19 @@ def run_pairs(args, rank, world):
     from paper_2603_12118_b200.fabric import DeviceFabric
 
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # FSX_PAIRS_DEVICE=<d> pins every rank to one device: the protocol test on
+    # a 1-GPU box (CUDA IPC works between processes of one device; NCCL does
+    # not allow that, so the setup/timing group is gloo there).
+    pinned = os.environ.get("FSX_PAIRS_DEVICE")
+    if pinned is not None:
+        local = int(pinned)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if pinned is None:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        red_dev = "cuda"
+    else:
+        dist.init_process_group("gloo")
+        red_dev = "cpu"
     me = PR.role(rank, world)
     P, Cg = me.producer_gpu, me.consumer_gpu
     rules = T.RULES[CONFIG]
@@ -459,7 +501,8 @@ def run_pairs(args, rank, world):
     offs = PR.exchange(None if (me.producer or me.alone) else batch.slab_off.tolist())
     if me.producer and not me.alone:
         batch.slab_off = np.array(offs[me.peer], dtype=np.int64)
-    chunks = [max(1, -(-it.rows // CHUNK_ROWS)) for it in lay.items]
+    chunk_rows = CHUNK_ROWS or max(1, max((it.rows for it in lay.items), default=1))
+    chunks = [max(1, -(-it.rows // chunk_rows)) for it in lay.items]
 
     def step(s):
         if me.alone:
@@ -474,7 +517,7 @@ def run_pairs(args, rank, world):
             for i, it in enumerate(lay.items):
                 fb, tok = sched[i]
                 fab.forward(P, base + int(batch.src_off[i]), Cg, int(batch.slab_off[i]),
-                            it.rows * batch.rb, CHUNK_ROWS * batch.rb, fb, stream, token=tok,
+                            it.rows * batch.rb, chunk_rows * batch.rb, fb, stream, token=tok,
                             host_notify=False)
         else:
             for i in range(len(lay.items)):
@@ -499,12 +542,25 @@ def run_pairs(args, rank, world):
             torch.cuda.synchronize()
         dist.barrier()
         launches = fab.stats()["kernel_launches"] - l0
+    verified = None
     if not me.producer or me.alone:
         st = batch.status_host()
         assert (st == 0).all(), st
-    ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device="cuda")
+        if args.verify:
+            # the pair-merged prompt embeddings must equal a local intra-device
+            # forward + merge of the same requests (both bit-exact to the oracle)
+            local_b = DataPlaneBatch(fab, reqs, rules, P, Cg, chunk_rows=CHUNK_ROWS)
+            local_b.synth_inputs()
+            assert local_b.alloc()
+            local_b.forward(host_notify=False)
+            local_b.merge()
+            torch.cuda.synchronize()
+            verified = bool(torch.equal(local_b.embeds, batch.embeds))
+            local_b.release()
+            assert verified, "pair-merged embeddings differ from the local reference pass"
+    ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    tot_launch = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    tot_launch = torch.tensor([launches], dtype=torch.float64, device=red_dev)
     dist.all_reduce(tot_launch)
     n_pairs = PR.pairs_in(world)
     payload_all = n_pairs * lay.payload_bytes * args.steps
@@ -517,15 +573,17 @@ def run_pairs(args, rank, world):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "merged_req_per_s": round(n_pairs * len(reqs) / (ms_step * 1e-3), 1),
-            "config": {"workload": "B: Qwen2.5-VL video->text, encoder GPU 2k -> LLM GPU 2k+1 "
-                                   "over NVLink (CUDA IPC slab), early-start merge on the consumer",
+            "config": {"workload": CONFIGS[CONFIG]["workload"] + ", encoder GPU 2k -> LLM GPU "
+                                   "2k+1 over NVLink (CUDA IPC slab), early-start merge on the consumer",
                        "requests_per_step_per_pair": len(reqs), "pairs": n_pairs,
-                       "chunk_bytes": CHUNK_ROWS * rules.row_bytes,
+                       "chunk_bytes": chunk_rows * rules.row_bytes,
                        "parallelism": f"{n_pairs} independent producer->consumer pairs"},
             "roofline": {"bound": "nvlink", "achieved": round(pair_gbs, 1), "peak": 900.0,
                          "unit": "GB/s", "frac": round(pair_gbs / 900.0, 4), "traffic": None,
                          "peak_kind": "nominal NVLink 5 per direction (measured peer copy ~770)"},
             "gpu_launches": int(tot_launch.item()),
+            "verified": bool(args.verify),
+            "pinned_device": pinned,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -535,7 +593,13 @@ def run_pairs(args, rank, world):
 
 
 def main():
+    global CONFIG, REQUESTS, CHUNK_ROWS
     args = parse()
+    CONFIG = args.config
+    REQUESTS = CONFIGS[CONFIG]["requests"]
+    CHUNK_ROWS = CONFIGS[CONFIG]["chunk_rows"]
+    if args.requests is None:
+        args.requests = REQUESTS
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     if args.impl == "reference":

@@ -57,6 +57,37 @@ def run_case(fab, name, src_gpu, dst_gpu, batch, row_bytes, steps=2000, slots=64
         e1.synchronize()
         ms = e0.elapsed_time(e1)
     assert torch.equal(out, rows)
+    # CUDA graph of one decode step (push + pull): the channel counters live
+    # on the device, so the same graph replays every step without host work.
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cs = torch.cuda.current_stream()
+        fab.channel_push(chs, rows.data_ptr(), row_bytes, cs)
+        fab.channel_pull(chs, out.data_ptr(), row_bytes, cs)
+    torch.cuda.synchronize()
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        for _ in range(20):
+            g.replay()
+        glat = []
+        for _ in range(min(steps, 500)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(gs)
+            g.replay()
+            e1.record(gs)
+            e1.synchronize()
+            glat.append(e0.elapsed_time(e1) * 1e3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(gs)
+        for _ in range(steps):
+            g.replay()
+        e1.record(gs)
+        e1.synchronize()
+        gms = e0.elapsed_time(e1)
+    assert torch.equal(out, rows)
+    graph = {"step_latency_us_p50": round(pct(glat, 50), 2),
+             "step_latency_us_p99": round(pct(glat, 99), 2),
+             "msgs_per_s": round(batch * steps / (gms * 1e-3), 1)}
     for ch in chs:
         fab.channel_close(ch)
     import oracle as O
@@ -71,7 +102,7 @@ def run_case(fab, name, src_gpu, dst_gpu, batch, row_bytes, steps=2000, slots=64
             "step_latency_us_p50": round(pct(lat, 50), 2), "step_latency_us_p99": round(pct(lat, 99), 2),
             "msgs_per_s": round(batch * steps / (ms * 1e-3), 1),
             "gbs": round(batch * steps * row_bytes / (ms * 1e-3) / 1e9, 3),
-            "launches_per_step": 2, "reference_cpu": ref}
+            "launches_per_step": 2, "cuda_graph": graph, "reference_cpu": ref}
 
 
 def main():

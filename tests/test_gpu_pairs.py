@@ -1,0 +1,39 @@
+"""The N>1 producer->consumer pair protocol end to end on ONE GPU: two
+processes (torchrun, gloo for setup), rank 0 pushes into rank 1's slab through
+a CUDA IPC mapping, rank 1 runs the early-start merge and acks each step into
+rank 0's ack slab.  Both ranks are pinned to device 0 (FSX_PAIRS_DEVICE), so
+this checks the protocol and the bytes, not NVLink bandwidth."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("config,requests", [("B", 1), ("A", 16)])
+def test_pairs_protocol_same_device(gpu, config, requests):
+    env = dict(os.environ, FSX_PAIRS_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", "bench.py", "--gpus", "2",
+           "--steps", "4", "--warmup", "2", "--config", config, "--requests", str(requests),
+           "--verify"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=400)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert lines, p.stdout[-2000:]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == 2 and d["verified"] and d["pinned_device"] == "0"
+    assert d["value"] > 0 and d["gpu_launches"] > 0
