@@ -296,9 +296,6 @@ def run_single(args):
         e2 = torch.cuda.Event(enable_timing=True) if record else None
         fork, scanned = torch.cuda.Event(), torch.cuda.Event()
         fork.record(stream)
-        side.wait_event(fork)
-        batch.scan(side)              # K3 phase 1 needs only token ids: overlaps K1
-        scanned.record(side)
         if record:
             e0.record(stream)
         # K1: 4 items x 16 flagged per-frame chunks; the consumer (K3) is
@@ -306,6 +303,11 @@ def run_single(args):
         batch.forward(stream, host_notify=False)
         if record:
             e1.record(stream)
+        # K3 phase 1 needs only token ids: issued after K1 so K1's CTAs are
+        # dispatched first, it fills SMs as K1 drains and is done before K3b
+        side.wait_event(fork)
+        batch.scan(side)
+        scanned.record(side)
         stream.wait_event(scanned)
         batch.merge(stream, mode=N.MERGE_COPY_ONLY)  # K3 phase 2: the row moves
         if record:

@@ -145,6 +145,8 @@ typedef struct fsx_transfer {
   int64_t chunk_bytes;
   int64_t flag_base;
   uint64_t token;
+  uint64_t* d_digest; /* optional device u64 (zeroed, see fsx_u64_slot): += dg64 of
+                         the bytes, fused into K1 (see fsx_digest) */
 } fsx_transfer;
 int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t options, void* stream);
 /* Same contract for a HOST source span (the reference send(span) path,
@@ -242,6 +244,22 @@ int fsx_channel_progress(fsx_fabric* f, int32_t channel, uint64_t* produced, uin
  * reference stream.  Used by producers/tests/bench to create inputs. */
 int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_t n,
                       void* stream);
+
+/* ---- integrity digest -------------------------------------
+ * checksum64 (common.hpp:221-241) is a serial chain; on the device hop fsx
+ * uses dg64, a lane-parallel, position-sensitive digest:
+ *   dg64 = n * 0x9e3779b97f4a7c15 + sum_k f(w_k ^ (k + 1) * 0xbf58476d1ce4e5b9) mod 2^64
+ *   f(x) = y ^ (y >> 29), y = x * 0x94d049bb133111eb,
+ * w_k the k-th little-endian 8-byte word (last one zero-padded).  K1 computes it
+ * for free while copying (fsx_transfer.d_digest); fsx_digest recomputes it
+ * over any device range (consumer-side verification of a slab segment).
+ *   fsx_digest: async, *d_accum += dg64(d_ptr[0..n)) on gpu's device.
+ *   fsx_u64_slot: a zeroed device u64 from a per-device ring (zeroed on stream).
+ *   fsx_read_u64: synchronous read of a device u64 through `stream`. */
+int fsx_digest(fsx_fabric* f, int gpu, const void* d_ptr, int64_t n, uint64_t* d_accum,
+               void* stream);
+int fsx_u64_slot(fsx_fabric* f, int gpu, uint64_t** d_slot, void* stream);
+int fsx_read_u64(fsx_fabric* f, int gpu, const uint64_t* d, uint64_t* h, void* stream);
 
 /* ---- host helpers -----------------------------------------------------------
  * Device ordinal owning p, or -1 for host / unregistered memory (never fails).

@@ -103,6 +103,20 @@ inline uint64_t checksum64(const uint8_t* p, size_t n) {
   return h ^ (h >> 32);
 }
 
+// dg64, the lane-parallel device digest (include/fsx.h): host form, used for
+// host-span payloads whose bytes never pass through K1's registers.
+inline uint64_t digest64(const uint8_t* p, size_t n) {
+  uint64_t h = static_cast<uint64_t>(n) * 0x9e3779b97f4a7c15ull;
+  for (size_t k = 0; k * 8 < n; ++k) {
+    uint64_t w = 0;
+    const size_t take = n - k * 8 < 8 ? n - k * 8 : 8;
+    std::memcpy(&w, p + k * 8, take);  // little-endian host, zero-padded tail
+    const uint64_t y = (w ^ (static_cast<uint64_t>(k + 1) * 0xbf58476d1ce4e5b9ull)) * 0x94d049bb133111ebull;
+    h += y ^ (y >> 29);
+  }
+  return h;
+}
+
 // Status codes of the C ABI are 1 + fissim::ErrorCode ordinal.
 namespace status {
 constexpr int kValidation = FSX_E_VALIDATION;
@@ -246,7 +260,9 @@ class Fabric {
                        [this, shared] { handle_network(shared->env, std::move(shared->bytes)); });
       return;
     }
-    ps.env.checksum = 0;  // local: NVLink/HBM hop, no serial host checksum
+    // local: the envelope carries dg64 (set while placing: fused into K1 for
+    // device payloads, host digest for host spans), not the serial checksum64
+    ps.env.checksum = 0;
     if (!place_local(ps)) {
       own_bytes(ps);  // borrowed span dies with the call: keep the bytes for the backlog
       const int slab = ps.env.dst_gpu;
@@ -402,15 +418,36 @@ class Fabric {
     *n_chunks = cb ? static_cast<int32_t>((n + cb - 1) / cb) : 1;
     check(fsx_flags_alloc(h_, dst, *n_chunks, flag_base));
     *token = 0;
-    if (ps.src_is_device)
-      check(fsx_forward(h_, ps.env.src_gpu, ps.src, dst, *off, n, cb, *flag_base, token, nullptr));
-    else
+    const bool local = Traits::is_local(ps.env);
+    if (ps.src_is_device) {
+      // K1, with the dg64 digest of the source fused into the copy
+      fsx_transfer t{ps.env.src_gpu, dst, ps.src, *off, n, cb, *flag_base, 0, nullptr};
+      if (local) check(fsx_u64_slot(h_, ps.env.src_gpu, &t.d_digest, nullptr));
+      check(fsx_forward_batch(h_, 1, &t, FSX_FWD_HOST_NOTIFY, nullptr));
+      *token = t.token;
+      digest_slot_ = t.d_digest;
+    } else {
+      if (local) ps.env.checksum = digest64(ps.src, static_cast<size_t>(n));
       check(fsx_forward_host(h_, ps.src, dst, *off, n, cb, *flag_base, token, nullptr));
+      digest_slot_ = nullptr;
+    }
     return true;
   }
 
   void wait_landed(int dst, int64_t flag_base, int32_t n_chunks, uint64_t token) {
     check(fsx_wait(h_, dst, flag_base, n_chunks, token, config_.wait_timeout_us));
+  }
+
+  // dg64 of a delivered slab segment, recomputed on the consumer GPU.
+  uint64_t slab_digest(int gpu, int64_t off, int64_t n) {
+    uint64_t* slot = nullptr;
+    check(fsx_u64_slot(h_, gpu, &slot, nullptr));
+    void* p = nullptr;
+    check(fsx_slab_ptr(h_, gpu, off, &p));
+    check(fsx_digest(h_, gpu, p, n, slot, nullptr));
+    uint64_t v = 0;
+    check(fsx_read_u64(h_, gpu, slot, &v, nullptr));
+    return v;
   }
 
   // sidecar.hpp:465-483: place now, notify after the modeled latency.
@@ -424,6 +461,7 @@ class Fabric {
     // reference's memcpy into the arena (sidecar.hpp:470).  The batched C ABI
     // (fsx_forward on a stream) is the asynchronous path.
     wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    if (digest_slot_) check(fsx_read_u64(h_, ps.env.src_gpu, digest_slot_, &ps.env.checksum, nullptr));
     ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
     const double lat = config_.latency_ms(Transport::LocalBuffer, ps.env.chunk_bytes);
     added_latency_ms_ += lat;
@@ -491,11 +529,15 @@ class Fabric {
         st.raw_cb(env, off);
         continue;
       }
+      // Verify before handing the bytes over, like sidecar.hpp:545-557: the
+      // device hop is checked with dg64 recomputed on the consumer GPU over
+      // the slab segment, the network hop with the reference checksum64.
+      const bool local = Traits::is_local(env);
+      const bool dev_ok = !local || slab_digest(env.dst_gpu, off, env.chunk_bytes) == env.checksum;
       std::vector<uint8_t> bytes(static_cast<size_t>(env.chunk_bytes));
       if (env.chunk_bytes > 0)
         check(fsx_slab_read(h_, env.dst_gpu, off, bytes.data(), env.chunk_bytes, nullptr));
-      const bool verify = !Traits::is_local(env);
-      const bool ok = !verify || checksum64(bytes.data(), bytes.size()) == env.checksum;
+      const bool ok = local ? dev_ok : checksum64(bytes.data(), bytes.size()) == env.checksum;
       release_segment(env.dst_gpu, off);
       place_backlog(env.dst_gpu);
       if (!ok) {
@@ -562,6 +604,7 @@ class Fabric {
   std::map<int, int> topo_;
   SidecarConfig config_;
   fsx_fabric* h_ = nullptr;
+  uint64_t* digest_slot_ = nullptr;  // K1 digest of the send being placed
   std::vector<int> slabs_;
   std::map<std::string, RefState> refs_;
   std::map<int, std::deque<Pending>> backlog_;

@@ -71,6 +71,18 @@ void or_synth_payload_into(uint64_t seed, uint8_t* out, size_t n) {
   }
 }
 
+/* fsx dg64 (include/fsx.h): n*G + sum over LE words of f(w ^ (k+1)*C1). */
+uint64_t or_digest64(const uint8_t* data, size_t len) {
+  uint64_t h = (uint64_t)len * 0x9e3779b97f4a7c15ull;
+  for (size_t k = 0; k * 8 < len; ++k) {
+    uint64_t w = 0;
+    for (size_t b = 0; b < 8 && k * 8 + b < len; ++b) w |= (uint64_t)data[k * 8 + b] << (8 * b);
+    uint64_t y = (w ^ ((uint64_t)(k + 1) * 0xbf58476d1ce4e5b9ull)) * 0x94d049bb133111ebull;
+    h += y ^ (y >> 29);
+  }
+  return h;
+}
+
 /* executor_sim.hpp:231-233 */
 uint64_t or_payload_seed(const char* ref_id, size_t n, int64_t seq) {
   return or_fnv1a64(ref_id, n) ^ (0x9e3779b97f4a7c15ull * (uint64_t)(seq + 1));

@@ -36,6 +36,11 @@ uint64_t or_fnv1a64(const char* s, size_t n);
 uint64_t or_checksum64(const uint8_t* data, size_t len);
 /* common.hpp:247-259 */
 void or_synth_payload_into(uint64_t seed, uint8_t* out, size_t n);
+/* fsx dg64 device digest (fsx's own definition, include/fsx.h "integrity
+ * digest"; NOT a reference function -- the reference's checksum64 is serial).
+ * Plain sequential restatement used to check the fused K1 digest and
+ * fsx_digest bit-exactly. */
+uint64_t or_digest64(const uint8_t* data, size_t len);
 /* executor_sim.hpp:231-233 */
 uint64_t or_payload_seed(const char* ref_id, size_t n, int64_t seq);
 

@@ -58,6 +58,8 @@ def _load_c():
     lib.or_checksum64.argtypes = [C_.c_void_p, C_.c_size_t]
     lib.or_synth_payload_into.restype = None
     lib.or_synth_payload_into.argtypes = [C_.c_uint64, C_.c_void_p, C_.c_size_t]
+    lib.or_digest64.restype = C_.c_uint64
+    lib.or_digest64.argtypes = [C_.c_void_p, C_.c_size_t]
     lib.or_payload_seed.restype = C_.c_uint64
     lib.or_payload_seed.argtypes = [C_.c_char_p, C_.c_size_t, C_.c_int64]
     lib.or_shape_rules_default.argtypes = [C_.POINTER(ShapeRules)]

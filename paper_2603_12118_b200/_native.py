@@ -83,6 +83,7 @@ class Transfer(C.Structure):
         ("chunk_bytes", C.c_int64),
         ("flag_base", C.c_int64),
         ("token", C.c_uint64),
+        ("d_digest", C.c_void_p),
     ]
 
 
@@ -136,6 +137,9 @@ _SIGS = {
     "fsx_channel_pull": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_channel_progress": [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "fsx_synth_payload": [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_digest": [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
+    "fsx_u64_slot": [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_void_p],
+    "fsx_read_u64": [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
     "fsx_pointer_device": [C.c_void_p, C.POINTER(C.c_int)],
     "fsx_copy_to_host": [C.c_void_p, C.c_void_p, C.c_int64],
     "fsx_get_stats": [C.c_void_p, C.POINTER(Stats)],

@@ -96,10 +96,53 @@ __device__ __forceinline__ uint64_t splitmix_word(uint64_t s0, uint64_t k) {
 // 16-byte aligned, so every 16-byte-aligned offset is a legal vector.  All
 // loads of a batch are issued before its stores (kFwdUnroll x 16 B per lane in
 // flight).
+// fsx integrity digest dg64 (replaces the serial checksum64 of
+// common.hpp:221-241 on the device hop): with w_k the k-th little-endian
+// 8-byte word of the payload (the last one zero-padded) and n its length,
+//   dg64 = n * 0x9e3779b97f4a7c15 + sum_k f(w_k ^ (k + 1) * 0xbf58476d1ce4e5b9)  (mod 2^64)
+//   f(x) = y ^ (y >> 29), y = x * 0x94d049bb133111eb
+// Every term is independent (order-free sum, position folded into the word),
+// so any partition of the bytes can be digested in parallel and combined with
+// one atomic add; a flipped bit, a dropped or a swapped word changes it.
+__device__ __forceinline__ uint64_t dg_word(uint64_t w, uint64_t k) {
+  const uint64_t y = (w ^ ((k + 1) * 0xbf58476d1ce4e5b9ull)) * 0x94d049bb133111ebull;
+  return y ^ (y >> 29);
+}
+
+__device__ __forceinline__ uint64_t dg_vec(const uint4& v, uint64_t word) {
+  const uint64_t lo = (uint64_t)v.x | ((uint64_t)v.y << 32);
+  const uint64_t hi = (uint64_t)v.z | ((uint64_t)v.w << 32);
+  return dg_word(lo, word) + dg_word(hi, word + 1);
+}
+
+// digest of the words that start in [from, end) of a buffer whose byte 0 is
+// word 0 (zero padding past `end`), read byte-wise
+__device__ __forceinline__ uint64_t dg_bytes(const uint8_t* p, int64_t from, int64_t end) {
+  uint64_t acc = 0;
+  for (int64_t w = from >> 3; w * 8 < end; ++w) {
+    uint64_t v = 0;
+    for (int b = 0; b < 8 && w * 8 + b < end; ++b) v |= (uint64_t)p[w * 8 + b] << (8 * b);
+    acc += dg_word(v, (uint64_t)w);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Copy [beg, end) of src into dst with one warp; `vec` means src and dst are
+// 16-byte aligned (and beg is a multiple of 16), so every 16-byte-aligned
+// offset is a legal vector.  All loads of a batch are issued before its
+// stores (U x 16 B per lane in flight).  With `dig`, the lane also digests the
+// words it moved (returned per lane; lane 0 adds the byte tail).
 template <int U>
-__device__ __forceinline__ void warp_copy_range(const uint8_t* __restrict__ src,
-                                                uint8_t* __restrict__ dst, int64_t beg,
-                                                int64_t end, bool vec, int lane) {
+__device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ src,
+                                                    uint8_t* __restrict__ dst, int64_t beg,
+                                                    int64_t end, bool vec, bool dig, int lane) {
+  uint64_t acc = 0;
   if (vec) {
     const int64_t vbeg = (beg + 15) & ~int64_t{15};
     const int64_t vend = end & ~int64_t{15};
@@ -107,6 +150,7 @@ __device__ __forceinline__ void warp_copy_range(const uint8_t* __restrict__ src,
       const uint4* s = reinterpret_cast<const uint4*>(src + vbeg);
       uint4* d = reinterpret_cast<uint4*>(dst + vbeg);
       const int64_t nv = (vend - vbeg) >> 4;
+      const uint64_t w0 = (uint64_t)(vbeg >> 3);
       for (int64_t base = 0; base < nv; base += 32 * U) {
         uint4 r[U];
 #pragma unroll
@@ -119,13 +163,23 @@ __device__ __forceinline__ void warp_copy_range(const uint8_t* __restrict__ src,
           const int64_t i = base + k * 32 + lane;
           if (i < nv) st_v4(d + i, r[k]);
         }
+        if (dig) {
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int64_t i = base + k * 32 + lane;
+            if (i < nv) acc += dg_vec(r[k], w0 + 2 * (uint64_t)i);
+          }
+        }
       }
       for (int64_t i = beg + lane; i < vbeg && i < end; i += 32) dst[i] = src[i];
       for (int64_t i = vend + lane; i < end; i += 32) dst[i] = src[i];
-      return;
+      if (dig && lane == 0 && vend < end) acc += dg_bytes(src, vend, end);
+      return acc;
     }
   }
   for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
+  if (vec && dig && lane == 0) acc += dg_bytes(src, beg, end);  // < 16-byte unit
+  return acc;  // unaligned path: the runtime digests the source separately
 }
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bool sys) {
@@ -162,7 +216,15 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
     const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
     const int64_t beg = cbeg + s * a.slice;
     const int64_t end = min(beg + a.slice, cend);
-    warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, lane);
+    const bool dig = a.digest != nullptr;
+    uint64_t acc = warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, dig, lane);
+    if (dig) {  // fused dg64: one atomic per unit, ordered before the counter release
+      acc = warp_sum_u64(acc);
+      if (lane == 0) {
+        if (u == 0) acc += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.digest), (unsigned long long)acc);
+      }
+    }
     __syncwarp();
     if (lane == 0) {
       const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
@@ -185,6 +247,30 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
       }
     }
   }
+}
+
+// Stand-alone dg64 of n device bytes, accumulated into *out (zeroed by the
+// caller): consumer-side verification of a delivered slab segment, and the
+// producer digest when K1 ran its unaligned byte path.
+__global__ void __launch_bounds__(256) digest_kernel(const uint8_t* __restrict__ p, int64_t n,
+                                                     uint64_t* out) {
+  uint64_t acc = 0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t tail_from = 0;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const int64_t nv = n >> 4;
+    const uint4* v = reinterpret_cast<const uint4*>(p);
+    for (int64_t i = tid; i < nv; i += stride) acc += dg_vec(ld_v4(v + i), 2 * (uint64_t)i);
+    tail_from = nv << 4;
+  } else {
+    const int64_t nw = n >> 3;  // whole words, byte-assembled
+    for (int64_t w = tid; w < nw; w += stride) acc += dg_bytes(p, w * 8, w * 8 + 8);
+    tail_from = nw << 3;
+  }
+  if (tid == 0) acc += dg_bytes(p, tail_from, n) + (uint64_t)n * 0x9e3779b97f4a7c15ull;
+  acc = warp_sum_u64(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)acc);
 }
 
 __global__ void set_flags_kernel(FlagSetArgs a) {
@@ -602,6 +688,11 @@ __global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, u
 }
 
 constexpr int kTmaStages = 4;
+
+cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, cudaStream_t st) {
+  digest_kernel<<<grid, 256, 0, st>>>(p, n, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st) {
   if (s.n <= 0) return cudaSuccess;

@@ -26,6 +26,7 @@ struct FwdArgs {
   uint64_t* dflags;    // [n_chunks] consumer-device flags (may be peer memory)
   uint64_t* hflags;    // [n_chunks] mapped pinned host flags, or nullptr
   uint64_t token;
+  uint64_t* digest;    // optional: += dg64 of the bytes (vec path; see fsx_kernels.cu)
 };
 
 // Up to kFwdMaxBatch transfers of one source device in one K1 launch (kernel
@@ -67,6 +68,7 @@ struct ChanStep {
 };
 
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
+cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, cudaStream_t st);
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);

@@ -160,9 +160,17 @@ struct Device {
   int merge_grid = 0;
   uint64_t* state = nullptr;  // channel head/tail counters (kStatePool u64)
   int64_t state_next = 0;
+  uint64_t* scratch = nullptr;  // short-lived u64 slots (digests), ring
+  Ring scratch_ring;
 };
 
 constexpr int64_t kStatePool = 1 << 16;
+constexpr int64_t kScratchRing = 1 << 14;
+
+int digest_grid(const Device* d, int64_t n) {
+  const int64_t want = (n / 16 + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)d->sms * 8));
+}
 
 // A streaming channel: one producer->consumer stream (a streaming DataRef,
 // e.g. one request's thinker hidden states) delivered in seq order through a
@@ -306,6 +314,7 @@ int fsx_close(fsx_fabric* f) {
     cudaSetDevice(o);
     if (d->counters) cudaFree(d->counters);
     if (d->state) cudaFree(d->state);
+    if (d->scratch) cudaFree(d->scratch);
     if (d->stream) cudaStreamDestroy(d->stream);
   }
   delete f;
@@ -569,6 +578,9 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
       if (x.token == 0) x.token = f->next_token.fetch_add(1);
       a.token = x.token;
+      // the fused digest needs the 16-byte path; otherwise digest the source
+      // with a separate pass after the copy (below)
+      a.digest = a.vec ? x.d_digest : nullptr;
       b.unit_off[k + 1] = b.unit_off[k] + a.total_units;
       f->bytes_forwarded += x.bytes;
       f->forwards++;
@@ -578,7 +590,74 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
                                             dev->fwd_grid);
     FSX_CUDA(fsx::launch_forward(b, fwd_variant(), grid, st));
     f->launches++;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const fsx_transfer& x = t[first + k];
+      if (x.d_digest && !b.t[k].vec) {
+        FSX_CUDA(fsx::launch_digest(static_cast<const uint8_t*>(x.d_src), x.bytes, x.d_digest,
+                                    digest_grid(dev, x.bytes), st));
+        f->launches++;
+      }
+    }
   }
+  return FSX_OK;
+}
+
+int fsx_digest(fsx_fabric* f, int gpu, const void* d_ptr, int64_t n, uint64_t* d_accum,
+               void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, gpu, &ordinal);
+  if (rc) return rc;
+  if (n < 0 || !d_accum) return fail(FSX_E_VALIDATION, "bad digest range");
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  FSX_CUDA(fsx::launch_digest(static_cast<const uint8_t*>(d_ptr), n, d_accum, digest_grid(dev, n),
+                              pick_stream(dev, stream)));
+  f->launches++;
+  return FSX_OK;
+}
+
+int fsx_u64_slot(fsx_fabric* f, int gpu, uint64_t** d_slot, void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, gpu, &ordinal);
+  if (rc) return rc;
+  Device* dev = nullptr;
+  uint64_t* slot = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+    if (!dev->scratch) {
+      FSX_CUDA(cudaSetDevice(ordinal));
+      FSX_CUDA(cudaMalloc(&dev->scratch, kScratchRing * sizeof(uint64_t)));
+      dev->scratch_ring.size = kScratchRing;
+    }
+    slot = dev->scratch + dev->scratch_ring.take(1);
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  FSX_CUDA(cudaMemsetAsync(slot, 0, sizeof(uint64_t), pick_stream(dev, stream)));
+  *d_slot = slot;
+  return FSX_OK;
+}
+
+int fsx_read_u64(fsx_fabric* f, int gpu, const uint64_t* d, uint64_t* h, void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, gpu, &ordinal);
+  if (rc) return rc;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  cudaStream_t st = pick_stream(dev, stream);
+  FSX_CUDA(cudaMemcpyAsync(h, d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  FSX_CUDA(cudaStreamSynchronize(st));
   return FSX_OK;
 }
 

@@ -152,8 +152,9 @@ class DeviceFabric:
         chunk_bytes, flag_base, token); returns the tokens used."""
         n = len(transfers)
         arr = (N.Transfer * max(n, 1))()
-        for i, (sg, sp, dg, do, nb, cb, fb, tok) in enumerate(transfers):
-            arr[i] = N.Transfer(sg, dg, sp, do, nb, cb, fb, tok)
+        for i, t in enumerate(transfers):
+            sg, sp, dg, do, nb, cb, fb, tok = t[:8]
+            arr[i] = N.Transfer(sg, dg, sp, do, nb, cb, fb, tok, t[8] if len(t) > 8 else None)
         N.call("fsx_forward_batch", self._h, n, arr, N.FWD_HOST_NOTIFY if host_notify else 0,
                _stream_ptr(stream))
         return [arr[i].token for i in range(n)]
@@ -164,6 +165,23 @@ class DeviceFabric:
         N.call("fsx_forward_host", self._h, host_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
                flag_base, C.byref(tok), _stream_ptr(stream))
         return tok.value
+
+    # -- dg64 integrity digest ---------------------------------------------------
+    def u64_slot(self, gpu: int, stream=None) -> int:
+        p = C.c_void_p()
+        N.call("fsx_u64_slot", self._h, gpu, C.byref(p), _stream_ptr(stream))
+        return p.value
+
+    def read_u64(self, gpu: int, ptr: int, stream=None) -> int:
+        v = C.c_uint64()
+        N.call("fsx_read_u64", self._h, gpu, ptr, C.byref(v), _stream_ptr(stream))
+        return v.value
+
+    def digest(self, gpu: int, ptr: int, nbytes: int, stream=None) -> int:
+        """dg64 of device bytes (synchronous convenience)."""
+        slot = self.u64_slot(gpu, stream)
+        N.call("fsx_digest", self._h, gpu, ptr, nbytes, slot, _stream_ptr(stream))
+        return self.read_u64(gpu, slot, stream)
 
     # -- streaming channels (config C) ---------------------------------------
     def channel_open(self, src_gpu: int, dst_gpu: int, row_bytes: int, slots: int = 64) -> int:

@@ -141,6 +141,34 @@ TEST_CASE("device payloads take the K1 path and land byte-exact") {
   CHECK(f.stats().segments_in_use == 0);
 }
 
+TEST_CASE("local envelopes carry the dg64 digest of the payload") {
+  for (size_t n : {size_t{0}, size_t{3}, size_t{8}, size_t{4097}, size_t{1} << 20}) {
+    auto p = synth(n + 1, n);
+    CHECK(fsx::digest64(p.data(), n) == or_digest64(p.data(), n));
+  }
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  for (bool device : {false, true}) {
+    const size_t n = 777777;
+    const std::string id = std::string("req-d/r") + (device ? "1" : "0");
+    auto payload = synth(seed_of(id), n);
+    DeviceBuffer d(n);
+    REQUIRE(cudaMemcpy(d.p, payload.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
+    Got g;
+    collect(f, 2, id, g);
+    const uint8_t* src = device ? static_cast<const uint8_t*>(d.p) : payload.data();
+    k.post("send", [&, id, src] {
+      f.send_payload("req-d", ref_of(id, n), 0, 2, std::span<const uint8_t>(src, n));
+    });
+    k.run_until_idle();
+    REQUIRE(g.envs.size() == 1);
+    CHECK(g.envs[0].checksum == or_digest64(payload.data(), n));
+    CHECK(g.chunks[0] == payload);
+    CHECK(!g.error);
+  }
+  CHECK(f.stats().integrity_errors == 0);
+}
+
 TEST_CASE("raw interest reads the slab in place and frees on ack") {
   EventLoop k;
   SidecarFabric f(k, two_nodes());

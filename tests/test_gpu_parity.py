@@ -145,6 +145,42 @@ def test_forward_batch_mixed(fab, oracle_mod):
         fab.slab_free(d, off)
 
 
+@pytest.mark.parametrize("n,chunk,shift", [(0, 0, 0), (5, 0, 0), (4096, 0, 0), (4099, 0, 0),
+                                           (1 << 20, 65536, 0), (7_340_032 * 2 + 40, 7_340_032, 0),
+                                           (100_003, 0, 3), (65536 + 9, 4096, 8)])
+def test_fused_digest_matches_oracle(fab, oracle_mod, n, chunk, shift):
+    """dg64 fused into K1 (aligned path) or the fallback pass (unaligned), and
+    fsx_digest over the delivered slab segment, equal the oracle restatement."""
+    torch = _torch()
+    seed = 4242 + n
+    src = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
+    fab.synth(0, seed, src.data_ptr() + shift, n)
+    want = oracle_mod.C.or_digest64(oracle_mod.synth_payload(seed, n), n)
+    off = fab.slab_alloc(1, n)
+    nch = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
+    fb = fab.flags_alloc(1, nch)
+    slot = fab.u64_slot(0)
+    (tok,) = fab.forward_batch([(0, src.data_ptr() + shift, 1, off, n, chunk, fb, 0, slot)])
+    fab.wait(1, fb, nch, tok, timeout_us=20_000_000)
+    torch.cuda.synchronize()
+    assert fab.read_u64(0, slot) == want
+    assert fab.digest(1, fab.slab_ptr(1, off), n) == want
+    fab.slab_free(1, off)
+
+
+def test_digest_detects_corruption(fab, oracle_mod):
+    torch = _torch()
+    buf = torch.empty(1 << 16, dtype=torch.uint8, device="cuda")
+    fab.synth(0, 9, buf.data_ptr(), buf.numel())
+    d0 = fab.digest(0, buf.data_ptr(), buf.numel())
+    buf[1000] ^= 1
+    assert fab.digest(0, buf.data_ptr(), buf.numel()) != d0
+    buf[1000] ^= 1
+    swapped = torch.cat([buf[32768:], buf[:32768]])
+    assert fab.digest(0, swapped.data_ptr(), swapped.numel()) != d0
+    assert fab.digest(0, buf.data_ptr(), buf.numel()) == d0
+
+
 def test_forward_host_span_path(fab, oracle_mod):
     for n, chunk in [(0, 0), (1, 0), (4097, 0), (3 << 20, 1 << 20)]:
         payload = np.frombuffer(oracle_mod.synth_payload(n + 11, n), np.uint8).copy()
