@@ -53,6 +53,17 @@ build/ref_test_sidecar: $(FISSIM_REF_TESTS)/test_sidecar.cpp tests/cpp/shim_main
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ $(FISSIM_REF_TESTS)/test_sidecar.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 
+# The reference's executor and dispatcher unit tests (encoder/LLM/talker/
+# generator executors and the TaskDispatcher wired through the sidecar), also
+# compiled unmodified against the drop-in.
+build/ref_test_executors: $(FISSIM_REF_TESTS)/test_executor_sim.cpp $(FISSIM_REF_TESTS)/test_dispatcher.cpp \
+                          tests/cpp/shim_main.cpp include/fsx/fabric.hpp \
+                          include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) -o $@ \
+	    $(FISSIM_REF_TESTS)/test_executor_sim.cpp $(FISSIM_REF_TESTS)/test_dispatcher.cpp \
+	    tests/cpp/shim_main.cpp $(LINKFSX)
+
 build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp \
                          include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
 	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
@@ -60,7 +71,7 @@ build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp 
 
 cpptests: build/test_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
-	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4; fi
+	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -56,6 +56,9 @@ const char* fsx_last_error(void);
 const char* fsx_version(void);
 /* Number of visible CUDA devices (0 on a GPU-less host; never a fallback). */
 int fsx_device_count(int* n);
+/* sizeof of the ABI structs (fsx_merge_batch, fsx_transfer, fsx_stats), so
+ * bindings can check their layouts without a GPU. */
+int fsx_abi_sizes(int32_t* merge_batch, int32_t* transfer, int32_t* stats);
 
 /* ---- fabric lifetime ------------------------------------------------------
  * Replaces SidecarFabric(SimKernel&, std::map<int,int> gpu_to_node, SidecarConfig)
@@ -84,6 +87,12 @@ int fsx_slab_register(fsx_fabric* f, int gpu, int64_t bytes);
 int fsx_slab_alloc(fsx_fabric* f, int gpu, int64_t len, int64_t* off);
 /* NodeArena::free_seg (sidecar.hpp:165-186): FSX_E_INTERNAL on double free. */
 int fsx_slab_free(fsx_fabric* f, int gpu, int64_t off);
+/* Batch forms for a whole request batch (one call instead of one per item):
+ * alloc_n is all-or-nothing (offs[i] = -1 for every i when the batch does not
+ * fit, nothing held); free_n frees every offset (FSX_E_INTERNAL on the first
+ * double free, after freeing the rest). */
+int fsx_slab_alloc_n(fsx_fabric* f, int gpu, int32_t n, const int64_t* lens, int64_t* offs);
+int fsx_slab_free_n(fsx_fabric* f, int gpu, int32_t n, const int64_t* offs);
 /* NodeArena::data (sidecar.hpp:188), as a device pointer into the slab. */
 int fsx_slab_ptr(fsx_fabric* f, int gpu, int64_t off, void** d_ptr);
 /* NodeArena::segments_in_use / bytes_in_use / peak_bytes / capacity

@@ -87,6 +87,19 @@ class Transfer(C.Structure):
     ]
 
 
+def _transfer_dtype():
+    import numpy as np
+
+    kinds = {C.c_int32: "<i4", C.c_void_p: "<u8", C.c_int64: "<i8", C.c_uint64: "<u8"}
+    return np.dtype({"names": [n for n, _ in Transfer._fields_],
+                     "formats": [kinds[t] for _, t in Transfer._fields_],
+                     "offsets": [getattr(Transfer, n).offset for n, _ in Transfer._fields_],
+                     "itemsize": C.sizeof(Transfer)})
+
+
+TRANSFER_DTYPE = _transfer_dtype()
+
+
 class Stats(C.Structure):
     _fields_ = [
         ("forwards", C.c_int64),
@@ -102,6 +115,7 @@ class Stats(C.Structure):
 # name -> (argtypes); every function returns int status except the two strings.
 _SIGS = {
     "fsx_device_count": [C.POINTER(C.c_int)],
+    "fsx_abi_sizes": [C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
     "fsx_open": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)],
     "fsx_close": [C.c_void_p],
     "fsx_node_of": [C.c_void_p, C.c_int, C.POINTER(C.c_int)],
@@ -110,6 +124,8 @@ _SIGS = {
     "fsx_slab_register": [C.c_void_p, C.c_int, C.c_int64],
     "fsx_slab_alloc": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_int64)],
     "fsx_slab_free": [C.c_void_p, C.c_int, C.c_int64],
+    "fsx_slab_alloc_n": [C.c_void_p, C.c_int, C.c_int32, C.c_void_p, C.c_void_p],
+    "fsx_slab_free_n": [C.c_void_p, C.c_int, C.c_int32, C.c_void_p],
     "fsx_slab_ptr": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_void_p)],
     "fsx_slab_usage": [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)],

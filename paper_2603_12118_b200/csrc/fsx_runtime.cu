@@ -254,6 +254,13 @@ int fsx_device_count(int* n) {
   return FSX_OK;
 }
 
+int fsx_abi_sizes(int32_t* merge_batch, int32_t* transfer, int32_t* stats) {
+  *merge_batch = (int32_t)sizeof(fsx_merge_batch);
+  *transfer = (int32_t)sizeof(fsx_transfer);
+  *stats = (int32_t)sizeof(fsx_stats);
+  return FSX_OK;
+}
+
 int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* devices,
              fsx_fabric** out) {
   *out = nullptr;
@@ -390,6 +397,31 @@ int fsx_slab_free(fsx_fabric* f, int gpu, int64_t off) {
   if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
   if (!s->blocks.release(off)) return fail(FSX_E_INTERNAL, "double free in slab");
   return FSX_OK;
+}
+
+int fsx_slab_alloc_n(fsx_fabric* f, int gpu, int32_t n, const int64_t* lens, int64_t* offs) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  if (s->imported) return fail(FSX_E_CONFIG, "imported slabs are allocated by their owner");
+  for (int32_t i = 0; i < n; ++i) {
+    offs[i] = s->blocks.alloc(lens[i]);
+    if (offs[i] < 0) {
+      for (int32_t j = 0; j < i; ++j) s->blocks.release(offs[j]);
+      for (int32_t j = 0; j < n; ++j) offs[j] = -1;
+      return FSX_OK;
+    }
+  }
+  return FSX_OK;
+}
+
+int fsx_slab_free_n(fsx_fabric* f, int gpu, int32_t n, const int64_t* offs) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+  bool ok = true;
+  for (int32_t i = 0; i < n; ++i) ok = s->blocks.release(offs[i]) && ok;
+  return ok ? FSX_OK : fail(FSX_E_INTERNAL, "double free in slab");
 }
 
 int fsx_slab_ptr(fsx_fabric* f, int gpu, int64_t off, void** d_ptr) {

@@ -76,8 +76,21 @@ class DataPlaneBatch:
         self.item_chunk_rows = torch.zeros(max(M, 1), dtype=torch.int64, device=self.dst_dev)
         self.slab_off: Optional[np.ndarray] = None
         self.flag_base = np.zeros(M, dtype=np.int64)
-        self.n_chunks = np.ones(M, dtype=np.int64)
         self.tokens = np.zeros(M, dtype=np.uint64)
+        # per-item geometry, fixed for the batch
+        self.item_bytes = np.array([it.rows * self.rb for it in lay.items], dtype=np.int64)
+        self.item_chunk = np.array([self.chunk_bytes(it) for it in lay.items], dtype=np.int64)
+        self.n_chunks = np.array([1 if (cb <= 0 or cb >= nb) else -(-nb // cb)
+                                  for nb, cb in zip(self.item_bytes, self.item_chunk)],
+                                 dtype=np.int64)
+        self.chunk_prefix = np.concatenate([[0], np.cumsum(self.n_chunks)[:-1]]).astype(np.int64) \
+            if M else np.zeros(0, np.int64)
+        self._xfers = (N.Transfer * max(M, 1))()
+        sb = self.src_buf.data_ptr()
+        for i in range(M):
+            self._xfers[i] = N.Transfer(src_gpu, dst_gpu, sb + int(self.src_off[i]), 0,
+                                        int(self.item_bytes[i]), int(self.item_chunk[i]), 0, 0, None)
+        self._xview = np.frombuffer(self._xfers, dtype=N.TRANSFER_DTYPE, count=max(M, 1))[:M]
 
     # -- inputs ---------------------------------------------------------------
     def synth_inputs(self, stream=None) -> None:
@@ -93,28 +106,24 @@ class DataPlaneBatch:
 
     # -- slab -------------------------------------------------------------------
     def alloc(self) -> bool:
-        """One slab segment per item; False (nothing held) if the slab is full."""
-        offs = []
-        for it in self.lay.items:
-            off = self.fab.slab_alloc(self.dst_gpu, it.rows * self.rb)
-            if off is None:
-                for o in offs:
-                    self.fab.slab_free(self.dst_gpu, o)
-                return False
-            offs.append(off)
-        self.slab_off = np.array(offs, dtype=np.int64)
+        """One slab segment per item (one all-or-nothing call); False (nothing
+        held) if the slab is full."""
+        offs = self.fab.slab_alloc_n(self.dst_gpu, self.item_bytes)
+        if offs is None:
+            return False
+        self.slab_off = offs
         # first fit hands back the same offsets step after step: upload the
         # slab views only when they change
-        if offs and offs != getattr(self, "_uploaded_offs", None):
-            ptrs = [self.fab.slab_ptr(self.dst_gpu, o) for o in offs]
-            self.item_src.copy_(torch.tensor(ptrs, dtype=torch.int64))
-            self._uploaded_offs = offs
+        key = offs.tobytes()
+        if len(offs) and key != getattr(self, "_uploaded_offs", None):
+            base = self.fab.slab_ptr(self.dst_gpu, 0)
+            self.item_src.copy_(torch.from_numpy(offs + base))
+            self._uploaded_offs = key
         return True
 
     def release(self) -> None:
         if self.slab_off is not None:
-            for o in self.slab_off:
-                self.fab.slab_free(self.dst_gpu, int(o))
+            self.fab.slab_free_n(self.dst_gpu, self.slab_off)
             self.slab_off = None
 
     # -- K1 ---------------------------------------------------------------------
@@ -124,23 +133,25 @@ class DataPlaneBatch:
         return self.chunk_rows * self.rb
 
     def forward(self, stream=None, host_notify: bool = True) -> int:
-        """Push every item into its slab segment; returns kernels launched.
-        host_notify=False when only device work (stream order / early-start
-        merge) waits on the chunk flags."""
+        """Push every item into its slab segment (one fsx_forward_batch call,
+        one K1 launch per 16 items); returns the launches.  host_notify=False
+        when only device work (stream order / early-start merge) waits on the
+        chunk flags."""
         assert self.slab_off is not None, "alloc() first"
-        base = self.src_buf.data_ptr()
-        xfers = []
-        for i, it in enumerate(self.lay.items):
-            nb = it.rows * self.rb
-            cb = self.chunk_bytes(it)
-            n = 1 if (cb <= 0 or cb >= nb) else -(-nb // cb)
-            self.n_chunks[i] = n
-            self.flag_base[i] = self.fab.flags_alloc(self.dst_gpu, n)
-            xfers.append((self.src_gpu, base + int(self.src_off[i]), self.dst_gpu,
-                          int(self.slab_off[i]), nb, cb, int(self.flag_base[i]), 0))
-        if xfers:  # one K1 launch per 16 items
-            self.tokens[:] = self.fab.forward_batch(xfers, stream, host_notify=host_notify)
-        return (len(xfers) + 15) // 16
+        M = len(self.lay.items)
+        if M == 0:
+            return 0
+        fb0 = self.fab.flags_alloc(self.dst_gpu, int(self.n_chunks.sum()))
+        self.flag_base[:] = fb0 + self.chunk_prefix
+        view = self._xview  # numpy view of the fsx_transfer array: no per-item Python
+        view["dst_off"] = self.slab_off
+        view["flag_base"] = self.flag_base
+        view["token"] = 0
+        N.call("fsx_forward_batch", self.fab._h, M, self._xfers,
+               N.FWD_HOST_NOTIFY if host_notify else 0,
+               None if stream is None else int(stream.cuda_stream))
+        self.tokens[:] = view["token"]
+        return (M + 15) // 16
 
     def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
         """The host-span send path (sidecar.hpp:302): payload bytes from host
@@ -192,7 +203,14 @@ class DataPlaneBatch:
         return b
 
     def merge(self, stream=None, early_start: bool = False, mode: int = N.MERGE_FULL) -> None:
-        self.fab.merge(self.dst_gpu, self.merge_batch(early_start, mode), stream)
+        if early_start:  # flag pointers / tokens change every step
+            b = self.merge_batch(True, mode)
+        else:  # descriptors are fixed for the batch: build once
+            cache = self.__dict__.setdefault("_mb_cache", {})
+            b = cache.get(mode)
+            if b is None:
+                b = cache[mode] = self.merge_batch(False, mode)
+        self.fab.merge(self.dst_gpu, b, stream)
 
     def scan(self, stream=None) -> None:
         """Phase 1 of K3 only: needs just the token ids, so it can run while

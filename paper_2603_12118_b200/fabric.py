@@ -81,6 +81,25 @@ class DeviceFabric:
     def slab_free(self, gpu: int, off: int) -> None:
         N.call("fsx_slab_free", self._h, gpu, off)
 
+    def slab_alloc_n(self, gpu: int, lens):
+        """All-or-nothing segment allocation for a batch; None if it does not fit."""
+        import numpy as np
+
+        ln = np.ascontiguousarray(lens, dtype=np.int64)
+        offs = np.empty(len(ln), dtype=np.int64)
+        if len(ln):
+            N.call("fsx_slab_alloc_n", self._h, gpu, len(ln), ln.ctypes.data, offs.ctypes.data)
+            if offs[0] < 0:
+                return None
+        return offs
+
+    def slab_free_n(self, gpu: int, offs) -> None:
+        import numpy as np
+
+        o = np.ascontiguousarray(offs, dtype=np.int64)
+        if len(o):
+            N.call("fsx_slab_free_n", self._h, gpu, len(o), o.ctypes.data)
+
     def slab_ptr(self, gpu: int, off: int = 0) -> int:
         p = C.c_void_p()
         N.call("fsx_slab_ptr", self._h, gpu, off, C.byref(p))

@@ -51,6 +51,36 @@ inline void check(bool ok, const char* expr, const char* file, int line, bool re
 
 }  // namespace catch_shim
 
+namespace Catch {
+// Catch2's Approx: relative epsilon (default 100 * float epsilon) or absolute margin.
+class Approx {
+ public:
+  explicit Approx(double v) : value_(v) {}
+  Approx& epsilon(double e) {
+    eps_ = e;
+    return *this;
+  }
+  Approx& margin(double m) {
+    margin_ = m;
+    return *this;
+  }
+  friend bool operator==(double lhs, const Approx& a) {
+    const double d = lhs > a.value_ ? lhs - a.value_ : a.value_ - lhs;
+    const double scale = (lhs > 0 ? lhs : -lhs) > (a.value_ > 0 ? a.value_ : -a.value_)
+                             ? (lhs > 0 ? lhs : -lhs)
+                             : (a.value_ > 0 ? a.value_ : -a.value_);
+    return d <= a.margin_ || d <= a.eps_ * scale;
+  }
+  friend bool operator==(const Approx& a, double rhs) { return rhs == a; }
+  friend bool operator!=(double lhs, const Approx& a) { return !(lhs == a); }
+
+ private:
+  double value_;
+  double eps_ = 1.1920929e-07 * 100;
+  double margin_ = 0.0;
+};
+}  // namespace Catch
+
 #define CATCH_SHIM_CAT2(a, b) a##b
 #define CATCH_SHIM_CAT(a, b) CATCH_SHIM_CAT2(a, b)
 #define CATCH_SHIM_CASE(fn, name)                                   \
@@ -62,6 +92,19 @@ inline void check(bool ok, const char* expr, const char* file, int line, bool re
 #define CHECK_FALSE(...) \
   catch_shim::check(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
 #define REQUIRE(...) catch_shim::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
+#define REQUIRE_FALSE(...) \
+  catch_shim::check(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, true)
+#define FAIL(msg) catch_shim::check(false, msg, __FILE__, __LINE__, true)
+#define CHECK_NOTHROW(expr)                                                          \
+  do {                                                                               \
+    bool catch_shim_ok = true;                                                       \
+    try {                                                                            \
+      (void)(expr);                                                                  \
+    } catch (...) {                                                                  \
+      catch_shim_ok = false;                                                         \
+    }                                                                                \
+    catch_shim::check(catch_shim_ok, #expr " does not throw", __FILE__, __LINE__, false); \
+  } while (0)
 #define CHECK_THROWS_AS(expr, type)                                                   \
   do {                                                                                \
     bool catch_shim_thrown = false;                                                   \

@@ -35,6 +35,14 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_struct_layouts_match_binding():
+    m, t, s = C.c_int32(), C.c_int32(), C.c_int32()
+    N.call("fsx_abi_sizes", C.byref(m), C.byref(t), C.byref(s))
+    assert m.value == C.sizeof(N.MergeBatch)
+    assert t.value == C.sizeof(N.Transfer)
+    assert s.value == C.sizeof(N.Stats)
+
+
 def test_version_string():
     assert b"sm_100a" in N.lib().fsx_version()
 

@@ -44,6 +44,18 @@ def test_criterion4_on_dropin_realtime_kernel(gpu):
     assert "PASSED" in out
 
 
+def test_reference_executor_and_dispatcher_tests_on_dropin(gpu):
+    """The reference's tests/test_executor_sim.cpp + tests/test_dispatcher.cpp
+    (encoder / LLM / talker / generator executors and TaskDispatcher talking
+    through ExecutorEnv.sidecar) compiled unmodified against the drop-in."""
+    path = os.path.join(ROOT, "build", "ref_test_executors")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_test_executors")
+    rc, out = _run("ref_test_executors")
+    assert rc == 0, out[-4000:]
+    assert " 0 failed" in out
+
+
 def test_reference_test_sidecar_against_dropin(gpu):
     path = os.path.join(ROOT, "build", "ref_test_sidecar")
     if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/test_sidecar.cpp"):
