@@ -11,7 +11,7 @@
  *   - or_checksum64 / or_synth_payload_into / or_fnv1a64 / or_splitmix64 /
  *     or_payload_seed / or_item_tokens: PINNED -- checked against vectors
  *     produced by the reference's own functions (oracle/_ref, built unmodified
- *     from include/fissim/*.hpp) committed in tests/golden/.
+ *     from the include/fissim headers) committed in tests/golden/.
  *   - or_arena_*: PINNED against the reference NodeArena through oracle/_ref.
  *   - or_merge_*: the reference has NO merge (executor_sim.hpp:386 drops the
  *     bytes).  The contract is derived (DESIGN.md "Merge

@@ -89,7 +89,7 @@ def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1):
     fab.slab_free(dst_gpu, off)
 
 
-@pytest.mark.parametrize("n", [0, 1, 7, 256, 4096, 65536, 1 << 20, 8 << 20, 64 << 20])
+@pytest.mark.parametrize("n", [0, 1, 7, 256, 4096, 65536, 1 << 20, 8 << 20, 64 << 20, 256 << 20])
 def test_forward_single_shot_byte_exact(fab, oracle_mod, n):
     # tests/test_sidecar.cpp:60-87 sizes; single-shot = one chunk, one flag
     _forward_check(fab, oracle_mod, n, 0)
@@ -252,7 +252,9 @@ def _run_batch(fab, reqs, rules, chunk_rows=None, early=False, tok_override=None
 
 
 @pytest.mark.parametrize("config,count,chunk_rows", [("A", 64, None), ("A", 5, 64), ("D", 24, 1024),
-                                                     ("B", 1, 1024)])
+                                                     ("B", 1, 1024),
+                                                     # the bench batches at full BASELINE size
+                                                     ("B", 4, 1024), ("D", 32, 1024)])
 def test_merge_bit_exact(fab, oracle_mod, config, count, chunk_rows):
     rules = {"A": T.RULES["A"], "B": T.RULES["B"], "D": T.RULES["D"]}[config]
     reqs = T.config_requests(config, count)
