@@ -69,7 +69,10 @@ build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp 
 	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -o $@ tests/cpp/dropin_criterion4.cpp $(LINKFSX)
 
-cpptests: build/test_fabric
+build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
+	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
+
+cpptests: build/test_fabric build/bench_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors; fi
 

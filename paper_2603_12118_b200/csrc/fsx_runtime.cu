@@ -162,7 +162,12 @@ struct Device {
   int64_t state_next = 0;
   uint64_t* scratch = nullptr;  // short-lived u64 slots (digests), ring
   Ring scratch_ring;
+  cudaStream_t notify = nullptr;     // flag stores of host->device forwards
+  std::vector<cudaEvent_t> events;   // ring of copy-completion events
+  uint64_t next_event = 0;
 };
+
+constexpr size_t kEventRing = 1024;
 
 constexpr int64_t kStatePool = 1 << 16;
 constexpr int64_t kScratchRing = 1 << 14;
@@ -307,6 +312,7 @@ int fsx_close(fsx_fabric* f) {
   for (auto& [o, d] : f->devices) {
     cudaSetDevice(o);
     cudaStreamSynchronize(d->stream);
+    if (d->notify) cudaStreamSynchronize(d->notify);
   }
   for (auto& [g, s] : f->slabs) {
     cudaSetDevice(s->device);
@@ -322,6 +328,8 @@ int fsx_close(fsx_fabric* f) {
     if (d->counters) cudaFree(d->counters);
     if (d->state) cudaFree(d->state);
     if (d->scratch) cudaFree(d->scratch);
+    for (auto e : d->events) cudaEventDestroy(e);
+    if (d->notify) cudaStreamDestroy(d->notify);
     if (d->stream) cudaStreamDestroy(d->stream);
   }
   delete f;
@@ -716,14 +724,25 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
   const uint64_t tok = (token && *token) ? *token : f->next_token.fetch_add(1);
   cudaStream_t st = pick_stream(dev, stream);
   FSX_CUDA(cudaSetDevice(s->device));
+  // The copies stay back to back on `st` (the copy engine never idles); each
+  // chunk's flag store runs on the device's notify stream once an event
+  // recorded after that chunk's copy has fired.
+  if (!dev->notify) {
+    FSX_CUDA(cudaStreamCreateWithFlags(&dev->notify, cudaStreamNonBlocking));
+    dev->events.resize(kEventRing);
+    for (auto& e : dev->events) FSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int64_t beg = c * chunk_bytes, len = std::min(chunk_bytes, bytes - beg);
     if (len > 0)
       FSX_CUDA(cudaMemcpyAsync(s->base + dst_off + beg, static_cast<const uint8_t*>(h_src) + beg,
                                len, cudaMemcpyHostToDevice, st));
+    cudaEvent_t ev = dev->events[dev->next_event++ % kEventRing];
+    FSX_CUDA(cudaEventRecord(ev, st));
+    FSX_CUDA(cudaStreamWaitEvent(dev->notify, ev, 0));
     fsx::FlagSetArgs fa{s->dflags + flag_base + c, s->hflags ? s->hflags + flag_base + c : nullptr,
                         1, tok};
-    FSX_CUDA(fsx::launch_set_flags(fa, st));
+    FSX_CUDA(fsx::launch_set_flags(fa, dev->notify));
     f->launches++;
   }
   f->forwards++;
@@ -1059,6 +1078,7 @@ int fsx_synchronize(fsx_fabric* f) {
   for (auto& [o, d] : f->devices) {
     FSX_CUDA(cudaSetDevice(o));
     FSX_CUDA(cudaStreamSynchronize(d->stream));
+    if (d->notify) FSX_CUDA(cudaStreamSynchronize(d->notify));
   }
   return FSX_OK;
 }
