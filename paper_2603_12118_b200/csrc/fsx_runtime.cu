@@ -301,7 +301,11 @@ int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* dev
   for (int d : devs) {
     Device* st = nullptr;
     int rc = device_state(f.get(), d, &st);
-    if (rc) return rc;
+    if (rc) {
+      const std::string msg = t_err;
+      fsx_close(f.release());  // release the streams/counters created so far
+      return fail(rc, msg);
+    }
   }
   *out = f.release();
   return FSX_OK;
