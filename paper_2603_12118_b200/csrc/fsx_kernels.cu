@@ -368,8 +368,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_bat
   const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
   const int64_t rb = b.row_bytes;
   const bool vec_rows = (rb & 15) == 0;
-  for (int64_t g = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
-       g < b.total_item_rows; g += warps) {
+  const bool newest_first = b.d_item_flag == nullptr;  // L2 reuse, see merge_copy_tma_kernel
+  for (int64_t k = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
+       k < b.total_item_rows; k += warps) {
+    const int64_t g = newest_first ? b.total_item_rows - 1 - k : k;
     int64_t item = 0, req = 0;
     if (lane == 0) {
       item = upper_index(b.d_item_row_off, b.num_items + 1, g);
@@ -663,9 +665,15 @@ __global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, u
   const int64_t first = blockIdx.x, stride = gridDim.x, n = b.total_item_rows;
   uint8_t* dst_of[S];
   uint32_t parity = 0;  // bit s = phase parity expected next on stage s
+  // Newest rows first when the slab was filled before this launch (stream
+  // order): the tail of what K1 just wrote is still in the 126 MB L2, so
+  // walking the rows backwards turns part of the slab reads into L2 hits.
+  // With early start (flags) rows are taken in arrival order instead.
+  const bool newest_first = b.d_item_flag == nullptr;
   auto issue = [&](int64_t k) {  // load this CTA's k-th row into stage k % S
     const int s = (int)(k % S);
-    const RowRef r = resolve_row(b, first + k * stride);
+    const int64_t idx = first + k * stride;
+    const RowRef r = resolve_row(b, newest_first ? n - 1 - idx : idx);
     dst_of[s] = r.dst;
     if (!r.src) return;
     const uint32_t bar = tma::smem_u32(&bars[s]);

@@ -173,8 +173,20 @@ class DataPlaneBatch:
                           int(self.tokens[i]), timeout_us)
 
     # -- K3 ---------------------------------------------------------------------
-    def merge_batch(self, early_start: bool = False, mode: int = N.MERGE_FULL) -> N.MergeBatch:
+    def _scan_slot(self, slot: int):
+        """(scratch, status) of scan slot `slot`: slot 0 is the batch's own
+        pair; slot 1 a second pair so the scan of the next pass can run while
+        the current pass still reads slot 0 (software pipelining)."""
+        if slot == 0:
+            return self.scratch, self.status
+        if not hasattr(self, "_slot1"):
+            self._slot1 = (torch.empty_like(self.scratch), torch.full_like(self.status, -1))
+        return self._slot1
+
+    def merge_batch(self, early_start: bool = False, mode: int = N.MERGE_FULL,
+                    slot: int = 0) -> N.MergeBatch:
         lay = self.lay
+        scratch, status = self._scan_slot(slot)
         b = N.MergeBatch()
         b.mode = mode
         b.num_requests = len(lay.requests)
@@ -187,8 +199,8 @@ class DataPlaneBatch:
         b.d_req_item_off = self.req_item_off.data_ptr()
         b.d_item_src = self.item_src.data_ptr()
         b.d_item_row_off = self.item_row_off.data_ptr()
-        b.d_scratch = self.scratch.data_ptr()
-        b.d_status = self.status.data_ptr()
+        b.d_scratch = scratch.data_ptr()
+        b.d_status = status.data_ptr()
         b.total_rows = lay.total_rows
         b.total_item_rows = lay.total_item_rows
         if early_start and len(lay.items):
@@ -202,27 +214,29 @@ class DataPlaneBatch:
             b.d_item_chunk_rows = self.item_chunk_rows.data_ptr()
         return b
 
-    def merge(self, stream=None, early_start: bool = False, mode: int = N.MERGE_FULL) -> None:
+    def merge(self, stream=None, early_start: bool = False, mode: int = N.MERGE_FULL,
+              slot: int = 0) -> None:
         if early_start:  # flag pointers / tokens change every step
-            b = self.merge_batch(True, mode)
+            b = self.merge_batch(True, mode, slot)
         else:  # descriptors are fixed for the batch: build once
             cache = self.__dict__.setdefault("_mb_cache", {})
-            b = cache.get(mode)
+            b = cache.get((mode, slot))
             if b is None:
-                b = cache[mode] = self.merge_batch(False, mode)
+                b = cache[(mode, slot)] = self.merge_batch(False, mode, slot)
         self.fab.merge(self.dst_gpu, b, stream)
 
-    def scan(self, stream=None) -> None:
+    def scan(self, stream=None, slot: int = 0) -> None:
         """Phase 1 of K3 only: needs just the token ids, so it can run while
-        the payload is still being forwarded."""
-        self.merge(stream, mode=N.MERGE_SCAN_ONLY)
+        the payload is still being forwarded (or, pipelined, during the
+        previous pass)."""
+        self.merge(stream, mode=N.MERGE_SCAN_ONLY, slot=slot)
 
     # -- readback -----------------------------------------------------------------
     def embeds_host(self) -> np.ndarray:
         return self.embeds[: self.lay.total_rows * self.rb].cpu().numpy()
 
-    def status_host(self) -> np.ndarray:
-        return self.status[: len(self.lay.requests)].cpu().numpy()
+    def status_host(self, slot: int = 0) -> np.ndarray:
+        return self._scan_slot(slot)[1][: len(self.lay.requests)].cpu().numpy()
 
     def slab_item_host(self, i: int) -> np.ndarray:
         it = self.lay.items[i]
