@@ -629,9 +629,14 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       f->bytes_forwarded += x.bytes;
       f->forwards++;
     }
-    const int warps_per_cta = fsx::forward_block_threads() / 32;
-    const int grid = (int)std::min<int64_t>((b.unit_off[cnt] + warps_per_cta - 1) / warps_per_cta,
-                                            dev->fwd_grid);
+    // Balanced persistent grid: every warp gets the same number of units
+    // (rounds), instead of a full first round and a half-empty last one.
+    const int64_t warps_per_cta = fsx::forward_block_threads() / 32;
+    const int64_t units = b.unit_off[cnt];
+    const int64_t max_warps = (int64_t)dev->fwd_grid * warps_per_cta;
+    const int64_t rounds = std::max<int64_t>(1, (units + max_warps - 1) / max_warps);
+    const int64_t warps = (units + rounds - 1) / rounds;
+    const int grid = (int)std::max<int64_t>(1, (warps + warps_per_cta - 1) / warps_per_cta);
     FSX_CUDA(fsx::launch_forward(b, fwd_variant(), grid, st));
     f->launches++;
     for (int32_t k = 0; k < cnt; ++k) {

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .fabric import DeviceFabric
+from .fabric import DeviceFabric, _stream_ptr
 from .trace import (PLACEHOLDER_ID, BatchLayout, Request, ShapeRules, layout, payload_seed,
                     prompt_tokens, text_seed)
 
@@ -149,7 +149,7 @@ class DataPlaneBatch:
         view["token"] = 0
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers,
                N.FWD_HOST_NOTIFY if host_notify else 0,
-               None if stream is None else int(stream.cuda_stream))
+               _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return (M + 15) // 16
 

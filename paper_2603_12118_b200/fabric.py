@@ -15,12 +15,24 @@ from typing import Dict, Optional
 from . import _native as N
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the per-device legacy default stream
+
+
 def _stream_ptr(stream) -> Optional[int]:
+    """cudaStream_t for the C ABI.  None means torch's current stream (so fsx
+    work is ordered with the surrounding torch ops, e.g. the copy that fills a
+    source buffer); torch's default stream has handle 0, which the C ABI would
+    read as "the fabric's own stream", so it is passed as cudaStreamLegacy.
+    Pass an explicit stream when the call targets another device than the
+    current one."""
     if stream is None:
-        return None
+        import torch
+
+        stream = torch.cuda.current_stream()
     if isinstance(stream, int):
         return stream
-    return int(stream.cuda_stream)  # torch.cuda.Stream
+    h = int(stream.cuda_stream)  # torch.cuda.Stream
+    return h if h else CUDA_STREAM_LEGACY
 
 
 class DeviceFabric:
