@@ -47,6 +47,10 @@ CONFIGS = {
           "workload": "D: servegen-like mixed image/video/audio trace (seed 42), 3584-d bf16"},
 }
 METRIC = "forwarded GB/s per producer->consumer pair vs 900 GB/s NVLink; merged req/s"
+# N=1: the consumer merges right after K1 on the same GPU; storing the slab with
+# L2 evict_last priority (FSX_FWD_L2_KEEP) measured 1-3 % slower than normal
+# priority (profiles/README.md), so it is off unless FSX_BENCH_L2_KEEP=1.
+L2_KEEP = os.environ.get("FSX_BENCH_L2_KEEP", "0") == "1"
 
 
 def parse():
@@ -315,7 +319,7 @@ def run_single(args):
             e0.record(stream)
         # K1: 4 items x 16 flagged per-frame chunks; the consumer (K3) is
         # stream-ordered on this GPU, so no host mirror of the flags
-        batch.forward(stream, host_notify=False)
+        batch.forward(stream, host_notify=False, l2_keep=L2_KEEP)
         if record:
             e1.record(stream)
         side.wait_event(fork)

@@ -138,6 +138,10 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * early start, fsx_stream_wait_flags, or plain stream order) wait on the chunks,
  * which saves the posted PCIe store at the kernel tail. */
 #define FSX_FWD_HOST_NOTIFY 1u
+/* FSX_FWD_L2_KEEP: store the slab bytes with L2 evict_last priority, for a
+ * consumer on the same GPU that reads them right after (the merge); the
+ * producer's source is always read with evict_first. */
+#define FSX_FWD_L2_KEEP 2u
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                    uint32_t options, void* stream);

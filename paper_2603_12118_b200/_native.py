@@ -35,6 +35,7 @@ LOCAL_BUFFER = 0
 NETWORK_STREAM = 1
 
 FWD_HOST_NOTIFY = 1
+FWD_L2_KEEP = 2
 
 MERGE_FULL = 0
 MERGE_SCAN_ONLY = 1

@@ -52,6 +52,32 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
   return r;
 }
 
+// L2 eviction-priority policies (createpolicy) for the .L2::cache_hint forms.
+__device__ __forceinline__ uint64_t l2_policy(int which) {
+  uint64_t p;
+  if (which == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (which == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4_pol(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4_pol(void* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
@@ -141,7 +167,8 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 template <int U>
 __device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ src,
                                                     uint8_t* __restrict__ dst, int64_t beg,
-                                                    int64_t end, bool vec, bool dig, int lane) {
+                                                    int64_t end, bool vec, bool dig, int lane,
+                                                    uint64_t ld_pol, uint64_t st_pol) {
   uint64_t acc = 0;
   if (vec) {
     const int64_t vbeg = (beg + 15) & ~int64_t{15};
@@ -156,12 +183,12 @@ __device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ 
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const int64_t i = base + k * 32 + lane;
-          if (i < nv) r[k] = ld_nc_v4(s + i);
+          if (i < nv) r[k] = ld_nc_v4_pol(s + i, ld_pol);
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4(d + i, r[k]);
+          if (i < nv) st_v4_pol(d + i, r[k], st_pol);
         }
         if (dig) {
 #pragma unroll
@@ -204,6 +231,10 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kFwdThreads / 32);
   const int64_t total = b.unit_off[b.n];
+  // The producer's source is read once (evict first); slab writes may be
+  // kept in L2 for a consumer that merges right after on this GPU.
+  const uint64_t ld_pol = l2_policy(1);
+  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
   int i = 0;  // transfer of the current unit; units only grow per warp
   for (int64_t gu = (int64_t)blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5); gu < total;
        gu += warps) {
@@ -217,7 +248,7 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
     const int64_t beg = cbeg + s * a.slice;
     const int64_t end = min(beg + a.slice, cend);
     const bool dig = a.digest != nullptr;
-    uint64_t acc = warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, dig, lane);
+    uint64_t acc = warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, dig, lane, ld_pol, st_pol);
     if (dig) {  // fused dg64: one atomic per unit, ordered before the counter release
       acc = warp_sum_u64(acc);
       if (lane == 0) {

@@ -34,7 +34,7 @@ struct FwdArgs {
 constexpr int kFwdMaxBatch = 16;
 struct FwdBatch {
   int32_t n;
-  int32_t _pad;
+  int32_t l2_keep_dst;  // slab stores with L2 evict_last (consumer merges next)
   int64_t unit_off[kFwdMaxBatch + 1];
   FwdArgs t[kFwdMaxBatch];
 };

@@ -132,7 +132,7 @@ class DataPlaneBatch:
             return 0
         return self.chunk_rows * self.rb
 
-    def forward(self, stream=None, host_notify: bool = True) -> int:
+    def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
         one K1 launch per 16 items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
@@ -147,9 +147,8 @@ class DataPlaneBatch:
         view["dst_off"] = self.slab_off
         view["flag_base"] = self.flag_base
         view["token"] = 0
-        N.call("fsx_forward_batch", self.fab._h, M, self._xfers,
-               N.FWD_HOST_NOTIFY if host_notify else 0,
-               _stream_ptr(stream))
+        opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0)
+        N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return (M + 15) // 16
 
