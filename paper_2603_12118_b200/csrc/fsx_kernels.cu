@@ -78,6 +78,45 @@ __device__ __forceinline__ void st_v4_pol(void* p, const uint4& v, uint64_t pol)
                : "memory");
 }
 
+// 32-byte vectors: sm_100 has 256-bit global loads/stores (LDG/STG .256).
+struct alignas(32) v8u32 {
+  uint4 lo, hi;
+};
+
+__device__ __forceinline__ v8u32 ld_nc_v8_pol(const void* p, uint64_t pol) {
+  v8u32 r;
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x), "=r"(r.hi.y),
+        "=r"(r.hi.z), "=r"(r.hi.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+
+__device__ __forceinline__ void st_v8_pol(void* p, const v8u32& v, uint64_t pol) {
+  asm volatile(
+      "st.global.L1::no_allocate.L2::cache_hint.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+      "r"(v.lo.x), "r"(v.lo.y), "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z),
+      "r"(v.hi.w), "l"(pol)
+      : "memory");
+}
+
+// Loads/stores of one V-byte vector (V = 16 or 32) with L2 policies.
+template <int V>
+struct VecIO;
+template <>
+struct VecIO<16> {
+  using T = uint4;
+  static __device__ __forceinline__ T ld(const void* p, uint64_t pol) { return ld_nc_v4_pol(p, pol); }
+  static __device__ __forceinline__ void st(void* p, const T& v, uint64_t pol) { st_v4_pol(p, v, pol); }
+};
+template <>
+struct VecIO<32> {
+  using T = v8u32;
+  static __device__ __forceinline__ T ld(const void* p, uint64_t pol) { return ld_nc_v8_pol(p, pol); }
+  static __device__ __forceinline__ void st(void* p, const T& v, uint64_t pol) { st_v8_pol(p, v, pol); }
+};
+
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
@@ -118,10 +157,6 @@ __device__ __forceinline__ uint64_t splitmix_word(uint64_t s0, uint64_t k) {
 // ---------------------------------------------------------------------------
 // K1 forward
 
-// Copy [beg, end) of src into dst with one warp.  `vec` means src and dst are
-// 16-byte aligned, so every 16-byte-aligned offset is a legal vector.  All
-// loads of a batch are issued before its stores (kFwdUnroll x 16 B per lane in
-// flight).
 // fsx integrity digest dg64 (replaces the serial checksum64 of
 // common.hpp:221-241 on the device hop): with w_k the k-th little-endian
 // 8-byte word of the payload (the last one zero-padded) and n its length,
@@ -159,54 +194,72 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
-// Copy [beg, end) of src into dst with one warp; `vec` means src and dst are
-// 16-byte aligned (and beg is a multiple of 16), so every 16-byte-aligned
-// offset is a legal vector.  All loads of a batch are issued before its
-// stores (U x 16 B per lane in flight).  With `dig`, the lane also digests the
-// words it moved (returned per lane; lane 0 adds the byte tail).
-template <int U>
-__device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ src,
-                                                    uint8_t* __restrict__ dst, int64_t beg,
-                                                    int64_t end, bool vec, bool dig, int lane,
-                                                    uint64_t ld_pol, uint64_t st_pol) {
+__device__ __forceinline__ uint64_t dg_any(const uint4& v, uint64_t word) { return dg_vec(v, word); }
+__device__ __forceinline__ uint64_t dg_any(const v8u32& v, uint64_t word) {
+  return dg_vec(v.lo, word) + dg_vec(v.hi, word + 2);
+}
+
+// Copy [beg, end) of src into dst with one warp using V-byte vectors (src, dst
+// and beg are 16-byte aligned; V = 32 also needs 32-byte aligned src/dst).  All
+// loads of a batch are issued before its stores (U x V bytes per lane in
+// flight).  With `dig`, the lane also digests the words it moved (returned per
+// lane; lane 0 adds the unvectorised head/tail bytes).
+template <int U, int V>
+__device__ __forceinline__ uint64_t warp_copy_vec(const uint8_t* __restrict__ src,
+                                                  uint8_t* __restrict__ dst, int64_t beg, int64_t end,
+                                                  bool dig, int lane, uint64_t ld_pol, uint64_t st_pol) {
+  using IO = VecIO<V>;
+  using T = typename IO::T;
   uint64_t acc = 0;
-  if (vec) {
-    const int64_t vbeg = (beg + 15) & ~int64_t{15};
-    const int64_t vend = end & ~int64_t{15};
-    if (vbeg < vend) {
-      const uint4* s = reinterpret_cast<const uint4*>(src + vbeg);
-      uint4* d = reinterpret_cast<uint4*>(dst + vbeg);
-      const int64_t nv = (vend - vbeg) >> 4;
-      const uint64_t w0 = (uint64_t)(vbeg >> 3);
-      for (int64_t base = 0; base < nv; base += 32 * U) {
-        uint4 r[U];
+  const int64_t vbeg = (beg + V - 1) & ~int64_t{V - 1};
+  const int64_t vend = end & ~int64_t{V - 1};
+  if (vbeg < vend) {
+    const int64_t nv = (vend - vbeg) / V;
+    const uint64_t w0 = (uint64_t)(vbeg >> 3);
+    for (int64_t base = 0; base < nv; base += 32 * U) {
+      T r[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + k * 32 + lane;
+        if (i < nv) r[k] = IO::ld(src + vbeg + i * V, ld_pol);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + k * 32 + lane;
+        if (i < nv) IO::st(dst + vbeg + i * V, r[k], st_pol);
+      }
+      if (dig) {
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const int64_t i = base + k * 32 + lane;
-          if (i < nv) r[k] = ld_nc_v4_pol(s + i, ld_pol);
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4_pol(d + i, r[k], st_pol);
-        }
-        if (dig) {
-#pragma unroll
-          for (int k = 0; k < U; ++k) {
-            const int64_t i = base + k * 32 + lane;
-            if (i < nv) acc += dg_vec(r[k], w0 + 2 * (uint64_t)i);
-          }
+          if (i < nv) acc += dg_any(r[k], w0 + (uint64_t)i * (V / 8));
         }
       }
-      for (int64_t i = beg + lane; i < vbeg && i < end; i += 32) dst[i] = src[i];
-      for (int64_t i = vend + lane; i < end; i += 32) dst[i] = src[i];
-      if (dig && lane == 0 && vend < end) acc += dg_bytes(src, vend, end);
-      return acc;
     }
+    for (int64_t i = beg + lane; i < vbeg; i += 32) dst[i] = src[i];
+    for (int64_t i = vend + lane; i < end; i += 32) dst[i] = src[i];
+    if (dig && lane == 0) {
+      if (beg < vbeg) acc += dg_bytes(src, beg, vbeg);
+      if (vend < end) acc += dg_bytes(src, vend, end);
+    }
+    return acc;
   }
   for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
-  if (vec && dig && lane == 0) acc += dg_bytes(src, beg, end);  // < 16-byte unit
-  return acc;  // unaligned path: the runtime digests the source separately
+  if (dig && lane == 0) acc += dg_bytes(src, beg, end);  // unit smaller than a vector
+  return acc;
+}
+
+// `vec`: 0 = byte path (unaligned; the runtime digests the source
+// separately), otherwise the kernel's vector width V (16 or 32; the runtime
+// launches the V = 32 instance only when every transfer allows it).
+template <int U, int V>
+__device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ src,
+                                                    uint8_t* __restrict__ dst, int64_t beg,
+                                                    int64_t end, int vec, bool dig, int lane,
+                                                    uint64_t ld_pol, uint64_t st_pol) {
+  if (vec) return warp_copy_vec<U, V>(src, dst, beg, end, dig, lane, ld_pol, st_pol);
+  for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
+  return 0;
 }
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bool sys) {
@@ -226,7 +279,7 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bo
 // scope for a local slab, system scope when the slab is peer memory), and the
 // warp that completes the chunk fences at system scope and publishes the token
 // to the consumer-device flag and the host-mapped flag.
-template <int U, int MINB>
+template <int U, int MINB, int V>
 __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid_constant__ FwdBatch b) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kFwdThreads / 32);
@@ -248,7 +301,7 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
     const int64_t beg = cbeg + s * a.slice;
     const int64_t end = min(beg + a.slice, cend);
     const bool dig = a.digest != nullptr;
-    uint64_t acc = warp_copy_range<U>(a.src, a.dst, beg, end, a.vec != 0, dig, lane, ld_pol, st_pol);
+    uint64_t acc = warp_copy_range<U, V>(a.src, a.dst, beg, end, a.vec, dig, lane, ld_pol, st_pol);
     if (dig) {  // fused dg64: one atomic per unit, ordered before the counter release
       acc = warp_sum_u64(acc);
       if (lane == 0) {
@@ -257,6 +310,7 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
       }
     }
     __syncwarp();
+    if (a.counters == nullptr) continue;  // diagnostic only: no completion tracking
     if (lane == 0) {
       const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
       const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
@@ -485,11 +539,13 @@ int merge_copy_block_threads() { return kMergeThreads; }
 
 namespace {
 using FwdFn = void (*)(FwdBatch);
-FwdFn forward_variant(int v) {
+// variant: 0 <16 x 16 B, 2 CTAs/SM>, 1 <8 x 16 B, 4 CTAs/SM>, 2 <8 x 16 B, 3 CTAs/SM>;
+// wide = 32-byte vectors with half the count (same bytes in flight).
+FwdFn forward_variant(int v, bool wide = false) {
   switch (v) {
-    case 1: return forward_kernel<8, 4>;
-    case 2: return forward_kernel<8, 3>;
-    default: return forward_kernel<16, 2>;
+    case 1: return wide ? forward_kernel<4, 4, 32> : forward_kernel<8, 4, 16>;
+    case 2: return wide ? forward_kernel<4, 3, 32> : forward_kernel<8, 3, 16>;
+    default: return wide ? forward_kernel<8, 2, 32> : forward_kernel<16, 2, 16>;
   }
 }
 }  // namespace
@@ -511,7 +567,13 @@ int merge_copy_blocks_per_sm() {
 }
 
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s) {
-  forward_variant(variant)<<<grid, kFwdThreads, 0, s>>>(b);
+  bool wide = true;  // every vectorised transfer allows 32-byte vectors
+  for (int k = 0; k < b.n; ++k) wide = wide && (b.t[k].vec == 32 || b.t[k].vec == 0);
+  FwdBatch bb = b;
+  if (!wide)
+    for (int k = 0; k < bb.n; ++k)
+      if (bb.t[k].vec == 32) bb.t[k].vec = 16;
+  forward_variant(variant, wide)<<<grid, kFwdThreads, 0, s>>>(bb);
   return cudaGetLastError();
 }
 

@@ -58,7 +58,7 @@ int64_t fwd_unit_bytes() {
 int fwd_variant() {
   static const int v = [] {
     const char* e = std::getenv("FSX_FWD_VARIANT");
-    return e ? std::atoi(e) : 1;  // 8 x 16 B per lane, 4 CTAs/SM (sweep2)
+    return e ? std::atoi(e) : 2;  // 8 x 16 B per lane, 3 CTAs/SM, no spills (profiles/README.md)
   }();
   return v;
 }
@@ -605,6 +605,10 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
         if (x.flag_base < 0 || x.flag_base + n_chunks > kFlagRing)
           return fail(FSX_E_VALIDATION, "flag range out of the ring");
         a.counters = dev->counters + dev->counter_ring.take(n_chunks);
+        // FSX_DIAG_NO_FLAGS=1: measure the copy without completion tracking
+        // (no chunk flags are ever set: stream-ordered consumers only)
+        static const bool diag_no_flags = std::getenv("FSX_DIAG_NO_FLAGS") != nullptr;
+        if (diag_no_flags) a.counters = nullptr;
         a.dst = s->base + x.dst_off;
         a.dflags = s->dflags + x.flag_base;
         a.hflags = (s->hflags && (options & FSX_FWD_HOST_NOTIFY)) ? s->hflags + x.flag_base : nullptr;
@@ -620,7 +624,16 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       a.last_units = std::max<int64_t>(1, (last_len + a.slice - 1) / a.slice);
       a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
       a.n_chunks = (int32_t)n_chunks;
-      a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
+      {
+        // widest vector both ends allow: 32 B (LDG/STG.256 on sm_100), 16 B, or bytes
+        const uintptr_t al = reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst);
+        static const bool v32 = [] {
+          // 256-bit vectors measured no better than 16-byte ones (profiles/README.md)
+          const char* e = std::getenv("FSX_FWD_V32");
+          return e && e[0] == '1';
+        }();
+        a.vec = (v32 && (al & 31) == 0) ? 32 : ((al & 15) == 0 ? 16 : 0);
+      }
       if (x.token == 0) x.token = f->next_token.fetch_add(1);
       a.token = x.token;
       // the fused digest needs the 16-byte path; otherwise digest the source
