@@ -334,6 +334,88 @@ __global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid
   }
 }
 
+// K1, tile form (default).  One CTA per tile of kTileThreads x U x 16 B, no
+// persistence: the hardware CTA scheduler hands tiles to SMs as earlier ones
+// retire, which on B200 sustains ~6.7 TB/s for a plain copy where a persistent
+// grid-stride loop tops out near 5.9-6.3 (scripts/probe_sm_copy.cu).  Tiles are
+// chunk-major in blockIdx order, so chunks complete roughly in order.  After
+// its loads and stores the CTA barriers, and one thread counts the tile into
+// the chunk counter with an acq_rel atomic (bar.sync makes every thread's
+// stores part of that release; gpu scope for a local slab, system scope for
+// peer memory); the CTA that completes the chunk publishes the token.
+constexpr int kTileThreads = 256;
+
+template <int U>
+__global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid_constant__ FwdBatch b) {
+  __shared__ uint64_t red[kTileThreads / 32];
+  const int64_t gt = blockIdx.x;
+  int i = 0;
+  while (gt >= b.unit_off[i + 1]) ++i;
+  const FwdArgs& a = b.t[i];
+  const int64_t u = gt - b.unit_off[i];
+  const int64_t c = u / a.chunk_units;
+  const int64_t s = u - c * a.chunk_units;
+  const int64_t cbeg = c * a.chunk_bytes;
+  const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
+  const int64_t beg = cbeg + s * a.slice;
+  const int64_t end = min(beg + a.slice, cend);
+  const uint64_t ld_pol = l2_policy(1);
+  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
+  const bool dig = a.digest != nullptr;
+  uint64_t acc = 0;
+  if (a.vec) {
+    // beg is 16-byte aligned (slices and chunks are multiples of 16)
+    const int64_t vend = end & ~int64_t{15};
+    const int64_t nv = (vend - beg) >> 4;
+    uint4 r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t v = k * kTileThreads + threadIdx.x;
+      if (v < nv) r[k] = ld_nc_v4_pol(a.src + beg + v * 16, ld_pol);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t v = k * kTileThreads + threadIdx.x;
+      if (v < nv) st_v4_pol(a.dst + beg + v * 16, r[k], st_pol);
+    }
+    if (dig) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t v = k * kTileThreads + threadIdx.x;
+        if (v < nv) acc += dg_vec(r[k], (uint64_t)((beg >> 3) + 2 * v));
+      }
+      if (threadIdx.x == 0 && vend < end) acc += dg_bytes(a.src, vend, end);
+    }
+    for (int64_t j = vend + threadIdx.x; j < end; j += kTileThreads) a.dst[j] = a.src[j];
+  } else {
+    for (int64_t j = beg + threadIdx.x; j < end; j += kTileThreads) a.dst[j] = a.src[j];
+  }
+  if (dig) {  // block-reduce the digest, one atomic per tile
+    acc = warp_sum_u64(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0 || a.counters == nullptr) return;
+  if (dig) {
+    uint64_t t = 0;
+    for (int w = 0; w < kTileThreads / 32; ++w) t += red[w];
+    if (u == 0) t += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.digest), (unsigned long long)t);
+  }
+  const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
+  const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
+  if (prev == units - 1) {
+    a.counters[c] = 0u;
+    if (a.peer) {
+      __threadfence_system();
+      st_release_sys(&a.dflags[c], a.token);
+    } else {
+      st_release_gpu(&a.dflags[c], a.token);
+    }
+    if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
+  }
+}
+
 // Stand-alone dg64 of n device bytes, accumulated into *out (zeroed by the
 // caller): consumer-side verification of a delivered slab segment, and the
 // producer digest when K1 ran its unaligned byte path.
@@ -552,6 +634,7 @@ FwdFn forward_variant(int v, bool wide = false) {
 
 int forward_blocks_per_sm(int variant) {
   int n = 0;
+  if (variant >= 3) variant = 2;  // tile kernels are not persistent: grid = tiles
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, forward_variant(variant), kFwdThreads, 0) !=
       cudaSuccess)
     return 1;
@@ -566,7 +649,24 @@ int merge_copy_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
+int forward_tile_bytes(int variant) {
+  if (variant == 3) return kTileThreads * 4 * 16;  // 16 KiB tiles
+  if (variant == 4) return kTileThreads * 8 * 16;  // 32 KiB tiles
+  return 0;                                        // persistent warp kernels
+}
+
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s) {
+  if (forward_tile_bytes(variant)) {
+    // one CTA per tile: grid = total tiles of the batch (16-byte vectors)
+    FwdBatch bb = b;
+    for (int k = 0; k < bb.n; ++k)
+      if (bb.t[k].vec) bb.t[k].vec = 16;
+    const int64_t tiles = bb.unit_off[bb.n];
+    if (tiles <= 0) return cudaSuccess;
+    if (variant == 3) forward_tile_kernel<4><<<(unsigned)tiles, kTileThreads, 0, s>>>(bb);
+    else forward_tile_kernel<8><<<(unsigned)tiles, kTileThreads, 0, s>>>(bb);
+    return cudaGetLastError();
+  }
   bool wide = true;  // every vectorised transfer allows 32-byte vectors
   for (int k = 0; k < b.n; ++k) wide = wide && (b.t[k].vec == 32 || b.t[k].vec == 0);
   FwdBatch bb = b;
@@ -839,7 +939,12 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     return e;
   }
   const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-  const int grid = (int)(need < copy_grid ? need : copy_grid);
+  // one warp per row and no persistence (full grid) unless FSX_MERGE_PERSIST=1
+  static const bool persist = [] {
+    const char* e = std::getenv("FSX_MERGE_PERSIST");
+    return e && e[0] == '1';
+  }();
+  const int grid = (int)((persist && need > copy_grid) ? copy_grid : need);
   merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
   e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;

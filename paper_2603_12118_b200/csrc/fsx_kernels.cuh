@@ -80,6 +80,8 @@ cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaS
 // Occupancy helpers.
 int forward_block_threads();
 int forward_blocks_per_sm(int variant);
+// Tile size of the one-CTA-per-tile K1 variants (3, 4), 0 for the persistent ones.
+int forward_tile_bytes(int variant);
 int merge_copy_block_threads();
 int merge_copy_blocks_per_sm();
 

@@ -58,7 +58,9 @@ int64_t fwd_unit_bytes() {
 int fwd_variant() {
   static const int v = [] {
     const char* e = std::getenv("FSX_FWD_VARIANT");
-    return e ? std::atoi(e) : 2;  // 8 x 16 B per lane, 3 CTAs/SM, no spills (profiles/README.md)
+    // 4: one CTA per 32 KiB tile (non-persistent), 6.4 TB/s in the bench step;
+    // the persistent warp variants 0-2 top out near 5.7 (profiles/README.md)
+    return e ? std::atoi(e) : 4;
   }();
   return v;
 }
@@ -576,7 +578,8 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
   // Work unit: one warp, one release + counter bump.  Large enough to
   // amortise the release, small enough that mid-size batches still spread
   // over every resident warp (sweep3: 16 KiB >= 64 MiB, down to 4 KiB).
-  int64_t unit = fwd_unit_bytes();
+  int64_t unit = fsx::forward_tile_bytes(fwd_variant());  // tile kernels: unit = tile
+  if (unit == 0) unit = fwd_unit_bytes();
   if (unit == 0) {
     const int64_t warps =
         std::max<int64_t>(1, (int64_t)dev->fwd_grid * (fsx::forward_block_threads() / 32));
