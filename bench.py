@@ -70,6 +70,16 @@ def parse():
     return p.parse_args()
 
 
+def fwd_kernel_name() -> str:
+    """K1 instance libfsx launches (fwd_variant() in fsx_runtime.cu)."""
+    v = int(os.environ.get("FSX_FWD_VARIANT", "4"))
+    if v == 3:
+        return "fsx::kern::forward_tile_kernel<4> (one CTA per 16 KiB tile)"
+    if v == 4:
+        return "fsx::kern::forward_tile_kernel<8> (one CTA per 32 KiB tile)"
+    return f"fsx::kern::forward_kernel (persistent warps, variant {v})"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -365,7 +375,7 @@ def run_single(args):
     fwd_gbs = fwd_bytes / (fwd_ms * 1e-3) / 1e9
     mrg_gbs = merge_bytes / (mrg_ms * 1e-3) / 1e9
     kernels = {
-        "forward": {"kernel": "fsx::kern::forward_kernel (batched: all items of the step)",
+        "forward": {"kernel": fwd_kernel_name() + " (batched: all items of the step)",
                     "launches_per_step": fwd_launches,
                     "ms_per_step": round(fwd_ms, 4),
                     "algorithmic_bytes_per_launch": fwd_bytes // fwd_launches,

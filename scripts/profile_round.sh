@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
     --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --profile > $OUT/launches_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"forward_kernel|merge_copy|merge_scan" -s 12 -c 6 \
+    -k regex:"forward|merge_copy|merge_scan" -s 9 -c 6 \
     -o $OUT/full_$TAG python bench.py --steps 2 --warmup 3 --profile > $OUT/full_$TAG.log 2>&1
 tail -2 $OUT/full_$TAG.log

@@ -32,7 +32,7 @@ METRICS = [
 
 
 def short(name: str) -> str:
-    for k in ("forward_kernel", "merge_copy_tma_kernel", "merge_copy_kernel", "merge_scan_kernel",
+    for k in ("forward_tile_kernel", "forward_kernel", "merge_copy_tma_kernel", "merge_copy_kernel", "merge_scan_kernel",
               "synth_kernel", "set_flags_kernel", "wait_flags_kernel"):
         if k in name:
             return k
@@ -86,7 +86,7 @@ def main(tag: str) -> None:
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    tr = {"forward_kernel": traffic.get("forward_kernel"),
+    tr = {"forward_kernel": traffic.get("forward_tile_kernel") or traffic.get("forward_kernel"),
           "merge": traffic.get("merge_copy_tma_kernel") or traffic.get("merge_copy_kernel"),
           "merge_scan_kernel": traffic.get("merge_scan_kernel"), "source": f"profiles/ncu_{tag}.md",
           "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)"}

@@ -26,7 +26,7 @@ def main():
     src = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     fab.synth(0, 1234, src.data_ptr(), src.numel())
     ref = torch.empty_like(src)
-    variant = os.environ.get("FSX_FWD_VARIANT", "0")
+    variant = os.environ.get("FSX_FWD_VARIANT", "4")
     unit = os.environ.get("FSX_FWD_UNIT", "32768")
     cases = [(n, 0) for n in sizes] + [(117_440_512, 7_340_032), (256 << 20, 1 << 20),
                                        (256 << 20, 64 << 10)]
