@@ -69,12 +69,43 @@ build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp 
 	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -o $@ tests/cpp/dropin_criterion4.cpp $(LINKFSX)
 
+# Multi-process executors: the worker executable and the
+# REFERENCE's tests/test_worker.cpp, compiled unmodified against the drop-in
+# executor_worker.hpp + sidecar.hpp.  The test reads two reference data files
+# (profiles/mllm.json, apps/mllm-gemma.json) from FISSIM_REPO_ROOT; they are
+# staged into build/refdata (git-ignored, travels to the GPU box with build/).
+REFDATA := $(CURDIR)/build/refdata
+build/fsx_worker: tests/cpp/fsx_worker_main.cpp include/fsx/dropin/fissim/executor_worker.hpp \
+                  include/fsx/dropin/fissim/sidecar.hpp include/fsx/fabric.hpp $(LIB) | build
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	    -o $@ tests/cpp/fsx_worker_main.cpp $(LINKFSX)
+
+build/refdata: | build
+	mkdir -p $(REFDATA)/profiles $(REFDATA)/apps
+	cp $(FISSIM_REF_TESTS)/../profiles/*.json $(REFDATA)/profiles/
+	cp $(FISSIM_REF_TESTS)/../apps/*.json $(REFDATA)/apps/
+
+build/ref_test_worker: $(FISSIM_REF_TESTS)/test_worker.cpp tests/cpp/shim_main.cpp build/fsx_worker \
+                       include/fsx/dropin/fissim/executor_worker.hpp | build/refdata
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
+	    -o $@ $(FISSIM_REF_TESTS)/test_worker.cpp tests/cpp/shim_main.cpp $(LINKFSX)
+
+build/test_worker_ipc: tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp build/fsx_worker \
+                       include/fsx/dropin/fissim/executor_worker.hpp | build/refdata
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	    -DFSX_REFDATA='"$(REFDATA)"' -DFSX_WORKER_BIN='"$(CURDIR)/build/fsx_worker"' \
+	    -o $@ tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp $(LINKFSX)
+
 build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
 
 cpptests: build/test_fabric build/bench_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
-	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors; fi
+	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
+	        build/fsx_worker build/ref_test_worker build/test_worker_ipc; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -80,6 +80,13 @@ def fwd_kernel_name() -> str:
     return f"fsx::kern::forward_kernel (persistent warps, variant {v})"
 
 
+def merge_kernel_name() -> str:
+    """K3 copy instance libfsx launches (launch_merge in fsx_kernels.cu)."""
+    if os.environ.get("FSX_MERGE_TMA", "0") == "1":
+        return "fsx::merge_copy_tma_kernel<4> (persistent TMA bulk-copy ring)"
+    return "fsx::kern::merge_copy_kernel (warp per placeholder row, full grid)"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -381,8 +388,8 @@ def run_single(args):
                     "algorithmic_bytes_per_launch": fwd_bytes // fwd_launches,
                     "achieved_gbs": round(fwd_gbs, 1), "frac": round(fwd_gbs / peak, 4),
                     "traffic": traffic.get("forward_kernel")},
-        "merge": {"kernel": "fsx::merge_copy_tma_kernel (merge_scan_kernel pipelined one pass "
-                            "ahead on a side stream)",
+        "merge": {"kernel": merge_kernel_name() + " (merge_scan_kernel pipelined one pass "
+                              "ahead on a side stream)",
                   "launches_per_step": 1, "ms_per_step": round(mrg_ms, 4),
                   "algorithmic_bytes_per_launch": merge_bytes,
                   "achieved_gbs": round(mrg_gbs, 1), "frac": round(mrg_gbs / peak, 4),

@@ -103,11 +103,22 @@ int fsx_slab_usage(fsx_fabric* f, int gpu, int64_t* segments, int64_t* bytes_in_
  * owned-vector delivery of the reference ChunkCallback path
  * (sidecar.hpp:543-544).  Zero-copy consumers use fsx_slab_ptr instead. */
 int fsx_slab_read(fsx_fabric* f, int gpu, int64_t off, void* h_dst, int64_t n, void* stream);
+/* Host -> slab copy of n bytes at off, waited for: the producer half of the
+ * multi-process boundary, where a worker stages its payload in its own
+ * exported outbox slab instead of copying it into a TCP frame
+ * (executor_worker.hpp:245-256). */
+int fsx_slab_write(fsx_fabric* f, int gpu, int64_t off, const void* h_src, int64_t n, void* stream);
 /* Cross-process slabs (executor_worker.hpp:63-87 shm-name handshake ->
  * cudaIpcMemHandle).  export writes 64 handle bytes; import maps a slab owned
  * by another process as logical `gpu` (chunk flags included). */
 int fsx_slab_export(fsx_fabric* f, int gpu, void* handle64, int64_t* bytes);
 int fsx_slab_import(fsx_fabric* f, int gpu, const void* handle64, int64_t bytes);
+/* Raw CUDA IPC mapping of memory exported by another process (a worker's
+ * outbox slab, fsx_slab_export there), opened on `gpu`'s device; replaces the
+ * worker-side MappedArena shm_open/mmap (executor_worker.hpp:210-227) on the
+ * parent side.  fsx_close() closes mappings still open. */
+int fsx_ipc_open(fsx_fabric* f, int gpu, const void* handle64, void** d_ptr);
+int fsx_ipc_close(fsx_fabric* f, void* d_ptr);
 
 /* ---- chunk flags ----------------------------------------------------------
  * Per-consumer-GPU ring of 64-bit completion flags, mirrored in device memory

@@ -12,8 +12,8 @@
 //   * one receive slab per destination GPU (the reference: one arena per node),
 //     so ForwardEnvelope::location reads "gpu<G>:off<K>" and ack_raw() takes
 //     the slab's GPU;
-//   * LocalBuffer envelopes carry checksum 0 (no serial host checksum on the
-//     NVLink/HBM hop); NetworkStream envelopes keep checksum64 end to end;
+//   * LocalBuffer envelopes carry the lane-parallel dg64 digest (fused into K1)
+//     instead of the serial checksum64; NetworkStream envelopes keep checksum64;
 //   * arena(n).shm_name() is empty (device slabs are not shm segments).
 #pragma once
 
@@ -199,6 +199,10 @@ class SidecarFabric : public SidecarPort {
                                               const std::string& ref_id, const Error&)> fn) {
     engine_.set_failure_handler(std::move(fn));
   }
+
+  // fsx additions for the multi-process boundary (dropin executor_worker.hpp).
+  int64_t export_slab(int gpu, void* handle64) { return engine_.export_slab(gpu, handle64); }
+  fsx_fabric* native_handle() const { return engine_.handle(); }
 
   // Zero-copy view for raw consumers (fsx addition).
   void* slab_ptr(int gpu, int64_t offset) { return engine_.slab_ptr(gpu, offset); }

@@ -340,6 +340,17 @@ class Fabric {
     return s;
   }
 
+  // CUDA IPC export of gpu's receive slab (created on first use), for worker
+  // processes that read delivered segments in place: the role of the shm
+  // arena name in the reference's worker handshake (executor_worker.hpp:63-87).
+  int64_t export_slab(int gpu, void* handle64) {
+    node_of(gpu);
+    ensure_slab(gpu);
+    int64_t bytes = 0;
+    check(fsx_slab_export(h_, gpu, handle64, &bytes));
+    return bytes;
+  }
+
   const SidecarConfig& config() const { return config_; }
   void set_failure_handler(FailureHandler fn) { failure_handler_ = std::move(fn); }
   fsx_fabric* handle() const { return h_; }

@@ -133,6 +133,9 @@ _SIGS = {
     "fsx_slab_read": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_slab_export": [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_int64)],
     "fsx_slab_import": [C.c_void_p, C.c_int, C.c_void_p, C.c_int64],
+    "fsx_slab_write": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_ipc_open": [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)],
+    "fsx_ipc_close": [C.c_void_p, C.c_void_p],
     "fsx_flags_alloc": [C.c_void_p, C.c_int, C.c_int32, C.POINTER(C.c_int64)],
     "fsx_flag_ptr": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_void_p)],
     "fsx_forward": [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,

@@ -918,9 +918,13 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     *launches = 1;
   }
   if (b.mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
+  // Default: the LDG/STG warp-per-row kernel over a full (non-persistent)
+  // grid, 6.80 TB/s in the config-B step against 5.98 for the persistent TMA
+  // bulk-copy ring (profiles/merge_ab_r01c.jsonl, 3 alternating runs each);
+  // FSX_MERGE_TMA=1 selects the TMA kernel.
   static const bool use_tma = [] {
     const char* e = std::getenv("FSX_MERGE_TMA");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const uint32_t stage = (uint32_t)((b.row_bytes + 127) & ~int64_t{127});
   if (use_tma && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
@@ -944,7 +948,10 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     const char* e = std::getenv("FSX_MERGE_PERSIST");
     return e && e[0] == '1';
   }();
-  const int grid = (int)((persist && need > copy_grid) ? copy_grid : need);
+  // Early start (item flags) keeps the grid persistent: spinning warps must
+  // not queue thousands of CTAs behind rows whose chunks have not landed.
+  const bool bounded = persist || b.d_item_flag != nullptr;
+  const int grid = (int)((bounded && need > copy_grid) ? copy_grid : need);
   merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
   e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;

@@ -201,6 +201,7 @@ struct fsx_fabric {
   std::map<int, std::unique_ptr<Slab>> slabs;
   std::map<int, std::unique_ptr<Device>> devices;
   std::vector<Channel> channels;
+  std::map<void*, int> ipc_maps;  // fsx_ipc_open mappings -> device
   std::atomic<uint64_t> next_token{1};
   std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
 };
@@ -328,6 +329,10 @@ int fsx_close(fsx_fabric* f) {
       if (s->base) cudaFree(s->base);
       if (s->hflags) cudaFreeHost(s->hflags);
     }
+  }
+  for (auto& [p, o] : f->ipc_maps) {
+    cudaSetDevice(o);
+    cudaIpcCloseMemHandle(p);
   }
   for (auto& [o, d] : f->devices) {
     cudaSetDevice(o);
@@ -476,6 +481,56 @@ int fsx_slab_read(fsx_fabric* f, int gpu, int64_t off, void* h_dst, int64_t n, v
   cudaStream_t st = pick_stream(dev, stream);
   FSX_CUDA(cudaMemcpyAsync(h_dst, s->base + off, n, cudaMemcpyDeviceToHost, st));
   FSX_CUDA(cudaStreamSynchronize(st));
+  return FSX_OK;
+}
+
+int fsx_slab_write(fsx_fabric* f, int gpu, int64_t off, const void* h_src, int64_t n, void* stream) {
+  Slab* s = nullptr;
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    s = slab_of(f, gpu);
+    if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(gpu));
+    if (off < 0 || n < 0 || off + n > s->capacity)
+      return fail(FSX_E_VALIDATION, "slab write out of range");
+    int rc = device_state(f, s->device, &dev);
+    if (rc) return rc;
+  }
+  if (n == 0) return FSX_OK;
+  FSX_CUDA(cudaSetDevice(s->device));
+  cudaStream_t st = pick_stream(dev, stream);
+  FSX_CUDA(cudaMemcpyAsync(s->base + off, h_src, n, cudaMemcpyDefault, st));
+  FSX_CUDA(cudaStreamSynchronize(st));
+  return FSX_OK;
+}
+
+int fsx_ipc_open(fsx_fabric* f, int gpu, const void* handle64, void** d_ptr) {
+  int dev = 0;
+  int rc = find_gpu(f, gpu, &dev);
+  if (rc) return rc;
+  *d_ptr = nullptr;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  FSX_CUDA(cudaSetDevice(dev));
+  void* p = nullptr;
+  FSX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  std::lock_guard<std::mutex> lk(f->mu);
+  f->ipc_maps[p] = dev;
+  *d_ptr = p;
+  return FSX_OK;
+}
+
+int fsx_ipc_close(fsx_fabric* f, void* d_ptr) {
+  int dev = -1;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    auto it = f->ipc_maps.find(d_ptr);
+    if (it == f->ipc_maps.end()) return fail(FSX_E_NOT_FOUND, "pointer was not opened by fsx_ipc_open");
+    dev = it->second;
+    f->ipc_maps.erase(it);
+  }
+  FSX_CUDA(cudaSetDevice(dev));
+  FSX_CUDA(cudaIpcCloseMemHandle(d_ptr));
   return FSX_OK;
 }
 

@@ -6,6 +6,7 @@
 // and run on the GPU.  Supports the subset those files use: TEST_CASE, CHECK,
 // CHECK_FALSE, REQUIRE, CHECK_THROWS_AS.  main() lives in shim_main.cpp.
 #pragma once
+#include <iostream>
 
 #include <cstdio>
 #include <exception>
@@ -95,6 +96,7 @@ class Approx {
 #define REQUIRE_FALSE(...) \
   catch_shim::check(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, true)
 #define FAIL(msg) catch_shim::check(false, msg, __FILE__, __LINE__, true)
+#define WARN(msg) (std::cerr << "WARN: " << msg << "\n")
 #define CHECK_NOTHROW(expr)                                                          \
   do {                                                                               \
     bool catch_shim_ok = true;                                                       \

@@ -63,3 +63,29 @@ def test_reference_test_sidecar_against_dropin(gpu):
     rc, out = _run("ref_test_sidecar")
     assert rc == 0, out[-4000:]
     assert "13 test cases, 0 failed" in out
+
+
+def test_reference_test_worker_against_dropin(gpu):
+    """The reference's tests/test_worker.cpp (multi-process executors: encoder
+    and LLM replicas as worker processes, an mllm request across real sockets)
+    compiled unmodified against the drop-in executor_worker.hpp, with
+    build/fsx_worker as the worker binary (FISSIM_CLI_BIN)."""
+    path = os.path.join(ROOT, "build", "ref_test_worker")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/test_worker.cpp"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_test_worker")
+    rc, out = _run("ref_test_worker", timeout=300)
+    assert rc == 0, out[-4000:]
+    assert "1 test cases, 0 failed" in out, out[-4000:]
+    assert "skipping" not in out, out[-4000:]  # the worker binary was found and used
+
+
+def test_worker_ipc_outbox_and_inline_paths(gpu):
+    """Multi-process boundary on device memory: worker payloads go outbox ->
+    K1 -> receive slab -> CUDA IPC read with dg64 verification; a full outbox
+    falls back to inline frames (tests/cpp/test_worker_ipc.cpp)."""
+    path = os.path.join(ROOT, "build", "test_worker_ipc")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/include"):
+        pytest.skip("reference tree absent here and no prebuilt build/test_worker_ipc")
+    rc, out = _run("test_worker_ipc", timeout=300)
+    assert rc == 0, out[-4000:]
+    assert "2 test cases, 0 failed" in out, out[-4000:]

@@ -324,3 +324,23 @@ def test_merge_edge_cases(fab, oracle_mod):
 def test_stats_and_launch_count(fab):
     s = fab.stats()
     assert s["forwards"] > 0 and s["merges"] > 0 and s["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("env", [{"FSX_MERGE_TMA": "1", "FSX_FWD_VARIANT": "0"},
+                                 {"FSX_FWD_VARIANT": "3", "FSX_MERGE_PERSIST": "1"},
+                                 {"FSX_FWD_VARIANT": "2", "FSX_FWD_V32": "1"}])
+def test_alternate_kernel_instances(gpu, env):
+    """The non-default K1 / K3 instances (persistent-warp K1 with 16- or
+    32-byte vectors, 16 KiB tiles, TMA bulk-copy merge, persistent LDG merge)
+    are read from the environment once per process, so the forward and merge
+    parity cases are re-run in a subprocess per combination."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "(merge or forward or digest) and not alternate"],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
