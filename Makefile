@@ -81,9 +81,27 @@ build/fsx_worker: tests/cpp/fsx_worker_main.cpp include/fsx/dropin/fissim/execut
 	    -o $@ tests/cpp/fsx_worker_main.cpp $(LINKFSX)
 
 build/refdata: | build
-	mkdir -p $(REFDATA)/profiles $(REFDATA)/apps
-	cp $(FISSIM_REF_TESTS)/../profiles/*.json $(REFDATA)/profiles/
-	cp $(FISSIM_REF_TESTS)/../apps/*.json $(REFDATA)/apps/
+	mkdir -p $(REFDATA)/tests
+	cp -r $(FISSIM_REF_TESTS)/../profiles $(FISSIM_REF_TESTS)/../apps $(FISSIM_REF_TESTS)/../mixes \
+	    $(FISSIM_REF_TESTS)/../clusters $(REFDATA)/
+	cp -r $(FISSIM_REF_TESTS)/fixtures $(REFDATA)/tests/
+
+# The reference's acceptance test (all 10 criteria; criterion 4 is the
+# sidecar) and its control-plane unit tests, compiled unmodified against the
+# drop-in headers, reading the staged reference data from build/refdata.
+build/ref_acceptance: $(FISSIM_REF_TESTS)/acceptance_test.cpp build/fsx_worker \
+                      include/fsx/dropin/fissim/sidecar.hpp include/fsx/dropin/fissim/executor_worker.hpp \
+                      | build/refdata
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
+	    -o $@ $(FISSIM_REF_TESTS)/acceptance_test.cpp $(LINKFSX)
+
+build/ref_test_control_plane: $(FISSIM_REF_TESTS)/test_control_plane.cpp tests/cpp/shim_main.cpp \
+                              build/fsx_worker include/fsx/dropin/fissim/sidecar.hpp | build/refdata
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) \
+	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
+	    -o $@ $(FISSIM_REF_TESTS)/test_control_plane.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
 build/ref_test_worker: $(FISSIM_REF_TESTS)/test_worker.cpp tests/cpp/shim_main.cpp build/fsx_worker \
                        include/fsx/dropin/fissim/executor_worker.hpp | build/refdata
@@ -105,7 +123,8 @@ build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_
 cpptests: build/test_fabric build/bench_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
-	        build/fsx_worker build/ref_test_worker build/test_worker_ipc; fi
+	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \
+	        build/ref_acceptance build/ref_test_control_plane; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -585,6 +585,7 @@ def run_pairs(args, rank, world):
             torch.cuda.synchronize()
         dist.barrier()
         launches = fab.stats()["kernel_launches"] - l0
+    e2e = run_pairs_e2e(args, me, batch, lay, reqs, step, stream, red_dev)
     verified = None
     if not me.producer or me.alone:
         st = batch.status_host()
@@ -625,6 +626,7 @@ def run_pairs(args, rank, world):
                          "unit": "GB/s", "frac": round(pair_gbs / 900.0, 4), "traffic": None,
                          "peak_kind": "nominal NVLink 5 per direction (measured peer copy ~770)"},
             "gpu_launches": int(tot_launch.item()),
+            "e2e": e2e,
             "verified": bool(args.verify),
             "pinned_device": pinned,
             "clocks": clk.summary(),
@@ -633,6 +635,65 @@ def run_pairs(args, rank, world):
     dist.barrier()
     fab.close()
     dist.destroy_process_group()
+
+
+def run_pairs_e2e(args, me, batch, lay, reqs, step, stream, red_dev):
+    """e2e at N > 1 through the same public calls with HOST buffers: every
+    step the producer copies its items from pinned host memory into its own
+    GPU (H2D) and pushes them over NVLink (K1) into the consumer's slab; the
+    consumer merges with early start and reads the per-request status back
+    (D2H).  Wall clock per step, synchronised per step, max over ranks; the
+    flag/token schedule continues after the device-timed steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_12118_b200 import pairs as PR
+
+    sends = me.producer or me.alone
+    host, spans = [], []
+    if sends:
+        for i, it in enumerate(lay.items):
+            nb = it.rows * batch.rb
+            off = int(batch.src_off[i])
+            h = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+            h.copy_(batch.src_buf[off:off + nb])
+            host.append(h)
+            spans.append(batch.src_buf[off:off + nb])
+    status_h = torch.empty(len(reqs), dtype=torch.int32, pin_memory=True)
+    first = args.warmup + args.steps
+
+    def e2e_step(s):
+        if sends:
+            for h, d in zip(host, spans):
+                d.copy_(h, non_blocking=True)
+        step(s)
+        if not me.producer or me.alone:
+            status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
+        stream.synchronize()
+        if (not me.producer or me.alone) and int(status_h.numpy().max()) != 0:
+            raise RuntimeError("merge validation failed in e2e step")
+
+    steps = max(5, min(args.steps, 20))
+    with torch.cuda.stream(stream):
+        for s in range(first, first + 3):
+            e2e_step(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(first + 3, first + 3 + steps):
+            e2e_step(s)
+        dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n_pairs = PR.pairs_in(dist.get_world_size())
+    per_step = t.item() / steps
+    return {"value": round(n_pairs * lay.payload_bytes / per_step / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": n_pairs * lay.payload_bytes,
+            "d2h_bytes_per_step": n_pairs * 4 * len(reqs), "ms_per_step": round(per_step * 1e3, 3),
+            "steps": steps,
+            "path": "producer: pinned host -> own GPU (H2D) -> fsx_forward (K1 over NVLink into the "
+                    "consumer slab); consumer: early-start fsx_merge -> status D2H; wall clock per "
+                    "step, max over ranks"}
 
 
 def main():

@@ -836,6 +836,8 @@ __device__ __forceinline__ RowRef resolve_row(const fsx_merge_batch& b, int64_t 
   if (b.d_item_flag) {
     const int64_t cr = b.d_item_chunk_rows[item];
     spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
+    // the row is read by the bulk-copy (async) proxy after a generic acquire
+    asm volatile("fence.proxy.async.global;" ::: "memory");
   }
   const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * b.row_bytes;
   uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * b.row_bytes;

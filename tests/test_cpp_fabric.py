@@ -89,3 +89,27 @@ def test_worker_ipc_outbox_and_inline_paths(gpu):
     rc, out = _run("test_worker_ipc", timeout=300)
     assert rc == 0, out[-4000:]
     assert "2 test cases, 0 failed" in out, out[-4000:]
+
+
+def test_reference_acceptance_suite_on_dropin(gpu):
+    """The reference's tests/acceptance_test.cpp -- all 10 criteria, criterion
+    4 being the sidecar (24-size byte-exactness sweep, RealTime soak, 8 MiB
+    envelope) -- compiled unmodified against the drop-in headers, reading the
+    reference's data files staged into build/refdata by `make cpptests`."""
+    path = os.path.join(ROOT, "build", "ref_acceptance")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/acceptance_test.cpp"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_acceptance")
+    rc, out = _run("ref_acceptance", timeout=900)
+    assert rc == 0, out[-4000:]
+    assert "all 10 acceptance criteria passed" in out, out[-4000:]
+
+
+def test_reference_control_plane_tests_on_dropin(gpu):
+    """The reference's tests/test_control_plane.cpp (Cluster, Gateway,
+    ResourceManager, metrics_snapshot -> stats) unmodified on the drop-in."""
+    path = os.path.join(ROOT, "build", "ref_test_control_plane")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/test_control_plane.cpp"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_test_control_plane")
+    rc, out = _run("ref_test_control_plane", timeout=600)
+    assert rc == 0, out[-4000:]
+    assert " 0 failed," in out and "0 failed checks" in out, out[-4000:]

@@ -37,3 +37,4 @@ def test_pairs_protocol_same_device(gpu, config, requests):
     d = json.loads(lines[-1])
     assert d["n_gpus"] == 2 and d["verified"] and d["pinned_device"] == "0"
     assert d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
