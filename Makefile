@@ -117,6 +117,13 @@ build/test_worker_ipc: tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp bui
 	    -DFSX_REFDATA='"$(REFDATA)"' -DFSX_WORKER_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
+build/ref_test_bench: $(FISSIM_REF_TESTS)/test_bench.cpp tests/cpp/shim_main.cpp \
+                      include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build/refdata
+	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) \
+	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
+	    -o $@ $(FISSIM_REF_TESTS)/test_bench.cpp tests/cpp/shim_main.cpp $(LINKFSX)
+
 build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
 
@@ -124,7 +131,7 @@ cpptests: build/test_fabric build/bench_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \
-	        build/ref_acceptance build/ref_test_control_plane; fi
+	        build/ref_acceptance build/ref_test_control_plane build/ref_test_bench; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -474,9 +474,22 @@ def run_e2e(args, fab, reqs, rules, stream):
         for _ in range(steps):
             step()
         dt = (time.perf_counter() - t0) / steps
+        # PCIe ceiling of this box: one pinned host -> device copy of the same
+        # bytes (torch copy_, cudaMemcpyAsync), timed the same way
+        dev_buf = torch.empty(h2d, dtype=torch.uint8, device="cuda")
+        pin = torch.empty(h2d, dtype=torch.uint8, pin_memory=True)
+        dev_buf.copy_(pin, non_blocking=True)
+        stream.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(3):
+            dev_buf.copy_(pin, non_blocking=True)
+        stream.synchronize()
+        h2d_peak = h2d / ((time.perf_counter() - t1) / 3) / 1e9
+        del dev_buf, pin
     return {"value": round(h2d / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * len(reqs), "ms_per_step": round(dt * 1e3, 3),
-            "steps": steps,
+            "steps": steps, "pcie_h2d_copy_gbs": round(h2d_peak, 2),
+            "frac_of_pcie_h2d": round(h2d / dt / 1e9 / h2d_peak, 3),
             "path": "fsx_forward_host (pinned host -> consumer slab, per-frame chunks + flags) "
                     "-> fsx_merge -> status D2H, wall clock per step"}
 
@@ -499,20 +512,7 @@ def run_pairs(args, rank, world):
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
     from paper_2603_12118_b200.fabric import DeviceFabric
 
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    # FSX_PAIRS_DEVICE=<d> pins every rank to one device: the protocol test on
-    # a 1-GPU box (CUDA IPC works between processes of one device; NCCL does
-    # not allow that, so the setup/timing group is gloo there).
-    pinned = os.environ.get("FSX_PAIRS_DEVICE")
-    if pinned is not None:
-        local = int(pinned)
-    torch.cuda.set_device(local)
-    if pinned is None:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        red_dev = "cuda"
-    else:
-        dist.init_process_group("gloo")
-        red_dev = "cpu"
+    local, pinned, red_dev = _rank_device(rank)
     me = PR.role(rank, world)
     P, Cg = me.producer_gpu, me.consumer_gpu
     rules = T.RULES[CONFIG]
@@ -585,7 +585,10 @@ def run_pairs(args, rank, world):
             torch.cuda.synchronize()
         dist.barrier()
         launches = fab.stats()["kernel_launches"] - l0
-    e2e = run_pairs_e2e(args, me, batch, lay, reqs, step, stream, red_dev)
+    e2e = _e2e_phase(args, step, stream, red_dev, PR.pairs_in(world) * lay.payload_bytes,
+                     [batch.src_buf] if (me.producer or me.alone) else [],
+                     batch if (not me.producer or me.alone) else None,
+                     first=args.warmup + args.steps, n_requests=PR.pairs_in(world) * len(reqs))
     verified = None
     if not me.producer or me.alone:
         st = batch.status_host()
@@ -637,40 +640,223 @@ def run_pairs(args, rank, world):
     dist.destroy_process_group()
 
 
-def run_pairs_e2e(args, me, batch, lay, reqs, step, stream, red_dev):
-    """e2e at N > 1 through the same public calls with HOST buffers: every
-    step the producer copies its items from pinned host memory into its own
-    GPU (H2D) and pushes them over NVLink (K1) into the consumer's slab; the
-    consumer merges with early start and reads the per-request status back
-    (D2H).  Wall clock per step, synchronised per step, max over ranks; the
-    flag/token schedule continues after the device-timed steps."""
+def _rank_device(rank):
+    """(device, pinned, reduction device) for one rank: LOCAL_RANK's GPU with
+    NCCL for setup/timing, or every rank pinned to FSX_PAIRS_DEVICE with gloo
+    (the protocol tests on a 1-GPU box: CUDA IPC works between processes of
+    one device, NCCL does not allow that)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2603_12118_b200 import pairs as PR
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    pinned = os.environ.get("FSX_PAIRS_DEVICE")
+    if pinned is not None:
+        local = int(pinned)
+    torch.cuda.set_device(local)
+    if pinned is None:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return local, pinned, "cuda"
+    dist.init_process_group("gloo")
+    return local, pinned, "cpu"
 
-    sends = me.producer or me.alone
-    host, spans = [], []
-    if sends:
-        for i, it in enumerate(lay.items):
-            nb = it.rows * batch.rb
-            off = int(batch.src_off[i])
-            h = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
-            h.copy_(batch.src_buf[off:off + nb])
-            host.append(h)
-            spans.append(batch.src_buf[off:off + nb])
-    status_h = torch.empty(len(reqs), dtype=torch.int32, pin_memory=True)
-    first = args.warmup + args.steps
+
+def run_fanout(args, rank, world):
+    """Config D across the box (BASELINE.json configs[3]): encoder replicas on
+    the even ranks, LLM replicas on the odd ranks; every item goes to the LLM
+    replica the reference dispatcher policy assigns its request to
+    (paper_2603_12118_b200/fanout.py), so encoders fan out to several LLMs and
+    LLMs fan in from several encoders.  Each encoder maps the slabs of the LLMs
+    it feeds (CUDA IPC) and pushes all its items of a step with one batched K1
+    call over NVLink; each LLM merges with in-kernel early start and acks
+    every encoder that fed it.  No collective on the data path."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_12118_b200 import _native as N
+    from paper_2603_12118_b200 import fanout as FO
+    from paper_2603_12118_b200 import pairs as PR
+    from paper_2603_12118_b200 import trace as T
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch, _align
+    from paper_2603_12118_b200.fabric import DeviceFabric, _stream_ptr
+
+    local, pinned, red_dev = _rank_device(rank)
+    rules = T.RULES[CONFIG]
+    rb = rules.row_bytes
+    n_prod = len(range(0, world, 2))
+    reqs = T.config_requests(CONFIG, args.requests * n_prod)  # weak scaling: per encoder
+    chunk_rows = CHUNK_ROWS or max(it.rows for q in reqs for it in q.items)
+    pl = FO.plan(reqs, world, chunk_rows)
+    producer = rank % 2 == 0
+    me = rank // 2  # encoder ordinal (even ranks) / LLM ordinal (odd ranks)
+    stream = torch.cuda.Stream(device=local)
+    fab = DeviceFabric({g: 0 for g in range(world)}, {g: local for g in range(world)})
+    batch = None
+    if producer:
+        fab.slab_register(rank, 1 << 20)  # ack flags: index = LLM ordinal
+        mine = fab.slab_export(rank)
+    else:
+        reqs_c = [reqs[k] for k in pl.consumer_requests(me)]
+        batch = DataPlaneBatch(fab, reqs_c, rules, rank, rank, chunk_rows=chunk_rows)
+        fab.slab_register(rank, max(1 << 30, 2 * batch.lay.payload_bytes))
+        mine = fab.slab_export(rank)
+    handles = PR.exchange(mine)
+    peers = ([pl.consumers[c] for c in pl.consumers_of(me)] if producer
+             else [pl.producers[p] for p in pl.producers_of(me)])
+    for r in peers:
+        fab.slab_import(r, *handles[r])
+    if batch is not None:
+        with torch.cuda.stream(stream):
+            batch.synth_inputs(stream)
+        assert batch.alloc()
+    torch.cuda.synchronize()
+    offs = PR.exchange(None if producer else batch.slab_off.tolist())
+
+    items = pl.producer_items(me) if producer else []
+    xfers = (N.Transfer * max(len(items), 1))()
+    view = np.frombuffer(xfers, dtype=N.TRANSFER_DTYPE, count=max(len(items), 1))[:len(items)]
+    slots = [pl.item_slot(k, j) for k, j in items]
+    my_bytes = 0
+    src_buf = None
+    if producer:
+        sizes = [reqs[k].items[j].rows * rb for k, j in items]
+        src_off = np.concatenate([[0], np.cumsum([_align(n) for n in sizes])]).astype(np.int64)
+        src_buf = torch.empty(max(int(src_off[-1]), 256), dtype=torch.uint8, device=local)
+        for i, (k, j) in enumerate(items):
+            it = reqs[k].items[j]
+            fab.synth(rank, T.payload_seed(it.ref_id, 0), src_buf.data_ptr() + int(src_off[i]),
+                      sizes[i], stream)
+            c, idx = slots[i]
+            xfers[i] = N.Transfer(rank, pl.consumers[c], src_buf.data_ptr() + int(src_off[i]),
+                                  int(offs[pl.consumers[c]][idx]), sizes[i], chunk_rows * rb, 0, 0, None)
+        my_bytes = int(sum(sizes))
+        torch.cuda.synchronize()
+    acks_from = pl.consumers_of(me) if producer else []
+    acks_to = pl.producers_of(me) if not producer else []
+
+    def step(s):
+        if producer:
+            if s > 0:  # every LLM this encoder fed acked step s-1: slab segments free again
+                for c in acks_from:
+                    fab.stream_wait_flags(rank, c, 1, PR.ack_token(s - 1), stream)
+            if items:
+                sch = [pl.schedule(s, c, idx) for c, idx in slots]
+                view["flag_base"] = [b for b, _ in sch]
+                view["token"] = [t for _, t in sch]
+                N.call("fsx_forward_batch", fab._h, len(items), xfers, 0, _stream_ptr(stream))
+        else:
+            for idx, (k, j) in enumerate(pl.consumer_items[me]):
+                batch.flag_base[idx], batch.tokens[idx] = pl.schedule(s, me, idx)
+                batch.n_chunks[idx] = pl.chunks[k][j]
+            batch.merge(stream, early_start=True)  # waits per chunk inside K3
+            for p in acks_to:
+                fab.signal_flags(pl.producers[p], me, 1, PR.ack_token(s), rank, stream)
+
+    with torch.cuda.stream(stream):
+        for s in range(args.warmup):
+            step(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        l0 = fab.stats()["kernel_launches"]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            start.record(stream)
+            for s in range(args.warmup, args.warmup + args.steps):
+                step(s)
+            end.record(stream)
+            torch.cuda.synchronize()
+        dist.barrier()
+        launches = fab.stats()["kernel_launches"] - l0
+    total_payload = sum(it.rows * rb for q in reqs for it in q.items)
+    e2e = _e2e_phase(args, step, stream, red_dev, total_payload,
+                     [src_buf] if producer else [], batch if not producer else None,
+                     first=args.warmup + args.steps, n_requests=len(reqs))
+    if not producer:
+        st = batch.status_host()
+        assert (st == 0).all(), st
+        if args.verify:
+            local_b = DataPlaneBatch(fab, batch.lay.requests, rules, rank, rank, chunk_rows=chunk_rows)
+            local_b.synth_inputs()
+            assert local_b.alloc()
+            local_b.forward(host_notify=False)
+            local_b.merge()
+            torch.cuda.synchronize()
+            ok = bool(torch.equal(local_b.embeds, batch.embeds))
+            local_b.release()
+            assert ok, "fan-in merged embeddings differ from the local reference pass"
+    ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    tot_launch = torch.tensor([launches], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(tot_launch)
+    # per-encoder egress and per-LLM ingress bytes of a step (NVLink direction bound)
+    io = torch.tensor([my_bytes if producer else batch.lay.payload_bytes], dtype=torch.float64,
+                      device=red_dev)
+    io_all = [torch.zeros_like(io) for _ in range(world)]
+    dist.all_gather(io_all, io)
+    ms_step = ms.item() / args.steps
+    if rank == 0:
+        egress = [io_all[r].item() for r in pl.producers]
+        ingress = [io_all[r].item() for r in pl.consumers]
+        busiest = max(egress + ingress) / (ms_step * 1e-3) / 1e9
+        fan_out = [len(pl.consumers_of(p)) for p in range(len(pl.producers))]
+        fan_in = [len(pl.producers_of(c)) for c in range(len(pl.consumers))]
+        line = {
+            "metric": METRIC, "value": round(total_payload / (ms_step * 1e-3) / 1e9, 2),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "merged_req_per_s": round(len(reqs) / (ms_step * 1e-3), 1),
+            "config": {"workload": CONFIGS[CONFIG]["workload"] + ", encoders on even ranks -> LLM "
+                                   "replicas on odd ranks, reference select_replica placement "
+                                   "(fan-out / fan-in over NVLink), early-start merge",
+                       "requests_per_step": len(reqs), "requests_per_encoder": args.requests,
+                       "encoders": len(pl.producers), "llms": len(pl.consumers),
+                       "fan_out": fan_out, "fan_in": fan_in,
+                       "egress_bytes_per_encoder": egress, "ingress_bytes_per_llm": ingress,
+                       "chunk_bytes": chunk_rows * rb,
+                       "parallelism": f"{len(pl.producers)} encoder GPUs x {len(pl.consumers)} LLM GPUs"},
+            "roofline": {"bound": "nvlink", "achieved": round(busiest, 1), "peak": 900.0,
+                         "unit": "GB/s", "frac": round(busiest / 900.0, 4), "traffic": None,
+                         "what": "busiest GPU's NVLink direction (max encoder egress / LLM ingress)",
+                         "peak_kind": "nominal NVLink 5 per direction (measured peer copy ~770)"},
+            "gpu_launches": int(tot_launch.item()),
+            "e2e": e2e,
+            "verified": bool(args.verify),
+            "pinned_device": pinned,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    fab.close()
+    dist.destroy_process_group()
+
+
+def _e2e_phase(args, step, stream, red_dev, payload_all, src_bufs, recv_batch, first, n_requests):
+    """e2e at N > 1 with HOST buffers: every step each sender copies its
+    source buffer from pinned host memory onto its GPU (H2D) before pushing
+    it (K1 over NVLink); each receiver merges and reads its per-request status
+    back (D2H).  Wall clock per step, synchronised per step, max over ranks;
+    the flag/token schedule continues after the device-timed steps."""
+    import torch
+    import torch.distributed as dist
+
+    host = []
+    for b in src_bufs:
+        h = torch.empty(b.numel(), dtype=torch.uint8, pin_memory=True)
+        h.copy_(b)
+        host.append(h)
+    nreq = len(recv_batch.lay.requests) if recv_batch is not None else 0
+    status_h = torch.empty(max(nreq, 1), dtype=torch.int32, pin_memory=True)
 
     def e2e_step(s):
-        if sends:
-            for h, d in zip(host, spans):
-                d.copy_(h, non_blocking=True)
+        for h, d in zip(host, src_bufs):
+            d.copy_(h, non_blocking=True)
         step(s)
-        if not me.producer or me.alone:
-            status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
+        if recv_batch is not None:
+            status_h[:nreq].copy_(recv_batch.status[:nreq], non_blocking=True)
         stream.synchronize()
-        if (not me.producer or me.alone) and int(status_h.numpy().max()) != 0:
+        if recv_batch is not None and nreq and int(status_h[:nreq].numpy().max()) != 0:
             raise RuntimeError("merge validation failed in e2e step")
 
     steps = max(5, min(args.steps, 20))
@@ -685,15 +871,13 @@ def run_pairs_e2e(args, me, batch, lay, reqs, step, stream, red_dev):
         dt = time.perf_counter() - t0
     t = torch.tensor([dt], dtype=torch.float64, device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    n_pairs = PR.pairs_in(dist.get_world_size())
     per_step = t.item() / steps
-    return {"value": round(n_pairs * lay.payload_bytes / per_step / 1e9, 3), "unit": "GB/s",
-            "h2d_bytes_per_step": n_pairs * lay.payload_bytes,
-            "d2h_bytes_per_step": n_pairs * 4 * len(reqs), "ms_per_step": round(per_step * 1e3, 3),
-            "steps": steps,
-            "path": "producer: pinned host -> own GPU (H2D) -> fsx_forward (K1 over NVLink into the "
-                    "consumer slab); consumer: early-start fsx_merge -> status D2H; wall clock per "
-                    "step, max over ranks"}
+    return {"value": round(payload_all / per_step / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": payload_all, "d2h_bytes_per_step": 4 * n_requests,
+            "ms_per_step": round(per_step * 1e3, 3), "steps": steps,
+            "path": "senders: pinned host -> own GPU (H2D) -> fsx_forward (K1 over NVLink into the "
+                    "receiver's slab); receivers: early-start fsx_merge -> status D2H; wall clock "
+                    "per step, max over ranks"}
 
 
 def main():
@@ -711,6 +895,8 @@ def main():
         return
     if world <= 1:
         run_single(args)
+    elif CONFIG == "D":
+        run_fanout(args, rank, world)
     else:
         run_pairs(args, rank, world)
 

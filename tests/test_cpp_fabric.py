@@ -113,3 +113,15 @@ def test_reference_control_plane_tests_on_dropin(gpu):
     rc, out = _run("ref_test_control_plane", timeout=600)
     assert rc == 0, out[-4000:]
     assert " 0 failed," in out and "0 failed checks" in out, out[-4000:]
+
+
+def test_reference_bench_harness_tests_on_dropin(gpu):
+    """The reference's tests/test_bench.cpp (run_experiment over a Cluster:
+    end-to-end serving whose every intermediate tensor crosses the sidecar)
+    unmodified on the drop-in."""
+    path = os.path.join(ROOT, "build", "ref_test_bench")
+    if not os.path.exists(path) and not os.path.exists("/root/reference/proj/tests/test_bench.cpp"):
+        pytest.skip("reference tree absent here and no prebuilt build/ref_test_bench")
+    rc, out = _run("ref_test_bench", timeout=600)
+    assert rc == 0, out[-4000:]
+    assert " 0 failed," in out and "0 failed checks" in out, out[-4000:]

@@ -38,3 +38,24 @@ def test_pairs_protocol_same_device(gpu, config, requests):
     assert d["n_gpus"] == 2 and d["verified"] and d["pinned_device"] == "0"
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+def test_fanout_config_d_four_ranks_same_device(gpu):
+    """Config D fan-out (2 encoders -> 2 LLM replicas, reference select_replica
+    placement, so both LLMs receive from both encoders) as 4 processes pinned to
+    one device: IPC slab imports per edge, batched K1 into several peers'
+    slabs, early-start merge with fan-in, per-edge acks; merged embeddings
+    verified against a local pass on every LLM rank."""
+    env = dict(os.environ, FSX_PAIRS_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", "bench.py", "--gpus", "4",
+           "--steps", "3", "--warmup", "2", "--config", "D", "--requests", "6", "--verify"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert lines, p.stdout[-2000:]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == 4 and d["verified"]
+    assert d["config"]["encoders"] == 2 and d["config"]["llms"] == 2
+    assert max(d["config"]["fan_in"]) == 2 and max(d["config"]["fan_out"]) == 2
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0

@@ -84,3 +84,53 @@ def test_setup_exchange_and_agreement(world):
     assert res[0][3] == res[1][3]
     if world == 3:
         assert res[2][1] is None  # odd rank out runs alone
+
+
+def test_fanout_plan_follows_select_replica():
+    """Config D placement (paper_2603_12118_b200/fanout.py): least-outstanding
+    + round-robin selection per task, many-to-many edges, per-consumer flag
+    schedule disjoint across items and steps."""
+    from paper_2603_12118_b200 import fanout
+    from paper_2603_12118_b200 import trace as T
+
+    reqs = T.config_requests("D", 64)
+    pl = fanout.plan(reqs, 8, 1024)
+    assert pl.producers == [0, 2, 4, 6] and pl.consumers == [1, 3, 5, 7]
+    # with nothing completing inside a step, least-outstanding + RR is exact
+    # round robin per task: LLM replicas in request order ...
+    assert pl.llm_of == [k % 4 for k in range(64)]
+    # ... and each modality's encoder replicas in item order
+    for mod in ("image", "video", "audio"):
+        seq = [pl.enc_of[k][j] for k, q in enumerate(reqs) for j, it in enumerate(q.items)
+               if it.modality == mod]
+        assert seq == [i % 4 for i in range(len(seq))]
+    # every item is produced by exactly one encoder and lands in exactly one LLM list
+    all_items = sorted(kj for p in range(4) for kj in pl.producer_items(p))
+    assert all_items == sorted((k, j) for k, q in enumerate(reqs) for j in range(len(q.items)))
+    assert sorted(kj for c in range(4) for kj in pl.consumer_items[c]) == all_items
+    # fan-out and fan-in both happen
+    assert any(len(pl.consumers_of(p)) > 1 for p in range(4))
+    assert any(len(pl.producers_of(c)) > 1 for c in range(4))
+    # flag ranges of one consumer are disjoint within a step and tokens unique
+    for c in range(4):
+        for s in (0, 1, 63, 64):
+            spans, toks = [], set()
+            for idx, (k, j) in enumerate(pl.consumer_items[c]):
+                b, t = pl.schedule(s, c, idx)
+                spans.append((b, b + pl.chunks[k][j]))
+                assert t != 0 and t not in toks
+                toks.add(t)
+                assert pl.item_slot(k, j) == (c, idx)
+            spans.sort()
+            assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_fanout_plan_two_ranks_is_a_pair():
+    from paper_2603_12118_b200 import fanout
+    from paper_2603_12118_b200 import trace as T
+
+    reqs = T.config_requests("D", 8)
+    pl = fanout.plan(reqs, 2, 1024)
+    assert pl.producers == [0] and pl.consumers == [1]
+    assert set(pl.llm_of) == {0}
+    assert all(e == 0 for es in pl.enc_of for e in es)
