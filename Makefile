@@ -129,7 +129,7 @@ build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_
 
 cpptests: build/test_fabric build/bench_fabric
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
-	    $(MAKE) -s build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
+	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \
 	        build/ref_acceptance build/ref_test_control_plane build/ref_test_bench; fi
 

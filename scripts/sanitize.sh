@@ -13,3 +13,9 @@ for tool in memcheck racecheck synccheck; do
   echo "$tool rc=$?" | tee -a $OUT/sanitize_summary.txt
   grep -E "ERROR SUMMARY|passed|failed" $OUT/sanitize_$tool.txt | tail -3 | tee -a $OUT/sanitize_summary.txt
 done
+# the non-default kernel instances (persistent-warp K1, TMA bulk-copy merge)
+FSX_FWD_VARIANT=0 FSX_MERGE_TMA=1 timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 \
+    --error-exitcode 3 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider \
+    -k "$SEL" > $OUT/sanitize_memcheck_alt.txt 2>&1
+echo "memcheck (FSX_FWD_VARIANT=0 FSX_MERGE_TMA=1) rc=$?" | tee -a $OUT/sanitize_summary.txt
+grep -E "ERROR SUMMARY|passed|failed" $OUT/sanitize_memcheck_alt.txt | tail -3 | tee -a $OUT/sanitize_summary.txt

@@ -3,7 +3,11 @@
 chunk-size sweep of BASELINE config E plus the config-B video item, timed with
 CUDA events on the launching stream.  Tuning knobs come from the environment
 (FSX_FWD_VARIANT, FSX_FWD_UNIT).  Prints one JSON line per size; compares with
-cudaMemcpyAsync D2D (torch copy_) of the same bytes."""
+cudaMemcpyAsync D2D (torch copy_) of the same bytes.
+
+  --graph   capture the repetitions of both arms in a CUDA graph and time the
+            replay: kernel throughput without the per-call host path (which
+            dominates below ~16 MiB when each call goes through Python)."""
 from __future__ import annotations
 
 import json
@@ -15,7 +19,13 @@ sys.path.insert(0, ROOT)
 
 
 def main():
+    import argparse
+
     import torch
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--graph", action="store_true")
+    args = ap.parse_args()
 
     from paper_2603_12118_b200.fabric import DeviceFabric
 
@@ -33,27 +43,50 @@ def main():
     for n, chunk in cases:
         # enough repetitions that each measurement moves >= 2 GiB
         reps = max(8, (2 << 30) // n)
+        if args.graph:
+            reps = min(reps, 256)
         off = fab.slab_alloc(1, n)
         nch = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
         with torch.cuda.stream(s):
             for _ in range(3):
                 fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+            torch.cuda.synchronize()
+            if args.graph:
+                fb = fab.flags_alloc(1, nch)
+                g, gc = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(reps):  # fixed flags/token: nobody waits on them here
+                        fab.forward(0, src.data_ptr(), 1, off, n, chunk, fb, s, token=(1 << 40) + n,
+                                    host_notify=False)
+                with torch.cuda.graph(gc, stream=s):
+                    for _ in range(reps):
+                        ref[:n].copy_(src[:n])
+                g.replay()
+                gc.replay()
+                torch.cuda.synchronize()
+                fwd_run, cpy_run = g.replay, gc.replay
+            else:
+                def fwd_run():
+                    for _ in range(reps):
+                        fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+
+                def cpy_run():
+                    for _ in range(reps):
+                        ref[:n].copy_(src[:n])
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            for _ in range(reps):
-                fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+            fwd_run()
             e1.record(s)
             e1.synchronize()
             ms = e0.elapsed_time(e1) / reps
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(s)
-            for _ in range(reps):
-                ref[:n].copy_(src[:n])
+            cpy_run()
             c1.record(s)
             c1.synchronize()
             cms = c0.elapsed_time(c1) / reps
         fab.slab_free(1, off)
-        print(json.dumps({"variant": variant, "unit": unit, "bytes": n, "chunk_bytes": chunk,
+        print(json.dumps({"variant": variant, "graph": args.graph, "bytes": n, "chunk_bytes": chunk,
                           "chunks": nch, "us": round(ms * 1e3, 2),
                           "hbm_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),
                           "memcpy_us": round(cms * 1e3, 2),
