@@ -356,6 +356,14 @@ class Fabric {
   fsx_fabric* handle() const { return h_; }
 
  private:
+  // A delivered chunk waiting for its turn: envelope, slab offset, and the
+  // small-message ticket (fsx_put_small) whose read-back it owns, or -1.
+  struct Parked {
+    Envelope env;
+    int64_t off = -1;
+    int64_t ticket = -1;
+  };
+
   struct RefState {
     std::string request_id;
     int dst_gpu = -1;
@@ -364,7 +372,7 @@ class Fabric {
     RawChunkCallback raw_cb;
     RefErrorCallback on_error;
     int64_t next_seq = 0;
-    std::map<int64_t, std::pair<Envelope, int64_t>> parked;  // seq -> (env, slab offset)
+    std::map<int64_t, Parked> parked;  // by seq
     std::shared_ptr<Error> failed;
   };
 
@@ -418,18 +426,32 @@ class Fabric {
   }
 
   // Allocate a segment and start moving the bytes; false when the slab is full.
-  bool start_copy(Pending& ps, int64_t* off, uint64_t* token, int64_t* flag_base, int32_t* n_chunks) {
+  bool start_copy(Pending& ps, int64_t* off, uint64_t* token, int64_t* flag_base, int32_t* n_chunks,
+                  int64_t* ticket) {
     const int dst = ps.env.dst_gpu;
     ensure_slab(dst);
     check(fsx_slab_alloc(h_, dst, std::max<int64_t>(ps.env.chunk_bytes, 1), off));
     if (*off < 0) return false;
     const int64_t n = ps.env.chunk_bytes;
+    const bool local = Traits::is_local(ps.env);
+    *ticket = -1;
+    if (!ps.src_is_device && n > 0 && n <= FSX_SMALL_MAX) {
+      // small host span (per-token hidden states, codes): one asynchronous
+      // H2D + device read-back, waited for at delivery
+      check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
+      if (*ticket >= 0) {
+        if (local) ps.env.checksum = digest64(ps.src, static_cast<size_t>(n));
+        *n_chunks = 0;
+        *token = 0;
+        digest_slot_ = nullptr;
+        return true;
+      }
+    }
     int64_t cb = config_.device_chunk_bytes;
     if (cb <= 0 || cb >= n) cb = 0;
     *n_chunks = cb ? static_cast<int32_t>((n + cb - 1) / cb) : 1;
     check(fsx_flags_alloc(h_, dst, *n_chunks, flag_base));
     *token = 0;
-    const bool local = Traits::is_local(ps.env);
     if (ps.src_is_device) {
       // K1, with the dg64 digest of the source fused into the copy
       fsx_transfer t{ps.env.src_gpu, dst, ps.src, *off, n, cb, *flag_base, 0, nullptr};
@@ -463,48 +485,50 @@ class Fabric {
 
   // sidecar.hpp:465-483: place now, notify after the modeled latency.
   bool place_local(Pending& ps) {
-    int64_t off = -1, flag_base = 0;
+    int64_t off = -1, flag_base = 0, ticket = -1;
     uint64_t token = 0;
     int32_t n_chunks = 1;
-    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks)) return false;
+    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks, &ticket)) return false;
     // The source is borrowed (caller span) or owned by a Pending about to be
     // dropped, so the copy completes before we return, exactly like the
-    // reference's memcpy into the arena (sidecar.hpp:470).  The batched C ABI
-    // (fsx_forward on a stream) is the asynchronous path.
-    wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    // reference's memcpy into the arena (sidecar.hpp:470); a small message has
+    // been staged in the pinned mailbox instead and is waited for at delivery.
+    // The batched C ABI (fsx_forward on a stream) is the asynchronous path.
+    if (ticket < 0) wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
     if (digest_slot_) check(fsx_read_u64(h_, ps.env.src_gpu, digest_slot_, &ps.env.checksum, nullptr));
     ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
     const double lat = config_.latency_ms(Transport::LocalBuffer, ps.env.chunk_bytes);
     added_latency_ms_ += lat;
     auto env = std::make_shared<Envelope>(ps.env);
     Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.deliver",
-                     [this, env, off] { deliver(*env, off); });
+                     [this, env, off, ticket] { deliver(*env, off, ticket); });
     return true;
   }
 
   // sidecar.hpp:487-496: stage a network arrival into the slab, deliver now.
   bool stage_network(Pending& ps) {
-    int64_t off = -1, flag_base = 0;
+    int64_t off = -1, flag_base = 0, ticket = -1;
     uint64_t token = 0;
     int32_t n_chunks = 1;
-    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks)) return false;
+    if (!start_copy(ps, &off, &token, &flag_base, &n_chunks, &ticket)) return false;
     ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
-    wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
-    deliver(ps.env, off);
+    if (ticket < 0) wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    deliver(ps.env, off, ticket);
     return true;
   }
 
   // sidecar.hpp:498-525
-  void deliver(const Envelope& env, int64_t off) {
+  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1) {
     const std::string key = key_of(env.ref_id, env.dst_gpu);
     RefState& st = refs_[key];
     if (st.request_id.empty()) st.request_id = env.request_id;
     if (st.failed) {
+      drop_ticket(ticket);
       release_segment(env.dst_gpu, off);
       place_backlog(env.dst_gpu);
       return;
     }
-    st.parked.emplace(env.seq, std::make_pair(env, off));
+    st.parked.emplace(env.seq, Parked{env, off, ticket});
     if (st.has_interest) {
       drain(st);
       return;
@@ -519,8 +543,9 @@ class Fabric {
     if (it == refs_.end() || it->second.has_interest) return;
     auto p = it->second.parked.find(seq);
     if (p == it->second.parked.end()) return;
-    const int slab = p->second.first.dst_gpu;
-    release_segment(slab, p->second.second);
+    const int slab = p->second.env.dst_gpu;
+    drop_ticket(p->second.ticket);
+    release_segment(slab, p->second.off);
     it->second.parked.erase(p);
     ++orphan_reclaims_;
     place_backlog(slab);
@@ -530,10 +555,12 @@ class Fabric {
   void drain(RefState& st) {
     for (auto it = st.parked.find(st.next_seq); it != st.parked.end();
          it = st.parked.find(st.next_seq)) {
-      Envelope env = it->second.first;
-      const int64_t off = it->second.second;
+      Envelope env = it->second.env;
+      const int64_t off = it->second.off;
+      const int64_t ticket = it->second.ticket;
       st.parked.erase(it);
       if (st.raw_cb) {
+        drop_ticket(ticket);  // waits until the bytes are in the slab
         ++transfers_;
         bytes_forwarded_ += env.chunk_bytes;
         ++st.next_seq;
@@ -544,10 +571,22 @@ class Fabric {
       // device hop is checked with dg64 recomputed on the consumer GPU over
       // the slab segment, the network hop with the reference checksum64.
       const bool local = Traits::is_local(env);
-      const bool dev_ok = !local || slab_digest(env.dst_gpu, off, env.chunk_bytes) == env.checksum;
       std::vector<uint8_t> bytes(static_cast<size_t>(env.chunk_bytes));
-      if (env.chunk_bytes > 0)
-        check(fsx_slab_read(h_, env.dst_gpu, off, bytes.data(), env.chunk_bytes, nullptr));
+      bool dev_ok = true;
+      if (ticket >= 0) {
+        // small message: bytes and dg64 were read back from the slab on the
+        // device right after they landed (fsx_put_small)
+        const void* mail = nullptr;
+        uint64_t dev_digest = 0;
+        check(fsx_ticket_wait(h_, ticket, &mail, &dev_digest));
+        std::memcpy(bytes.data(), mail, bytes.size());
+        check(fsx_ticket_free(h_, ticket));
+        dev_ok = !local || dev_digest == env.checksum;
+      } else {
+        dev_ok = !local || slab_digest(env.dst_gpu, off, env.chunk_bytes) == env.checksum;
+        if (env.chunk_bytes > 0)
+          check(fsx_slab_read(h_, env.dst_gpu, off, bytes.data(), env.chunk_bytes, nullptr));
+      }
       const bool ok = local ? dev_ok : checksum64(bytes.data(), bytes.size()) == env.checksum;
       release_segment(env.dst_gpu, off);
       place_backlog(env.dst_gpu);
@@ -570,8 +609,17 @@ class Fabric {
   void release_segment(int slab, int64_t off) { check(fsx_slab_free(h_, slab, off)); }
 
   void drop_parked(RefState& st) {
-    for (auto& [seq, e] : st.parked) release_segment(e.first.dst_gpu, e.second);
+    for (auto& [seq, e] : st.parked) {
+      drop_ticket(e.ticket);
+      release_segment(e.env.dst_gpu, e.off);
+    }
     st.parked.clear();
+  }
+
+  // Wait for a small message's copy and read-back, then recycle its mailbox
+  // slot; the slab segment may be reused only after that.
+  void drop_ticket(int64_t ticket) {
+    if (ticket >= 0) check(fsx_ticket_free(h_, ticket));
   }
 
   // sidecar.hpp:571-582

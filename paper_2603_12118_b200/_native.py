@@ -136,6 +136,10 @@ _SIGS = {
     "fsx_slab_write": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_ipc_open": [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)],
     "fsx_ipc_close": [C.c_void_p, C.c_void_p],
+    "fsx_put_small": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)],
+    "fsx_ticket_wait": [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
+    "fsx_ticket_free": [C.c_void_p, C.c_int64],
+    "fsx_flush_small": [C.c_void_p],
     "fsx_flags_alloc": [C.c_void_p, C.c_int, C.c_int32, C.POINTER(C.c_int64)],
     "fsx_flag_ptr": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_void_p)],
     "fsx_forward": [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,

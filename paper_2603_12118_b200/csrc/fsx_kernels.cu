@@ -440,6 +440,48 @@ __global__ void __launch_bounds__(256) digest_kernel(const uint8_t* __restrict__
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)acc);
 }
 
+// Small host messages (fsx_put_small), one CTA per message: copy the staged
+// bytes from the mapped pinned mailbox (PCIe reads) into the slab segment,
+// then read the landed segment back into the slot while computing its dg64,
+// so a ChunkCallback consumer gets the bytes that are in device memory,
+// verified on the device.  bar.sync orders the CTA's slab stores before its
+// own re-reads (coherent loads, no .nc).
+constexpr int kMailThreads = 256;
+__global__ void __launch_bounds__(kMailThreads) mailbox_kernel(const __grid_constant__ MailStep m) {
+  __shared__ uint64_t red[kMailThreads / 32];
+  uint8_t* slot = m.mail + m.slot[blockIdx.x];
+  MailHeader* h = reinterpret_cast<MailHeader*>(slot);
+  uint8_t* bytes = slot + kMailHeader;
+  uint8_t* dst = h->dst;
+  const int64_t n = h->n;
+  const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;  // slots are 64 B aligned
+  const int64_t nv = vec ? n >> 4 : 0;
+  for (int64_t i = threadIdx.x; i < nv; i += kMailThreads)
+    st_v4(dst + 16 * i, ld_v4(bytes + 16 * i));
+  for (int64_t j = nv * 16 + threadIdx.x; j < n; j += kMailThreads) dst[j] = bytes[j];
+  __syncthreads();
+  uint64_t acc = 0;
+  for (int64_t i = threadIdx.x; i < nv; i += kMailThreads) {
+    const uint4 v = ld_v4(dst + 16 * i);
+    *reinterpret_cast<uint4*>(bytes + 16 * i) = v;
+    acc += dg_vec(v, 2 * (uint64_t)i);
+  }
+  __syncthreads();  // every vector store into the slot precedes the tail rewrite below
+  if (threadIdx.x == 0) {
+    const int64_t from = nv * 16;
+    for (int64_t j = from; j < n; ++j) bytes[j] = dst[j];
+    acc += dg_bytes(dst, from, n) + (uint64_t)n * 0x9e3779b97f4a7c15ull;
+  }
+  acc = warp_sum_u64(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < kMailThreads / 32; ++w) t += red[w];
+    h->digest = t;
+  }
+}
+
 __global__ void set_flags_kernel(FlagSetArgs a) {
   for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
     st_release_sys(&a.dflags[i], a.token);
@@ -891,6 +933,12 @@ __global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, u
 }
 
 constexpr int kTmaStages = 4;
+
+cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st) {
+  if (m.n <= 0) return cudaSuccess;
+  mailbox_kernel<<<m.n, kMailThreads, 0, st>>>(m);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, cudaStream_t st) {
   digest_kernel<<<grid, 256, 0, st>>>(p, n, out);

@@ -67,8 +67,25 @@ struct ChanStep {
   ChanRow c[kChanMaxRows];
 };
 
+// Small host messages (fsx_put_small): each staged in a slot of a mapped
+// pinned mailbox, header first.  One launch moves a batch of them.
+struct MailHeader {
+  uint8_t* dst;     // slab destination (device)
+  int64_t n;        // bytes (<= FSX_SMALL_MAX)
+  uint64_t digest;  // dg64 of the landed bytes, written by the kernel
+};
+constexpr int64_t kMailHeader = 64;  // bytes start 64 B into the slot
+constexpr int kMailMaxBatch = 256;
+struct MailStep {
+  uint8_t* mail;                  // mailbox base (mapped pinned host memory)
+  int32_t n;
+  int32_t _pad;
+  int64_t slot[kMailMaxBatch];    // slot offsets
+};
+
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
 cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, cudaStream_t st);
+cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st);
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);

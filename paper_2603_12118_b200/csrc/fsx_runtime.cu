@@ -202,6 +202,25 @@ struct fsx_fabric {
   std::map<int, std::unique_ptr<Device>> devices;
   std::vector<Channel> channels;
   std::map<void*, int> ipc_maps;  // fsx_ipc_open mappings -> device
+  // fsx_put_small: pinned mapped mailbox (first-fit slots), tickets, and per
+  // device the staged messages not yet flushed to the GPU
+  uint8_t* mail = nullptr;
+  BlockList mail_blocks;
+  struct Ticket {
+    int64_t slot = -1;   // mailbox offset of the slot header, -1 = free ticket
+    int device = -1;
+    int64_t batch = -1;  // flush batch (its event), -1 = still staged
+  };
+  std::vector<Ticket> tickets;
+  std::vector<int64_t> free_tickets;
+  struct MailBatch {
+    cudaEvent_t ev = nullptr;
+    int refs = 0;
+  };
+  std::vector<MailBatch> batches;
+  std::vector<int64_t> free_batches;
+  std::map<int, std::vector<int64_t>> staged;  // device -> staged tickets
+  std::map<int, int64_t> staged_bytes;         // device -> their payload bytes
   std::atomic<uint64_t> next_token{1};
   std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
 };
@@ -330,6 +349,9 @@ int fsx_close(fsx_fabric* f) {
       if (s->hflags) cudaFreeHost(s->hflags);
     }
   }
+  for (auto& b : f->batches)
+    if (b.ev) cudaEventDestroy(b.ev);
+  if (f->mail) cudaFreeHost(f->mail);
   for (auto& [p, o] : f->ipc_maps) {
     cudaSetDevice(o);
     cudaIpcCloseMemHandle(p);
@@ -829,6 +851,130 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
   f->forwards++;
   f->bytes_forwarded += bytes;
   if (token) *token = tok;
+  return FSX_OK;
+}
+
+constexpr int64_t kMailBytes = int64_t{16} << 20;
+constexpr int64_t kMailStageBytes = int64_t{2} << 20;  // flush once this much is staged
+
+namespace {
+
+// Launch the staged messages of `device` as one batch (caller holds f->mu).
+int flush_staged(fsx_fabric* f, int device) {
+  auto it = f->staged.find(device);
+  if (it == f->staged.end() || it->second.empty()) return FSX_OK;
+  std::vector<int64_t>& q = it->second;
+  Device* dev = nullptr;
+  int rc = device_state(f, device, &dev);
+  if (rc) return rc;
+  int64_t bid;
+  if (f->free_batches.empty()) {
+    f->batches.emplace_back();
+    bid = (int64_t)f->batches.size() - 1;
+  } else {
+    bid = f->free_batches.back();
+    f->free_batches.pop_back();
+  }
+  fsx_fabric::MailBatch& mb = f->batches[bid];
+  FSX_CUDA(cudaSetDevice(device));
+  if (!mb.ev) FSX_CUDA(cudaEventCreateWithFlags(&mb.ev, cudaEventDisableTiming));
+  for (size_t at = 0; at < q.size(); at += fsx::kMailMaxBatch) {
+    fsx::MailStep ms{};
+    ms.mail = f->mail;
+    ms.n = (int32_t)std::min<size_t>(fsx::kMailMaxBatch, q.size() - at);
+    for (int32_t k = 0; k < ms.n; ++k) ms.slot[k] = f->tickets[q[at + k]].slot;
+    FSX_CUDA(fsx::launch_mailbox(ms, dev->stream));
+    f->launches++;
+  }
+  FSX_CUDA(cudaEventRecord(mb.ev, dev->stream));
+  mb.refs = (int)q.size();
+  for (int64_t t : q) f->tickets[t].batch = bid;
+  q.clear();
+  f->staged_bytes[device] = 0;
+  return FSX_OK;
+}
+
+}  // namespace
+
+int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
+                  int64_t* ticket) {
+  *ticket = -1;
+  if (n <= 0 || n > FSX_SMALL_MAX) return FSX_OK;
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, dst_gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (dst_off < 0 || dst_off + n > s->capacity)
+    return fail(FSX_E_VALIDATION, "small put overruns the destination slab");
+  if (!f->mail) {
+    FSX_CUDA(cudaHostAlloc(&f->mail, kMailBytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    f->mail_blocks.reset(kMailBytes);
+  }
+  const int64_t slot = f->mail_blocks.alloc(fsx::kMailHeader + (n + 63) / 64 * 64);
+  if (slot < 0) return FSX_OK;  // mailbox full: caller takes the synchronous path
+  int64_t id;
+  if (f->free_tickets.empty()) {
+    f->tickets.emplace_back();
+    id = (int64_t)f->tickets.size() - 1;
+  } else {
+    id = f->free_tickets.back();
+    f->free_tickets.pop_back();
+  }
+  f->tickets[id] = fsx_fabric::Ticket{slot, s->device, -1};
+  // slot: header {slab destination, bytes, digest} then the bytes
+  fsx::MailHeader* h = reinterpret_cast<fsx::MailHeader*>(f->mail + slot);
+  h->dst = s->base + dst_off;
+  h->n = n;
+  h->digest = 0;
+  std::memcpy(f->mail + slot + fsx::kMailHeader, h_src, (size_t)n);
+  std::vector<int64_t>& q = f->staged[s->device];
+  q.push_back(id);
+  f->forwards++;
+  f->bytes_forwarded += n;
+  *ticket = id;
+  if ((f->staged_bytes[s->device] += n) >= kMailStageBytes) return flush_staged(f, s->device);
+  return FSX_OK;
+}
+
+int fsx_flush_small(fsx_fabric* f) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  for (auto& [device, q] : f->staged) {
+    int rc = flush_staged(f, device);
+    if (rc) return rc;
+  }
+  return FSX_OK;
+}
+
+int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest) {
+  cudaEvent_t ev = nullptr;
+  int64_t slot = -1;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || f->tickets[ticket].slot < 0)
+      return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
+    if (f->tickets[ticket].batch < 0) {
+      int rc = flush_staged(f, f->tickets[ticket].device);  // everything staged on that device
+      if (rc) return rc;
+    }
+    ev = f->batches[f->tickets[ticket].batch].ev;
+    slot = f->tickets[ticket].slot;
+  }
+  FSX_CUDA(cudaEventSynchronize(ev));
+  const fsx::MailHeader* h = reinterpret_cast<const fsx::MailHeader*>(f->mail + slot);
+  if (h_bytes) *h_bytes = f->mail + slot + fsx::kMailHeader;
+  if (digest) *digest = *reinterpret_cast<const volatile uint64_t*>(&h->digest);
+  return FSX_OK;
+}
+
+int fsx_ticket_free(fsx_fabric* f, int64_t ticket) {
+  // the slot and the slab segment may only be reused once the batch has run
+  int rc = fsx_ticket_wait(f, ticket, nullptr, nullptr);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(f->mu);
+  fsx_fabric::Ticket& t = f->tickets[ticket];
+  f->mail_blocks.release(t.slot);
+  if (--f->batches[t.batch].refs == 0) f->free_batches.push_back(t.batch);
+  t = fsx_fabric::Ticket{};
+  f->free_tickets.push_back(ticket);
   return FSX_OK;
 }
 

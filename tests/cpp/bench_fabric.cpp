@@ -68,5 +68,37 @@ int main(int argc, char** argv) {
                 (long long)f.stats().integrity_errors);
   }
   cudaFree(d);
+
+  // Config C through the same API: per decode step every active request's
+  // thinker sends one hidden-state row (host span, streaming ref, seq = step)
+  // and the talker's ChunkCallback receives it (executor_sim.hpp:370-381,
+  // 556-562).  Reported as microseconds per step and messages per second.
+  for (int row : {7168, 2048}) {
+    const int batch = 32, steps = 200;
+    EventLoop k;
+    SidecarConfig cfg;
+    SidecarFabric f(k, topo, cfg);
+    std::vector<uint8_t> rowbuf(row);
+    or_synth_payload_into(7, rowbuf.data(), row);
+    int64_t got = 0;
+    for (int r = 0; r < batch; ++r)
+      f.register_interest(1, "req-" + std::to_string(r) + "/r0001",
+                          [&](const ForwardEnvelope&, std::vector<uint8_t> b) { got += (int64_t)b.size(); });
+    auto step = [&](int s) {
+      for (int r = 0; r < batch; ++r)
+        f.send("req-" + std::to_string(r), DataRef{"req-" + std::to_string(r) + "/r0001", 0, true}, 0, 1,
+               std::span<const uint8_t>(rowbuf.data(), row), s, false);
+      k.run_until_idle();
+    };
+    for (int s = 0; s < 10; ++s) step(s);
+    got = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int s = 10; s < 10 + steps; ++s) step(s);
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("{\"mode\": \"stream_host_span_chunk_callback\", \"rows_per_step\": %d, \"row_bytes\": %d, "
+                "\"us_per_step\": %.1f, \"msgs_per_s\": %.0f, \"bytes_ok\": %s}\n",
+                batch, row, sec / steps * 1e6, batch * steps / sec,
+                got == (int64_t)batch * steps * row ? "true" : "false");
+  }
   return 0;
 }

@@ -344,3 +344,37 @@ def test_alternate_kernel_instances(gpu, env):
                         "-k", "(merge or forward or digest) and not alternate"],
                        env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+
+
+def test_small_put_batch_roundtrip(fab, oracle_mod):
+    """fsx_put_small (config C per-token messages through the drop-in's host
+    span path): many staged messages flushed as one launch; every slab segment
+    holds the bytes, the read-back equals them, and the device dg64 equals the
+    oracle restatement.  Sizes cover 4 B codes, unaligned tails and the 64 KiB
+    limit; over-limit and empty puts decline (ticket -1)."""
+    import ctypes as C
+
+    sizes = [4, 1, 7, 15, 16, 17, 2048, 7168, 4099, 65536] * 4
+    msgs = [oracle_mod.synth_payload(1000 + i, n) for i, n in enumerate(sizes)]
+    offs, tickets = [], []
+    for m in msgs:
+        off = fab.slab_alloc(2, len(m))
+        t = C.c_int64(-2)
+        N.call("fsx_put_small", fab._h, 2, off, m, len(m), C.byref(t))
+        assert t.value >= 0
+        offs.append(off)
+        tickets.append(t.value)
+    for m, off, t in zip(msgs, offs, tickets):
+        p, d = C.c_void_p(), C.c_uint64()
+        N.call("fsx_ticket_wait", fab._h, t, C.byref(p), C.byref(d))
+        assert C.string_at(p.value, len(m)) == m
+        assert d.value == oracle_mod.C.or_digest64(m, len(m))
+        assert fab.slab_read(2, off, len(m)) == m
+        N.call("fsx_ticket_free", fab._h, t)
+        fab.slab_free(2, off)
+    for n in (0, 65537):
+        t = C.c_int64(-2)
+        N.call("fsx_put_small", fab._h, 2, 0, b"\0" * max(n, 1), n, C.byref(t))
+        assert t.value == -1
+    with pytest.raises(N.FsxError):
+        N.call("fsx_ticket_wait", fab._h, tickets[0], None, None)  # already freed
