@@ -153,6 +153,14 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * consumer on the same GPU that reads them right after (the merge); the
  * producer's source is always read with evict_first. */
 #define FSX_FWD_L2_KEEP 2u
+/* FSX_FWD_BULK: move this batch's tiles with the bulk-copy engine
+ * (forward_tma_kernel: cp.async.bulk global->shared->global, 32 KiB per
+ * 32-thread CTA, 16 registers) instead of register loads/stores -- the faster
+ * K1 when it runs alone (1.01 of the measured copy peak on 256 MiB).  Applies
+ * to local, 16-byte aligned transfers without a fused digest; others in the
+ * batch keep the register tile kernel.  FSX_FWD_VARIANT=5 makes it the
+ * default for every call. */
+#define FSX_FWD_BULK 4u
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                    uint32_t options, void* stream);
@@ -239,6 +247,18 @@ int fsx_signal_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, u
 #define FSX_MERGE_FULL 0
 #define FSX_MERGE_SCAN_ONLY 1
 #define FSX_MERGE_COPY_ONLY 2
+/* Option bits OR-ed into `mode` (copy phase, LDG kernel):
+ * FSX_MERGE_DISCARD   once a placeholder row has been read from its slab
+ *   segment, discard the row's L2 lines (discard.global.L2): a merged slab
+ *   segment is dead until it is released and rewritten, so its bytes, which
+ *   K1 (or the peer's NVLink stores) left in this GPU's L2, are never written
+ *   back to HBM.  The segment must not be read again before it is rewritten.
+ * FSX_MERGE_COLOCATED early start while the producer's K1 runs on this same
+ *   GPU: at most one merge CTA per SM, so spinning merge warps can never take
+ *   every slot K1 needs to make progress. */
+#define FSX_MERGE_DISCARD 0x100
+#define FSX_MERGE_COLOCATED 0x200
+#define FSX_MERGE_MODE_MASK 0xff
 typedef struct fsx_merge_batch {
   int32_t num_requests;
   int32_t num_items;

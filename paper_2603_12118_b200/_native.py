@@ -36,10 +36,13 @@ NETWORK_STREAM = 1
 
 FWD_HOST_NOTIFY = 1
 FWD_L2_KEEP = 2
+FWD_BULK = 4
 
 MERGE_FULL = 0
 MERGE_SCAN_ONLY = 1
 MERGE_COPY_ONLY = 2
+MERGE_DISCARD = 0x100
+MERGE_COLOCATED = 0x200
 
 
 class FsxError(RuntimeError):

@@ -24,6 +24,7 @@ namespace fsx {
 namespace kern {
 
 constexpr int kFwdThreads = 256;
+constexpr int kTmaTileBytes = 32768;  // K1 bulk-copy tile (forward_tma_kernel)
 // K1 variants: <vectors per lane per batch, min CTAs per SM>.  0: 16 x 16 B
 // (8 KiB per warp batch, 2 CTAs/SM), 1: 8 x 16 B at 4 CTAs/SM (register cap 64).
 constexpr int kMergeThreads = 256;
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_bat
   const int64_t rb = b.row_bytes;
   const bool vec_rows = (rb & 15) == 0;
   const bool newest_first = b.d_item_flag == nullptr;  // L2 reuse, see merge_copy_tma_kernel
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
   for (int64_t k = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
        k < b.total_item_rows; k += warps) {
     const int64_t g = newest_first ? b.total_item_rows - 1 - k : k;
@@ -623,6 +625,209 @@ __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_bat
     } else {
       for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
     }
+    if (discard) {
+      // the row's values are in registers and stored: drop its slab lines
+      // from L2 without writing them back (whole 128-byte lines only)
+      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
+      for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
+  }
+}
+
+// K3 merge, phase 2, early-start form: rows are taken in arrival order in runs
+// of kStreamRun consecutive placeholder rows per warp.  The warp resolves the
+// run's first row once (binary searches), prefetches the run's placeholder
+// positions with one coalesced load (one lane per row), and walks the rows
+// keeping item- and request-level values in registers, re-reading them only
+// when the run crosses into the next item or request, and spinning on a chunk
+// flag only when the run enters a new chunk.  A persistent grid of these warps
+// follows the producer's K1 chunk by chunk with far less per-row latency than
+// resolving every row from scratch (merge_copy_kernel).
+constexpr int kStreamRun = 16;
+__global__ void __launch_bounds__(kMergeThreads) merge_stream_kernel(fsx_merge_batch b,
+                                                                     unsigned long long* work) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
+  const int64_t rb = b.row_bytes;
+  const int64_t n = b.total_item_rows;
+  const int64_t runs = (n + kStreamRun - 1) / kStreamRun;
+  const bool vec_rows = (rb & 15) == 0;
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
+  const bool early = b.d_item_flag != nullptr;
+  // runs are claimed from the work counter in arrival order (every warp works
+  // on the earliest rows whose chunk has landed), or statically without one
+  auto claim = [&](int64_t prev) -> int64_t {
+    if (!work) return prev < 0 ? (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5) : prev + warps;
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(work, 1ull);
+    return (int64_t)__shfl_sync(0xffffffffu, u, 0);
+  };
+  for (int64_t u = claim(-1); u < runs; u = claim(u)) {
+    const int64_t g0 = u * kStreamRun;
+    const int64_t g1 = min(g0 + kStreamRun, n);
+    const int32_t mypos = (g0 + lane < g1) ? b.d_scratch[g0 + lane] : 0;
+    // every lane runs the same (uniform) resolution: same addresses, broadcast loads
+    int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g0);
+    while (b.d_item_row_off[item + 1] <= g0) ++item;
+    int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+    while (b.d_req_item_off[req + 1] <= item) ++req;
+    int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
+    const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+    int64_t req_row = b.d_req_row_off[req];
+    int32_t req_ok = b.d_status[req] == 0;
+    int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
+    int64_t waited = -1;  // chunk of the current item already waited for
+    for (int64_t g = g0; g < g1; ++g) {
+      if (g >= item_end) {  // next item (skipping zero-row items), maybe next request
+        do {
+          ++item;
+        } while (b.d_item_row_off[item + 1] <= g);
+        item_beg = b.d_item_row_off[item];
+        item_end = b.d_item_row_off[item + 1];
+        item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+        if (b.d_req_item_off[req + 1] <= item) {
+          do {
+            ++req;
+          } while (b.d_req_item_off[req + 1] <= item);
+          req_row = b.d_req_row_off[req];
+          req_ok = b.d_status[req] == 0;
+        }
+        if (early) chunk_rows = b.d_item_chunk_rows[item];
+        waited = -1;
+      }
+      const int32_t pos = __shfl_sync(0xffffffffu, mypos, (int)(g - g0));
+      if (!req_ok) continue;  // validation failed: request untouched
+      const int64_t j = g - item_beg;
+      if (early) {
+        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
+        if (c != waited) {
+          if (lane == 0) spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+          __syncwarp();
+          waited = c;
+        }
+      }
+      const uint8_t* src = item_src + j * rb;
+      uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb;
+      if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const int64_t nv = rb >> 4;
+        const uint4* sv = reinterpret_cast<const uint4*>(src);
+        uint4* dv = reinterpret_cast<uint4*>(dst);
+        for (int64_t base = 0; base < nv; base += 32 * kMergeUnroll) {
+          uint4 r[kMergeUnroll];
+#pragma unroll
+          for (int k = 0; k < kMergeUnroll; ++k) {
+            const int64_t i = base + k * 32 + lane;
+            if (i < nv) r[k] = ld_v4(sv + i);
+          }
+#pragma unroll
+          for (int k = 0; k < kMergeUnroll; ++k) {
+            const int64_t i = base + k * 32 + lane;
+            if (i < nv) st_v4(dv + i, r[k]);
+          }
+        }
+      } else {
+        for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
+      }
+      if (discard) {
+        const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
+        for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+      }
+    }
+  }
+}
+
+// K3 merge, phase 2, "follow" form for early start: warp w of W moves the
+// placeholder rows g = w, w + W, w + 2W, ... in increasing order, so at any
+// moment the whole grid works on a window of about W rows right behind the
+// producer (one chunk's worth for W ~ chunk rows) instead of some warps
+// holding runs many chunks ahead.  Behind K1 on the same GPU that window is
+// still in L2 when it is read, and with FSX_MERGE_DISCARD its lines are
+// dropped from L2 right after, so the slab never round-trips through HBM.
+// Item / request values are re-read only when the warp's row crosses into the
+// next item; the row's chunk flag is checked (lane 0, acquire) before its
+// loads; the position comes from the scan's scratch.
+template <int U>
+__global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_batch b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (kMergeThreads / 32);
+  const int64_t w = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
+  const int64_t rb = b.row_bytes;
+  const int64_t n = b.total_item_rows;
+  if (w >= n) return;
+  const bool vec_rows = (rb & 15) == 0;
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
+  const bool early = b.d_item_flag != nullptr;
+  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, w);
+  while (b.d_item_row_off[item + 1] <= w) ++item;
+  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+  while (b.d_req_item_off[req + 1] <= item) ++req;
+  int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
+  const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
+  int64_t req_row = b.d_req_row_off[req];
+  bool req_ok = b.d_status[req] == 0;
+  int64_t waited = -1;
+  for (int64_t g = w; g < n; g += W) {
+    if (g >= item_end) {
+      do {
+        ++item;
+      } while (b.d_item_row_off[item + 1] <= g);
+      item_beg = b.d_item_row_off[item];
+      item_end = b.d_item_row_off[item + 1];
+      item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+      if (early) chunk_rows = b.d_item_chunk_rows[item];
+      waited = -1;
+      if (b.d_req_item_off[req + 1] <= item) {
+        do {
+          ++req;
+        } while (b.d_req_item_off[req + 1] <= item);
+        req_row = b.d_req_row_off[req];
+        req_ok = b.d_status[req] == 0;
+      }
+    }
+    if (!req_ok) continue;  // validation failed: request untouched
+    const int64_t j = g - item_beg;
+    const int32_t pos = b.d_scratch[g];
+    if (early) {
+      const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
+      if (c != waited) {
+        if (lane == 0) spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+        __syncwarp();
+        waited = c;
+      }
+    }
+    const uint8_t* src = item_src + j * rb;
+    uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb;
+    if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      const int64_t nv = rb >> 4;
+      const uint4* sv = reinterpret_cast<const uint4*>(src);
+      uint4* dv = reinterpret_cast<uint4*>(dst);
+      for (int64_t base = 0; base < nv; base += 32 * U) {
+        uint4 r[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) r[k] = ld_v4(sv + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) st_v4(dv + i, r[k]);
+        }
+      }
+    } else {
+      for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
+    }
+    if (discard) {
+      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
+      for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
   }
 }
 
@@ -654,6 +859,8 @@ __global__ void synth_kernel(uint64_t s0, uint8_t* __restrict__ dst, int64_t n) 
 }  // namespace kern
 
 using namespace kern;
+
+__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b);
 
 // ---------------------------------------------------------------------------
 // Launchers
@@ -692,12 +899,31 @@ int merge_copy_blocks_per_sm() {
 }
 
 int forward_tile_bytes(int variant) {
+  if (variant == 5) return kTmaTileBytes;          // 32 KiB bulk-copy tiles
   if (variant == 3) return kTileThreads * 4 * 16;  // 16 KiB tiles
   if (variant == 4) return kTileThreads * 8 * 16;  // 32 KiB tiles
   return 0;                                        // persistent warp kernels
 }
 
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s) {
+  if (variant == 5) {
+    // bulk-copy tiles for local, 16-byte aligned transfers without a fused
+    // digest; anything else in the batch takes the register tile kernel
+    bool ok = true;
+    for (int k = 0; k < b.n; ++k) ok = ok && b.t[k].vec && !b.t[k].peer && !b.t[k].digest;
+    if (ok) {
+      const int64_t tiles = b.unit_off[b.n];
+      if (tiles <= 0) return cudaSuccess;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaTileBytes);
+        attr = true;
+      }
+      forward_tma_kernel<<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
+      return cudaGetLastError();
+    }
+    variant = 4;
+  }
   if (forward_tile_bytes(variant)) {
     // one CTA per tile: grid = total tiles of the batch (16-byte vectors)
     FwdBatch bb = b;
@@ -934,6 +1160,305 @@ __global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, u
 
 constexpr int kTmaStages = 4;
 
+// K1, bulk-copy tile form (FSX_FWD_VARIANT=5; local slabs, no fused digest).
+// One 32-thread CTA per 32 KiB tile, one elected thread: two 16 KiB halves are
+// loaded global->shared by the copy engine (mbarrier complete_tx), each half
+// is stored shared->global as soon as it has landed, then the thread waits
+// for the stores, orders them (async proxy) before its generic acq_rel count
+// into the chunk counter, and the CTA completing the chunk publishes the flag
+// like forward_tile_kernel.  Bytes in flight cost shared memory, not
+// registers: 6 such CTAs per SM keep 192 KiB in flight with ~2 K registers,
+// which leaves the register file to a merge running next to K1.
+__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b) {
+  extern __shared__ __align__(128) uint8_t tile_mem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x != 0) return;
+  const int64_t gt = blockIdx.x;
+  int i = 0;
+  while (gt >= b.unit_off[i + 1]) ++i;
+  const FwdArgs& a = b.t[i];
+  const int64_t u = gt - b.unit_off[i];
+  const int64_t c = u / a.chunk_units;
+  const int64_t sl = u - c * a.chunk_units;
+  const int64_t cbeg = c * a.chunk_bytes;
+  const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
+  const int64_t beg = cbeg + sl * a.slice;
+  const int64_t end = min(beg + a.slice, cend);
+  const int64_t vend = beg + ((end - beg) & ~int64_t{15});  // beg is 16-byte aligned
+  const uint32_t sbase = tma::smem_u32(tile_mem);
+  const int64_t half = ((vend - beg) / 2 + 15) & ~int64_t{15};
+  const int64_t len0 = min(half, vend - beg), len1 = (vend - beg) - len0;
+  tma::mbar_init(tma::smem_u32(&bars[0]), 1);
+  tma::mbar_init(tma::smem_u32(&bars[1]), 1);
+  tma::mbar_fence_init();
+  if (len0 > 0) {
+    tma::mbar_expect_tx(tma::smem_u32(&bars[0]), (uint32_t)len0);
+    tma::bulk_load(sbase, a.src + beg, (uint32_t)len0, tma::smem_u32(&bars[0]));
+  }
+  if (len1 > 0) {
+    tma::mbar_expect_tx(tma::smem_u32(&bars[1]), (uint32_t)len1);
+    tma::bulk_load(sbase + (uint32_t)len0, a.src + beg + len0, (uint32_t)len1, tma::smem_u32(&bars[1]));
+  }
+  if (len0 > 0) {
+    tma::mbar_wait(tma::smem_u32(&bars[0]), 0);
+    tma::bulk_store(a.dst + beg, sbase, (uint32_t)len0);
+  }
+  if (len1 > 0) {
+    tma::mbar_wait(tma::smem_u32(&bars[1]), 0);
+    tma::bulk_store(a.dst + beg + len0, sbase + (uint32_t)len0, (uint32_t)len1);
+  }
+  tma::bulk_commit();
+  for (int64_t j = vend; j < end; ++j) a.dst[j] = a.src[j];  // sub-16-byte tail
+  tma::bulk_wait_all();
+  // the tile's bulk stores are complete: order them (async proxy) before the
+  // generic release that counts the tile
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (a.counters == nullptr) return;
+  const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
+  const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
+  if (prev == units - 1) {
+    a.counters[c] = 0u;
+    if (a.peer) {
+      __threadfence_system();
+      st_release_sys(&a.dflags[c], a.token);
+    } else {
+      st_release_gpu(&a.dflags[c], a.token);
+    }
+    if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
+  }
+}
+
+
+
+// K3 merge, phase 2, early-start form (default whenever the batch carries item
+// flags: the N>1 consumer following NVLink pushes, and the N=1 colocated
+// pipeline following K1 on the same GPU).  One elected thread per 32-thread
+// CTA claims runs of kTmaRun consecutive placeholder rows from a global work
+// counter, so every CTA works on the earliest rows whose chunk has landed
+// (dynamic, arrival order), and moves each row with the bulk-copy engine:
+// cp.async.bulk global->shared (mbarrier complete_tx) then shared->global,
+// an S-stage ring with S-1 rows in flight per CTA and no registers spent on
+// the bytes -- so the merge CTAs sit next to K1's CTAs on every SM without
+// taking the registers K1 needs.  Within a run the thread walks rows
+// incrementally (item / request values re-read only at boundaries, a chunk
+// flag spun on only when the run enters a new chunk).  With FSX_MERGE_DISCARD
+// a row's slab lines are discarded from L2 once its bulk load has completed.
+// Bulk-copy form of the follow kernel (FSX_MERGE_STREAM=3): CTA c of C (32
+// threads, one elected thread) moves rows g = c, c + C, ... in increasing
+// order through an S-stage shared-memory ring (S-1 rows in flight), so the
+// grid's window behind the producer stays about (S-1) x C rows wide while the
+// bytes in flight cost shared memory instead of registers.
+template <int S>
+__global__ void __launch_bounds__(32) merge_follow_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  __shared__ __align__(8) uint64_t bars[S];
+  if (threadIdx.x != 0) return;
+  const uint32_t sbase = tma::smem_u32(stage_mem);
+  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
+  tma::mbar_fence_init();
+  const int64_t rb = b.row_bytes, n = b.total_item_rows, C = gridDim.x;
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
+  const bool early = b.d_item_flag != nullptr;
+  int64_t g = blockIdx.x;
+  if (g >= n) return;
+  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g);
+  while (b.d_item_row_off[item + 1] <= g) ++item;
+  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+  while (b.d_req_item_off[req + 1] <= item) ++req;
+  int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
+  const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
+  int64_t req_row = b.d_req_row_off[req];
+  bool req_ok = b.d_status[req] == 0;
+  int64_t waited = -1;
+  auto next = [&](uint8_t** dst, const uint8_t** src) -> bool {
+    for (; g < n; g += C) {
+      if (g >= item_end) {
+        do {
+          ++item;
+        } while (b.d_item_row_off[item + 1] <= g);
+        item_beg = b.d_item_row_off[item];
+        item_end = b.d_item_row_off[item + 1];
+        item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+        if (early) chunk_rows = b.d_item_chunk_rows[item];
+        waited = -1;
+        if (b.d_req_item_off[req + 1] <= item) {
+          do {
+            ++req;
+          } while (b.d_req_item_off[req + 1] <= item);
+          req_row = b.d_req_row_off[req];
+          req_ok = b.d_status[req] == 0;
+        }
+      }
+      if (!req_ok) continue;
+      const int64_t j = g - item_beg;
+      if (early) {
+        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
+        if (c != waited) {
+          spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          waited = c;
+        }
+      }
+      const uint8_t* sr = item_src + j * rb;
+      uint8_t* d = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[g]) * rb;
+      if ((reinterpret_cast<uintptr_t>(sr) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)rb) & 15) {
+        for (int64_t i = 0; i < rb; ++i) d[i] = sr[i];
+        continue;
+      }
+      *dst = d;
+      *src = sr;
+      g += C;
+      return true;
+    }
+    return false;
+  };
+  uint8_t* dst_of[S];
+  const uint8_t* src_of[S];
+  auto issue = [&](int64_t k) -> bool {
+    const int s = (int)(k % S);
+    if (!next(&dst_of[s], &src_of[s])) return false;
+    const uint32_t bar = tma::smem_u32(&bars[s]);
+    tma::mbar_expect_tx(bar, (uint32_t)rb);
+    tma::bulk_load(sbase + s * stage_bytes, src_of[s], (uint32_t)rb, bar);
+    return true;
+  };
+  int64_t issued = 0;
+  while (issued < S - 1 && issue(issued)) ++issued;
+  uint32_t parity = 0;
+  for (int64_t k = 0; k < issued; ++k) {
+    const int s = (int)(k % S);
+    tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
+    parity ^= 1u << s;
+    tma::bulk_store(dst_of[s], sbase + s * stage_bytes, (uint32_t)rb);
+    tma::bulk_commit();
+    if (discard) {
+      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src_of[s]) + 127) & ~uintptr_t{127};
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src_of[s]) + rb) & ~uintptr_t{127};
+      for (uintptr_t a = lo; a < hi; a += 128) asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
+    tma::bulk_wait_read1();
+    if (issue(issued)) ++issued;
+  }
+  tma::bulk_wait_all();
+}
+
+constexpr int kTmaRun = 8;
+
+template <int S>
+__global__ void __launch_bounds__(32) merge_stream_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes,
+                                                              unsigned long long* work) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  __shared__ __align__(8) uint64_t bars[S];
+  if (threadIdx.x != 0) return;
+  const uint32_t sbase = tma::smem_u32(stage_mem);
+  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
+  tma::mbar_fence_init();
+  const int64_t rb = b.row_bytes, n = b.total_item_rows;
+  const int64_t runs = (n + kTmaRun - 1) / kTmaRun;
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
+  const bool early = b.d_item_flag != nullptr;
+  // row generator state
+  int64_t g = 0, g_end = 0, item = 0, req = 0, item_beg = 0, item_end = 0, req_row = 0, chunk_rows = 0;
+  int64_t waited = -1;
+  bool req_ok = true, done = false;
+  const uint8_t* item_src = nullptr;
+  auto load_item = [&]() {
+    item_beg = b.d_item_row_off[item];
+    item_end = b.d_item_row_off[item + 1];
+    item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+    if (early) chunk_rows = b.d_item_chunk_rows[item];
+    waited = -1;
+  };
+  auto load_req = [&]() {
+    req_row = b.d_req_row_off[req];
+    req_ok = b.d_status[req] == 0;
+  };
+  // next placeholder row to move: false once the work counter is exhausted
+  auto next = [&](uint8_t** dst, const uint8_t** src) -> bool {
+    for (;;) {
+      if (g >= g_end) {
+        if (done) return false;
+        const int64_t u = (int64_t)atomicAdd(work, 1ull);
+        if (u >= runs) {
+          done = true;
+          return false;
+        }
+        g = u * kTmaRun;
+        g_end = min(g + kTmaRun, n);
+        item = upper_index(b.d_item_row_off, b.num_items + 1, g);
+        while (b.d_item_row_off[item + 1] <= g) ++item;
+        req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+        while (b.d_req_item_off[req + 1] <= item) ++req;
+        load_item();
+        load_req();
+      } else if (g >= item_end) {
+        do {
+          ++item;
+        } while (b.d_item_row_off[item + 1] <= g);
+        load_item();
+        if (b.d_req_item_off[req + 1] <= item) {
+          do {
+            ++req;
+          } while (b.d_req_item_off[req + 1] <= item);
+          load_req();
+        }
+      }
+      const int64_t row = g++;
+      if (!req_ok) continue;  // validation failed: request untouched
+      const int64_t j = row - item_beg;
+      if (early) {
+        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
+        if (c != waited) {
+          spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+          // the row is read by the bulk-copy (async) proxy after a generic acquire
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          waited = c;
+        }
+      }
+      const uint8_t* s = item_src + j * rb;
+      uint8_t* d = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[row]) * rb;
+      if ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)rb) & 15) {
+        for (int64_t i = 0; i < rb; ++i) d[i] = s[i];  // bulk copies need 16-byte alignment
+        continue;
+      }
+      *dst = d;
+      *src = s;
+      return true;
+    }
+  };
+  uint8_t* dst_of[S];
+  const uint8_t* src_of[S];
+  auto issue = [&](int64_t k) -> bool {
+    const int s = (int)(k % S);
+    if (!next(&dst_of[s], &src_of[s])) return false;
+    const uint32_t bar = tma::smem_u32(&bars[s]);
+    tma::mbar_expect_tx(bar, (uint32_t)rb);
+    tma::bulk_load(sbase + s * stage_bytes, src_of[s], (uint32_t)rb, bar);
+    return true;
+  };
+  int64_t issued = 0;
+  while (issued < S - 1 && issue(issued)) ++issued;
+  uint32_t parity = 0;
+  for (int64_t k = 0; k < issued; ++k) {
+    const int s = (int)(k % S);
+    tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
+    parity ^= 1u << s;
+    tma::bulk_store(dst_of[s], sbase + s * stage_bytes, (uint32_t)rb);
+    tma::bulk_commit();
+    if (discard) {  // the slab row has been read into shared memory: drop its L2 lines
+      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src_of[s]) + 127) & ~uintptr_t{127};
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src_of[s]) + rb) & ~uintptr_t{127};
+      for (uintptr_t a = lo; a < hi; a += 128) asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
+    tma::bulk_wait_read1();  // the store issued one row ago has left shared memory
+    if (issue(issued)) ++issued;
+  }
+  tma::bulk_wait_all();
+}
+
+
+
 cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st) {
   if (m.n <= 0) return cudaSuccess;
   mailbox_kernel<<<m.n, kMailThreads, 0, st>>>(m);
@@ -957,17 +1482,19 @@ cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches,
+                         unsigned long long* work) {
   *launches = 0;
   if (b.num_requests <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
-  if (b.mode != FSX_MERGE_COPY_ONLY) {
+  const int base_mode = b.mode & FSX_MERGE_MODE_MASK;
+  if (base_mode != FSX_MERGE_COPY_ONLY) {
     merge_scan_kernel<<<b.num_requests, kScanThreads, 0, s>>>(b);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *launches = 1;
   }
-  if (b.mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
+  if (base_mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
   // Default: the LDG/STG warp-per-row kernel over a full (non-persistent)
   // grid, 6.80 TB/s in the config-B step against 5.98 for the persistent TMA
   // bulk-copy ring (profiles/merge_ab_r01c.jsonl, 3 alternating runs each);
@@ -977,7 +1504,8 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     return e && e[0] == '1';
   }();
   const uint32_t stage = (uint32_t)((b.row_bytes + 127) & ~int64_t{127});
-  if (use_tma && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
+  if (use_tma && !b.d_item_flag && !(b.mode & FSX_MERGE_DISCARD) && b.row_bytes % 16 == 0 &&
+      stage * kTmaStages <= 48 * 1024) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -992,16 +1520,67 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     if (e == cudaSuccess) ++*launches;
     return e;
   }
+  if (b.d_item_flag) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // early-start kernel: 0 follow (default), 1 register runs, 2 bulk-copy runs
+    static const int stream_kind = [] {
+      const char* e = std::getenv("FSX_MERGE_STREAM");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (stream_kind == 0) {
+      // one CTA per SM beside K1 on the same GPU, else the copy grid
+      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
+      const int64_t want = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
+      static const int unroll = [] {
+        const char* e = std::getenv("FSX_FOLLOW_UNROLL");
+        return e ? std::atoi(e) : 16;
+      }();
+      if (unroll == 8)
+        merge_follow_kernel<8><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
+      else
+        merge_follow_kernel<16><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
+    } else if (stream_kind == 3 && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
+      static const int per_sm_env = [] {
+        const char* e = std::getenv("FSX_FOLLOW_TMA_PER_SM");
+        return e ? std::atoi(e) : 4;
+      }();
+      const size_t smem = (size_t)stage * kTmaStages;
+      const int64_t cap = (int64_t)sms * per_sm_env;
+      merge_follow_tma_kernel<kTmaStages>
+          <<<(unsigned)(b.total_item_rows < cap ? b.total_item_rows : cap), 32, smem, s>>>(b, stage);
+    } else if (stream_kind == 2 && work && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
+      // early start: bulk-copy rows claimed in arrival order; colocated with
+      // K1: 4 CTAs per SM (registers stay with K1), else the occupancy limit
+      const size_t smem = (size_t)stage * kTmaStages;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_stream_tma_kernel<kTmaStages>, 32,
+                                                        smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      if ((b.mode & FSX_MERGE_COLOCATED) && per_sm > 4) per_sm = 4;
+      const int64_t runs = (b.total_item_rows + kTmaRun - 1) / kTmaRun;
+      const int64_t cap = (int64_t)sms * per_sm;
+      merge_stream_tma_kernel<kTmaStages><<<(unsigned)(runs < cap ? runs : cap), 32, smem, s>>>(b, stage, work);
+    } else {
+      // register form (FSX_MERGE_STREAM_LDG=1): static run assignment; one
+      // CTA per SM when the producer shares this GPU
+      const int64_t runs = (b.total_item_rows + kStreamRun - 1) / kStreamRun;
+      const int64_t want = (runs + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
+      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
+      merge_stream_kernel<<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b, work);
+    }
+    e = cudaGetLastError();
+    if (e == cudaSuccess) ++*launches;
+    return e;
+  }
   const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
   // one warp per row and no persistence (full grid) unless FSX_MERGE_PERSIST=1
   static const bool persist = [] {
     const char* e = std::getenv("FSX_MERGE_PERSIST");
     return e && e[0] == '1';
   }();
-  // Early start (item flags) keeps the grid persistent: spinning warps must
-  // not queue thousands of CTAs behind rows whose chunks have not landed.
-  const bool bounded = persist || b.d_item_flag != nullptr;
-  const int grid = (int)((bounded && need > copy_grid) ? copy_grid : need);
+  const int grid = (int)((persist && need > copy_grid) ? copy_grid : need);
   merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
   e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;

@@ -91,7 +91,9 @@ cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);
+// `work`: a zeroed device counter for the early-start (item flags) kernel.
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches,
+                         unsigned long long* work);
 cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s);
 
 // Occupancy helpers.

@@ -731,7 +731,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     const int64_t rounds = std::max<int64_t>(1, (units + max_warps - 1) / max_warps);
     const int64_t warps = (units + rounds - 1) / rounds;
     const int grid = (int)std::max<int64_t>(1, (warps + warps_per_cta - 1) / warps_per_cta);
-    FSX_CUDA(fsx::launch_forward(b, fwd_variant(), grid, st));
+    FSX_CUDA(fsx::launch_forward(b, (options & FSX_FWD_BULK) ? 5 : fwd_variant(), grid, st));
     f->launches++;
     for (int32_t k = 0; k < cnt; ++k) {
       const fsx_transfer& x = t[first + k];
@@ -1076,8 +1076,12 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
     return fail(FSX_E_VALIDATION, "merge batch is missing a device array");
   if (b->d_item_flag && (!b->d_item_token || !b->d_item_chunk_rows))
     return fail(FSX_E_VALIDATION, "early-start merge needs tokens and chunk rows");
-  if (b->mode < FSX_MERGE_FULL || b->mode > FSX_MERGE_COPY_ONLY)
+  const int base_mode = b->mode & FSX_MERGE_MODE_MASK;
+  if (base_mode > FSX_MERGE_COPY_ONLY ||
+      (b->mode & ~(FSX_MERGE_MODE_MASK | FSX_MERGE_DISCARD | FSX_MERGE_COLOCATED)))
     return fail(FSX_E_VALIDATION, "unknown merge mode");
+  if ((b->mode & FSX_MERGE_COLOCATED) && !b->d_item_flag)
+    return fail(FSX_E_VALIDATION, "FSX_MERGE_COLOCATED is an early-start option (item flags)");
   Device* dev = nullptr;
   {
     std::lock_guard<std::mutex> lk(f->mu);
@@ -1086,10 +1090,20 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
   }
   FSX_CUDA(cudaSetDevice(ordinal));
   int launched = 0;
-  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched);
+  unsigned long long* work = nullptr;  // run counter of the early-start kernel
+  if (b->d_item_flag && base_mode != FSX_MERGE_SCAN_ONLY) {
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (!dev->scratch) {
+      FSX_CUDA(cudaMalloc(&dev->scratch, kScratchRing * sizeof(uint64_t)));
+      dev->scratch_ring.size = kScratchRing;
+    }
+    work = reinterpret_cast<unsigned long long*>(dev->scratch + dev->scratch_ring.take(1));
+    FSX_CUDA(cudaMemsetAsync(work, 0, sizeof(uint64_t), pick_stream(dev, stream)));
+  }
+  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched, work);
   f->launches += launched;
   if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge launch: ") + cudaGetErrorString(e));
-  if (b->mode != FSX_MERGE_SCAN_ONLY) {
+  if (base_mode != FSX_MERGE_SCAN_ONLY) {
     f->merges++;
     f->merged_rows += b->total_item_rows;
   }

@@ -132,7 +132,8 @@ class DataPlaneBatch:
             return 0
         return self.chunk_rows * self.rb
 
-    def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False) -> int:
+    def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False,
+                bulk: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
         one K1 launch per 16 items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
@@ -147,7 +148,8 @@ class DataPlaneBatch:
         view["dst_off"] = self.slab_off
         view["flag_base"] = self.flag_base
         view["token"] = 0
-        opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0)
+        opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0) | \
+            (N.FWD_BULK if bulk else 0)
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return (M + 15) // 16
@@ -203,13 +205,31 @@ class DataPlaneBatch:
         b.total_rows = lay.total_rows
         b.total_item_rows = lay.total_item_rows
         if early_start and len(lay.items):
-            flags = [self.fab.flag_ptr(self.dst_gpu, int(fb)) for fb in self.flag_base]
-            self.item_flag.copy_(torch.tensor(flags, dtype=torch.int64))
-            self.item_token.copy_(torch.from_numpy(self.tokens.astype(np.int64)))
-            cr = [self.chunk_rows or it.rows for it in lay.items]
-            self.item_chunk_rows.copy_(torch.tensor(cr, dtype=torch.int64))
-            b.d_item_flag = self.item_flag.data_ptr()
-            b.d_item_token = self.item_token.data_ptr()
+            M = len(lay.items)
+            if not hasattr(self, "_es"):
+                # flags are one contiguous u64 ring per slab; chunk rows are
+                # fixed for the batch (uploaded once)
+                self._flag0 = self.fab.flag_ptr(self.dst_gpu, 0)
+                cr = [self.chunk_rows or it.rows for it in lay.items]
+                self.item_chunk_rows.copy_(torch.tensor(cr, dtype=torch.int64))
+                # double-buffered pinned staging of (flag pointer, token) per
+                # item: uploaded with a non-blocking copy on the current
+                # stream, reused only once its previous copy has run
+                self._es = [(torch.empty((2, M), dtype=torch.int64, pin_memory=True),
+                             torch.empty((2, M), dtype=torch.int64, device=self.dst_dev),
+                             torch.cuda.Event()) for _ in range(2)]
+                self._es_next = 0
+            host, dev, ev = self._es[self._es_next]
+            self._es_next ^= 1
+            if not getattr(self, "es_device_idle", False):  # caller synchronized the device
+                ev.synchronize()
+            hv = host.numpy()
+            hv[0] = self._flag0 + 8 * self.flag_base
+            hv[1] = self.tokens.astype(np.int64)
+            dev.copy_(host, non_blocking=True)
+            ev.record()
+            b.d_item_flag = dev[0].data_ptr()
+            b.d_item_token = dev[1].data_ptr()
             b.d_item_chunk_rows = self.item_chunk_rows.data_ptr()
         return b
 

@@ -32,7 +32,7 @@ METRICS = [
 
 
 def short(name: str) -> str:
-    for k in ("forward_tile_kernel", "forward_kernel", "merge_copy_tma_kernel", "merge_copy_kernel", "merge_scan_kernel",
+    for k in ("forward_tma_kernel", "forward_tile_kernel", "forward_kernel", "merge_follow_kernel", "merge_copy_tma_kernel", "merge_copy_kernel", "merge_scan_kernel",
               "synth_kernel", "set_flags_kernel", "wait_flags_kernel"):
         if k in name:
             return k
@@ -71,7 +71,10 @@ def main(tag: str) -> None:
         per[k].append(rec)
     lines = [f"# ncu --set full, round tag {tag}",
              "", "Captured with `scripts/profile_round.sh` on one B200 (`--clock-control none`):",
-             "`python bench.py --steps 2 --warmup 3 --profile` (config B, 4 requests).",
+             ("`python bench.py --steps 2 --warmup 3 --profile` (config B, default colocated pass; ncu "
+              "serialises the two kernels)" if tag.endswith("_pipe") else
+              "`python bench.py --serial --steps 2 --warmup 3 --profile` (config B, 4 requests; K1 "
+              "and the merge in stream order, each kernel captured alone)."),
              "Per-launch values; ncu replays each kernel, so durations are cold-cache.", "",
              "| kernel | launches | " + " | ".join(n for _, n in METRICS) + " |",
              "|---|---|" + "---|" * len(METRICS)]
@@ -86,12 +89,14 @@ def main(tag: str) -> None:
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    tr = {"forward_kernel": traffic.get("forward_tile_kernel") or traffic.get("forward_kernel"),
+    tr = {"forward_kernel": traffic.get("forward_tma_kernel") or traffic.get("forward_tile_kernel")
+          or traffic.get("forward_kernel"),
           "merge": traffic.get("merge_copy_tma_kernel") or traffic.get("merge_copy_kernel"),
           "merge_scan_kernel": traffic.get("merge_scan_kernel"), "source": f"profiles/ncu_{tag}.md",
           "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)"}
-    with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
-        json.dump(tr, fh, indent=1)
+    if not tag.endswith("_pipe"):
+        with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
+            json.dump(tr, fh, indent=1)
     # launch list
     lpath = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lpath):

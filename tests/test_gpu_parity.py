@@ -378,3 +378,43 @@ def test_small_put_batch_roundtrip(fab, oracle_mod):
         assert t.value == -1
     with pytest.raises(N.FsxError):
         N.call("fsx_ticket_wait", fab._h, tickets[0], None, None)  # already freed
+
+
+@pytest.mark.parametrize("config,count,chunk_rows", [("B", 2, 1024), ("D", 16, 512), ("A", 12, 64)])
+def test_merge_colocated_pipeline_discard(fab, oracle_mod, config, count, chunk_rows):
+    """The N=1 bench pass: K1 on one stream, the early-start merge on another
+    running concurrently on the same GPU (FSX_MERGE_COLOCATED, one CTA per
+    SM), discarding each slab row's L2 lines after reading it
+    (FSX_MERGE_DISCARD).  Merged embeddings stay bit-exact with the oracle,
+    repeated passes over the same slab segments included."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    rules = T.RULES[config]
+    b = DataPlaneBatch(fab, T.config_requests(config, count), rules, 0, 1, chunk_rows=chunk_rows)
+    b.synth_inputs()
+    torch.cuda.synchronize()
+    want, st = _expected(oracle_mod, b)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    mode = N.MERGE_FULL | N.MERGE_DISCARD | N.MERGE_COLOCATED
+    for _ in range(3):
+        assert b.alloc()
+        b.forward(s1, host_notify=False, l2_keep=True)
+        with torch.cuda.stream(s2):
+            b.merge(s2, early_start=True, mode=mode)
+        torch.cuda.synchronize()
+        assert (b.status_host() == 0).all() and (st == 0).all()
+        assert np.array_equal(b.embeds_host(), want)
+        b.release()
+
+
+def test_merge_mode_bits_validated(fab):
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    b = DataPlaneBatch(fab, T.config_requests("A", 2), T.RULES["A"], 0, 1)
+    mb = b.merge_batch(False, N.MERGE_FULL | N.MERGE_COLOCATED)  # colocated needs item flags
+    with pytest.raises(N.FsxError):
+        fab.merge(1, mb)
+    mb = b.merge_batch(False, N.MERGE_FULL | 0x4000)
+    with pytest.raises(N.FsxError):
+        fab.merge(1, mb)
