@@ -354,7 +354,8 @@ def run_single(args):
             stream.wait_event(merged[(s - 1) % 2])  # slab segments free: pass s-1 merged
         if record:
             e0.record(stream)
-        batch.forward(stream, host_notify=False, l2_keep=L2_KEEP_PIPE)
+        batch.forward(stream, host_notify=False, l2_keep=L2_KEEP_PIPE,
+                      bulk=os.environ.get("FSX_BENCH_PIPE_BULK") == "1")
         if record:
             e1.record(stream)
         with torch.cuda.stream(mstream):
@@ -432,6 +433,12 @@ def run_single(args):
         torch.cuda.synchronize()
         return start.elapsed_time(end) / nsteps, list(ev), fab.stats()["kernel_launches"] - launches0
 
+    # The colocated pipeline pays off once a pass is long enough to hide its
+    # extra host work (early-start descriptors, two streams): config B / D
+    # passes of ~0.25 ms do; config A's 70 MB passes are host-bound and run
+    # faster stream-ordered.
+    if not args.serial and payload < (128 << 20):
+        args.serial = True
     step = step_serial if args.serial else step_pipelined
     with torch.cuda.stream(stream):
         prologue()

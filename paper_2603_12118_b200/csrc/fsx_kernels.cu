@@ -914,12 +914,16 @@ cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_
     if (ok) {
       const int64_t tiles = b.unit_off[b.n];
       if (tiles <= 0) return cudaSuccess;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaTileBytes);
-        attr = true;
-      }
-      forward_tma_kernel<<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
+      // FSX_FWD_BULK_SMEM pads the shared memory per CTA (bytes >= 32 KiB) to cap
+      // the resident K1 CTAs per SM, e.g. beside a concurrent merge
+      static const int smem = [] {
+        const char* e = std::getenv("FSX_FWD_BULK_SMEM");
+        const int v = e ? std::atoi(e) : kTmaTileBytes;
+        const int bytes = v < kTmaTileBytes ? kTmaTileBytes : v;
+        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        return bytes;
+      }();
+      forward_tma_kernel<<<(unsigned)tiles, 32, smem, s>>>(b);
       return cudaGetLastError();
     }
     variant = 4;

@@ -212,15 +212,16 @@ class DataPlaneBatch:
                 self._flag0 = self.fab.flag_ptr(self.dst_gpu, 0)
                 cr = [self.chunk_rows or it.rows for it in lay.items]
                 self.item_chunk_rows.copy_(torch.tensor(cr, dtype=torch.int64))
-                # double-buffered pinned staging of (flag pointer, token) per
+                # a ring of pinned staging buffers of (flag pointer, token) per
                 # item: uploaded with a non-blocking copy on the current
-                # stream, reused only once its previous copy has run
+                # stream, each reused only once its previous copy has run (the
+                # host may run a few passes ahead of the GPU)
                 self._es = [(torch.empty((2, M), dtype=torch.int64, pin_memory=True),
                              torch.empty((2, M), dtype=torch.int64, device=self.dst_dev),
-                             torch.cuda.Event()) for _ in range(2)]
+                             torch.cuda.Event()) for _ in range(4)]
                 self._es_next = 0
             host, dev, ev = self._es[self._es_next]
-            self._es_next ^= 1
+            self._es_next = (self._es_next + 1) % len(self._es)
             if not getattr(self, "es_device_idle", False):  # caller synchronized the device
                 ev.synchronize()
             hv = host.numpy()
