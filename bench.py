@@ -59,8 +59,8 @@ L2_KEEP_PIPE = os.environ.get("FSX_BENCH_L2_KEEP_PIPE", "1") == "1"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["fsx", "reference"], default="fsx")
     p.add_argument("--config", choices=sorted(CONFIGS), default="B")
     p.add_argument("--requests", type=int, default=None)
