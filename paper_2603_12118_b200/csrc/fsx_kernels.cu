@@ -24,6 +24,12 @@ namespace fsx {
 namespace kern {
 
 constexpr int kFwdThreads = 256;
+// L2 policy of the follow merge's prompt-row stores (l2_policy: 0 normal,
+// 1 evict_first, 2 evict_last); FSX_FOLLOW_OUT_POLICY selects at build time
+#ifndef FSX_FOLLOW_OUT_POLICY
+#define FSX_FOLLOW_OUT_POLICY 1
+#endif
+constexpr int kFollowOutPolicy = FSX_FOLLOW_OUT_POLICY;
 constexpr int kTmaTileBytes = 32768;  // K1 bulk-copy tile (forward_tma_kernel)
 // K1 variants: <vectors per lane per batch, min CTAs per SM>.  0: 16 x 16 B
 // (8 KiB per warp batch, 2 CTAs/SM), 1: 8 x 16 B at 4 CTAs/SM (register cap 64).
@@ -761,6 +767,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_b
   const bool vec_rows = (rb & 15) == 0;
   const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
   const bool early = b.d_item_flag != nullptr;
+  // the prompt rows are written once and not re-read here: evict them from L2
+  // first, so they do not push out slab rows K1 has just written
+  const uint64_t out_pol = l2_policy(kFollowOutPolicy);
   int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, w);
   while (b.d_item_row_off[item + 1] <= w) ++item;
   int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
@@ -816,7 +825,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_b
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4(dv + i, r[k]);
+          if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
         }
       }
     } else {
