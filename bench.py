@@ -203,7 +203,7 @@ def cpu_reference_pass(reqs, rules, merge_threads):
     return time.perf_counter() - t0, lay.payload_bytes, "port"
 
 
-def cpu_baseline(min_seconds=10.0, max_passes=40):
+def cpu_baseline(min_seconds=12.0, max_passes=80):
     from paper_2603_12118_b200 import trace as T
 
     rules = T.RULES[CONFIG]
