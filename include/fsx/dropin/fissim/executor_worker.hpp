@@ -38,6 +38,7 @@
 
 #include "fissim/control_plane.hpp"
 #include "fsx.h"
+#include "fsx/envelope_codec.hpp"
 
 namespace fissim {
 
@@ -258,12 +259,20 @@ class MultiProcessHost : public ExecutorHost {
     fabric_->register_interest_raw(
         gpu, ref_id,
         [this](const ForwardEnvelope& env, int64_t offset) {
-          // notify-then-read: the worker reads (gpu, offset) of the mapped slab
-          send_frame(Frame{json{{"type", "sidecar_envelope"},
-                                {"envelope", env.to_json()},
-                                {"offset", offset},
-                                {"gpu", env.dst_gpu}},
-                           {}});
+          // notify-then-read: the worker reads (gpu, offset) of the mapped
+          // slab; the envelope travels in its binary form (envelope_codec.hpp)
+          // followed by the slab offset
+          std::vector<uint8_t> body;
+          if (!fsx::encode_envelope(env, body)) {
+            send_frame(Frame{json{{"type", "sidecar_envelope"},
+                                  {"envelope", env.to_json()},
+                                  {"offset", offset},
+                                  {"gpu", env.dst_gpu}},
+                             {}});
+            return;
+          }
+          fsx::codec_detail::put<int64_t>(body, offset);
+          send_frame(Frame{json{{"type", "sidecar_envelope_bin"}}, std::move(body)});
         },
         [this, ref_id](const Error& e) {
           send_frame(Frame{json{{"type", "sidecar_error"},
@@ -381,9 +390,20 @@ class WorkerSidecar : public SidecarPort {
   // Parent notification: read the segment out of device memory, release it,
   // verify, deliver (executor_worker.hpp:264-282).
   void on_envelope(const Frame& f) {
-    const ForwardEnvelope env = ForwardEnvelope::from_json(f.header.at("envelope"));
-    const int gpu = f.header.value("gpu", env.dst_gpu);
-    const int64_t offset = f.header.value("offset", int64_t{0});
+    ForwardEnvelope env;
+    int gpu = 0;
+    int64_t offset = 0;
+    if (f.header.value("type", "") == "sidecar_envelope_bin") {
+      const size_t used = fsx::decode_envelope(f.payload.data(), f.payload.size(), &env);
+      if (used == 0 || f.payload.size() - used != sizeof(int64_t))
+        fail(ErrorCode::Protocol, "malformed binary sidecar envelope");
+      std::memcpy(&offset, f.payload.data() + used, sizeof(int64_t));
+      gpu = env.dst_gpu;
+    } else {
+      env = ForwardEnvelope::from_json(f.header.at("envelope"));
+      gpu = f.header.value("gpu", env.dst_gpu);
+      offset = f.header.value("offset", int64_t{0});
+    }
     if (!in_) fail(ErrorCode::Internal, "worker has no slab mappings");
     std::vector<uint8_t> bytes(static_cast<size_t>(env.chunk_bytes));
     if (env.chunk_bytes > 0)
@@ -483,7 +503,7 @@ inline int run_executor_worker(const std::string& host, int port) {
         } else if (type == "shutdown") {
           done = true;
           sock.shutdown_both();
-        } else if (type == "sidecar_envelope") {
+        } else if (type == "sidecar_envelope" || type == "sidecar_envelope_bin") {
           kernel.post("worker.envelope", [&, f = std::move(f)] { sidecar->on_envelope(f); });
         } else if (type == "outbox_free") {
           kernel.post("worker.outbox_free", [&, f = std::move(f)] { sidecar->on_outbox_free(f); });
