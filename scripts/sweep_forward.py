@@ -25,7 +25,15 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--bulk", action="store_true", help="bulk-copy K1 tiles (FSX_FWD_BULK)")
+    ap.add_argument("--cpu-ref", action="store_true",
+                    help="also time the reference CPU forward (oracle/_ref SidecarFabric, 1 thread) per size")
     args = ap.parse_args()
+    cref = None
+    if args.cpu_ref:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O  # the reference CPU path, timed beside the kernel (checker library)
+        cref = O.REF
 
     from paper_2603_12118_b200.fabric import DeviceFabric
 
@@ -57,7 +65,7 @@ def main():
                 with torch.cuda.graph(g, stream=s):
                     for _ in range(reps):  # fixed flags/token: nobody waits on them here
                         fab.forward(0, src.data_ptr(), 1, off, n, chunk, fb, s, token=(1 << 40) + n,
-                                    host_notify=False)
+                                    host_notify=False, bulk=args.bulk)
                 with torch.cuda.graph(gc, stream=s):
                     for _ in range(reps):
                         ref[:n].copy_(src[:n])
@@ -86,7 +94,13 @@ def main():
             c1.synchronize()
             cms = c0.elapsed_time(c1) / reps
         fab.slab_free(1, off)
-        print(json.dumps({"variant": variant, "graph": args.graph, "bytes": n, "chunk_bytes": chunk,
+        cpu = {}
+        if cref is not None and chunk == 0:
+            iters = max(2, min(200, (256 << 20) // max(n, 1)))
+            secs = cref.ref_forward_bench(n, iters, 1)
+            cpu = {"cpu_ref_us": round(secs / iters * 1e6, 1),
+                   "cpu_ref_payload_gbs": round(n * iters / secs / 1e9, 3), "cpu_ref_threads": 1}
+        print(json.dumps({"variant": "bulk" if args.bulk else variant, "graph": args.graph, "bytes": n, **cpu, "chunk_bytes": chunk,
                           "chunks": nch, "us": round(ms * 1e3, 2),
                           "hbm_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),
                           "memcpy_us": round(cms * 1e3, 2),
