@@ -328,12 +328,17 @@ def test_stats_and_launch_count(fab):
 
 @pytest.mark.parametrize("env", [{"FSX_MERGE_TMA": "1", "FSX_FWD_VARIANT": "0"},
                                  {"FSX_FWD_VARIANT": "3", "FSX_MERGE_PERSIST": "1"},
-                                 {"FSX_FWD_VARIANT": "2", "FSX_FWD_V32": "1"}])
+                                 {"FSX_FWD_VARIANT": "2", "FSX_FWD_V32": "1"},
+                                 {"FSX_FWD_VARIANT": "5", "FSX_MERGE_STREAM": "2"},
+                                 {"FSX_MERGE_STREAM": "1", "FSX_FOLLOW_UNROLL": "8"},
+                                 {"FSX_MERGE_STREAM": "3"}])
 def test_alternate_kernel_instances(gpu, env):
     """The non-default K1 / K3 instances (persistent-warp K1 with 16- or
-    32-byte vectors, 16 KiB tiles, TMA bulk-copy merge, persistent LDG merge)
-    are read from the environment once per process, so the forward and merge
-    parity cases are re-run in a subprocess per combination."""
+    32-byte vectors, 16 KiB tiles, bulk-copy K1 for every call, TMA bulk-copy
+    merge, persistent LDG merge, the early-start run / bulk-copy run /
+    bulk-copy follow merges) are read from the environment once per process,
+    so the forward and merge parity cases (early start and the colocated pass
+    included) are re-run in a subprocess per combination."""
     import os
     import subprocess
     import sys
