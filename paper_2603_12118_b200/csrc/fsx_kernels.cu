@@ -148,8 +148,27 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device spin on a completion flag.  A flag that never arrives (a producer
+// that died, or a kernel the spinning CTAs keep from being scheduled) would
+// hang the GPU, so after FSX_SPIN_TIMEOUT_S seconds the kernel traps: the
+// launch fails with an error the host sees instead of a hang.
+// (set per device by the runtime from FSX_SPIN_TIMEOUT_S, default 30 s)
+__constant__ uint64_t c_spin_timeout_ns = 30ull * 1000000000ull;
+
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t token) {
-  while (ld_acquire_sys(flag) != token) __nanosleep(64);
+  if (ld_acquire_sys(flag) == token) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (ld_acquire_sys(flag) != token) {
+    __nanosleep(64);
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
+  }
 }
 
 // splitmix64 finaliser (common.hpp:203-208): output k (1-based) of a stream
@@ -875,6 +894,10 @@ __global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__
 // Launchers
 
 int forward_block_threads() { return kFwdThreads; }
+
+cudaError_t set_spin_timeout(uint64_t ns) {
+  return cudaMemcpyToSymbol(c_spin_timeout_ns, &ns, sizeof(ns));
+}
 int merge_copy_block_threads() { return kMergeThreads; }
 
 namespace {
@@ -1007,7 +1030,12 @@ __global__ void __launch_bounds__(32) chan_push_kernel(const __grid_constant__ C
   const int lane = threadIdx.x;
   const uint64_t seq = *c.head;
   if (lane == 0) {  // backpressure: the slot's previous message was consumed
-    while (seq - ld_acquire_sys(c.tail) >= c.slots) __nanosleep(64);
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
+    while (seq - ld_acquire_sys(c.tail) >= c.slots) {
+      __nanosleep(64);
+      if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
+    }
   }
   __syncwarp();
   uint8_t* dst = c.ring + (seq % c.slots) * (uint64_t)c.row_bytes;

@@ -96,6 +96,9 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
                          unsigned long long* work);
 cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s);
 
+// Device spin watchdog (spin_until traps after this long), current device.
+cudaError_t set_spin_timeout(uint64_t ns);
+
 // Occupancy helpers.
 int forward_block_threads();
 int forward_blocks_per_sm(int variant);

@@ -23,6 +23,17 @@
 
 #include "fsx.h"
 #include "fsx_kernels.cuh"
+#include "nvtx3/nvToolsExt.h"
+
+namespace {
+// NVTX range over one C-ABI call (forward / merge / small-message flush /
+// channel step), so nsys timelines and `ncu --nvtx` filters see the data
+// plane's own phases.  Header-only NVTX v3: a no-op unless a tool attaches.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -256,6 +267,12 @@ int device_state(fsx_fabric* f, int ordinal, Device** out) {
   d->counter_ring.size = kCounterRing;
   FSX_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, ordinal));
   d->fwd_grid = d->sms * fsx::forward_blocks_per_sm(fwd_variant());
+  {
+    // device spin watchdog: flags that never arrive trap instead of hanging
+    const char* e = std::getenv("FSX_SPIN_TIMEOUT_S");
+    const double secs = e ? std::atof(e) : 30.0;
+    FSX_CUDA(fsx::set_spin_timeout((uint64_t)(std::max(secs, 0.001) * 1e9)));
+  }
   d->merge_grid = d->sms * fsx::merge_copy_blocks_per_sm();
   *out = d.get();
   f->devices.emplace(ordinal, std::move(d));
@@ -631,6 +648,7 @@ int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, i
 }
 
 int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t options, void* stream) {
+  NvtxRange nvtx_range("fsx.forward");
   if (n <= 0) return n == 0 ? FSX_OK : fail(FSX_E_VALIDATION, "negative transfer count");
   int src_dev = 0;
   int rc = find_gpu(f, t[0].src_gpu, &src_dev);
@@ -807,6 +825,7 @@ int fsx_read_u64(fsx_fabric* f, int gpu, const uint64_t* d, uint64_t* h, void* s
 int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
                      int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                      void* stream) {
+  NvtxRange nvtx_range("fsx.forward_host");
   if (bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
   if (chunk_bytes <= 0 || chunk_bytes >= bytes) chunk_bytes = std::max<int64_t>(bytes, 1);
   else if (chunk_bytes % 16) return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
@@ -861,6 +880,7 @@ namespace {
 
 // Launch the staged messages of `device` as one batch (caller holds f->mu).
 int flush_staged(fsx_fabric* f, int device) {
+  NvtxRange nvtx_range("fsx.small_flush");
   auto it = f->staged.find(device);
   if (it == f->staged.end() || it->second.empty()) return FSX_OK;
   std::vector<int64_t>& q = it->second;
@@ -1065,6 +1085,7 @@ int fsx_signal_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, u
 // Merge / synth / stats
 
 int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
+  NvtxRange nvtx_range("fsx.merge");
   int ordinal = 0;
   int rc = find_gpu(f, gpu, &ordinal);
   if (rc) return rc;
@@ -1278,11 +1299,13 @@ int fsx_channel_close(fsx_fabric* f, int32_t channel) {
 
 int fsx_channel_push(fsx_fabric* f, int32_t n, const int32_t* channels, const void* d_rows,
                      int64_t row_stride, void* stream) {
+  NvtxRange nvtx_range("fsx.channel_push");
   return chan_step(f, n, channels, d_rows, row_stride, true, stream);
 }
 
 int fsx_channel_pull(fsx_fabric* f, int32_t n, const int32_t* channels, void* d_out,
                      int64_t out_stride, void* stream) {
+  NvtxRange nvtx_range("fsx.channel_pull");
   return chan_step(f, n, channels, d_out, out_stride, false, stream);
 }
 

@@ -423,3 +423,35 @@ def test_merge_mode_bits_validated(fab):
     mb = b.merge_batch(False, N.MERGE_FULL | 0x4000)
     with pytest.raises(N.FsxError):
         fab.merge(1, mb)
+
+
+def test_spin_watchdog_traps_instead_of_hanging(gpu):
+    """A device wait on a flag that never arrives (a dead producer) must fail
+    the launch after FSX_SPIN_TIMEOUT_S instead of hanging the GPU.  Run in a
+    subprocess: the trap leaves that process's CUDA context unusable."""
+    import os
+    import subprocess
+    import sys
+    import time
+
+    code = (
+        "import sys, torch\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2603_12118_b200.fabric import DeviceFabric\n"
+        "f = DeviceFabric({0: 0, 1: 0}, {0: 0, 1: 0})\n"
+        "f.slab_register(1, 1 << 20)\n"
+        "fb = f.flags_alloc(1, 1)\n"
+        "f.stream_wait_flags(1, fb, 1, 0xdead, None)\n"
+        "try:\n"
+        "    torch.cuda.synchronize()\n"
+        "except Exception as e:\n"
+        "    print('TRAPPED', type(e).__name__)\n"
+        "    sys.exit(0)\n"
+        "print('NO ERROR')\n"
+        "sys.exit(1)\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    t0 = time.time()
+    p = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FSX_SPIN_TIMEOUT_S": "1"},
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0 and "TRAPPED" in p.stdout, (p.stdout + p.stderr)[-2000:]
+    assert time.time() - t0 < 90
