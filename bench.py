@@ -515,9 +515,9 @@ def run_single(args):
         # The pass: K1 (forward_tile_kernel<8>) and the early-start merge
         # (merge_follow_kernel, one CTA per SM, FSX_MERGE_COLOCATED |
         # FSX_MERGE_DISCARD) run concurrently; algorithmic bytes are both
-        # kernels' (2 x payload each).  The slab round trip
-        # mostly stays in L2, so the rate can exceed the DRAM copy peak; the
-        # DRAM floor of the pass is src read + embedding write (2 x payload).
+        # kernels' (2 x payload each).  Part of the slab round
+        # trip never reaches DRAM, so the rate can exceed the DRAM copy peak;
+        # the DRAM floor of the pass is src read + embedding write (2 x payload).
         alg = fwd_bytes + merge_bytes
         pass_gbs = alg / (ms_step * 1e-3) / 1e9
         floor_gbs = (fwd_bytes // 2 + merge_bytes // 2) / (ms_step * 1e-3) / 1e9
@@ -533,8 +533,9 @@ def run_single(args):
                     "dram_floor_gbs": round(floor_gbs, 1),
                     "dram_floor_frac": round(floor_gbs / peak, 4),
                     "why_above_peak": "algorithmic bytes count the slab write (K1) and read (merge); "
-                                      "behind K1 on the same GPU those mostly hit L2 and are "
-                                      "discarded instead of written back"}
+                                      "part of that round trip never reaches DRAM (merged rows are "
+                                      "discarded from L2 instead of written back, some reads hit "
+                                      "L2), so the pass moves fewer DRAM bytes than it counts"}
         kernels["pipeline"] = {
             "k1_ms": round(statistics.mean(a.elapsed_time(b) for a, b, _ in ev_main), 4),
             "merge_tail_after_k1_ms": round(statistics.mean(b.elapsed_time(c) for _, b, c in ev_main), 4),
