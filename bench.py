@@ -355,7 +355,8 @@ def run_single(args):
         if record:
             e0.record(stream)
         batch.forward(stream, host_notify=False, l2_keep=L2_KEEP_PIPE,
-                      bulk=os.environ.get("FSX_BENCH_PIPE_BULK") == "1")
+                      bulk=os.environ.get("FSX_BENCH_PIPE_BULK") == "1",
+                      share_sm=os.environ.get("FSX_BENCH_SHARE_SM", "0") == "1")
         if record:
             e1.record(stream)
         with torch.cuda.stream(mstream):

@@ -161,6 +161,11 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * batch keep the register tile kernel.  FSX_FWD_VARIANT=5 makes it the
  * default for every call. */
 #define FSX_FWD_BULK 4u
+/* FSX_FWD_SHARE_SM: cap this launch at two K1 CTAs per SM (register tiles,
+ * padded shared memory) so a consumer kernel running concurrently on the
+ * same GPU (the colocated early-start merge) always finds a free slot on
+ * every SM, whatever order the CTA dispatcher takes the two grids in. */
+#define FSX_FWD_SHARE_SM 8u
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                    uint32_t options, void* stream);

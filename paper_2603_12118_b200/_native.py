@@ -37,6 +37,7 @@ NETWORK_STREAM = 1
 FWD_HOST_NOTIFY = 1
 FWD_L2_KEEP = 2
 FWD_BULK = 4
+FWD_SHARE_SM = 8
 
 MERGE_FULL = 0
 MERGE_SCAN_ONLY = 1

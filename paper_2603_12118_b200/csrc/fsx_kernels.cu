@@ -161,6 +161,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // (set per device by the runtime from FSX_SPIN_TIMEOUT_S, default 30 s)
 __constant__ uint64_t c_spin_timeout_ns = 30ull * 1000000000ull;
 
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// gpu-scope wait: producer and consumer on the same GPU (colocated pass)
+__device__ __forceinline__ void spin_until_gpu(const uint64_t* flag, uint64_t token) {
+  if (ld_acquire_gpu(flag) == token) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (ld_acquire_gpu(flag) != token) {
+    __nanosleep(64);
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
+  }
+}
+
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t token) {
   if (ld_acquire_sys(flag) == token) return;
   const uint64_t t0 = globaltimer_ns();
@@ -786,6 +803,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_b
   const bool vec_rows = (rb & 15) == 0;
   const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
   const bool early = b.d_item_flag != nullptr;
+  // the producer's K1 runs on this GPU: a gpu-scope acquire pairs with its
+  // gpu-scope release; across GPUs the wait is system scope
+#ifndef FSX_COLOCATED_GPU_SCOPE
+#define FSX_COLOCATED_GPU_SCOPE 1
+#endif
+  const bool colocated = FSX_COLOCATED_GPU_SCOPE && (b.mode & FSX_MERGE_COLOCATED) != 0;
   // the prompt rows are written once and not re-read here: evict them from L2
   // first, so they do not push out slab rows K1 has just written
   const uint64_t out_pol = l2_policy(kFollowOutPolicy);
@@ -823,7 +846,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_b
     if (early) {
       const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
       if (c != waited) {
-        if (lane == 0) spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+        if (lane == 0) {
+          if (colocated) spin_until_gpu(b.d_item_flag[item] + c, b.d_item_token[item]);
+          else spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
+        }
         __syncwarp();
         waited = c;
       }
@@ -937,7 +963,7 @@ int forward_tile_bytes(int variant) {
   return 0;                                        // persistent warp kernels
 }
 
-cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s) {
+cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s, bool share_sm) {
   if (variant == 5) {
     // bulk-copy tiles for local, 16-byte aligned transfers without a fused
     // digest; anything else in the batch takes the register tile kernel
@@ -967,8 +993,19 @@ cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_
       if (bb.t[k].vec) bb.t[k].vec = 16;
     const int64_t tiles = bb.unit_off[bb.n];
     if (tiles <= 0) return cudaSuccess;
-    if (variant == 3) forward_tile_kernel<4><<<(unsigned)tiles, kTileThreads, 0, s>>>(bb);
-    else forward_tile_kernel<8><<<(unsigned)tiles, kTileThreads, 0, s>>>(bb);
+    // share_sm: pad shared memory so at most two K1 CTAs fit per SM
+    static const int pad = [] {
+      int dev = 0, smem = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+      const int p = smem / 2 - 8 * 1024;  // 2 x pad + reserved fits, 3 x pad does not
+      cudaFuncSetAttribute(forward_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, p);
+      cudaFuncSetAttribute(forward_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p);
+      return p;
+    }();
+    const size_t smem = share_sm ? (size_t)pad : 0;
+    if (variant == 3) forward_tile_kernel<4><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
+    else forward_tile_kernel<8><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
     return cudaGetLastError();
   }
   bool wide = true;  // every vectorised transfer allows 32-byte vectors

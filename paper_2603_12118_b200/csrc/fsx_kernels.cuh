@@ -88,7 +88,7 @@ cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, 
 cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st);
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
-cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s);
+cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s, bool share_sm = false);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
 // `work`: a zeroed device counter for the early-start (item flags) kernel.

@@ -749,7 +749,10 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     const int64_t rounds = std::max<int64_t>(1, (units + max_warps - 1) / max_warps);
     const int64_t warps = (units + rounds - 1) / rounds;
     const int grid = (int)std::max<int64_t>(1, (warps + warps_per_cta - 1) / warps_per_cta);
-    FSX_CUDA(fsx::launch_forward(b, (options & FSX_FWD_BULK) ? 5 : fwd_variant(), grid, st));
+    const bool share = (options & FSX_FWD_SHARE_SM) != 0;
+    int variant = (options & FSX_FWD_BULK) ? 5 : fwd_variant();
+    if (share && variant != 3) variant = 4;  // the capped form is the register tile kernel
+    FSX_CUDA(fsx::launch_forward(b, variant, grid, st, share));
     f->launches++;
     for (int32_t k = 0; k < cnt; ++k) {
       const fsx_transfer& x = t[first + k];

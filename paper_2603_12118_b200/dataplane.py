@@ -133,7 +133,7 @@ class DataPlaneBatch:
         return self.chunk_rows * self.rb
 
     def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False,
-                bulk: bool = False) -> int:
+                bulk: bool = False, share_sm: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
         one K1 launch per 16 items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
@@ -149,7 +149,7 @@ class DataPlaneBatch:
         view["flag_base"] = self.flag_base
         view["token"] = 0
         opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0) | \
-            (N.FWD_BULK if bulk else 0)
+            (N.FWD_BULK if bulk else 0) | (N.FWD_SHARE_SM if share_sm else 0)
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return (M + 15) // 16

@@ -404,7 +404,7 @@ def test_merge_colocated_pipeline_discard(fab, oracle_mod, config, count, chunk_
     mode = N.MERGE_FULL | N.MERGE_DISCARD | N.MERGE_COLOCATED
     for _ in range(3):
         assert b.alloc()
-        b.forward(s1, host_notify=False, l2_keep=True)
+        b.forward(s1, host_notify=False, l2_keep=True, share_sm=True)
         with torch.cuda.stream(s2):
             b.merge(s2, early_start=True, mode=mode)
         torch.cuda.synchronize()
