@@ -1,0 +1,206 @@
+// fsx/dataplane.hpp -- one producer -> consumer data-plane pass in C++ over the
+// C ABI: the native counterpart of paper_2603_12118_b200/dataplane.py.
+//
+// A pass is what the reference does per request between the encoder's
+// emit_output (executor_sim.hpp:221-229, 321-336) and the LLM's admission
+// (executor_sim.hpp:382-392), plus the merge the reference leaves out
+// (SURVEY.md 8a-8):
+//   alloc()    one receive-slab segment per item (fsx_slab_alloc_n: the
+//              NodeArena policy, sidecar.hpp:149-163), all or nothing;
+//   forward()  K1 pushes every item into its segment, chunk by chunk with a
+//              completion flag per chunk (fsx_forward_batch);
+//   merge()    K3 scans the placeholder rows and moves each item row into its
+//              prompt row (fsx_merge), stream-ordered after forward() or with
+//              early start on the chunk flags;
+//   release()  the segments go back to the slab (the ack, sidecar.hpp:287-290).
+// The batch's device arrays (prompt embedding, token ids, offsets, item
+// views, scratch, status) are allocated once; a pass costs a handful of C-ABI
+// calls and one small descriptor upload when segment offsets change.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fsx.h"
+
+namespace fsx {
+
+class DataPlanePass {
+ public:
+  struct Item {
+    const void* d_src;  // producer bytes on src_gpu's device (rows x row_bytes)
+    int64_t rows;
+  };
+  struct Request {
+    std::vector<int32_t> token_ids;  // prompt: text ids and placeholder_id rows
+    std::vector<Item> items;         // input slots 1..m in items order
+  };
+
+  DataPlanePass(fsx_fabric* f, int src_gpu, int dst_gpu, int64_t row_bytes, int32_t placeholder_id,
+                int64_t chunk_rows, const std::vector<Request>& reqs)
+      : f_(f), src_(src_gpu), dst_(dst_gpu), rb_(row_bytes), pid_(placeholder_id), chunk_rows_(chunk_rows) {
+    int dev = 0;
+    check(fsx_device_of(f_, dst_gpu, &dev));
+    dev_ = dev;
+    std::vector<int64_t> req_row_off{0}, req_item_off{0}, item_row_off{0};
+    std::vector<int32_t> tok;
+    for (const Request& r : reqs) {
+      tok.insert(tok.end(), r.token_ids.begin(), r.token_ids.end());
+      req_row_off.push_back(req_row_off.back() + static_cast<int64_t>(r.token_ids.size()));
+      for (const Item& it : r.items) {
+        items_.push_back(it);
+        item_row_off.push_back(item_row_off.back() + it.rows);
+      }
+      req_item_off.push_back(static_cast<int64_t>(items_.size()));
+    }
+    const int64_t R = static_cast<int64_t>(reqs.size()), M = static_cast<int64_t>(items_.size());
+    total_rows_ = req_row_off.back();
+    total_item_rows_ = item_row_off.back();
+    cuda(cudaSetDevice(dev_));
+    embeds_ = alloc_dev<uint8_t>(std::max<int64_t>(total_rows_ * rb_, 16));
+    tok_ = upload(tok);
+    req_row_off_ = upload(req_row_off);
+    req_item_off_ = upload(req_item_off);
+    item_row_off_ = upload(item_row_off);
+    scratch_ = alloc_dev<int32_t>(std::max<int64_t>(total_item_rows_, 1));
+    status_ = alloc_dev<int32_t>(std::max<int64_t>(R, 1));
+    item_src_ = alloc_dev<const void*>(std::max<int64_t>(M, 1));
+    xfers_.resize(static_cast<size_t>(M));
+    lens_.resize(static_cast<size_t>(M));
+    chunks_.resize(static_cast<size_t>(M));
+    for (int64_t i = 0; i < M; ++i) {
+      const int64_t nb = items_[i].rows * rb_, cb = chunk_rows_ > 0 ? chunk_rows_ * rb_ : 0;
+      lens_[i] = nb;
+      chunks_[i] = (cb <= 0 || cb >= nb) ? 1 : (nb + cb - 1) / cb;
+      xfers_[i] = fsx_transfer{src_, dst_, items_[i].d_src, 0, nb, cb, 0, 0, nullptr};
+      n_chunks_ += chunks_[i];
+    }
+    b_.num_requests = static_cast<int32_t>(R);
+    b_.num_items = static_cast<int32_t>(M);
+    b_.row_bytes = rb_;
+    b_.placeholder_id = pid_;
+    b_.mode = FSX_MERGE_FULL;
+    b_.d_embeds = embeds_;
+    b_.d_token_ids = tok_;
+    b_.d_req_row_off = req_row_off_;
+    b_.d_req_item_off = req_item_off_;
+    b_.d_item_src = item_src_;
+    b_.d_item_row_off = item_row_off_;
+    b_.d_scratch = scratch_;
+    b_.d_status = status_;
+    b_.total_rows = total_rows_;
+    b_.total_item_rows = total_item_rows_;
+  }
+
+  DataPlanePass(const DataPlanePass&) = delete;
+  DataPlanePass& operator=(const DataPlanePass&) = delete;
+
+  ~DataPlanePass() {
+    if (held_) fsx_slab_free_n(f_, dst_, static_cast<int32_t>(offs_.size()), offs_.data());
+    cudaSetDevice(dev_);
+    for (void* p : owned_) cudaFree(p);
+  }
+
+  // Segments for every item; false (nothing held) when the slab is full.
+  bool alloc() {
+    offs_.assign(items_.size(), -1);
+    check(fsx_slab_alloc_n(f_, dst_, static_cast<int32_t>(items_.size()), lens_.data(), offs_.data()));
+    if (!items_.empty() && offs_[0] < 0) return false;
+    held_ = true;
+    if (offs_ != uploaded_offs_) {  // first fit hands back the same offsets pass after pass
+      void* base = nullptr;
+      check(fsx_slab_ptr(f_, dst_, 0, &base));
+      std::vector<const void*> views(items_.size());
+      for (size_t i = 0; i < items_.size(); ++i) views[i] = static_cast<const uint8_t*>(base) + offs_[i];
+      cuda(cudaSetDevice(dev_));
+      if (!views.empty())
+        cuda(cudaMemcpy(item_src_, views.data(), views.size() * sizeof(void*), cudaMemcpyHostToDevice));
+      uploaded_offs_ = offs_;
+    }
+    return true;
+  }
+
+  // K1 for every item (flags drawn from the consumer slab's ring).
+  void forward(cudaStream_t st, uint32_t options = 0) {
+    if (items_.empty()) return;
+    int64_t fb = 0;
+    check(fsx_flags_alloc(f_, dst_, static_cast<int32_t>(n_chunks_), &fb));
+    for (size_t i = 0; i < items_.size(); ++i) {
+      xfers_[i].dst_off = offs_[i];
+      xfers_[i].flag_base = fb;
+      xfers_[i].token = 0;
+      fb += chunks_[i];
+    }
+    check(fsx_forward_batch(f_, static_cast<int32_t>(items_.size()), xfers_.data(), options, st));
+  }
+
+  // K3, stream-ordered after forward() on the same stream.
+  void merge(cudaStream_t st) { check(fsx_merge(f_, dst_, &b_, st)); }
+
+  void release() {
+    if (!held_) return;
+    check(fsx_slab_free_n(f_, dst_, static_cast<int32_t>(offs_.size()), offs_.data()));
+    held_ = false;
+  }
+
+  // alloc -> forward -> merge -> release; false when the slab was full.
+  bool run(cudaStream_t st, uint32_t fwd_options = 0) {
+    if (!alloc()) return false;
+    forward(st, fwd_options);
+    merge(st);
+    release();  // host bookkeeping; the next pass's K1 is stream-ordered after this merge
+    return true;
+  }
+
+  uint8_t* embeds() const { return embeds_; }
+  const int32_t* status() const { return status_; }
+  int64_t total_rows() const { return total_rows_; }
+  int64_t total_item_rows() const { return total_item_rows_; }
+  int64_t payload_bytes() const { return total_item_rows_ * rb_; }
+  int device() const { return dev_; }
+
+ private:
+  static void check(int rc) {
+    if (rc != FSX_OK) throw std::runtime_error(std::string("fsx: ") + fsx_last_error());
+  }
+  static void cuda(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + cudaGetErrorString(e));
+  }
+  template <class T>
+  T* alloc_dev(int64_t n) {
+    void* p = nullptr;
+    cuda(cudaMalloc(&p, static_cast<size_t>(n) * sizeof(T)));
+    owned_.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc_dev<T>(std::max<int64_t>(static_cast<int64_t>(v.size()), 1));
+    if (!v.empty()) cuda(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+
+  fsx_fabric* f_;
+  int src_, dst_, dev_ = 0;
+  int64_t rb_;
+  int32_t pid_;
+  int64_t chunk_rows_;
+  std::vector<Item> items_;
+  int64_t total_rows_ = 0, total_item_rows_ = 0, n_chunks_ = 0;
+  std::vector<fsx_transfer> xfers_;
+  std::vector<int64_t> lens_, chunks_, offs_, uploaded_offs_;
+  bool held_ = false;
+  std::vector<void*> owned_;
+  uint8_t* embeds_ = nullptr;
+  int32_t* tok_ = nullptr;
+  int64_t *req_row_off_ = nullptr, *req_item_off_ = nullptr, *item_row_off_ = nullptr;
+  int32_t *scratch_ = nullptr, *status_ = nullptr;
+  const void** item_src_ = nullptr;
+  fsx_merge_batch b_{};
+};
+
+}  // namespace fsx
