@@ -102,6 +102,14 @@ class DataPlanePass {
   ~DataPlanePass() {
     if (held_) fsx_slab_free_n(f_, dst_, static_cast<int32_t>(offs_.size()), offs_.data());
     cudaSetDevice(dev_);
+    cudaDeviceSynchronize();
+    if (ev_ready_) {
+      cudaEventDestroy(merged_ev_);
+      for (auto& sl : stage_) {
+        cudaFreeHost(sl.host);
+        cudaEventDestroy(sl.ev);
+      }
+    }
     for (void* p : owned_) cudaFree(p);
   }
 
@@ -156,6 +164,57 @@ class DataPlanePass {
     return true;
   }
 
+  // The colocated pass (producer and consumer on the same GPU): K1 on
+  // `k1_stream`, the early-start merge on `merge_stream` (create it with the
+  // highest priority) following K1 chunk by chunk, one CTA per SM, merged
+  // slab rows discarded from L2 (FSX_MERGE_COLOCATED | FSX_MERGE_DISCARD;
+  // DESIGN.md §3).  The next pass's K1 waits for this pass's merge (slab
+  // reuse).  False when the slab was full.
+  bool run_colocated(cudaStream_t k1_stream, cudaStream_t merge_stream) {
+    if (!alloc()) return false;
+    if (!ev_ready_) {
+      cuda(cudaSetDevice(dev_));
+      cuda(cudaEventCreateWithFlags(&merged_ev_, cudaEventDisableTiming));
+      for (auto& sl : stage_) {
+        cuda(cudaHostAlloc(&sl.host, 2 * std::max<size_t>(items_.size(), 1) * sizeof(uint64_t),
+                           cudaHostAllocDefault));
+        sl.dev = alloc_dev<uint64_t>(2 * std::max<int64_t>(static_cast<int64_t>(items_.size()), 1));
+        cuda(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+      }
+      std::vector<int64_t> cr(items_.size());
+      for (size_t i = 0; i < items_.size(); ++i) cr[i] = chunk_rows_ > 0 ? chunk_rows_ : items_[i].rows;
+      chunk_rows_dev_ = upload(cr);
+      uint64_t* f0 = nullptr;
+      check(fsx_flag_ptr(f_, dst_, 0, &f0));
+      flag0_ = f0;
+      ev_ready_ = true;
+    } else {
+      cuda(cudaStreamWaitEvent(k1_stream, merged_ev_, 0));  // pass s-1 merged: segments free
+    }
+    forward(k1_stream);
+    // early-start descriptors: (flag pointer, token) per item, staged in a
+    // pinned ring slot whose previous upload has run
+    Stage& sl = stage_[next_stage_];
+    next_stage_ = (next_stage_ + 1) % kStages;
+    cuda(cudaEventSynchronize(sl.ev));
+    const size_t M = items_.size();
+    for (size_t i = 0; i < M; ++i) {
+      sl.host[i] = reinterpret_cast<uint64_t>(flag0_ + xfers_[i].flag_base);
+      sl.host[M + i] = xfers_[i].token;
+    }
+    cuda(cudaMemcpyAsync(sl.dev, sl.host, 2 * M * sizeof(uint64_t), cudaMemcpyHostToDevice, merge_stream));
+    cuda(cudaEventRecord(sl.ev, merge_stream));
+    fsx_merge_batch mb = b_;
+    mb.mode = FSX_MERGE_FULL | FSX_MERGE_COLOCATED | FSX_MERGE_DISCARD;
+    mb.d_item_flag = reinterpret_cast<const uint64_t* const*>(sl.dev);
+    mb.d_item_token = sl.dev + M;
+    mb.d_item_chunk_rows = chunk_rows_dev_;
+    check(fsx_merge(f_, dst_, &mb, merge_stream));
+    cuda(cudaEventRecord(merged_ev_, merge_stream));
+    release();
+    return true;
+  }
+
   uint8_t* embeds() const { return embeds_; }
   const int32_t* status() const { return status_; }
   int64_t total_rows() const { return total_rows_; }
@@ -201,6 +260,19 @@ class DataPlanePass {
   int32_t *scratch_ = nullptr, *status_ = nullptr;
   const void** item_src_ = nullptr;
   fsx_merge_batch b_{};
+  // colocated pass state
+  static constexpr int kStages = 4;
+  struct Stage {
+    uint64_t* host = nullptr;
+    uint64_t* dev = nullptr;
+    cudaEvent_t ev = nullptr;
+  };
+  Stage stage_[kStages];
+  int next_stage_ = 0;
+  bool ev_ready_ = false;
+  cudaEvent_t merged_ev_ = nullptr;
+  int64_t* chunk_rows_dev_ = nullptr;
+  uint64_t* flag0_ = nullptr;
 };
 
 }  // namespace fsx
