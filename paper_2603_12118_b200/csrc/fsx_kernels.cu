@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_stream_kernel(fsx_merge_b
 // next item; the row's chunk flag is checked (lane 0, acquire) before its
 // loads; the position comes from the scan's scratch.
 template <int U>
-__global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_batch b) {
+__global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merge_batch b) {
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (kMergeThreads / 32);
   const int64_t w = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
@@ -882,6 +882,138 @@ __global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_b
       for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
         asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
     }
+  }
+}
+
+// Follow kernel, software-pipelined (FSX_MERGE_STREAM=4): the same row order
+// as merge_follow_kernel, but while a row's loads are in flight the warp
+// already resolves its next row (placeholder position, source view) and lane 0
+// issues that row's chunk-flag acquire, so the flag and position latencies
+// overlap the data instead of preceding it.  lane 0's acquire plus the
+// __syncwarp before the next row's loads order them after the flag.
+struct FollowRow {
+  const uint8_t* src;
+  uint8_t* dst;
+  const uint64_t* flag;
+  uint64_t token;
+  bool valid, ok;
+};
+
+template <int U>
+__global__ void __launch_bounds__(kMergeThreads, 2) merge_follow2_kernel(fsx_merge_batch b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (kMergeThreads / 32);
+  const int64_t w = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
+  const int64_t rb = b.row_bytes;
+  const int64_t n = b.total_item_rows;
+  if (w >= n) return;
+  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
+  const bool early = b.d_item_flag != nullptr;
+  const bool colocated = FSX_COLOCATED_GPU_SCOPE && (b.mode & FSX_MERGE_COLOCATED) != 0;
+  const bool vec_rows = (rb & 15) == 0;
+  const uint64_t out_pol = l2_policy(kFollowOutPolicy);
+  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, w);
+  while (b.d_item_row_off[item + 1] <= w) ++item;
+  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
+  while (b.d_req_item_off[req + 1] <= item) ++req;
+  int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
+  const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
+  const uint64_t* item_flags = early ? b.d_item_flag[item] : nullptr;
+  uint64_t item_token = early ? b.d_item_token[item] : 0;
+  int64_t req_row = b.d_req_row_off[req];
+  bool req_ok = b.d_status[req] == 0;
+  auto resolve = [&](int64_t g, FollowRow& m) {
+    m.valid = g < n;
+    if (!m.valid) return;
+    if (g >= item_end) {
+      do {
+        ++item;
+      } while (b.d_item_row_off[item + 1] <= g);
+      item_beg = b.d_item_row_off[item];
+      item_end = b.d_item_row_off[item + 1];
+      item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
+      if (early) {
+        chunk_rows = b.d_item_chunk_rows[item];
+        item_flags = b.d_item_flag[item];
+        item_token = b.d_item_token[item];
+      }
+      if (b.d_req_item_off[req + 1] <= item) {
+        do {
+          ++req;
+        } while (b.d_req_item_off[req + 1] <= item);
+        req_row = b.d_req_row_off[req];
+        req_ok = b.d_status[req] == 0;
+      }
+    }
+    m.ok = req_ok;
+    const int64_t j = g - item_beg;
+    m.src = item_src + j * rb;
+    m.dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[g]) * rb;
+    m.flag = early ? item_flags + (chunk_rows > 0 ? j / chunk_rows : 0) : nullptr;
+    m.token = item_token;
+  };
+  auto acquire = [&](const uint64_t* f) { return colocated ? ld_acquire_gpu(f) : ld_acquire_sys(f); };
+  FollowRow cur, nxt;
+  resolve(w, cur);
+  uint64_t seen = (early && lane == 0 && cur.ok) ? acquire(cur.flag) : 0;
+  for (int64_t g = w; cur.valid; g += W) {
+    if (early && cur.ok) {
+      if (lane == 0 && seen != cur.token) {  // not landed yet when prefetched: wait
+        const uint64_t t0 = globaltimer_ns();
+        uint32_t spins = 0;
+        while ((seen = acquire(cur.flag)) != cur.token) {
+          __nanosleep(64);
+          if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
+        }
+      }
+      __syncwarp();
+    }
+    const bool vec = vec_rows && ((reinterpret_cast<uintptr_t>(cur.src) | reinterpret_cast<uintptr_t>(cur.dst)) & 15) == 0;
+    const int64_t nv = vec ? rb >> 4 : 0;
+    const uint4* sv = reinterpret_cast<const uint4*>(cur.src);
+    uint4* dv = reinterpret_cast<uint4*>(cur.dst);
+    uint4 r[U];
+    if (cur.ok) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = k * 32 + lane;
+        if (i < nv) r[k] = ld_v4(sv + i);
+      }
+    }
+    // the next row: position, view and flag acquire overlap this row's loads
+    resolve(g + W, nxt);
+    uint64_t nseen = 0;
+    if (early && lane == 0 && nxt.valid && nxt.ok) nseen = acquire(nxt.flag);
+    if (cur.ok) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = k * 32 + lane;
+        if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
+      }
+      for (int64_t base = 32 * U; base < nv; base += 32 * U) {  // rows wider than one batch
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) r[k] = ld_v4(sv + i);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t i = base + k * 32 + lane;
+          if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
+        }
+      }
+      if (!vec)
+        for (int64_t i = lane; i < rb; i += 32) cur.dst[i] = cur.src[i];
+      if (discard) {
+        const uintptr_t lo = (reinterpret_cast<uintptr_t>(cur.src) + 127) & ~uintptr_t{127};
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(cur.src) + rb) & ~uintptr_t{127};
+        for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+      }
+    }
+    cur = nxt;
+    seen = nseen;
   }
 }
 
@@ -1607,7 +1739,11 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
       const char* e = std::getenv("FSX_MERGE_STREAM");
       return e ? std::atoi(e) : 0;
     }();
-    if (stream_kind == 0) {
+    if (stream_kind == 4) {
+      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
+      const int64_t want = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
+      merge_follow2_kernel<16><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
+    } else if (stream_kind == 0) {
       // one CTA per SM beside K1 on the same GPU, else the copy grid
       const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
       const int64_t want = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);

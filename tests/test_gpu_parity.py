@@ -331,7 +331,8 @@ def test_stats_and_launch_count(fab):
                                  {"FSX_FWD_VARIANT": "2", "FSX_FWD_V32": "1"},
                                  {"FSX_FWD_VARIANT": "5", "FSX_MERGE_STREAM": "2"},
                                  {"FSX_MERGE_STREAM": "1", "FSX_FOLLOW_UNROLL": "8"},
-                                 {"FSX_MERGE_STREAM": "3"}])
+                                 {"FSX_MERGE_STREAM": "3"},
+                                 {"FSX_MERGE_STREAM": "4"}])
 def test_alternate_kernel_instances(gpu, env):
     """The non-default K1 / K3 instances (persistent-warp K1 with 16- or
     32-byte vectors, 16 KiB tiles, bulk-copy K1 for every call, TMA bulk-copy
