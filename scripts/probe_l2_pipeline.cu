@@ -25,8 +25,13 @@ __device__ __forceinline__ uint64_t ld_acq(const uint64_t* p) {
   return v;
 }
 
+__device__ int g_store_policy = 0;  // 0 plain stores, 1 L2::evict_last, 2 L2::evict_first
+
 __global__ void __launch_bounds__(256) writer(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                               unsigned* counters, uint64_t* flags, uint64_t token) {
+  uint64_t pol;
+  if (g_store_policy == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * (kTile / 16);
   uint4 r[8];
@@ -35,11 +40,20 @@ __global__ void __launch_bounds__(256) writer(const uint4* __restrict__ src, uin
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[k].x), "=r"(r[k].y), "=r"(r[k].z), "=r"(r[k].w)
                  : "l"(src + base + k * 256 + threadIdx.x));
+  if (g_store_policy == 0) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + base + k * 256 + threadIdx.x),
-                 "r"(r[k].x), "r"(r[k].y), "r"(r[k].z), "r"(r[k].w)
-                 : "memory");
+    for (int k = 0; k < 8; ++k)
+      asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + base + k * 256 + threadIdx.x),
+                   "r"(r[k].x), "r"(r[k].y), "r"(r[k].z), "r"(r[k].w)
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                       dst + base + k * 256 + threadIdx.x),
+                   "r"(r[k].x), "r"(r[k].y), "r"(r[k].z), "r"(r[k].w), "l"(pol)
+                   : "memory");
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     const int64_t c = tile * kTile / kChunk;
@@ -133,13 +147,20 @@ int main() {
     }
     std::printf("{\"case\": \"%s\", \"ms\": %.4f, \"payload_gbs\": %.1f}\n", name, best, bytes / (best * 1e-3) / 1e9);
   };
-  run("writer alone (src -> slab)", true, 0, 6);
-  run("follower alone, cold slab (slab -> out)", false, 3, 6);
-  run("pass: writer || follower on the hot slab", true, 1, 6);
-  run("pass: writer || follower on the hot slab + discard", true, 2, 6);
-  run("pass: writer || follower reading a cold buffer", true, 3, 6);
+  for (int pol : {0, 1}) {
+    cudaMemcpyToSymbol(g_store_policy, &pol, sizeof(pol));
+    std::printf("{\"writer_stores\": \"%s\"}\n", pol ? "L2::evict_last" : "plain");
+    run("writer alone (src -> slab)", true, 0, 6);
+    run("follower alone, cold slab (slab -> out)", false, 3, 6);
+    run("pass: writer || follower on the hot slab", true, 1, 6);
+    run("pass: writer || follower on the hot slab + discard", true, 2, 6);
+    run("pass: writer || follower reading a cold buffer", true, 3, 6);
+  }
   // stream-ordered: does a reader right after the writer hit L2 at all?
-  for (int64_t nch : {2, 4, 8, 16}) {
+  // (once with plain stores, once with L2::evict_last stores)
+  for (int pol : {0, 1})
+  for (int64_t nch : {2, 8, 16}) {
+    cudaMemcpyToSymbol(g_store_policy, &pol, sizeof(pol));
     const int64_t b = nch * kChunk, r = nch * kChunkRows;
     for (int hot = 1; hot >= 0; --hot) {
       float best = 1e9f;
@@ -155,8 +176,9 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         if (it > 0 && ms < best) best = ms;
       }
-      std::printf("{\"case\": \"serial read of %lld MiB right after the write, %s\", \"ms\": %.4f, \"payload_gbs\": %.1f}\n",
-                  (long long)(b >> 20), hot ? "same (hot) buffer" : "cold buffer", best, b / (best * 1e-3) / 1e9);
+      std::printf("{\"case\": \"serial read of %lld MiB right after the write (%s stores), %s\", \"ms\": %.4f, \"payload_gbs\": %.1f}\n",
+                  (long long)(b >> 20), pol ? "evict_last" : "plain", hot ? "same (hot) buffer" : "cold buffer", best,
+                  b / (best * 1e-3) / 1e9);
     }
   }
   cudaError_t e = cudaDeviceSynchronize();
