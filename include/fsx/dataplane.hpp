@@ -110,6 +110,7 @@ class DataPlanePass {
         cudaEventDestroy(sl.ev);
       }
     }
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (void* p : owned_) cudaFree(p);
   }
 
@@ -215,6 +216,39 @@ class DataPlanePass {
     return true;
   }
 
+  // CUDA-graph form of the stream-ordered pass for launch-bound batches:
+  // capture() records forward + merge once (segment offsets, flag ranges and
+  // tokens are baked in: the same first-fit offsets come back every pass, and
+  // nothing waits on the flags in stream order); run_graph() then does the
+  // host bookkeeping (alloc, release) and one graph launch per pass.
+  void capture(cudaStream_t st) {
+    if (!alloc()) throw std::runtime_error("fsx: slab full while capturing the pass");
+    cuda(cudaSetDevice(dev_));
+    cuda(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    forward(st);
+    merge(st);
+    cudaGraph_t g = nullptr;
+    cuda(cudaStreamEndCapture(st, &g));
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    cuda(cudaGraphInstantiate(&graph_exec_, g, 0));
+    cudaGraphDestroy(g);
+    captured_offs_ = offs_;
+    release();
+  }
+
+  bool run_graph(cudaStream_t st) {
+    if (!graph_exec_) throw std::runtime_error("fsx: capture() the pass first");
+    if (!alloc()) return false;
+    if (offs_ != captured_offs_) {  // the slab moved under us: re-record
+      release();
+      capture(st);
+      if (!alloc()) return false;
+    }
+    cuda(cudaGraphLaunch(graph_exec_, st));
+    release();
+    return true;
+  }
+
   uint8_t* embeds() const { return embeds_; }
   const int32_t* status() const { return status_; }
   int64_t total_rows() const { return total_rows_; }
@@ -273,6 +307,9 @@ class DataPlanePass {
   cudaEvent_t merged_ev_ = nullptr;
   int64_t* chunk_rows_dev_ = nullptr;
   uint64_t* flag0_ = nullptr;
+  // graph form
+  cudaGraphExec_t graph_exec_ = nullptr;
+  std::vector<int64_t> captured_offs_;
 };
 
 }  // namespace fsx

@@ -38,6 +38,7 @@ struct Case {
   int requests;
   int64_t item_rows, input_tokens, row_bytes, chunk_rows;
   bool colocated;  // K1 || early-start merge (DataPlanePass::run_colocated)
+  bool graph = false;  // stream-ordered pass replayed as a CUDA graph (run_graph)
 };
 
 int run_case(fsx_fabric* f, const Case& c, int passes) {
@@ -66,7 +67,11 @@ int run_case(fsx_fabric* f, const Case& c, int passes) {
     reqs[r].items.push_back({src + r * item_bytes, c.item_rows});
   }
   fsx::DataPlanePass pass(f, 0, 1, c.row_bytes, kPlaceholder, c.chunk_rows, reqs);
-  auto one = [&]() -> bool { return c.colocated ? pass.run_colocated(st, mst) : pass.run(st); };
+  if (c.graph) pass.capture(st);
+  auto one = [&]() -> bool {
+    if (c.graph) return pass.run_graph(st);
+    return c.colocated ? pass.run_colocated(st, mst) : pass.run(st);
+  };
   // prompt rows pre-filled like the Python batch (synth_payload(fnv1a64(id + "/text")))
   for (int r = 0, row = 0; r < c.requests; ++r) {
     const std::string key = rids[r] + "/text";
@@ -152,6 +157,10 @@ int main(int argc, char** argv) {
   rc |= run_case(f, Case{"B, colocated pass", 4, 16384, 1800, 7168, 1024, true}, passes);
   rc |= run_case(f, Case{"A-like: 64 x one 256-row 4096-d image", 64, 256, 500, 8192, 0, false}, passes);
   rc |= run_case(f, Case{"A-like, colocated pass", 64, 256, 500, 8192, 64, true}, passes);
+  rc |= run_case(f, Case{"A-like, stream-ordered pass as a CUDA graph", 64, 256, 500, 8192, 0, false, true},
+                 passes);
+  rc |= run_case(f, Case{"B, stream-ordered pass as a CUDA graph", 4, 16384, 1800, 7168, 1024, false, true},
+                 passes);
   fsx_close(f);
   return rc;
 }

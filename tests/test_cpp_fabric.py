@@ -136,4 +136,4 @@ def test_cpp_dataplane_pass_bit_exact(gpu):
     rc, out = _run("bench_pass", timeout=600)
     assert rc == 0, out[-4000:]
     lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
-    assert len(lines) == 4 and all(l["bit_exact_vs_oracle"] for l in lines), out[-2000:]
+    assert len(lines) == 6 and all(l["bit_exact_vs_oracle"] for l in lines), out[-2000:]
