@@ -31,6 +31,7 @@ constexpr int kFwdThreads = 256;
 #endif
 constexpr int kFollowOutPolicy = FSX_FOLLOW_OUT_POLICY;
 constexpr int kTmaTileBytes = 32768;  // K1 bulk-copy tile (forward_tma_kernel)
+constexpr int kMaxDevices = 64;       // per-device launch attributes
 // K1 variants: <vectors per lane per batch, min CTAs per SM>.  0: 16 x 16 B
 // (8 KiB per warp batch, 2 CTAs/SM), 1: 8 x 16 B at 4 CTAs/SM (register cap 64).
 constexpr int kMergeThreads = 256;
@@ -1109,10 +1110,16 @@ cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_
       static const int smem = [] {
         const char* e = std::getenv("FSX_FWD_BULK_SMEM");
         const int v = e ? std::atoi(e) : kTmaTileBytes;
-        const int bytes = v < kTmaTileBytes ? kTmaTileBytes : v;
-        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        return bytes;
+        return v < kTmaTileBytes ? kTmaTileBytes : v;
       }();
+      // the opt-in shared-memory limit is a per-device function attribute
+      static bool attr_set[kMaxDevices] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < kMaxDevices && !attr_set[dev]) {
+        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set[dev] = true;
+      }
       forward_tma_kernel<<<(unsigned)tiles, 32, smem, s>>>(b);
       return cudaGetLastError();
     }
@@ -1125,17 +1132,22 @@ cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_
       if (bb.t[k].vec) bb.t[k].vec = 16;
     const int64_t tiles = bb.unit_off[bb.n];
     if (tiles <= 0) return cudaSuccess;
-    // share_sm: pad shared memory so at most two K1 CTAs fit per SM
-    static const int pad = [] {
-      int dev = 0, smem = 0;
+    // share_sm: pad shared memory so at most two K1 CTAs fit per SM (the
+    // opt-in limit is a per-device function attribute)
+    static int pad[kMaxDevices] = {};
+    size_t smem = 0;
+    if (share_sm) {
+      int dev = 0;
       cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-      const int p = smem / 2 - 8 * 1024;  // 2 x pad + reserved fits, 3 x pad does not
-      cudaFuncSetAttribute(forward_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, p);
-      cudaFuncSetAttribute(forward_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p);
-      return p;
-    }();
-    const size_t smem = share_sm ? (size_t)pad : 0;
+      if (dev < kMaxDevices && pad[dev] == 0) {
+        int sm_smem = 0;
+        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        pad[dev] = sm_smem / 2 - 8 * 1024;  // 2 x pad + reserved fits, 3 x pad does not
+        cudaFuncSetAttribute(forward_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad[dev]);
+        cudaFuncSetAttribute(forward_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad[dev]);
+      }
+      smem = dev < kMaxDevices ? (size_t)pad[dev] : 0;
+    }
     if (variant == 3) forward_tile_kernel<4><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
     else forward_tile_kernel<8><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
     return cudaGetLastError();
