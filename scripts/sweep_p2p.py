@@ -31,7 +31,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=torch.cuda.device_count())
     ap.add_argument("--chunk", type=int, default=1 << 20)
+    ap.add_argument("--cpu-ref", action="store_true",
+                    help="also time the reference CPU forward (oracle/_ref SidecarFabric, 1 thread) per size")
     args = ap.parse_args()
+    cref = None
+    if args.cpu_ref:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O  # the reference CPU path, timed beside the kernel (checker library)
+        cref = O.REF
     n = min(args.gpus, torch.cuda.device_count())
     if n < 2:
         print(json.dumps({"note": "config E P2P sweep needs >= 2 GPUs", "gpus": n}))
@@ -78,6 +85,10 @@ def main():
                          "frac_of_770_measured": round(min(per) / 770.0, 3)}
         for _, c in pairs:
             fab.slab_free(c, offs[c])
+        if cref is not None:
+            iters = max(2, min(200, (256 << 20) // size))
+            secs = cref.ref_forward_bench(size, iters, 1)
+            res["cpu_reference"] = {"payload_gbs": round(size * iters / secs / 1e9, 3), "threads": 1}
         print(json.dumps({"gpus": n, "pairs": len(pairs), "bytes": size, "chunk_bytes": chunk,
                           **res}), flush=True)
     fab.close()
