@@ -127,6 +127,8 @@ def _load_ref():
                                        C_.c_void_p, C_.c_void_p, C_.c_void_p, C_.c_void_p,
                                        C_.c_void_p, C_.c_void_p, C_.c_void_p, C_.c_int, C_.c_int,
                                        C_.c_int, C_.c_void_p]
+    lib.ref_dataplane_pass_mt.restype = C_.c_double
+    lib.ref_dataplane_pass_mt.argtypes = lib.ref_dataplane_pass.argtypes
     lib.ref_stream_bench.restype = C_.c_double
     lib.ref_stream_bench.argtypes = [C_.c_int64, C_.c_int, C_.c_int]
     lib.ref_generate_workload.restype = C_.c_char_p

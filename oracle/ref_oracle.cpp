@@ -12,6 +12,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fissim/executor_sim.hpp"
@@ -235,6 +236,79 @@ double ref_dataplane_pass(int32_t num_requests, int32_t num_items, int64_t row_b
     g_err = e.what();
     return -1;
   }
+}
+
+// The same pass on all host threads the reference can use: the reference
+// fabric is single-threaded by construction (sim_kernel.hpp:147-183), so the
+// requests are split into `fwd_threads` contiguous groups and every thread
+// runs its own SimKernel + SidecarFabric (one reference sidecar per core)
+// forwarding its group, then merges its group's requests.  Returns wall
+// seconds of the whole pass, or a negative value on error.
+double ref_dataplane_pass_mt(int32_t num_requests, int32_t num_items, int64_t row_bytes,
+                             int32_t placeholder_id, uint8_t* embeds, const int32_t* token_ids,
+                             const int64_t* req_row_off, const int64_t* req_item_off,
+                             const uint8_t* const* item_payload, const int64_t* item_rows,
+                             const char* const* ref_ids, int src_gpu, int dst_gpu, int fwd_threads,
+                             int32_t* status) {
+  const int T = std::max(1, std::min<int>(fwd_threads, num_requests));
+  std::vector<std::thread> pool;
+  std::vector<double> err(T, 0.0);
+  std::vector<std::string> msg(T);
+  auto t0 = std::chrono::steady_clock::now();
+  for (int t = 0; t < T; ++t) {
+    pool.emplace_back([&, t] {
+      const int32_t r0 = static_cast<int32_t>(int64_t{num_requests} * t / T);
+      const int32_t r1 = static_cast<int32_t>(int64_t{num_requests} * (t + 1) / T);
+      const int64_t i0 = req_item_off[r0], i1 = req_item_off[r1];
+      try {
+        SimKernel k(ClockMode::Virtual);
+        int64_t total = 0;
+        for (int64_t i = i0; i < i1; ++i) total += item_rows[i] * row_bytes;
+        SidecarConfig cfg;
+        cfg.arena_bytes = std::max<int64_t>(cfg.arena_bytes, total + 64 * (i1 - i0 + 1));
+        SidecarFabric fabric(k, topo_8x2(), cfg);
+        std::vector<std::vector<uint8_t>> got(static_cast<size_t>(i1 - i0));
+        for (int64_t i = i0; i < i1; ++i)
+          fabric.register_interest(dst_gpu, ref_ids[i], [&got, i, i0](const ForwardEnvelope&, std::vector<uint8_t> b) {
+            got[static_cast<size_t>(i - i0)] = std::move(b);
+          });
+        k.post("send", [&] {
+          for (int64_t i = i0; i < i1; ++i) {
+            DataRef ref;
+            ref.ref_id = ref_ids[i];
+            ref.producer = "encoder";
+            ref.desc = {{item_rows[i], row_bytes / 2}, 2};
+            std::string rid(ref.ref_id.substr(0, ref.ref_id.find('/')));
+            fabric.send_payload(rid, ref, src_gpu, dst_gpu,
+                                std::span<const uint8_t>(item_payload[i], item_rows[i] * row_bytes));
+          }
+        });
+        k.run_until_idle();
+        // the merge of this group (item pointers indexed globally)
+        std::vector<const uint8_t*> src(static_cast<size_t>(num_items), nullptr);
+        for (int64_t i = i0; i < i1; ++i) {
+          if (static_cast<int64_t>(got[i - i0].size()) != item_rows[i] * row_bytes) {
+            err[t] = -2;
+            msg[t] = "item " + std::to_string(i) + " not delivered";
+            return;
+          }
+          src[i] = got[i - i0].data();
+        }
+        or_merge(r1 - r0, row_bytes, placeholder_id, embeds, token_ids, req_row_off + r0, req_item_off + r0,
+                 src.data(), item_rows, status + r0, 1);
+      } catch (const std::exception& e) {
+        err[t] = -1;
+        msg[t] = e.what();
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (int t = 0; t < T; ++t)
+    if (err[t] < 0) {
+      g_err = msg[t];
+      return err[t];
+    }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 // Reference small-message streaming (config C): `streams` streaming refs (one
