@@ -1301,6 +1301,23 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_
                : "memory");
 }
 
+// bulk store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_store_hint(void* dst, uint32_t src_smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(src_smem), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+// bulk load with an L2 eviction-priority policy
+__device__ __forceinline__ void bulk_load_hint(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -1413,21 +1430,26 @@ __global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__
   tma::mbar_init(tma::smem_u32(&bars[0]), 1);
   tma::mbar_init(tma::smem_u32(&bars[1]), 1);
   tma::mbar_fence_init();
+  // the producer's source is read once (evict first); slab stores keep L2
+  // priority when the consumer merges right behind (FSX_FWD_L2_KEEP)
+  const uint64_t ld_pol = l2_policy(1);
+  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
   if (len0 > 0) {
     tma::mbar_expect_tx(tma::smem_u32(&bars[0]), (uint32_t)len0);
-    tma::bulk_load(sbase, a.src + beg, (uint32_t)len0, tma::smem_u32(&bars[0]));
+    tma::bulk_load_hint(sbase, a.src + beg, (uint32_t)len0, tma::smem_u32(&bars[0]), ld_pol);
   }
   if (len1 > 0) {
     tma::mbar_expect_tx(tma::smem_u32(&bars[1]), (uint32_t)len1);
-    tma::bulk_load(sbase + (uint32_t)len0, a.src + beg + len0, (uint32_t)len1, tma::smem_u32(&bars[1]));
+    tma::bulk_load_hint(sbase + (uint32_t)len0, a.src + beg + len0, (uint32_t)len1, tma::smem_u32(&bars[1]),
+                        ld_pol);
   }
   if (len0 > 0) {
     tma::mbar_wait(tma::smem_u32(&bars[0]), 0);
-    tma::bulk_store(a.dst + beg, sbase, (uint32_t)len0);
+    tma::bulk_store_hint(a.dst + beg, sbase, (uint32_t)len0, st_pol);
   }
   if (len1 > 0) {
     tma::mbar_wait(tma::smem_u32(&bars[1]), 0);
-    tma::bulk_store(a.dst + beg + len0, sbase + (uint32_t)len0, (uint32_t)len1);
+    tma::bulk_store_hint(a.dst + beg + len0, sbase + (uint32_t)len0, (uint32_t)len1, st_pol);
   }
   tma::bulk_commit();
   for (int64_t j = vend; j < end; ++j) a.dst[j] = a.src[j];  // sub-16-byte tail
