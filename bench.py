@@ -23,6 +23,7 @@ step vs 126 MB L2), so no flush is needed between steps.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -812,9 +813,12 @@ def _rank_device(rank):
         local = int(pinned)
     torch.cuda.set_device(local)
     if pinned is None:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # a rank that dies must not leave the others waiting for the default
+        # 10 minutes in a setup collective or barrier
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=3))
         return local, pinned, "cuda"
-    dist.init_process_group("gloo")
+    dist.init_process_group("gloo", timeout=datetime.timedelta(minutes=3))
     return local, pinned, "cpu"
 
 
