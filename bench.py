@@ -657,18 +657,20 @@ def run_pairs(args, rank, world):
     """One process per GPU: rank 2k pushes its encoder outputs into rank
     2k+1's receive slab over NVLink (K1 on the producer, CUDA IPC mapping);
     rank 2k+1 merges with in-kernel early start on the chunk flags (K3) and
-    acks the step into the producer's ack flag.  No collective on the data
-    path; timing is the max over ranks of the device-timed region."""
+    acks the step into the producer's ack flag.  The consumer holds two sets
+    of slab segments (and two prompt batches) so step s+1's transfer never
+    waits for step s's merge and ack: the producer only waits for the ack of
+    step s-1 of the same set (FSX_PAIRS_SETS=1 turns that off).  No collective
+    on the data path; timing is the max over ranks of the device-timed region."""
     import numpy as np
     import torch
-
-    from paper_2603_12118_b200 import _native as N
     import torch.distributed as dist
 
+    from paper_2603_12118_b200 import _native as N
     from paper_2603_12118_b200 import pairs as PR
     from paper_2603_12118_b200 import trace as T
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
-    from paper_2603_12118_b200.fabric import DeviceFabric
+    from paper_2603_12118_b200.fabric import DeviceFabric, _stream_ptr
 
     local, pinned, red_dev = _rank_device(rank)
     me = PR.role(rank, world)
@@ -677,7 +679,8 @@ def run_pairs(args, rank, world):
     reqs = T.config_requests(CONFIG, args.requests)
     lay = T.layout(reqs, rules.row_bytes)
     stream = torch.cuda.Stream(device=local)
-    slab_bytes = max(1 << 30, 2 * lay.payload_bytes)
+    sets = 1 if me.alone else max(1, int(os.environ.get("FSX_PAIRS_SETS", "2")))
+    slab_bytes = max(1 << 30, sets * lay.payload_bytes + (64 << 20))
     # both logical gpus of the pair are bound to this process's device; the
     # peer's slab is imported (mapped over NVLink) under its logical id
     fab = DeviceFabric({P: 0, Cg: 0}, {P: local, Cg: local})
@@ -685,7 +688,7 @@ def run_pairs(args, rank, world):
         fab.slab_register(Cg, slab_bytes)
         mine = None
     elif me.producer:
-        fab.slab_register(P, 1 << 20)  # ack flags live in this small slab
+        fab.slab_register(P, 1 << 20)  # ack flags (one per segment set) live in this small slab
         mine = fab.slab_export(P)
     else:
         fab.slab_register(Cg, slab_bytes)
@@ -693,40 +696,51 @@ def run_pairs(args, rank, world):
     handles = PR.exchange(mine)
     if not me.alone:
         fab.slab_import(Cg if me.producer else P, *handles[me.peer])
-    batch = DataPlaneBatch(fab, reqs, rules, P, Cg, chunk_rows=CHUNK_ROWS)
+    consumer = me.alone or not me.producer
+    nb = sets if consumer else 1
+    batches = [DataPlaneBatch(fab, reqs, rules, P, Cg, chunk_rows=CHUNK_ROWS) for _ in range(nb)]
+    batch = batches[0]
     with torch.cuda.stream(stream):
-        batch.synth_inputs(stream)
-    if me.alone or not me.producer:
-        assert batch.alloc()
+        for b in batches:
+            b.synth_inputs(stream)
+    if consumer:
+        for b in batches:
+            assert b.alloc()
     torch.cuda.synchronize()
-    offs = PR.exchange(None if (me.producer or me.alone) else batch.slab_off.tolist())
-    if me.producer and not me.alone:
-        batch.slab_off = np.array(offs[me.peer], dtype=np.int64)
+    offs = PR.exchange(None if not consumer or me.alone else [b.slab_off.tolist() for b in batches])
+    set_offs = [np.array(o, dtype=np.int64) for o in offs[me.peer]] if (me.producer and not me.alone) \
+        else [b.slab_off for b in batches]
     chunk_rows = CHUNK_ROWS or max(1, max((it.rows for it in lay.items), default=1))
     chunks = [max(1, -(-it.rows // chunk_rows)) for it in lay.items]
+    M = len(lay.items)
+    xfers = (N.Transfer * max(M, 1))()
+    view = np.frombuffer(xfers, dtype=N.TRANSFER_DTYPE, count=max(M, 1))[:M]
+    for i, it in enumerate(lay.items):
+        xfers[i] = N.Transfer(P, Cg, batch.src_buf.data_ptr() + int(batch.src_off[i]), 0,
+                              it.rows * batch.rb, chunk_rows * batch.rb, 0, 0, None)
 
     def step(s):
         if me.alone:
             batch.forward(stream, host_notify=False)
             batch.merge(stream)
             return
+        k = s % sets
         sched = PR.schedule(s, chunks)
         if me.producer:
-            if s > 0:  # consumer acked step s-1: its slab segments are free again
-                fab.stream_wait_flags(P, 0, 1, PR.ack_token(s - 1), stream)
-            base = batch.src_buf.data_ptr()
-            for i, it in enumerate(lay.items):
-                fb, tok = sched[i]
-                fab.forward(P, base + int(batch.src_off[i]), Cg, int(batch.slab_off[i]),
-                            it.rows * batch.rb, chunk_rows * batch.rb, fb, stream, token=tok,
-                            host_notify=False)
+            if s >= sets:  # the consumer acked step s-sets: segment set k is free again
+                fab.stream_wait_flags(P, k, 1, PR.ack_token(s - sets), stream)
+            view["dst_off"] = set_offs[k]
+            view["flag_base"] = [fb for fb, _ in sched]
+            view["token"] = [tok for _, tok in sched]
+            N.call("fsx_forward_batch", fab._h, M, xfers, 0, _stream_ptr(stream))  # one K1 launch
         else:
-            for i in range(len(lay.items)):
-                batch.flag_base[i], batch.tokens[i] = sched[i]
-                batch.n_chunks[i] = chunks[i]
+            b = batches[k]
+            for i in range(M):
+                b.flag_base[i], b.tokens[i] = sched[i]
+                b.n_chunks[i] = chunks[i]
             # waits per chunk inside K3; merged slab rows are dropped from L2
-            batch.merge(stream, early_start=True, mode=N.MERGE_FULL | N.MERGE_DISCARD)
-            fab.signal_flags(P, 0, 1, PR.ack_token(s), Cg, stream)
+            b.merge(stream, early_start=True, mode=N.MERGE_FULL | N.MERGE_DISCARD)
+            fab.signal_flags(P, k, 1, PR.ack_token(s), Cg, stream)
 
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
@@ -746,22 +760,26 @@ def run_pairs(args, rank, world):
         launches = fab.stats()["kernel_launches"] - l0
     e2e = _e2e_phase(args, step, stream, red_dev, PR.pairs_in(world) * lay.payload_bytes,
                      [batch.src_buf] if (me.producer or me.alone) else [],
-                     batch if (not me.producer or me.alone) else None,
+                     (lambda s: batches[s % sets]) if consumer else None,
                      first=args.warmup + args.steps, n_requests=PR.pairs_in(world) * len(reqs))
     verified = None
-    if not me.producer or me.alone:
-        st = batch.status_host()
-        assert (st == 0).all(), st
+    if consumer:
+        for b in batches:
+            st = b.status_host()
+            assert (st == 0).all(), st
         if args.verify:
             # the pair-merged prompt embeddings must equal a local intra-device
             # forward + merge of the same requests (both bit-exact to the oracle)
+            torch.cuda.synchronize()
+            for b in batches:
+                b.release()  # the run is over: make room in the slab for the local pass
             local_b = DataPlaneBatch(fab, reqs, rules, P, Cg, chunk_rows=CHUNK_ROWS)
             local_b.synth_inputs()
             assert local_b.alloc()
             local_b.forward(host_notify=False)
             local_b.merge()
             torch.cuda.synchronize()
-            verified = bool(torch.equal(local_b.embeds, batch.embeds))
+            verified = all(bool(torch.equal(local_b.embeds, b.embeds)) for b in batches)
             local_b.release()
             assert verified, "pair-merged embeddings differ from the local reference pass"
     ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=red_dev)
@@ -783,6 +801,7 @@ def run_pairs(args, rank, world):
                                    "2k+1 over NVLink (CUDA IPC slab), early-start merge on the consumer",
                        "requests_per_step_per_pair": len(reqs), "pairs": n_pairs,
                        "chunk_bytes": chunk_rows * rules.row_bytes,
+                       "slab_segment_sets": sets,
                        "parallelism": f"{n_pairs} independent producer->consumer pairs"},
             "roofline": {"bound": "nvlink", "achieved": round(pair_gbs, 1), "peak": 900.0,
                          "unit": "GB/s", "frac": round(pair_gbs / 900.0, 4), "traffic": None,
@@ -1009,7 +1028,9 @@ def _e2e_phase(args, step, stream, red_dev, payload_all, src_bufs, recv_batch, f
         h = torch.empty(b.numel(), dtype=torch.uint8, pin_memory=True)
         h.copy_(b)
         host.append(h)
-    nreq = len(recv_batch.lay.requests) if recv_batch is not None else 0
+    recv_of = recv_batch if callable(recv_batch) else (lambda s: recv_batch)
+    first_recv = recv_of(first)
+    nreq = len(first_recv.lay.requests) if first_recv is not None else 0
     status_h = torch.empty(max(nreq, 1), dtype=torch.int32, pin_memory=True)
 
     def e2e_step(s):
@@ -1017,7 +1038,7 @@ def _e2e_phase(args, step, stream, red_dev, payload_all, src_bufs, recv_batch, f
             d.copy_(h, non_blocking=True)
         step(s)
         if recv_batch is not None:
-            status_h[:nreq].copy_(recv_batch.status[:nreq], non_blocking=True)
+            status_h[:nreq].copy_(recv_of(s).status[:nreq], non_blocking=True)
         stream.synchronize()
         if recv_batch is not None and nreq and int(status_h[:nreq].numpy().max()) != 0:
             raise RuntimeError("merge validation failed in e2e step")
