@@ -849,7 +849,9 @@ def run_fanout(args, rank, world):
     LLMs fan in from several encoders.  Each encoder maps the slabs of the LLMs
     it feeds (CUDA IPC) and pushes all its items of a step with one batched K1
     call over NVLink; each LLM merges with in-kernel early start and acks
-    every encoder that fed it.  No collective on the data path."""
+    every encoder that fed it.  Every LLM holds two sets of slab segments
+    (FSX_PAIRS_SETS), so an encoder's next transfer does not wait for the
+    current merge.  No collective on the data path."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -872,26 +874,29 @@ def run_fanout(args, rank, world):
     me = rank // 2  # encoder ordinal (even ranks) / LLM ordinal (odd ranks)
     stream = torch.cuda.Stream(device=local)
     fab = DeviceFabric({g: 0 for g in range(world)}, {g: local for g in range(world)})
-    batch = None
+    sets = max(1, int(os.environ.get("FSX_PAIRS_SETS", "2")))
+    batch, batches = None, []
     if producer:
-        fab.slab_register(rank, 1 << 20)  # ack flags: index = LLM ordinal
+        fab.slab_register(rank, 1 << 20)  # ack flags: index = LLM ordinal x sets + set
         mine = fab.slab_export(rank)
     else:
         reqs_c = [reqs[k] for k in pl.consumer_requests(me)]
-        batch = DataPlaneBatch(fab, reqs_c, rules, rank, rank, chunk_rows=chunk_rows)
-        fab.slab_register(rank, max(1 << 30, 2 * batch.lay.payload_bytes))
+        batches = [DataPlaneBatch(fab, reqs_c, rules, rank, rank, chunk_rows=chunk_rows)
+                   for _ in range(sets)]
+        batch = batches[0]
+        fab.slab_register(rank, max(1 << 30, (sets + 1) * batch.lay.payload_bytes + (64 << 20)))
         mine = fab.slab_export(rank)
     handles = PR.exchange(mine)
     peers = ([pl.consumers[c] for c in pl.consumers_of(me)] if producer
              else [pl.producers[p] for p in pl.producers_of(me)])
     for r in peers:
         fab.slab_import(r, *handles[r])
-    if batch is not None:
+    for b in batches:
         with torch.cuda.stream(stream):
-            batch.synth_inputs(stream)
-        assert batch.alloc()
+            b.synth_inputs(stream)
+        assert b.alloc()
     torch.cuda.synchronize()
-    offs = PR.exchange(None if producer else batch.slab_off.tolist())
+    offs = PR.exchange(None if producer else [b.slab_off.tolist() for b in batches])
 
     items = pl.producer_items(me) if producer else []
     xfers = (N.Transfer * max(len(items), 1))()
@@ -909,30 +914,36 @@ def run_fanout(args, rank, world):
                       sizes[i], stream)
             c, idx = slots[i]
             xfers[i] = N.Transfer(rank, pl.consumers[c], src_buf.data_ptr() + int(src_off[i]),
-                                  int(offs[pl.consumers[c]][idx]), sizes[i], chunk_rows * rb, 0, 0, None)
+                                  0, sizes[i], chunk_rows * rb, 0, 0, None)
         my_bytes = int(sum(sizes))
         torch.cuda.synchronize()
+    # destination offsets of every item in each segment set of its LLM
+    set_offs = [np.array([int(offs[pl.consumers[c]][k][idx]) for c, idx in slots], dtype=np.int64)
+                for k in range(sets)] if producer else []
     acks_from = pl.consumers_of(me) if producer else []
     acks_to = pl.producers_of(me) if not producer else []
 
     def step(s):
+        k = s % sets
         if producer:
-            if s > 0:  # every LLM this encoder fed acked step s-1: slab segments free again
+            if s >= sets:  # every LLM this encoder fed acked step s-sets: set k is free again
                 for c in acks_from:
-                    fab.stream_wait_flags(rank, c, 1, PR.ack_token(s - 1), stream)
+                    fab.stream_wait_flags(rank, c * sets + k, 1, PR.ack_token(s - sets), stream)
             if items:
                 sch = [pl.schedule(s, c, idx) for c, idx in slots]
+                view["dst_off"] = set_offs[k]
                 view["flag_base"] = [b for b, _ in sch]
                 view["token"] = [t for _, t in sch]
                 N.call("fsx_forward_batch", fab._h, len(items), xfers, 0, _stream_ptr(stream))
         else:
-            for idx, (k, j) in enumerate(pl.consumer_items[me]):
-                batch.flag_base[idx], batch.tokens[idx] = pl.schedule(s, me, idx)
-                batch.n_chunks[idx] = pl.chunks[k][j]
+            b = batches[k]
+            for idx, (q, j) in enumerate(pl.consumer_items[me]):
+                b.flag_base[idx], b.tokens[idx] = pl.schedule(s, me, idx)
+                b.n_chunks[idx] = pl.chunks[q][j]
             # waits per chunk inside K3; merged slab rows are dropped from L2
-            batch.merge(stream, early_start=True, mode=N.MERGE_FULL | N.MERGE_DISCARD)
+            b.merge(stream, early_start=True, mode=N.MERGE_FULL | N.MERGE_DISCARD)
             for p in acks_to:
-                fab.signal_flags(pl.producers[p], me, 1, PR.ack_token(s), rank, stream)
+                fab.signal_flags(pl.producers[p], me * sets + k, 1, PR.ack_token(s), rank, stream)
 
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
@@ -952,11 +963,13 @@ def run_fanout(args, rank, world):
         launches = fab.stats()["kernel_launches"] - l0
     total_payload = sum(it.rows * rb for q in reqs for it in q.items)
     e2e = _e2e_phase(args, step, stream, red_dev, total_payload,
-                     [src_buf] if producer else [], batch if not producer else None,
+                     [src_buf] if producer else [],
+                     (lambda s: batches[s % sets]) if not producer else None,
                      first=args.warmup + args.steps, n_requests=len(reqs))
     if not producer:
-        st = batch.status_host()
-        assert (st == 0).all(), st
+        for b in batches:
+            st = b.status_host()
+            assert (st == 0).all(), st
         if args.verify:
             local_b = DataPlaneBatch(fab, batch.lay.requests, rules, rank, rank, chunk_rows=chunk_rows)
             local_b.synth_inputs()
@@ -964,7 +977,7 @@ def run_fanout(args, rank, world):
             local_b.forward(host_notify=False)
             local_b.merge()
             torch.cuda.synchronize()
-            ok = bool(torch.equal(local_b.embeds, batch.embeds))
+            ok = all(bool(torch.equal(local_b.embeds, b.embeds)) for b in batches)
             local_b.release()
             assert ok, "fan-in merged embeddings differ from the local reference pass"
     ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=red_dev)
