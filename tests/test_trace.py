@@ -84,7 +84,8 @@ def test_bench_clock_summary_and_sample():
     s = cs.summary()
     assert s["sm_max_mhz"] == 1965 and s["reasons"] == ["sw_power_cap"]
     b.CONFIG, b.REQUESTS = "B", 4
-    assert len(b.cpu_sample(T)) == 1  # one video request (>= 100 MiB)
+    # >= 100 MiB and a request per host thread while the batch has them
+    assert len(b.cpu_sample(T)) == min(4, max(1, os.cpu_count() or 1))
     b.CONFIG, b.REQUESTS = "A", 64
     sample = b.cpu_sample(T)  # the whole 64-request batch is < 100 MiB
     assert len(sample) == 64
