@@ -598,7 +598,11 @@ def run_e2e(args, fab, reqs, rules, stream):
     from paper_2603_12118_b200 import trace as T
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
 
-    batch = DataPlaneBatch(fab, reqs, rules, src_gpu=0, dst_gpu=1, chunk_rows=CHUNK_ROWS)
+    # host->device copies per flagged chunk: 4 frames (28 MiB) -- every H2D copy
+    # costs a fixed gap on the copy engine, and 7 MiB copies lose ~3 % of the
+    # PCIe rate (FSX_E2E_CHUNK_ROWS overrides; profiles/README.md)
+    e2e_chunk = int(os.environ.get("FSX_E2E_CHUNK_ROWS", "0")) or (4 * CHUNK_ROWS if CHUNK_ROWS else None)
+    batch = DataPlaneBatch(fab, reqs, rules, src_gpu=0, dst_gpu=1, chunk_rows=e2e_chunk)
     with torch.cuda.stream(stream):
         batch.synth_inputs(stream)
     torch.cuda.synchronize()
@@ -611,12 +615,25 @@ def run_e2e(args, fab, reqs, rules, stream):
         host.append(h.numpy())
     status_h = torch.empty(len(reqs), dtype=torch.int32, pin_memory=True)
     h2d = sum(h.nbytes for h in host)
+    # the merge follows the host->device copy chunk by chunk (early start on
+    # the per-chunk flags the copy publishes) on a high-priority stream, so a
+    # step costs the PCIe transfer plus the last chunk's merge
+    from paper_2603_12118_b200 import _native as N
+    mstream = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
+    overlap = os.environ.get("FSX_E2E_OVERLAP", "1") == "1"
 
     def step():
         assert batch.alloc()
         batch.forward_host(host, stream)
-        batch.merge(stream)
-        status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
+        if overlap:
+            with torch.cuda.stream(mstream):
+                batch.merge(mstream, early_start=True,
+                            mode=N.MERGE_FULL | N.MERGE_COLOCATED | N.MERGE_DISCARD)
+                status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
+            mstream.synchronize()
+        else:
+            batch.merge(stream)
+            status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
         stream.synchronize()
         batch.release()
         if int(status_h.numpy().max()) != 0:
@@ -647,7 +664,8 @@ def run_e2e(args, fab, reqs, rules, stream):
             "steps": steps, "pcie_h2d_copy_gbs": round(h2d_peak, 2),
             "frac_of_pcie_h2d": round(h2d / dt / 1e9 / h2d_peak, 3),
             "path": "fsx_forward_host (pinned host -> consumer slab, per-frame chunks + flags) "
-                    "-> fsx_merge -> status D2H, wall clock per step"}
+                    "-> fsx_merge" + (" (early start on the copy's chunk flags)" if overlap else "") +
+                    " -> status D2H, wall clock per step"}
 
 
 # ---------------------------------------------------------------------------
