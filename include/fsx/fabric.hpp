@@ -448,6 +448,9 @@ class Fabric {
       }
     }
     int64_t cb = config_.device_chunk_bytes;
+    // host spans cross PCIe: every copy costs a fixed copy-engine gap, so
+    // they go in chunks of at least 32 MiB (send() waits for all of it anyway)
+    if (!ps.src_is_device && cb > 0) cb = std::max<int64_t>(cb, int64_t{32} << 20);
     if (cb <= 0 || cb >= n) cb = 0;
     *n_chunks = cb ? static_cast<int32_t>((n + cb - 1) / cb) : 1;
     check(fsx_flags_alloc(h_, dst, *n_chunks, flag_base));

@@ -134,3 +134,33 @@ def test_fanout_plan_two_ranks_is_a_pair():
     assert pl.producers == [0] and pl.consumers == [1]
     assert set(pl.llm_of) == {0}
     assert all(e == 0 for es in pl.enc_of for e in es)
+
+
+@pytest.mark.parametrize("world", [3, 5, 6])
+def test_fanout_plan_odd_and_uneven_worlds(world):
+    """Encoders on the even ranks, LLMs on the odd ones for any world size:
+    every item lands in exactly one LLM list, placement stays round robin per
+    task, and per-LLM flag ranges stay disjoint."""
+    from paper_2603_12118_b200 import fanout
+    from paper_2603_12118_b200 import trace as T
+
+    reqs = T.config_requests("D", 40)
+    pl = fanout.plan(reqs, world, 1024)
+    assert pl.producers == list(range(0, world, 2)) and pl.consumers == list(range(1, world, 2))
+    n_llm = len(pl.consumers)
+    assert pl.llm_of == [k % n_llm for k in range(40)]
+    everything = sorted((k, j) for k, q in enumerate(reqs) for j in range(len(q.items)))
+    assert sorted(kj for c in range(n_llm) for kj in pl.consumer_items[c]) == everything
+    assert sorted(kj for p in range(len(pl.producers)) for kj in pl.producer_items(p)) == everything
+    for c in range(n_llm):
+        spans = sorted((pl.schedule(7, c, i)[0], pl.schedule(7, c, i)[0] + pl.chunks[k][j])
+                       for i, (k, j) in enumerate(pl.consumer_items[c]))
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_fanout_plan_needs_an_llm_rank():
+    from paper_2603_12118_b200 import fanout
+    from paper_2603_12118_b200 import trace as T
+
+    with pytest.raises(ValueError):
+        fanout.plan(T.config_requests("D", 4), 1, 1024)
