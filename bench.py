@@ -606,13 +606,15 @@ def run_e2e(args, fab, reqs, rules, stream):
     with torch.cuda.stream(stream):
         batch.synth_inputs(stream)
     torch.cuda.synchronize()
+    # the producer's outputs in one pinned buffer, item i at src_off[i] (the
+    # same layout as on the device); views per item
+    pinned = torch.empty(batch.src_buf.numel(), dtype=torch.uint8, pin_memory=True)
+    pinned.copy_(batch.src_buf)
     host = []
     for i, it in enumerate(batch.lay.items):
         nb = it.rows * batch.rb
-        h = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
         off = int(batch.src_off[i])
-        h.copy_(batch.src_buf[off:off + nb])
-        host.append(h.numpy())
+        host.append(pinned[off:off + nb].numpy())
     status_h = torch.empty(len(reqs), dtype=torch.int32, pin_memory=True)
     h2d = sum(h.nbytes for h in host)
     # the merge follows the host->device copy chunk by chunk (early start on

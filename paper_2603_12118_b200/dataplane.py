@@ -156,8 +156,14 @@ class DataPlaneBatch:
 
     def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
         """The host-span send path (sidecar.hpp:302): payload bytes from host
-        memory straight into the consumer slab."""
+        memory straight into the consumer slab.  Single-chunk items whose host
+        buffers and slab segments are both back to back go as ONE copy (every
+        host->device copy costs a fixed copy-engine gap); they then share that
+        copy's flag and token."""
         assert self.slab_off is not None, "alloc() first"
+        if not self.chunk_rows and len(self.lay.items) > 1:
+            self._forward_host_coalesced(host_payload, stream)
+            return
         for i, it in enumerate(self.lay.items):
             nb = it.rows * self.rb
             cb = self.chunk_bytes(it)
@@ -167,6 +173,25 @@ class DataPlaneBatch:
             self.tokens[i] = self.fab.forward_host(host_payload[i].ctypes.data, self.dst_gpu,
                                                    int(self.slab_off[i]), nb, cb,
                                                    int(self.flag_base[i]), stream)
+
+    def _forward_host_coalesced(self, host_payload: List[np.ndarray], stream=None) -> None:
+        M = len(self.lay.items)
+        i = 0
+        while i < M:
+            j, nb = i, int(self.item_bytes[i])
+            while (j + 1 < M and
+                   host_payload[j + 1].ctypes.data == host_payload[j].ctypes.data + int(self.item_bytes[j]) and
+                   int(self.slab_off[j + 1]) == int(self.slab_off[j]) + int(self.item_bytes[j])):
+                j += 1
+                nb += int(self.item_bytes[j])
+            fb = self.fab.flags_alloc(self.dst_gpu, 1)
+            tok = self.fab.forward_host(host_payload[i].ctypes.data, self.dst_gpu, int(self.slab_off[i]),
+                                        nb, 0, fb, stream)
+            for k in range(i, j + 1):
+                self.n_chunks[k] = 1
+                self.flag_base[k] = fb
+                self.tokens[k] = tok
+            i = j + 1
 
     def wait_host(self, timeout_us: int = 30_000_000) -> None:
         for i in range(len(self.lay.items)):

@@ -456,3 +456,30 @@ def test_spin_watchdog_traps_instead_of_hanging(gpu):
                        capture_output=True, text=True, timeout=120)
     assert p.returncode == 0 and "TRAPPED" in p.stdout, (p.stdout + p.stderr)[-2000:]
     assert time.time() - t0 < 90
+
+
+def test_forward_host_coalesced_batch_bit_exact(fab, oracle_mod):
+    """The host-span batch path with back-to-back items (one pinned buffer, one
+    H2D copy for the whole run of single-chunk items, shared flag) followed by
+    the early-start merge: merged rows equal the oracle."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests("A", 16)
+    b = DataPlaneBatch(fab, reqs, T.RULES["A"], 0, 1)
+    b.synth_inputs()
+    torch.cuda.synchronize()
+    want, st = _expected(oracle_mod, b)
+    pinned = torch.empty(b.src_buf.numel(), dtype=torch.uint8, pin_memory=True)
+    pinned.copy_(b.src_buf)
+    host = [pinned[int(b.src_off[i]):int(b.src_off[i]) + int(b.item_bytes[i])].numpy()
+            for i in range(len(b.lay.items))]
+    for _ in range(2):
+        assert b.alloc()
+        b.forward_host(host)
+        assert len(set(b.tokens.tolist())) < len(b.lay.items)  # items were coalesced
+        b.merge(early_start=True)
+        torch.cuda.synchronize()
+        assert (b.status_host() == 0).all() and (st == 0).all()
+        assert np.array_equal(b.embeds_host(), want)
+        b.release()
