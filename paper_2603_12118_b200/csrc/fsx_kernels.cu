@@ -621,7 +621,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_bat
   const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
   const int64_t rb = b.row_bytes;
   const bool vec_rows = (rb & 15) == 0;
-  const bool newest_first = b.d_item_flag == nullptr;  // L2 reuse, see merge_copy_tma_kernel
+  // newest rows first (meant for L2 reuse of K1's tail; measured no effect on
+  // B200, DESIGN.md §3 -- kept, it costs nothing)
+  const bool newest_first = b.d_item_flag == nullptr;
   const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
   for (int64_t k = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
        k < b.total_item_rows; k += warps) {
