@@ -493,6 +493,29 @@ def run_single(args):
             _, ev_iso, _ = timed(step_serial, iso_steps)
         else:
             ev_iso = []
+        # Direct placement (fsx_forward_place): the forward fused with the
+        # merge -- the producer writes each row straight into the consumer's
+        # placeholder rows, no slab round trip.  Not the headline (the
+        # reference places payloads in the consumer's arena); reported beside it.
+        place_ms = None
+        if not args.profile and os.environ.get("FSX_BENCH_DIRECT", "1") == "1":
+            def step_place(record=False):
+                # the placeholder scan pipelined one pass ahead on the side
+                # stream, as in the stream-ordered pass; one copy-only launch
+                s = counter[0]
+                counter[0] += 1
+                if s > 0:
+                    stream.wait_event(merged[(s - 1) % 2])
+                cur, nxt = s % 2, (s + 1) % 2
+                fork_ev.record(stream)
+                side.wait_event(fork_ev)
+                batch.scan(side, slot=nxt)
+                scanned[nxt].record(side)
+                stream.wait_event(scanned[cur])
+                batch.place(stream, mode=N.MERGE_COPY_ONLY, slot=cur)
+            for _ in range(3):
+                step_place()
+            place_ms, _, place_launches = timed(step_place, max(5, min(args.steps, 20)))
     # parity guard on the measured data: status all zero, and the merged
     # embeddings of the timed passes equal a plain serial pass (K1, then the
     # merge without early start or discard) of the same requests
@@ -574,6 +597,21 @@ def run_single(args):
             "merge_tail_after_k1_ms": round(main_tail_ms, 4),
             "merge_stream_priority": "high"}
 
+    if place_ms:
+        place_bytes = merge_bytes + 4 * lay.total_rows  # SURVEY.md 8d merge bytes incl. the scan
+        place_gbs = place_bytes / (place_ms * 1e-3) / 1e9
+        kernels["direct_placement"] = {
+            "kernel": "fsx_forward_place: merge_scan_kernel + " + merge_kernel_name() +
+                      " reading the producer's buffers (copy-only; the scan pipelined "
+                      "one pass ahead on a side stream)",
+            "what": "the forward fused with the merge: producer rows straight into the consumer's "
+                    "placeholder rows, no slab segment (the payload crosses HBM once)",
+            "ms_per_step": round(place_ms, 4),
+            "payload_gbs": round(payload / (place_ms * 1e-3) / 1e9, 1),
+            "merged_req_per_s": round(len(reqs) / (place_ms * 1e-3), 1),
+            "launches_per_step": place_launches / max(5, min(args.steps, 20)),
+            "algorithmic_bytes_per_step": place_bytes,
+            "achieved_gbs": round(place_gbs, 1), "frac": round(place_gbs / peak, 4)}
     value = payload / (ms_step * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,

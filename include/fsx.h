@@ -286,6 +286,26 @@ typedef struct fsx_merge_batch {
 } fsx_merge_batch;
 int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream);
 
+/* Direct placement: the forward fused with the merge.  Where the reference
+ * copies a payload into the consumer's arena (sidecar.hpp:465-483) and the
+ * consumer then copies it out (:543-544) -- and here K1 pushes it into a slab
+ * that K3 then reads -- the producer writes every item row straight into the
+ * consumer's placeholder rows: one K3b launch on src_gpu's device with
+ *   d_item_src                      producer buffers (src_gpu memory),
+ *   d_embeds, d_scratch, d_status   consumer arrays (dst_gpu memory: the same
+ *                                   device, a peer, or IPC-opened),
+ * so the payload crosses HBM / NVLink once and no slab segment is held.
+ * mode: FSX_MERGE_COPY_ONLY uses the positions and statuses the consumer's scan
+ * (fsx_merge FSX_MERGE_SCAN_ONLY on dst_gpu, ordered before this call) left in
+ * d_scratch / d_status; FSX_MERGE_FULL scans first.  Rows of requests whose
+ * status is not 0 are left untouched, as in fsx_merge.  No early-start or
+ * discard bits (FSX_E_VALIDATION).  done_flag >= 0: after the rows have landed,
+ * dst_gpu's flag done_flag is set to token (release, system scope), for a
+ * consumer in another process (fsx_wait / fsx_stream_wait_flags).
+ * Counts as one forward of total_item_rows * row_bytes bytes and one merge. */
+int fsx_forward_place(fsx_fabric* f, int src_gpu, int dst_gpu, const fsx_merge_batch* b,
+                      int64_t done_flag, uint64_t token, void* stream);
+
 /* ---- streaming channels (config C) ------------------------------------------
  * The small-message streams of the reference: thinker hidden states, one
  * [hidden_dim] row per decoded token and request (executor_sim.hpp:556-562),

@@ -13,6 +13,8 @@
 //              prompt row (fsx_merge), stream-ordered after forward() or with
 //              early start on the chunk flags;
 //   release()  the segments go back to the slab (the ack, sidecar.hpp:287-290).
+// run_place() is the slab-free alternative: the forward fused with the merge
+// (fsx_forward_place), the producer's rows straight into the prompt rows.
 // The batch's device arrays (prompt embedding, token ids, offsets, item
 // views, scratch, status) are allocated once; a pass costs a handful of C-ABI
 // calls and one small descriptor upload when segment offsets change.
@@ -216,6 +218,24 @@ class DataPlanePass {
     return true;
   }
 
+  // Direct placement (fsx_forward_place): the forward fused with the merge.
+  // The producer writes every item row from its own buffer straight into the
+  // consumer's placeholder rows (scan + row copy, one fsx call, stream order);
+  // no slab segment is held and the payload crosses memory once.  Always
+  // succeeds (nothing to allocate).
+  bool run_place(cudaStream_t st) {
+    if (!place_src_) {
+      std::vector<const void*> src(items_.size());
+      for (size_t i = 0; i < items_.size(); ++i) src[i] = items_[i].d_src;
+      cuda(cudaSetDevice(dev_));
+      place_src_ = upload(src);
+    }
+    fsx_merge_batch mb = b_;
+    mb.d_item_src = place_src_;
+    check(fsx_forward_place(f_, src_, dst_, &mb, -1, 0, st));
+    return true;
+  }
+
   // CUDA-graph form of the stream-ordered pass for launch-bound batches:
   // capture() records forward + merge once (segment offsets, flag ranges and
   // tokens are baked in: the same first-fit offsets come back every pass, and
@@ -293,6 +313,7 @@ class DataPlanePass {
   int64_t *req_row_off_ = nullptr, *req_item_off_ = nullptr, *item_row_off_ = nullptr;
   int32_t *scratch_ = nullptr, *status_ = nullptr;
   const void** item_src_ = nullptr;
+  const void** place_src_ = nullptr;  // producer buffers, for run_place
   fsx_merge_batch b_{};
   // colocated pass state
   static constexpr int kStages = 4;

@@ -159,6 +159,8 @@ _SIGS = {
     "fsx_signal_flags": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_int,
                          C.c_void_p],
     "fsx_merge": [C.c_void_p, C.c_int, C.POINTER(MergeBatch), C.c_void_p],
+    "fsx_forward_place": [C.c_void_p, C.c_int, C.c_int, C.POINTER(MergeBatch), C.c_int64,
+                          C.c_uint64, C.c_void_p],
     "fsx_channel_open": [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int32, C.POINTER(C.c_int32)],
     "fsx_channel_close": [C.c_void_p, C.c_int32],
     "fsx_channel_push": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],

@@ -1134,6 +1134,29 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
   return FSX_OK;
 }
 
+int fsx_forward_place(fsx_fabric* f, int src_gpu, int dst_gpu, const fsx_merge_batch* b,
+                      int64_t done_flag, uint64_t token, void* stream) {
+  NvtxRange nvtx_range("fsx.forward_place");
+  int src_dev = 0, dst_dev = 0;
+  int rc = find_gpu(f, src_gpu, &src_dev);
+  if (rc) return rc;
+  rc = find_gpu(f, dst_gpu, &dst_dev);
+  if (rc) return rc;
+  if (!b) return fail(FSX_E_VALIDATION, "bad merge batch");
+  const int base_mode = b->mode & FSX_MERGE_MODE_MASK;
+  if (base_mode == FSX_MERGE_SCAN_ONLY || (b->mode & ~FSX_MERGE_MODE_MASK) || b->d_item_flag)
+    return fail(FSX_E_VALIDATION,
+                "forward_place takes FSX_MERGE_FULL or FSX_MERGE_COPY_ONLY, no early-start or discard bits");
+  // the kernel runs on the producer's device; every consumer array must be
+  // addressable from it (same device, or peer access enabled by fsx_open)
+  rc = fsx_merge(f, src_gpu, b, stream);
+  if (rc) return rc;
+  f->forwards++;
+  f->bytes_forwarded += b->total_item_rows * b->row_bytes;
+  if (done_flag >= 0) return fsx_signal_flags(f, dst_gpu, done_flag, 1, token, src_gpu, stream);
+  return FSX_OK;
+}
+
 int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_t n,
                       void* stream) {
   int ordinal = 0;

@@ -270,6 +270,24 @@ class DataPlaneBatch:
                 b = cache[(mode, slot)] = self.merge_batch(False, mode, slot)
         self.fab.merge(self.dst_gpu, b, stream)
 
+    def place(self, stream=None, mode: int = N.MERGE_FULL, slot: int = 0) -> None:
+        """Direct placement instead of forward + merge (fsx_forward_place):
+        the producer writes each item's rows from its own buffer straight into
+        the consumer's placeholder rows -- no slab segment, no chunk flags, the
+        payload crosses memory once.  mode MERGE_COPY_ONLY uses the positions
+        of a scan(slot) ordered before it."""
+        cache = self.__dict__.setdefault("_place_cache", {})
+        b = cache.get((mode, slot))
+        if b is None:
+            if not hasattr(self, "item_src_direct"):
+                sb = self.src_buf.data_ptr()
+                self.item_src_direct = torch.from_numpy(self.src_off + sb).to(self.dst_dev) \
+                    if len(self.src_off) else torch.zeros(1, dtype=torch.int64, device=self.dst_dev)
+            b = self.merge_batch(False, mode, slot)
+            b.d_item_src = self.item_src_direct.data_ptr()
+            cache[(mode, slot)] = b
+        self.fab.forward_place(self.src_gpu, self.dst_gpu, b, stream=stream)
+
     def scan(self, stream=None, slot: int = 0) -> None:
         """Phase 1 of K3 only: needs just the token ids, so it can run while
         the payload is still being forwarded (or, pipelined, during the

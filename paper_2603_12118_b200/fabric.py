@@ -244,6 +244,13 @@ class DeviceFabric:
     def merge(self, gpu: int, batch: N.MergeBatch, stream=None) -> None:
         N.call("fsx_merge", self._h, gpu, C.byref(batch), _stream_ptr(stream))
 
+    def forward_place(self, src_gpu: int, dst_gpu: int, batch: N.MergeBatch, done_flag: int = -1,
+                      token: int = 0, stream=None) -> None:
+        """Direct placement (fsx_forward_place): producer rows straight into
+        the consumer's placeholder rows, one launch on src_gpu's device."""
+        N.call("fsx_forward_place", self._h, src_gpu, dst_gpu, C.byref(batch), done_flag, token,
+               _stream_ptr(stream))
+
     def synth(self, gpu: int, seed: int, dst_ptr: int, nbytes: int, stream=None) -> None:
         N.call("fsx_synth_payload", self._h, gpu, seed, dst_ptr, nbytes, _stream_ptr(stream))
 

@@ -2,7 +2,8 @@
 // config B (4 Qwen2.5-VL videos, 16 x 1024 x 3584 bf16 each, 7 MiB flagged
 // chunks) and an A-like batch (64 requests x one 256 x 4096 bf16 image),
 // intra-device forward + merge per pass, stream-ordered or as the colocated
-// pass (K1 || early-start merge, DataPlanePass::run_colocated).  Prints one JSON line
+// pass (K1 || early-start merge, DataPlanePass::run_colocated), or direct
+// placement (DataPlanePass::run_place: no slab).  Prints one JSON line
 // per batch: device time per pass, host time per pass, payload GB/s; then
 // checks the merged prompt embeddings byte for byte against the oracle
 // restatement (test infrastructure: inputs built and checked with
@@ -39,6 +40,7 @@ struct Case {
   int64_t item_rows, input_tokens, row_bytes, chunk_rows;
   bool colocated;  // K1 || early-start merge (DataPlanePass::run_colocated)
   bool graph = false;  // stream-ordered pass replayed as a CUDA graph (run_graph)
+  bool place = false;  // direct placement, no slab (run_place)
 };
 
 int run_case(fsx_fabric* f, const Case& c, int passes) {
@@ -70,6 +72,7 @@ int run_case(fsx_fabric* f, const Case& c, int passes) {
   if (c.graph) pass.capture(st);
   auto one = [&]() -> bool {
     if (c.graph) return pass.run_graph(st);
+    if (c.place) return pass.run_place(st);
     return c.colocated ? pass.run_colocated(st, mst) : pass.run(st);
   };
   // prompt rows pre-filled like the Python batch (synth_payload(fnv1a64(id + "/text")))
@@ -161,6 +164,10 @@ int main(int argc, char** argv) {
                  passes);
   rc |= run_case(f, Case{"B, stream-ordered pass as a CUDA graph", 4, 16384, 1800, 7168, 1024, false, true},
                  passes);
+  rc |= run_case(f, Case{"B, direct placement (forward fused with the merge, no slab)", 4, 16384, 1800, 7168,
+                          1024, false, false, true},
+                 passes);
+  rc |= run_case(f, Case{"A-like, direct placement", 64, 256, 500, 8192, 0, false, false, true}, passes);
   fsx_close(f);
   return rc;
 }

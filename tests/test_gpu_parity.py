@@ -321,6 +321,64 @@ def test_merge_edge_cases(fab, oracle_mod):
     b2.release()
 
 
+@pytest.mark.parametrize("config,count,scan_first", [("A", 64, False), ("A", 7, True), ("D", 24, False),
+                                                     ("B", 4, True)])
+def test_forward_place_bit_exact(fab, oracle_mod, config, count, scan_first):
+    """Direct placement (fsx_forward_place): producer rows straight into the
+    consumer's placeholder rows == the oracle merge; no slab segment held."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests(config, count)
+    b = DataPlaneBatch(fab, reqs, T.RULES[config], 0, 1)
+    b.synth_inputs()
+    s0 = fab.stats()
+    if scan_first:  # the consumer's scan, then the producer's copy-only placement
+        b.scan()
+        b.place(mode=N.MERGE_COPY_ONLY)
+    else:
+        b.place()
+    torch.cuda.synchronize()
+    want, st = _expected(oracle_mod, b)
+    assert (b.status_host() == 0).all() and (st == 0).all()
+    assert np.array_equal(b.embeds_host(), want)
+    s1 = fab.stats()
+    assert s1["forwards"] == s0["forwards"] + 1
+    assert s1["bytes_forwarded"] - s0["bytes_forwarded"] == b.lay.total_item_rows * b.rb
+    assert fab.slab_usage(1)["segments_in_use"] == 0
+
+
+def test_forward_place_validation_and_flag(fab, oracle_mod):
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests("A", 10)
+    bad = next(r for r, q in enumerate(reqs) if q.items)
+    b = DataPlaneBatch(fab, reqs, T.RULES["A"], 0, 1)
+    t0, t1 = int(b.lay.req_row_off[bad]), int(b.lay.req_row_off[bad + 1])
+    idx = t0 + int(np.where(b.tok_host[t0:t1] == T.PLACEHOLDER_ID)[0][0])
+    b.tok_host = b.tok_host.copy()
+    b.tok_host[idx] = 7
+    b.tok[idx] = 7
+    b.synth_inputs()
+    flag = fab.flags_alloc(1, 1)
+    mb = b.merge_batch(False, N.MERGE_FULL)
+    sb = b.src_buf.data_ptr()
+    b.item_src.copy_(torch.from_numpy(b.src_off + sb))
+    fab.forward_place(0, 1, mb, done_flag=flag, token=0x5eed)
+    fab.wait(1, flag, 1, 0x5eed, timeout_us=10_000_000)
+    torch.cuda.synchronize()
+    want, st = _expected(oracle_mod, b)
+    got_st = b.status_host()
+    assert got_st[bad] == N.E_VALIDATION and st[bad] == 1
+    assert np.array_equal(b.embeds_host(), want)
+    # early-start / discard / scan-only are not placement modes
+    for mode in (N.MERGE_SCAN_ONLY, N.MERGE_FULL | N.MERGE_DISCARD):
+        mb2 = b.merge_batch(False, mode)
+        with pytest.raises(N.FsxError):
+            fab.forward_place(0, 1, mb2)
+
+
 def test_stats_and_launch_count(fab):
     s = fab.stats()
     assert s["forwards"] > 0 and s["merges"] > 0 and s["kernel_launches"] > 0
