@@ -462,6 +462,14 @@ def run_single(args):
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
+        if os.environ.get("FSX_BENCH_COLD_READ") == "1":
+            # diagnostic only: the merge follows K1's chunk flags but reads an
+            # identical copy of the payload that K1 never touches, so none of
+            # its reads can hit lines K1 just wrote (is the colocated gain L2
+            # reuse or overlap?)
+            shadow = batch.src_buf.clone()
+            batch.item_src.copy_(torch.from_numpy(batch.src_off + shadow.data_ptr()))
+            torch.cuda.synchronize()
         if not args.serial and not args.profile:
             # schedule choice: a short probe of both full passes; the timed run
             # uses the faster (the colocated pass normally; stream order if the
