@@ -591,8 +591,13 @@ def run_single(args):
                     "achieved": round(pass_gbs, 1), "peak": peak,
                     "peak_kind": f"{peak_kind} hbm_gbs (copy)", "unit": "GB/s",
                     "frac": round(pass_gbs / peak, 4), "traffic": None,
-                    "traffic_note": "the two kernels overlap; ncu serialises them, so no DRAM "
-                                    "count of the pass exists (per-kernel ncu traffic: kernels.*)",
+                    "traffic_note": "the two kernels overlap; ncu kernel replay serialises them and "
+                                    "under range replay the profiled merge lags K1 by ~0.95 ms, so no "
+                                    "DRAM count of the timed pass exists (per-kernel ncu traffic: "
+                                    "kernels.*; profiles/range_replay_r01i.md).  L2 reuse is shown "
+                                    "by a control instead: the merge reading a cold copy of the "
+                                    "payload (FSX_BENCH_COLD_READ=1) makes the pass ~0.06 ms slower "
+                                    "(profiles/l2_reuse_hot_cold_r01i.jsonl)",
                     "algorithmic_bytes_per_launch": alg,
                     "dram_floor_gbs": round(floor_gbs, 1),
                     "dram_floor_frac": round(floor_gbs / peak, 4),
