@@ -802,6 +802,28 @@ def run_pairs(args, rank, world):
     chunk_rows = CHUNK_ROWS or max(1, max((it.rows for it in lay.items), default=1))
     chunks = [max(1, -(-it.rows // chunk_rows)) for it in lay.items]
     M = len(lay.items)
+    # Direct placement over NVLink (FSX_PAIRS_DIRECT=1): the producer writes
+    # each row straight into the consumer's prompt embedding and status
+    # (CUDA IPC mappings of the consumer's tensors) with fsx_forward_place --
+    # the forward and the merge as ONE kernel over peer memory -- and sets a
+    # done flag in the consumer's ring; no slab segment, no consumer merge.
+    direct = (not me.alone) and os.environ.get("FSX_PAIRS_DIRECT") == "1"
+    place_mb = []
+    if direct:
+        from torch.multiprocessing.reductions import reduce_tensor
+        shared = PR.exchange([(reduce_tensor(b.embeds), reduce_tensor(b.status)) for b in batches]
+                             if consumer else None)
+        if me.producer:
+            remote = []  # keep the mapped tensors alive for the run
+            src_ptrs = torch.from_numpy(batch.src_off + batch.src_buf.data_ptr()).to(stream.device)
+            for (fe, ae), (fs, as_) in shared[me.peer]:
+                emb, st = fe(*ae), fs(*as_)
+                remote.append((emb, st))
+                mb = batch.merge_batch(False, N.MERGE_FULL)
+                mb.d_embeds = emb.data_ptr()
+                mb.d_status = st.data_ptr()
+                mb.d_item_src = src_ptrs.data_ptr()
+                place_mb.append(mb)
     xfers = (N.Transfer * max(M, 1))()
     view = np.frombuffer(xfers, dtype=N.TRANSFER_DTYPE, count=max(M, 1))[:M]
     for i, it in enumerate(lay.items):
@@ -815,6 +837,16 @@ def run_pairs(args, rank, world):
             return
         k = s % sets
         sched = PR.schedule(s, chunks)
+        if direct:
+            done, tok = sched[0]  # this step's first flag slot carries the done token
+            if me.producer:
+                if s >= sets:
+                    fab.stream_wait_flags(P, k, 1, PR.ack_token(s - sets), stream)
+                fab.forward_place(P, Cg, place_mb[k], done_flag=done, token=tok, stream=stream)
+            else:
+                fab.stream_wait_flags(Cg, done, 1, tok, stream)
+                fab.signal_flags(P, k, 1, PR.ack_token(s), Cg, stream)
+            return
         if me.producer:
             if s >= sets:  # the consumer acked step s-sets: segment set k is free again
                 fab.stream_wait_flags(P, k, 1, PR.ack_token(s - sets), stream)
@@ -891,6 +923,10 @@ def run_pairs(args, rank, world):
                        "requests_per_step_per_pair": len(reqs), "pairs": n_pairs,
                        "chunk_bytes": chunk_rows * rules.row_bytes,
                        "slab_segment_sets": sets,
+                       "transfer": ("direct placement: fsx_forward_place, producer rows straight "
+                                    "into the consumer's prompt rows over NVLink (one kernel), "
+                                    "done flag; no slab, no consumer merge") if direct else
+                                   "K1 into the consumer slab + early-start merge",
                        "parallelism": f"{n_pairs} independent producer->consumer pairs"},
             "roofline": {"bound": "nvlink", "achieved": round(pair_gbs, 1), "peak": 770.0,
                          "unit": "GB/s", "frac": round(pair_gbs / 770.0, 4), "traffic": None,

@@ -23,9 +23,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("config,requests", [("B", 1), ("A", 16)])
-def test_pairs_protocol_same_device(gpu, config, requests):
+@pytest.mark.parametrize("config,requests,direct", [("B", 1, False), ("A", 16, False),
+                                                    ("B", 2, True), ("A", 16, True)])
+def test_pairs_protocol_same_device(gpu, config, requests, direct):
+    """direct: FSX_PAIRS_DIRECT=1, the producer places rows straight into the
+    consumer's IPC-mapped prompt embedding (fsx_forward_place) + done flag."""
     env = dict(os.environ, FSX_PAIRS_DEVICE="0")
+    if direct:
+        env["FSX_PAIRS_DIRECT"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", "bench.py", "--gpus", "2",
            "--steps", "4", "--warmup", "2", "--config", config, "--requests", str(requests),
@@ -38,6 +43,7 @@ def test_pairs_protocol_same_device(gpu, config, requests):
     assert d["n_gpus"] == 2 and d["verified"] and d["pinned_device"] == "0"
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert ("direct placement" in d["config"]["transfer"]) == direct
 
 
 def test_fanout_config_d_four_ranks_same_device(gpu):
