@@ -379,6 +379,30 @@ def test_forward_place_validation_and_flag(fab, oracle_mod):
             fab.forward_place(0, 1, mb2)
 
 
+def test_forward_place_edge_cases(fab, oracle_mod):
+    """Direct placement on the merge edge cases: placeholder-only, text-only
+    and multi-item requests, and a row width that is not a multiple of 16
+    bytes (byte path)."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    rules = T.ShapeRules(hidden_dim=8, pixels_per_token=1, default_image_width=1,
+                         default_image_height=3, tokens_per_audio_second=1, default_audio_seconds=1)
+    reqs = [T.make_request(0, 0, ["image"], rules), T.make_request(1, 4, [], rules),
+            T.make_request(2, 1, ["image", "audio", "image"], rules),
+            T.make_request(3, 37, ["audio"], rules)]
+    rules2 = T.ShapeRules(hidden_dim=5, pixels_per_token=4096 * 4096)
+    reqs2 = [T.make_request(i, 3 + i, ["image"] * (i % 3), rules2) for i in range(6)]
+    for rq, ru in ((reqs, rules), (reqs2, rules2)):
+        b = DataPlaneBatch(fab, rq, ru, 0, 1)
+        b.synth_inputs()
+        b.place()
+        torch.cuda.synchronize()
+        want, st = _expected(oracle_mod, b)
+        assert (b.status_host() == 0).all()
+        assert np.array_equal(b.embeds_host(), want)
+
+
 def test_stats_and_launch_count(fab):
     s = fab.stats()
     assert s["forwards"] > 0 and s["merges"] > 0 and s["kernel_launches"] > 0
