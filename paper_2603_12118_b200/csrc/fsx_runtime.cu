@@ -227,6 +227,7 @@ struct fsx_fabric {
   struct MailBatch {
     cudaEvent_t ev = nullptr;
     int refs = 0;
+    bool done = false;  // ev seen complete (later waits skip the synchronize)
   };
   std::vector<MailBatch> batches;
   std::vector<int64_t> free_batches;
@@ -910,6 +911,7 @@ int flush_staged(fsx_fabric* f, int device) {
     f->launches++;
   }
   FSX_CUDA(cudaEventRecord(mb.ev, dev->stream));
+  mb.done = false;
   mb.refs = (int)q.size();
   for (int64_t t : q) f->tickets[t].batch = bid;
   q.clear();
@@ -978,10 +980,15 @@ int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_
       int rc = flush_staged(f, f->tickets[ticket].device);  // everything staged on that device
       if (rc) return rc;
     }
-    ev = f->batches[f->tickets[ticket].batch].ev;
+    auto& bt = f->batches[f->tickets[ticket].batch];
+    ev = bt.done ? nullptr : bt.ev;  // a batch seen complete is not synchronised again
     slot = f->tickets[ticket].slot;
   }
-  FSX_CUDA(cudaEventSynchronize(ev));
+  if (ev) {
+    FSX_CUDA(cudaEventSynchronize(ev));
+    std::lock_guard<std::mutex> lk(f->mu);
+    f->batches[f->tickets[ticket].batch].done = true;
+  }
   const fsx::MailHeader* h = reinterpret_cast<const fsx::MailHeader*>(f->mail + slot);
   if (h_bytes) *h_bytes = f->mail + slot + fsx::kMailHeader;
   if (digest) *digest = *reinterpret_cast<const volatile uint64_t*>(&h->digest);

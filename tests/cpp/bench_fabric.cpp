@@ -84,20 +84,28 @@ int main(int argc, char** argv) {
     for (int r = 0; r < batch; ++r)
       f.register_interest(1, "req-" + std::to_string(r) + "/r0001",
                           [&](const ForwardEnvelope&, std::vector<uint8_t> b) { got += (int64_t)b.size(); });
+    double send_s = 0, deliver_s = 0;  // host time split: the sends, then the deliveries
     auto step = [&](int s) {
+      const auto a = std::chrono::steady_clock::now();
       for (int r = 0; r < batch; ++r)
         f.send("req-" + std::to_string(r), DataRef{"req-" + std::to_string(r) + "/r0001", 0, true}, 0, 1,
                std::span<const uint8_t>(rowbuf.data(), row), s, false);
+      const auto b = std::chrono::steady_clock::now();
       k.run_until_idle();
+      send_s += std::chrono::duration<double>(b - a).count();
+      deliver_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - b).count();
     };
     for (int s = 0; s < 10; ++s) step(s);
     got = 0;
+    send_s = deliver_s = 0;
     const auto t0 = std::chrono::steady_clock::now();
     for (int s = 10; s < 10 + steps; ++s) step(s);
     const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::printf("{\"mode\": \"stream_host_span_chunk_callback\", \"rows_per_step\": %d, \"row_bytes\": %d, "
-                "\"us_per_step\": %.1f, \"msgs_per_s\": %.0f, \"bytes_ok\": %s}\n",
-                batch, row, sec / steps * 1e6, batch * steps / sec,
+                "\"us_per_step\": %.1f, \"send_us_per_step\": %.1f, \"deliver_us_per_step\": %.1f, "
+                "\"msgs_per_s\": %.0f, \"bytes_ok\": %s}\n",
+                batch, row, sec / steps * 1e6, send_s / steps * 1e6, deliver_s / steps * 1e6,
+                batch * steps / sec,
                 got == (int64_t)batch * steps * row ? "true" : "false");
   }
   return 0;
