@@ -31,7 +31,12 @@ int main(int argc, char** argv) {
   std::vector<uint8_t> host(n);
   or_synth_payload_into(or_payload_seed("req-000000/r0000", 16, 0), host.data(), n);
   cudaMemcpy(d, host.data(), n, cudaMemcpyHostToDevice);
-  for (int mode = 0; mode < 2; ++mode) {
+  // modes: 0 device payload -> raw interest (zero copy), 1 device payload ->
+  // ChunkCallback (owned vector), 2 HOST span (the reference executors' own
+  // send of a std::vector, pageable) -> raw interest, 3 host span -> ChunkCallback
+  static const char* kModes[] = {"raw_zero_copy", "chunk_callback_owned_vector", "host_span_raw",
+                                 "host_span_chunk_callback"};
+  for (int mode = 0; mode < 4; ++mode) {
     EventLoop k;
     SidecarConfig cfg;
     cfg.arena_bytes = 2 * n + 4096;
@@ -40,7 +45,7 @@ int main(int argc, char** argv) {
     int64_t delivered = 0;
     auto one = [&](int i) {
       const std::string id = "req-" + std::to_string(i) + "/r0000";
-      if (mode == 0) {
+      if (mode % 2 == 0) {
         f.register_interest_raw(1, id, [&](const ForwardEnvelope& env, int64_t off) {
           delivered += env.chunk_bytes;
           f.ack_raw(1, off);
@@ -52,7 +57,7 @@ int main(int argc, char** argv) {
       }
       k.post("send", [&, id] {
         f.send_payload("req", DataRef{id, n, false}, 0, 1,
-                       std::span<const uint8_t>(static_cast<const uint8_t*>(d), n));
+                       std::span<const uint8_t>(mode < 2 ? static_cast<const uint8_t*>(d) : host.data(), n));
       });
       k.run_until_idle();
     };
@@ -63,7 +68,7 @@ int main(int argc, char** argv) {
     const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::printf("{\"mode\": \"%s\", \"items\": %d, \"bytes\": %lld, \"gbs\": %.2f, \"ms_per_item\": %.3f,"
                 " \"integrity_errors\": %lld}\n",
-                mode == 0 ? "raw_zero_copy" : "chunk_callback_owned_vector", items,
+                kModes[mode], items,
                 (long long)delivered, delivered / s / 1e9, s / items * 1e3,
                 (long long)f.stats().integrity_errors);
   }
