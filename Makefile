@@ -132,13 +132,17 @@ build/test_envelope_codec: tests/cpp/test_envelope_codec.cpp tests/cpp/shim_main
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ tests/cpp/test_envelope_codec.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 
+# Host dg64 (fabric.hpp digest64 / digest64_par) vs the oracle restatement.  CPU only.
+build/test_host_digest: tests/cpp/test_host_digest.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o | build
+	$(CXXTEST) -Ioracle -o $@ tests/cpp/test_host_digest.cpp build/fsx_oracle_test.o -lpthread
+
 build/bench_pass: tests/cpp/bench_pass.cpp include/fsx/dataplane.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_pass.cpp build/fsx_oracle_test.o $(LINKFSX)
 
 build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
 
-cpptests: build/test_fabric build/bench_fabric build/bench_pass
+cpptests: build/test_fabric build/bench_fabric build/bench_pass build/test_host_digest
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \
