@@ -314,7 +314,7 @@ def run_single(args):
     torch.cuda.synchronize()
     payload = lay.payload_bytes
     n_items = len(lay.items)
-    fwd_launches = (n_items + 15) // 16  # fsx_forward_batch: 16 transfers per K1 launch
+    fwd_launches = -(-n_items // N.FWD_MAX_BATCH)  # fsx_forward_batch: transfers per K1 launch
     # merge_copy_kernel: read slab rows + write placeholder rows + read positions
     # (2*sum(n)*D*2; the sum(T)*4 token read is the scan, which
     # runs on a side stream under K1)
@@ -427,7 +427,7 @@ def run_single(args):
         streams involved); returns (ms per pass, per-pass events, launches)."""
         ev.clear()
         host_s.clear()
-        launches0 = fab.stats()["kernel_launches"]
+        launches0 = fab.stats()["kernel_launches"] + graph_launched[0]
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -447,7 +447,8 @@ def run_single(args):
         stream.wait_event(merged[(counter[0] - 1) % 2])
         end.record(stream)
         torch.cuda.synchronize()
-        return start.elapsed_time(end) / nsteps, list(ev), fab.stats()["kernel_launches"] - launches0
+        return (start.elapsed_time(end) / nsteps, list(ev),
+                fab.stats()["kernel_launches"] + graph_launched[0] - launches0)
 
     # The colocated pipeline pays off once a pass is long enough to hide its
     # extra host work (early-start descriptors, two streams): config B / D
@@ -455,6 +456,28 @@ def run_single(args):
     # faster stream-ordered.
     if not args.serial and payload < (128 << 20):
         args.serial = True
+    # launch-bound small passes (config A) are replayed as a CUDA graph of the
+    # stream-ordered pass when that is faster (probed like the colocated pass)
+    graph_pass = (args.serial and payload < (128 << 20) and not args.profile and
+                  os.environ.get("FSX_BENCH_GRAPH", "1") == "1")
+
+    graph_launched = [0]
+
+    def step_graph(record=False):
+        t_host = time.perf_counter()
+        assert batch.alloc()
+        e0, e1, e2 = timing_events(record)
+        if record:
+            e0.record(stream)
+        batch.run_graph(stream)       # K1 (bulk-copy tiles) + scan + merge, one graph launch
+        graph_launched[0] += batch.graph_kernels  # our kernels in the replay
+        if record:
+            e1.record(stream)
+            e2.record(stream)
+            ev.append((e0, e1, e2))
+        batch.release()
+        host_s.append(time.perf_counter() - t_host)
+
     step = step_serial if args.serial else step_pipelined
     probe = None
     with torch.cuda.stream(stream):
@@ -469,6 +492,21 @@ def run_single(args):
             # reuse or overlap?)
             shadow = batch.src_buf.clone()
             batch.item_src.copy_(torch.from_numpy(batch.src_off + shadow.data_ptr()))
+            torch.cuda.synchronize()
+        if graph_pass:
+            assert batch.alloc()
+            batch.capture(stream, bulk=True, l2_keep=L2_KEEP)
+            batch.release()
+            for _ in range(3):
+                step_graph()
+            g_ms, _, _ = timed(step_graph, 10)
+            s_ms, _, _ = timed(step_serial, 10)
+            probe = {"graph_ms": round(g_ms, 4), "serial_ms": round(s_ms, 4)}
+            graph_pass = g_ms < s_ms
+            if graph_pass:
+                step = step_graph
+            for _ in range(3):
+                step()
             torch.cuda.synchronize()
         if not args.serial and not args.profile:
             # schedule choice: a short probe of both full passes; the timed run
@@ -493,7 +531,7 @@ def run_single(args):
         # the same two kernels measured one after the other (K1 with the
         # bulk-copy engine, then the merge): per-kernel rooflines
         iso_steps = 0 if args.profile and not args.serial else max(5, min(args.steps, 20))
-        if args.serial:
+        if args.serial and not graph_pass:
             ev_iso = ev_main  # not re-recorded: no second timed phase
         elif iso_steps:
             for _ in range(3):
@@ -550,7 +588,7 @@ def run_single(args):
         fwd_gbs = fwd_bytes / (fwd_ms * 1e-3) / 1e9
         mrg_gbs = merge_bytes / (mrg_ms * 1e-3) / 1e9
         kernels = {
-            "measured": ("the timed passes (--serial)" if args.serial else
+            "measured": ("the timed passes (--serial)" if args.serial and not graph_pass else
                          f"{iso_steps} extra passes in the same run with K1 then the merge in "
                          "stream order, each event-timed on its stream"),
             "forward": {"kernel": "fsx::forward_tma_kernel (bulk-copy tiles, FSX_FWD_BULK; "
@@ -641,8 +679,9 @@ def run_single(args):
                    "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush needed)"},
         "roofline": roofline,
         "kernels": kernels,
-        "pass_schedule": {"used": "stream-ordered (K1 then merge)" if args.serial else
-                          "colocated (K1 || early-start merge)", "probe": probe},
+        "pass_schedule": {"used": ("stream-ordered (K1 then merge) as one CUDA graph launch per pass"
+                                   if graph_pass else "stream-ordered (K1 then merge)") if args.serial
+                          else "colocated (K1 || early-start merge)", "probe": probe},
         "nvlink": {"applies": False, "why": "N=1: producer and consumer share one B200"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,

@@ -172,7 +172,10 @@ int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, i
 /* Several transfers of one source device in one K1 launch (ExecutorBase::
  * emit_output fans one output out to every dest gpu, executor_sim.hpp:223-226;
  * an encoder batch emits several items at once, :321-336).  token is in/out
- * per transfer as above.  All t[i].src_gpu must be bound to the same device. */
+ * per transfer as above.  All t[i].src_gpu must be bound to the same device.
+ * Up to FSX_FWD_MAX_BATCH transfers go in one launch (kernel parameter
+ * space); more take ceil(n / FSX_FWD_MAX_BATCH) launches. */
+#define FSX_FWD_MAX_BATCH 64
 typedef struct fsx_transfer {
   int32_t src_gpu;
   int32_t dst_gpu;

@@ -38,6 +38,7 @@ FWD_HOST_NOTIFY = 1
 FWD_L2_KEEP = 2
 FWD_BULK = 4
 FWD_SHARE_SM = 8
+FWD_MAX_BATCH = 64  # FSX_FWD_MAX_BATCH: transfers per K1 launch
 
 MERGE_FULL = 0
 MERGE_SCAN_ONLY = 1

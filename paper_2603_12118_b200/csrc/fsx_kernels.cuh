@@ -30,8 +30,10 @@ struct FwdArgs {
 };
 
 // Up to kFwdMaxBatch transfers of one source device in one K1 launch (kernel
-// parameter space, ~2 KB): units are laid out transfer-major, chunk-major.
-constexpr int kFwdMaxBatch = 16;
+// parameter space: ~8.5 KB of the 32 KB sm_100 allows, so a 64-image batch is
+// one launch instead of four back-to-back launches with four tails): units
+// are laid out transfer-major, chunk-major.
+constexpr int kFwdMaxBatch = FSX_FWD_MAX_BATCH;
 struct FwdBatch {
   int32_t n;
   int32_t l2_keep_dst;  // slab stores with L2 evict_last (consumer merges next)

@@ -135,7 +135,7 @@ class DataPlaneBatch:
     def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False,
                 bulk: bool = False, share_sm: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
-        one K1 launch per 16 items); returns the launches.  host_notify=False
+        one K1 launch per N.FWD_MAX_BATCH items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
         chunk flags."""
         assert self.slab_off is not None, "alloc() first"
@@ -152,7 +152,7 @@ class DataPlaneBatch:
             (N.FWD_BULK if bulk else 0) | (N.FWD_SHARE_SM if share_sm else 0)
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
-        return (M + 15) // 16
+        return -(-M // N.FWD_MAX_BATCH)
 
     def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
         """The host-span send path (sidecar.hpp:302): payload bytes from host
@@ -287,6 +287,33 @@ class DataPlaneBatch:
             b.d_item_src = self.item_src_direct.data_ptr()
             cache[(mode, slot)] = b
         self.fab.forward_place(self.src_gpu, self.dst_gpu, b, stream=stream)
+
+    # -- CUDA-graph form of the stream-ordered pass -----------------------------
+    def capture(self, stream, bulk: bool = True, l2_keep: bool = False) -> None:
+        """Record forward + merge (FULL) once as a CUDA graph for the current
+        slab offsets; run_graph() replays it.  For launch-bound batches (config
+        A): segment offsets, flag ranges and tokens are baked in -- first fit
+        returns the same offsets pass after pass and nothing in stream order
+        waits on the flags."""
+        assert self.slab_off is not None, "alloc() first"
+        g = torch.cuda.CUDAGraph()
+        l0 = self.fab.stats()["kernel_launches"]
+        with torch.cuda.graph(g, stream=stream):
+            self.forward(stream, host_notify=False, l2_keep=l2_keep, bulk=bulk)
+            self.merge(stream)
+        self.graph_kernels = self.fab.stats()["kernel_launches"] - l0  # fsx kernels per replay
+        self._graph = g
+        self._graph_key = (self.slab_off.tobytes(), bulk, l2_keep)
+
+    def run_graph(self, stream) -> None:
+        """Replay the captured pass (alloc() first; re-captured if the slab
+        handed back different offsets)."""
+        assert self.slab_off is not None, "alloc() first"
+        key = (self.slab_off.tobytes(),) + self._graph_key[1:]
+        if key != self._graph_key:
+            self.capture(stream, *self._graph_key[1:])
+        with torch.cuda.stream(stream):
+            self._graph.replay()
 
     def scan(self, stream=None, slot: int = 0) -> None:
         """Phase 1 of K3 only: needs just the token ids, so it can run while

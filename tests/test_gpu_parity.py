@@ -120,12 +120,13 @@ def test_forward_rejects_bad_chunk_and_overrun(fab):
 
 
 def test_forward_batch_mixed(fab, oracle_mod):
-    """One K1 launch over transfers of different sizes, chunkings, alignments
-    and destination slabs (and more than 16, so two launches)."""
+    """K1 launches over transfers of different sizes, chunkings, alignments
+    and destination slabs (more than FSX_FWD_MAX_BATCH, so two launches)."""
     torch = _torch()
     specs = [(n, ch, sh, dst) for n, ch, sh, dst in
              [(0, 0, 0, 1), (1, 0, 0, 2), (4099, 0, 3, 1), (1 << 20, 65536, 0, 2),
-              (7_340_032 * 2 + 32, 7_340_032, 0, 1), (65536 * 3, 4096, 0, 2)] * 3]
+              (7_340_032 * 2 + 32, 7_340_032, 0, 1), (65536 * 3, 4096, 0, 2)] * 12]
+    assert len(specs) > N.FWD_MAX_BATCH
     srcs, xfers, offs = [], [], []
     for k, (n, ch, sh, dst) in enumerate(specs):
         buf = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
@@ -377,6 +378,38 @@ def test_forward_place_validation_and_flag(fab, oracle_mod):
         mb2 = b.merge_batch(False, mode)
         with pytest.raises(N.FsxError):
             fab.forward_place(0, 1, mb2)
+
+
+def test_pass_graph_replay_bit_exact(fab, oracle_mod):
+    """The stream-ordered pass captured once as a CUDA graph (DataPlaneBatch
+    capture / run_graph, bench.py's config-A schedule) and replayed: merged
+    rows == the oracle; a moved slab offset triggers a re-capture."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests("A", 24)
+    b = DataPlaneBatch(fab, reqs, T.RULES["A"], 0, 1)
+    b.synth_inputs()
+    s = torch.cuda.Stream()
+    assert b.alloc()
+    b.capture(s)
+    assert b.graph_kernels >= 3  # K1 + scan + merge
+    for _ in range(3):
+        b.run_graph(s)
+    b.release()
+    hold = fab.slab_alloc(1, 4096)  # the next alloc lands elsewhere: re-capture
+    assert b.alloc()
+    b.run_graph(s)
+    s.synchronize()
+    want, _ = _expected(oracle_mod, b)
+    assert (b.status_host() == 0).all()
+    assert np.array_equal(b.embeds_host(), want)
+    for i in range(min(2, len(b.lay.items))):
+        it = b.lay.items[i]
+        assert b.slab_item_host(i).tobytes() == oracle_mod.synth_payload(T.payload_seed(it.ref_id, 0),
+                                                                         it.rows * b.rb)
+    b.release()
+    fab.slab_free(1, hold)
 
 
 def test_forward_place_edge_cases(fab, oracle_mod):
