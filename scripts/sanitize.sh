@@ -5,7 +5,7 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-SEL='forward_single_shot and (0 or 1 or 7 or 256 or 4096) or forward_chunked_flags or unaligned or merge_edge_cases or validation or early_start or fused_digest or batch_mixed or small_put or colocated'
+SEL='forward_single_shot and (0 or 1 or 7 or 256 or 4096) or forward_chunked_flags or unaligned or merge_edge_cases or validation or early_start or fused_digest or batch_mixed or small_put or colocated or forward_place or graph_replay or host_span'
 for tool in memcheck racecheck synccheck; do
   timeout 1500 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 3 \
       python -m pytest tests/test_gpu_parity.py tests/test_gpu_stream.py -x -q -p no:cacheprovider \
