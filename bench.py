@@ -462,6 +462,7 @@ def run_single(args):
                   os.environ.get("FSX_BENCH_GRAPH", "1") == "1")
 
     graph_launched = [0]
+    graph_kind = "serial"
 
     def step_graph(record=False):
         t_host = time.perf_counter()
@@ -494,16 +495,30 @@ def run_single(args):
             batch.item_src.copy_(torch.from_numpy(batch.src_off + shadow.data_ptr()))
             torch.cuda.synchronize()
         if graph_pass:
-            assert batch.alloc()
-            batch.capture(stream, bulk=True, l2_keep=L2_KEEP)
-            batch.release()
-            for _ in range(3):
-                step_graph()
-            g_ms, _, _ = timed(step_graph, 10)
+            def capture(kind):
+                assert batch.alloc()
+                if kind == "colocated":
+                    batch.capture_colocated(stream, mstream,
+                                            merge_first=os.environ.get("FSX_GRAPH_MERGE_FIRST", "1") == "1")
+                else:
+                    batch.capture(stream, bulk=True, l2_keep=L2_KEEP)
+                batch.release()
+                for _ in range(3):
+                    step_graph()
+                return timed(step_graph, 10)[0]
+            # the colocated pass as a graph measured slower here (config A:
+            # 0.078 vs 0.062 ms per pass, profiles/README.md); probed on request
+            c_ms = capture("colocated") if os.environ.get("FSX_BENCH_GRAPH_COLO") == "1" else 1e9
+            g_ms = capture("serial")
             s_ms, _, _ = timed(step_serial, 10)
             probe = {"graph_ms": round(g_ms, 4), "serial_ms": round(s_ms, 4)}
-            graph_pass = g_ms < s_ms
+            if c_ms < 1e9:
+                probe["graph_colocated_ms"] = round(c_ms, 4)
+            graph_pass = min(g_ms, c_ms) < s_ms
+            graph_kind = "colocated" if c_ms < g_ms else "serial"
             if graph_pass:
+                if graph_kind == "colocated":
+                    capture("colocated")
                 step = step_graph
             for _ in range(3):
                 step()
@@ -679,7 +694,9 @@ def run_single(args):
                    "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush needed)"},
         "roofline": roofline,
         "kernels": kernels,
-        "pass_schedule": {"used": ("stream-ordered (K1 then merge) as one CUDA graph launch per pass"
+        "pass_schedule": {"used": (("colocated (K1 || early-start merge, flags reset per pass) "
+                                    "as one CUDA graph launch per pass" if graph_kind == "colocated"
+                                    else "stream-ordered (K1 then merge) as one CUDA graph launch per pass")
                                    if graph_pass else "stream-ordered (K1 then merge)") if args.serial
                           else "colocated (K1 || early-start merge)", "probe": probe},
         "nvlink": {"applies": False, "why": "N=1: producer and consumer share one B200"},

@@ -379,6 +379,12 @@ int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* dev
   for (int d : devs) {
     Device* st = nullptr;
     int rc = device_state(f.get(), d, &st);
+    if (rc == FSX_OK) {
+      // every kernel loaded now, not at its first launch (fsx_kernels.cuh)
+      cudaSetDevice(d);
+      const cudaError_t e = fsx::preload_kernels();
+      if (e != cudaSuccess) rc = fail(FSX_E_CONFIG, std::string("kernel preload: ") + cudaGetErrorString(e));
+    }
     if (rc) {
       const std::string msg = t_err;
       fsx_close(f.release());  // release the streams/counters created so far

@@ -412,6 +412,31 @@ def test_pass_graph_replay_bit_exact(fab, oracle_mod):
     fab.slab_free(1, hold)
 
 
+@pytest.mark.parametrize("config,count", [("A", 24), ("D", 8)])
+def test_colocated_pass_graph_bit_exact(fab, oracle_mod, config, count):
+    """The colocated pass (flag reset, K1 || scan + early-start merge) as one
+    CUDA graph (DataPlaneBatch.capture_colocated), replayed several times:
+    merged rows == the oracle, every request valid."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests(config, count)
+    b = DataPlaneBatch(fab, reqs, T.RULES[config], 0, 1,
+                       chunk_rows=512 if config == "D" else None)
+    b.synth_inputs()
+    s = torch.cuda.Stream()
+    ms = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
+    assert b.alloc()
+    b.capture_colocated(s, ms)
+    for _ in range(4):
+        b.run_graph(s)
+    s.synchronize()
+    want, _ = _expected(oracle_mod, b)
+    assert (b.status_host() == 0).all()
+    assert np.array_equal(b.embeds_host(), want)
+    b.release()
+
+
 def test_forward_place_edge_cases(fab, oracle_mod):
     """Direct placement on the merge edge cases: placeholder-only, text-only
     and multi-item requests, and a row width that is not a multiple of 16
