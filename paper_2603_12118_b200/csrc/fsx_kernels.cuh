@@ -96,8 +96,8 @@ cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token,
 // `work`: a zeroed device counter for the early-start (item flags) kernel.
 cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches,
                          unsigned long long* work);
-// Load every kernel now (cudaFuncGetAttributes) instead of at its first
-// launch; called per device by fsx_open.
+// Load the producer kernels (K1 forms, flag stores, channel push) now instead
+// of at their first launch; called per device by fsx_open.
 cudaError_t preload_kernels();
 cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s);
 

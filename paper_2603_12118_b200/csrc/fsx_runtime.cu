@@ -379,8 +379,9 @@ int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* dev
   for (int d : devs) {
     Device* st = nullptr;
     int rc = device_state(f.get(), d, &st);
-    if (rc == FSX_OK) {
-      // every kernel loaded now, not at its first launch (fsx_kernels.cuh)
+    static const bool no_preload = std::getenv("FSX_NO_PRELOAD") != nullptr;  // diagnostics
+    if (rc == FSX_OK && !no_preload) {
+      // producer kernels loaded now, not at their first launch (fsx_kernels.cuh)
       cudaSetDevice(d);
       const cudaError_t e = fsx::preload_kernels();
       if (e != cudaSuccess) rc = fail(FSX_E_CONFIG, std::string("kernel preload: ") + cudaGetErrorString(e));
