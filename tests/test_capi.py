@@ -68,3 +68,26 @@ def test_error_codes_follow_reference_ordinals():
     assert N.ERROR_CODES[N.E_TIMEOUT - 1] == "timeout"
     assert N.ERROR_CODES[N.E_CONFIG - 1] == "config"
     assert N.ERROR_CODES[N.E_INTERNAL - 1] == "internal"
+
+
+def test_python_constants_match_header():
+    """Every FSX_* constant the bindings restate (status codes, transports,
+    forward options, FSX_FWD_MAX_BATCH, merge modes) equals include/fsx.h."""
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hdr = open(os.path.join(root, "include", "fsx.h")).read()
+    defs = {m.group(1): int(m.group(2), 0)
+            for m in re.finditer(r"#define FSX_(\w+) (0x[0-9a-fA-F]+|\d+)u?\b", hdr)}
+    pairs = {"E_VALIDATION": "E_VALIDATION", "E_NOT_FOUND": "E_NOT_FOUND", "E_OOM": "E_OOM",
+             "E_INTEGRITY": "E_INTEGRITY", "E_PROTOCOL": "E_PROTOCOL", "E_TIMEOUT": "E_TIMEOUT",
+             "E_CONFIG": "E_CONFIG", "E_INTERNAL": "E_INTERNAL",
+             "TRANSPORT_LOCAL_BUFFER": "LOCAL_BUFFER", "TRANSPORT_NETWORK_STREAM": "NETWORK_STREAM",
+             "FWD_HOST_NOTIFY": "FWD_HOST_NOTIFY", "FWD_L2_KEEP": "FWD_L2_KEEP", "FWD_BULK": "FWD_BULK",
+             "FWD_SHARE_SM": "FWD_SHARE_SM", "FWD_MAX_BATCH": "FWD_MAX_BATCH",
+             "MERGE_FULL": "MERGE_FULL", "MERGE_SCAN_ONLY": "MERGE_SCAN_ONLY",
+             "MERGE_COPY_ONLY": "MERGE_COPY_ONLY", "MERGE_DISCARD": "MERGE_DISCARD",
+             "MERGE_COLOCATED": "MERGE_COLOCATED"}
+    for h, py in pairs.items():
+        assert h in defs, h
+        assert getattr(N, py) == defs[h], (h, defs[h], getattr(N, py))
