@@ -1864,6 +1864,28 @@ cudaError_t preload_kernels() {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
+  // FSX_DIAG_PRELOAD_ALL=1 (diagnostics, profiles/colocated_bimodality_r01k.md):
+  // also load the consumer kernels, which brings out the colocated pass's slow mode
+  static const bool all = std::getenv("FSX_DIAG_PRELOAD_ALL") != nullptr;
+  if (all) {
+    const void* more[] = {
+        reinterpret_cast<const void*>(merge_scan_kernel),
+        reinterpret_cast<const void*>(merge_copy_kernel),
+        reinterpret_cast<const void*>(merge_follow_kernel<8>),
+        reinterpret_cast<const void*>(merge_follow_kernel<16>),
+        reinterpret_cast<const void*>(merge_copy_tma_kernel<kTmaStages>),
+        reinterpret_cast<const void*>(merge_follow2_kernel<16>),
+        reinterpret_cast<const void*>(merge_follow_tma_kernel<kTmaStages>),
+        reinterpret_cast<const void*>(merge_stream_tma_kernel<kTmaStages>),
+        reinterpret_cast<const void*>(merge_stream_kernel),
+        reinterpret_cast<const void*>(synth_kernel),
+        reinterpret_cast<const void*>(mailbox_kernel),
+        reinterpret_cast<const void*>(digest_kernel),
+        reinterpret_cast<const void*>(wait_flags_kernel),
+        reinterpret_cast<const void*>(chan_pull_kernel),
+    };
+    for (const void* f : more) cudaFuncGetAttributes(&a, f);
+  }
   return cudaSuccess;
 }
 
