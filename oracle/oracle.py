@@ -133,6 +133,10 @@ def _load_ref():
     lib.ref_stream_bench.argtypes = [C_.c_int64, C_.c_int, C_.c_int]
     lib.ref_generate_workload.restype = C_.c_char_p
     lib.ref_generate_workload.argtypes = [C_.c_char_p, C_.c_double, C_.c_double, C_.c_uint64]
+    lib.ref_record.restype = C_.c_char_p
+    lib.ref_record.argtypes = [C_.c_char_p] * 5
+    lib.ref_dispatch.restype = C_.c_char_p
+    lib.ref_dispatch.argtypes = [C_.c_char_p] * 5
     return lib
 
 
@@ -195,3 +199,25 @@ def merge(row_bytes: int, placeholder_id: int, embeds, token_ids, req_row_off, r
                rro.ctypes.data, rio.ctypes.data, ptrs, rows.ctypes.data if len(rows) else None,
                status.ctypes.data, nthreads)
     return status[:R]
+
+
+def ref_record(kind: str, config: dict, request: dict, rules: dict, request_id: str) -> dict:
+    """The reference record() of one request (record_replay.hpp:510-528)."""
+    import json
+    out = REF.ref_record(kind.encode(), json.dumps(config).encode(), json.dumps(request).encode(),
+                         json.dumps(rules).encode(), request_id.encode())
+    if out is None:
+        raise RuntimeError(REF.ref_last_error().decode())
+    return json.loads(out)
+
+
+def ref_dispatch(kind: str, config: dict, requests, rules: dict, replica_gpus: dict) -> list:
+    """The reference TaskDispatcher::dispatch of a batch of (request_id,
+    request) pairs (task_dispatcher.hpp:178-266)."""
+    import json
+    out = REF.ref_dispatch(kind.encode(), json.dumps(config).encode(),
+                           json.dumps([[rid, rq] for rid, rq in requests]).encode(),
+                           json.dumps(rules).encode(), json.dumps(replica_gpus).encode())
+    if out is None:
+        raise RuntimeError(REF.ref_last_error().decode())
+    return json.loads(out)

@@ -17,7 +17,10 @@
 
 #include "fissim/executor_sim.hpp"
 #include "fissim/profiles.hpp"
+#include "fissim/record_replay.hpp"
 #include "fissim/sidecar.hpp"
+#include "fissim/task_dispatcher.hpp"
+#include "fissim/task_model.hpp"
 #include "fissim/workload.hpp"
 
 extern "C" {
@@ -358,6 +361,139 @@ double ref_stream_bench(int64_t row_bytes, int streams, int steps) {
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Merge inputs and placement, from the reference's own record / dispatch.
+//
+// The merge's slot order and row counts, and the config-D producer->consumer
+// placement, are derived from record() (record_replay.hpp:510-528) with the
+// built-in composite bodies invoke_mllm / invoke_omni (:404-454) and from
+// TaskDispatcher::dispatch (task_dispatcher.hpp:178-266).  These shims run
+// that code unmodified so tests can pin the repo's layout (trace.layout) and
+// fan-out plan (fanout.plan) to it.
+
+namespace {
+
+CompositeTaskSpec make_composite(const char* kind, const char* config_json) {
+  return CompositeLibrary::instance().make(kind, json::parse(config_json));
+}
+
+// The consumer of the encoder embeddings: the "llm" child of an mllm
+// composite, the "thinker" of an omni one (task_model.hpp:259-330).
+std::string consumer_digest(const CompositeTaskSpec& c) {
+  const char* name = c.children.count("thinker") ? "thinker" : "llm";
+  return canonical_hash(std::get<UnitTaskSpec>(c.children.at(name)));
+}
+
+std::map<std::string, std::string> child_of_digest(const CompositeTaskSpec& c) {
+  std::map<std::string, std::string> out;
+  for (const auto& [name, child] : c.children)
+    if (const auto* u = std::get_if<UnitTaskSpec>(&child)) out[canonical_hash(*u)] = name;
+  return out;
+}
+
+}  // namespace
+
+// record() of one request: {"graph": InvocationGraph::to_json(), "consumer":
+// invocation id of the embedding consumer, "children": {invocation id: child
+// task name}}.  The pointer stays valid until the next call on this thread.
+const char* ref_record(const char* kind, const char* config_json, const char* request_json,
+                       const char* rules_json, const char* request_id) {
+  static thread_local std::string out;
+  try {
+    CompositeTaskSpec comp = make_composite(kind, config_json);
+    ShapeRules shapes = ShapeRules::from_json(json::parse(rules_json));
+    RecordOutcome rec = record(comp, json::parse(request_json), shapes, request_id);
+    const std::string cdig = consumer_digest(comp);
+    auto names = child_of_digest(comp);
+    json children = json::object();
+    std::string consumer;
+    for (const auto& [id, inv] : rec.graph.nodes) {
+      children[id] = names.at(inv.task_digest);
+      if (inv.task_digest == cdig) consumer = id;
+    }
+    out = json{{"graph", rec.graph.to_json()}, {"consumer", consumer}, {"children", children}}.dump();
+    return out.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// TaskDispatcher::dispatch over a batch of requests, all dispatched before any
+// completes (the gateway dispatches each request as it arrives; executors
+// complete later).  Replicas: one per GPU listed for each child task, added
+// in list order (add_replica, task_dispatcher.hpp:101-103), replica ids
+// "<child>/<k>".  Returns, per request in order, {"request_id", "assign":
+// {invocation id: [child, replica ordinal, home gpu]}, "routes": {invocation
+// id: [[output index, [dest gpus]], ...]}} with the routes read back from the
+// invocation frames the dispatcher delivered (:224-266).
+const char* ref_dispatch(const char* kind, const char* config_json, const char* requests_json,
+                         const char* rules_json, const char* replica_gpus_json) {
+  static thread_local std::string out;
+  try {
+    CompositeTaskSpec comp = make_composite(kind, config_json);
+    ShapeRules shapes = ShapeRules::from_json(json::parse(rules_json));
+    json gpus = json::parse(replica_gpus_json);  // {child: [gpu, ...]}
+    auto names = child_of_digest(comp);
+    SimKernel k(ClockMode::Virtual);
+    std::map<int, int> topo;
+    for (int g = 0; g < 8; ++g) topo[g] = 0;  // one 8-GPU box
+    SidecarConfig cfg;
+    cfg.arena_bytes = 1 << 20;
+    SidecarFabric fabric(k, topo, cfg);
+    TaskDispatcher disp(k, fabric);
+    std::vector<Frame> delivered;
+    std::map<std::string, std::pair<std::string, int>> replica_info;  // id -> (child, ordinal)
+    for (const auto& [digest, child] : names) {
+      if (!gpus.contains(child)) continue;
+      int ordinal = 0;
+      for (int g : gpus.at(child).get<std::vector<int>>()) {
+        ReplicaEndpoint ep;
+        ep.replica_id = child + "/" + std::to_string(ordinal);
+        ep.task_digest = digest;
+        ep.home_gpu = g;
+        ep.gpus = {g};
+        ep.deliver = [&delivered](const Frame& f) { delivered.push_back(f); };
+        replica_info[ep.replica_id] = {child, ordinal++};
+        disp.add_replica(std::move(ep));
+      }
+    }
+    json reqs = json::parse(requests_json);  // [[request_id, request], ...]
+    json result = json::array();
+    std::vector<std::shared_ptr<DispatchHandle>> handles;
+    for (const auto& pair : reqs) {
+      std::string rid = pair.at(0).get<std::string>();
+      RecordOutcome rec = record(comp, pair.at(1), shapes, rid);
+      // the gateway->dispatcher hop carries the JSON graph (control_plane.hpp:772-774)
+      InvocationGraph wire = InvocationGraph::from_json(rec.graph.to_json());
+      handles.push_back(disp.dispatch(wire, pair.at(1)));
+    }
+    k.run_until_idle();  // runs the "dispatch.deliver" events: frames captured
+    std::map<std::string, json> routes;
+    for (const auto& f : delivered) {
+      InvocationMessage m = InvocationMessage::from_frame(f);
+      json r = json::array();
+      for (const auto& o : m.outputs) r.push_back(json::array({o.ref.output_index, o.dest_gpus}));
+      routes[m.invocation_id] = r;
+    }
+    for (const auto& h : handles) {
+      json assign = json::object(), rts = json::object();
+      for (const auto& [inv, rep] : h->record().assignments) {
+        const auto& info = replica_info.at(rep);
+        int home = gpus.at(info.first).at(info.second).get<int>();
+        assign[inv] = json::array({info.first, info.second, home});
+        rts[inv] = routes.at(inv);
+      }
+      result.push_back(json{{"request_id", h->request_id()}, {"assign", assign}, {"routes", rts}});
+    }
+    out = result.dump();
+    return out.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
   }
 }
 

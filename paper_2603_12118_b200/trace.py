@@ -176,6 +176,36 @@ def requests_from_trace(mix: str, rules: ShapeRules, count: int, start: int = 0)
     return out
 
 
+# Composite the BASELINE configs run through (record_replay.hpp:404-420,
+# task_model.hpp:259-283): an mllm with encoder fission and one encoder task
+# per modality; the embedding consumer is its "llm" child.
+MLLM_COMPOSITE = {"model_id": "fsx/mllm", "modalities": ["image", "video", "audio"],
+                  "encoder_fission": True}
+CONFIG_MIX = {"A": "mllm-chat", "D": "servegen-like"}
+
+
+def request_json(config: str, index: int) -> dict:
+    """The request object of request ``index`` of a config batch, as the
+    reference's generate_workload emits it (workload.hpp:226-233).  Config B
+    is one video per request with 1800 input tokens."""
+    if config == "B":
+        return {"class": "video_chat", "text": "q", "items": [{"modality": "video"}],
+                "audio_output": False,
+                "gen": {"input_tokens": 1800, "output_tokens": 150, "chunks": 0}}
+    tr = load_trace(CONFIG_MIX[config])["requests"]
+    r = tr[index % len(tr)]
+    return {"class": r["class"], "text": "q", "items": [{"modality": m} for m in r["items"]],
+            "audio_output": r["audio_output"],
+            "gen": {"input_tokens": r["input_tokens"], "output_tokens": r["output_tokens"],
+                    "chunks": r["chunks"]}}
+
+
+def rules_json(rules: ShapeRules) -> dict:
+    """ShapeRules::to_json (profiles.hpp:244-255)."""
+    from dataclasses import asdict
+    return asdict(rules)
+
+
 def config_requests(config: str, count: Optional[int] = None) -> List[Request]:
     """Request batches of the BASELINE.json configs."""
     if config == "A":

@@ -14,6 +14,17 @@ Outputs (committed):
                            SidecarFabric delivered-byte digests
   traces/*.json            generate_workload(mix, rate, duration, seed=42)
                            request traces (sizes only) for configs A and D
+  record_dispatch.json     the merge's inputs and the config-D placement:
+                           record() (record_replay.hpp:510-528) of every
+                           request of configs A/B/D -> the consumer's input
+                           DataRefs in slot order; TaskDispatcher::dispatch
+                           (task_dispatcher.hpp:178-266) of config-D batches
+                           at 2/4/8 GPUs -> replica assignments and dest_gpus;
+                           SHA-256 of the merged prompt embeddings built from
+                           the bytes the reference SidecarFabric delivered,
+                           placed in that slot order
+
+    python tests/golden/make_golden.py [--only record]
 """
 from __future__ import annotations
 
@@ -35,6 +46,92 @@ MIXES = "/root/reference/proj/mixes"
 
 def synth(seed, n):
     return O.synth_payload(seed, n, REF)
+
+
+def _consumer_refs(rec: dict) -> list:
+    node = next(n for n in rec["graph"]["nodes"] if n["invocation_id"] == rec["consumer"])
+    return [(pos, s["ref"]) for pos, s in enumerate(node["inputs"]) if s["kind"] == "ref"]
+
+
+def _ref_deliver(ref_id: str, n: int) -> bytes:
+    """The bytes the reference SidecarFabric hands the consumer's ChunkCallback
+    for this ref's payload (encoder gpu 0 -> LLM gpu 1, LocalBuffer)."""
+    p = synth(O.payload_seed(ref_id, 0, REF), n)
+    out = (C.c_uint8 * max(n, 1))()
+    stats = (C.c_int64 * 7)()
+    rc = REF.ref_forward(0, 1, ref_id.encode(), p, n, out, stats)
+    assert rc == 0 and stats[6] == 1, (ref_id, rc, REF.ref_last_error())
+    return bytes(out)[:n]
+
+
+def record_dispatch() -> None:
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    from paper_2603_12118_b200 import trace as T
+
+    doc: dict = {"source": "reference record()/TaskDispatcher/SidecarFabric compiled unmodified "
+                           "(oracle/_ref, ref_record / ref_dispatch / ref_forward)",
+                 "composite": {"kind": "mllm", "config": T.MLLM_COMPOSITE}}
+    # --- record(): consumer input slots (record_replay.hpp:404-420) -------
+    counts = {"A": 128, "B": 4, "D": 128}
+    rec_out = {}
+    for cfg, n in counts.items():
+        rules = T.RULES[cfg]
+        rows = []
+        for k in range(n):
+            rid = T.request_id(k)
+            rq = T.request_json(cfg, k)
+            rec = O.ref_record("mllm", T.MLLM_COMPOSITE, rq, T.rules_json(rules), rid)
+            slots = []
+            for pos, ref in _consumer_refs(rec):
+                shape, eb = ref["desc"]["shape"], ref["desc"]["elem_bytes"]
+                slots.append([pos, ref["ref_id"], rec["children"][ref["producer"]],
+                              ref["output_index"], shape[0], shape[1] * eb])
+            rows.append({"request_id": rid, "consumer": rec["consumer"],
+                         "input_tokens": rq["gen"]["input_tokens"], "slots": slots})
+        rec_out[cfg] = {"rules": T.rules_json(rules), "requests": rows}
+    doc["record"] = rec_out
+    # --- TaskDispatcher::dispatch: config-D placement at 2/4/8 GPUs --------
+    disp = {}
+    for world in (2, 4, 8):
+        enc, llm = list(range(0, world, 2)), list(range(1, world, 2))
+        gpus = {"encoder.image": enc, "encoder.video": enc, "encoder.audio": enc, "llm": llm}
+        for n in (32, 128):
+            reqs = [(T.request_id(k), T.request_json("D", k)) for k in range(n)]
+            res = O.ref_dispatch("mllm", T.MLLM_COMPOSITE, reqs, T.rules_json(T.RULES["D"]), gpus)
+            rows = []
+            for r in res:
+                inv = sorted(r["assign"])  # map order == record order
+                rows.append({"request_id": r["request_id"],
+                             "assign": [[i] + r["assign"][i] for i in inv],
+                             "routes": [[i, r["routes"][i]] for i in inv]})
+            disp[f"world{world}_n{n}"] = {"replica_gpus": gpus, "requests": rows}
+    doc["dispatch"] = disp
+    # --- merged prompt embeddings from the reference's delivered bytes ------
+    merged = {}
+    for cfg, n in (("A", 64), ("B", 4), ("D", 32)):
+        rules = T.RULES[cfg]
+        rb = rules.row_bytes
+        h = hashlib.sha256()
+        for row in rec_out[cfg]["requests"][:n]:
+            slots = row["slots"]
+            assert all(s[5] == rb for s in slots)
+            req = T.Request(row["request_id"], row["input_tokens"],
+                            [T.Item("?", s[4], s[1]) for s in slots])
+            tok = T.prompt_tokens(req)  # the prompt layout contract (DESIGN.md 4)
+            emb = np.frombuffer(synth(T.text_seed(req), req.total_rows * rb), np.uint8).copy()
+            emb = emb.reshape(-1, rb) if req.total_rows else emb.reshape(0, rb)
+            pos = np.flatnonzero(tok == T.PLACEHOLDER_ID)
+            if slots:
+                got = [np.frombuffer(_ref_deliver(s[1], s[4] * rb), np.uint8) for s in slots]
+                emb[pos] = np.concatenate(got).reshape(-1, rb)
+            h.update(emb.tobytes())
+        merged[cfg] = {"requests": n, "row_bytes": rb, "sha256": h.hexdigest()}
+    doc["merged_sha256"] = merged
+    with open(os.path.join(HERE, "record_dispatch.json"), "w") as fh:
+        json.dump(doc, fh, separators=(",", ":"))
+    print("record/dispatch fixtures written")
 
 
 def main() -> None:
@@ -166,4 +263,8 @@ def main() -> None:
 
 
 if __name__ == "__main__":
-    main()
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "record":
+        record_dispatch()
+    else:
+        main()
+        record_dispatch()

@@ -273,6 +273,25 @@ def test_merge_bit_exact(fab, oracle_mod, config, count, chunk_rows):
     assert fab.slab_usage(1)["segments_in_use"] == 0
 
 
+@pytest.mark.parametrize("config", ["A", "B", "D"])
+def test_merge_matches_reference_derived_golden(fab, config):
+    """The GPU pass (K1 into the slab, K3 merge) produces exactly the prompt
+    embeddings built from the bytes the REFERENCE SidecarFabric delivered,
+    placed in the slot order the reference record() gives the consumer
+    (tests/golden/record_dispatch.json, merged_sha256; make_golden.py)."""
+    import hashlib
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "record_dispatch.json")) as fh:
+        want = json.load(fh)["merged_sha256"][config]
+    reqs = T.config_requests(config, want["requests"])
+    b = _run_batch(fab, reqs, T.RULES[config], 1024 if config != "A" else None)
+    assert (b.status_host() == 0).all()
+    assert hashlib.sha256(b.embeds_host().tobytes()).hexdigest() == want["sha256"]
+    b.release()
+
+
 def test_merge_early_start_flags(fab, oracle_mod):
     reqs = T.config_requests("D", 12)
     b = _run_batch(fab, reqs, T.RULES["D"], chunk_rows=512, early=True)
