@@ -245,7 +245,15 @@ class MultiProcessHost : public ExecutorHost {
     struct Release {
       MultiProcessHost* h;
       int64_t off;
-      ~Release() { h->send_frame(Frame{json{{"type", "outbox_free"}, {"offset", off}}, {}}); }
+      // runs during unwinding too (a failed send): never let the socket
+      // error escape the destructor (std::terminate); a worker that is gone
+      // no longer needs its outbox range back
+      ~Release() {
+        try {
+          h->send_frame(Frame{json{{"type", "outbox_free"}, {"offset", off}}, {}});
+        } catch (...) {
+        }
+      }
     } release{this, off};
     if (!outbox_ || off + n > outbox_capacity_)
       fail(ErrorCode::Protocol, "worker send names an unmapped outbox range");

@@ -37,6 +37,7 @@
 #include <memory>
 #include <optional>
 #include <queue>
+#include <set>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -265,7 +266,15 @@ class Fabric {
 
   // Raw consumers release their segment.  `slab_gpu` is the destination GPU
   // whose slab holds it (the envelope location reads "gpu<G>:off<K>").
+  // Only segments handed to a raw callback and not yet acked are accepted:
+  // an ack naming any other (gpu, offset) -- e.g. a node id passed where the
+  // reference's ack_raw(node, off) took one -- raises Internal instead of
+  // freeing whatever live segment sits there.
   void ack_raw(int slab_gpu, int64_t offset) {
+    if (raw_held_.erase({slab_gpu, offset}) == 0)
+      Traits::raise(status::kInternal, "ack_raw of gpu " + std::to_string(slab_gpu) + " offset " +
+                                           std::to_string(offset) +
+                                           ": no segment held by a raw consumer there");
     release_segment(slab_gpu, offset);
     place_backlog(slab_gpu);
   }
@@ -426,6 +435,7 @@ class Fabric {
     Envelope env;
     int64_t off = -1;
     int64_t ticket = -1;
+    bool network = false;  // arrived as a network frame: verify the sender's checksum64
   };
 
   struct RefState {
@@ -497,7 +507,10 @@ class Fabric {
     check(fsx_slab_alloc(h_, dst, std::max<int64_t>(ps.env.chunk_bytes, 1), off));
     if (*off < 0) return false;
     const int64_t n = ps.env.chunk_bytes;
-    const bool local = Traits::is_local(ps.env);
+    // The envelope's checksum is the producer's: dg64 set here for local
+    // sends; a network arrival keeps the sender's checksum64 whatever its
+    // transport tag says (sidecar.hpp:351-364 verifies the frame as sent).
+    const bool local = Traits::is_local(ps.env) && !ps.network;
     *ticket = -1;
     if (!ps.src_is_device && n > 0 && n <= FSX_SMALL_MAX) {
       // small host span (per-token hidden states, codes): one asynchronous
@@ -581,12 +594,12 @@ class Fabric {
     if (!start_copy(ps, &off, &token, &flag_base, &n_chunks, &ticket)) return false;
     ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
     if (ticket < 0) wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
-    deliver(ps.env, off, ticket);
+    deliver(ps.env, off, ticket, /*network=*/true);
     return true;
   }
 
   // sidecar.hpp:498-525
-  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1) {
+  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1, bool network = false) {
     const std::string key = key_of(env.ref_id, env.dst_gpu);
     RefState& st = refs_[key];
     if (st.request_id.empty()) st.request_id = env.request_id;
@@ -596,7 +609,7 @@ class Fabric {
       place_backlog(env.dst_gpu);
       return;
     }
-    st.parked.emplace(env.seq, Parked{env, off, ticket});
+    st.parked.emplace(env.seq, Parked{env, off, ticket, network});
     if (st.has_interest) {
       drain(st);
       return;
@@ -626,19 +639,21 @@ class Fabric {
       Envelope env = it->second.env;
       const int64_t off = it->second.off;
       const int64_t ticket = it->second.ticket;
+      const bool network = it->second.network;
       st.parked.erase(it);
       if (st.raw_cb) {
         drop_ticket(ticket);  // waits until the bytes are in the slab
         ++transfers_;
         bytes_forwarded_ += env.chunk_bytes;
         ++st.next_seq;
+        raw_held_.insert({env.dst_gpu, off});
         st.raw_cb(env, off);
         continue;
       }
       // Verify before handing the bytes over, like sidecar.hpp:545-557: the
       // device hop is checked with dg64 recomputed on the consumer GPU over
       // the slab segment, the network hop with the reference checksum64.
-      const bool local = Traits::is_local(env);
+      const bool local = Traits::is_local(env) && !network;
       std::vector<uint8_t> bytes;
       bool dev_ok = true;
       if (ticket >= 0) {
@@ -736,6 +751,7 @@ class Fabric {
   uint64_t* digest_slot_ = nullptr;  // K1 digest of the send being placed
   std::vector<int> slabs_;
   std::map<std::string, RefState> refs_;
+  std::set<std::pair<int, int64_t>> raw_held_;  // (slab gpu, offset) handed to raw callbacks
   std::map<int, std::deque<Pending>> backlog_;
   FailureHandler failure_handler_;
   int64_t transfers_ = 0, bytes_forwarded_ = 0, integrity_errors_ = 0, orphan_reclaims_ = 0;

@@ -139,17 +139,54 @@ class BlockList {
   int64_t used_segments_ = 0, used_bytes_ = 0, peak_ = 0;
 };
 
-// Bump ring of contiguous index ranges (flags / counters).  Reuse is safe
-// because flag values are unique tokens and counters reset themselves.
+// Bump ring of contiguous index ranges (flags / counters / scratch).  Reuse
+// of eager ranges is safe because flag values are unique tokens and counters
+// reset themselves.  Ranges baked into a CUDA graph (taken, or named by a
+// launch, while the stream is capturing) are pinned: replays keep using them
+// for the life of the fabric, so the ring never hands them out again.
 struct Ring {
   int64_t size = 0, next = 0;
+  std::map<int64_t, int64_t> pinned;  // start -> end, disjoint
+  // First free range of n at or after `next`, wrapping once; -1 when every
+  // candidate overlaps a pinned range.
   int64_t take(int64_t n) {
-    if (next + n > size) next = 0;
-    const int64_t at = next;
-    next += n;
-    return at;
+    if (n > size) return -1;
+    bool wrapped = false;
+    for (;;) {
+      if (next + n > size) {
+        if (wrapped) return -1;
+        wrapped = true;
+        next = 0;
+      }
+      auto it = pinned.lower_bound(next + n);  // first pinned start >= end
+      if (it != pinned.begin() && std::prev(it)->second > next) {
+        next = std::prev(it)->second;  // overlaps a pinned range: skip past it
+        continue;
+      }
+      const int64_t at = next;
+      next += n;
+      return at;
+    }
+  }
+  void pin(int64_t at, int64_t n) {
+    if (n <= 0) return;
+    int64_t lo = at, hi = at + n;
+    auto it = pinned.upper_bound(lo);
+    if (it != pinned.begin() && std::prev(it)->second >= lo) --it;
+    while (it != pinned.end() && it->first <= hi) {
+      lo = std::min(lo, it->first);
+      hi = std::max(hi, it->second);
+      it = pinned.erase(it);
+    }
+    pinned[lo] = hi;
   }
 };
+
+// True while `st` is being captured into a CUDA graph.
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
 
 struct Slab {
   int gpu = -1;
@@ -668,6 +705,7 @@ int fsx_flags_alloc(fsx_fabric* f, int dst_gpu, int32_t n, int64_t* flag_base) {
   if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
   if (n <= 0 || n > kFlagRing / 4) return fail(FSX_E_VALIDATION, "bad flag count");
   *flag_base = s->flags.take(n);
+  if (*flag_base < 0) return fail(FSX_E_OOM, "flag ring exhausted by graph-pinned ranges");
   return FSX_OK;
 }
 
@@ -733,6 +771,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
   }
   FSX_CUDA(cudaSetDevice(src_dev));
   cudaStream_t st = pick_stream(dev, stream);
+  const bool graph = capturing(st);
   for (int32_t first = 0; first < n; first += fsx::kFwdMaxBatch) {
     const int32_t cnt = std::min<int32_t>(n - first, fsx::kFwdMaxBatch);
     fsx::FwdBatch b{};
@@ -752,7 +791,13 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
           return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
         if (x.flag_base < 0 || x.flag_base + n_chunks > kFlagRing)
           return fail(FSX_E_VALIDATION, "flag range out of the ring");
-        a.counters = dev->counters + dev->counter_ring.take(n_chunks);
+        const int64_t c0 = dev->counter_ring.take(n_chunks);
+        if (c0 < 0) return fail(FSX_E_OOM, "chunk counter ring exhausted by graph-pinned ranges");
+        if (graph) {  // baked into the graph: never handed out again
+          dev->counter_ring.pin(c0, n_chunks);
+          s->flags.pin(x.flag_base, n_chunks);
+        }
+        a.counters = dev->counters + c0;
         // FSX_DIAG_NO_FLAGS=1: measure the copy without completion tracking
         // (no chunk flags are ever set: stream-ordered consumers only)
         static const bool diag_no_flags = std::getenv("FSX_DIAG_NO_FLAGS") != nullptr;
@@ -850,7 +895,10 @@ int fsx_u64_slot(fsx_fabric* f, int gpu, uint64_t** d_slot, void* stream) {
       FSX_CUDA(cudaMalloc(&dev->scratch, kScratchRing * sizeof(uint64_t)));
       dev->scratch_ring.size = kScratchRing;
     }
-    slot = dev->scratch + dev->scratch_ring.take(1);
+    const int64_t at = dev->scratch_ring.take(1);
+    if (at < 0) return fail(FSX_E_OOM, "scratch ring exhausted by graph-pinned slots");
+    if (capturing(pick_stream(dev, stream))) dev->scratch_ring.pin(at, 1);
+    slot = dev->scratch + at;
   }
   FSX_CUDA(cudaSetDevice(ordinal));
   FSX_CUDA(cudaMemsetAsync(slot, 0, sizeof(uint64_t), pick_stream(dev, stream)));

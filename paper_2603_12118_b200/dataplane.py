@@ -113,11 +113,16 @@ class DataPlaneBatch:
             return False
         self.slab_off = offs
         # first fit hands back the same offsets step after step: upload the
-        # slab views only when they change
+        # slab views only when they change.  A merge still in flight (an
+        # early-start merge of the previous pass on another stream) reads
+        # item_src, so the device is drained first and the upload is
+        # synchronous: rare, and correct whatever streams the caller uses.
         key = offs.tobytes()
         if len(offs) and key != getattr(self, "_uploaded_offs", None):
             base = self.fab.slab_ptr(self.dst_gpu, 0)
+            torch.cuda.synchronize(self.dst_dev)
             self.item_src.copy_(torch.from_numpy(offs + base))
+            torch.cuda.synchronize(self.dst_dev)
             self._uploaded_offs = key
         return True
 

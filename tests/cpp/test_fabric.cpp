@@ -188,8 +188,16 @@ TEST_CASE("raw interest reads the slab in place and frees on ack") {
   std::vector<uint8_t> back(n);
   REQUIRE(cudaMemcpy(back.data(), f.slab_ptr(3, off), n, cudaMemcpyDeviceToHost) == cudaSuccess);
   CHECK(back == payload);
+  // an ack naming a node id / wrong gpu, or the right segment twice, is
+  // rejected without freeing anything
+  bool wrong = false, twice = false;
+  try { f.ack_raw(0, off); } catch (const fsx::Error& e) { wrong = e.status() == FSX_E_INTERNAL; }
+  CHECK(wrong);
+  CHECK(f.stats().segments_in_use == 1);
   f.ack_raw(3, off);
   CHECK(f.stats().segments_in_use == 0);
+  try { f.ack_raw(3, off); } catch (const fsx::Error& e) { twice = e.status() == FSX_E_INTERNAL; }
+  CHECK(twice);
   CHECK(seen.chunk_bytes == static_cast<int64_t>(n));
 }
 
@@ -272,6 +280,38 @@ TEST_CASE("streamed chunks arrive in seq order and corrupt ones fail") {
   CHECK(bad.error->status() == FSX_E_INTEGRITY);
   CHECK(failures == std::vector<std::string>({"req-i"}));
   CHECK(f.stats().integrity_errors == 1);
+  CHECK(f.stats().segments_in_use == 0);
+
+  // A network frame tagged local_buffer (an envelope whose JSON carries no
+  // transport key decodes that way) is still verified against the sender's
+  // checksum64 (sidecar.hpp:351-364), never re-digested on arrival.
+  Got tagged_ok, tagged_bad;
+  collect(f, 6, "req-t/r0", tagged_ok);
+  collect(f, 7, "req-u/r0", tagged_bad);
+  auto t = synth(4, 700);
+  auto e_ok = env_for(0, t, true, fsx::checksum64(t.data(), t.size()));
+  e_ok.request_id = "req-t";
+  e_ok.ref_id = "req-t/r0";
+  e_ok.dst_gpu = 6;
+  e_ok.transport = Transport::LocalBuffer;
+  auto corrupt = t;
+  corrupt[123] ^= 0x40;
+  auto e_bad = env_for(0, corrupt, true, fsx::checksum64(t.data(), t.size()));
+  e_bad.request_id = "req-u";
+  e_bad.ref_id = "req-u/r0";
+  e_bad.dst_gpu = 7;
+  e_bad.transport = Transport::LocalBuffer;
+  k.post("inject", [&] {
+    f.handle_network(e_ok, t);
+    f.handle_network(e_bad, corrupt);
+  });
+  k.run_until_idle();
+  REQUIRE(tagged_ok.chunks.size() == 1);
+  CHECK(tagged_ok.chunks[0] == t);
+  CHECK(tagged_bad.chunks.empty());
+  REQUIRE(tagged_bad.error.has_value());
+  CHECK(tagged_bad.error->status() == FSX_E_INTEGRITY);
+  CHECK(f.stats().integrity_errors == 2);
   CHECK(f.stats().segments_in_use == 0);
 }
 
