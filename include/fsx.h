@@ -156,16 +156,16 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
 /* FSX_FWD_BULK: move this batch's tiles with the bulk-copy engine
  * (forward_tma_kernel: cp.async.bulk global->shared->global, 32 KiB per
  * 32-thread CTA, 16 registers) instead of register loads/stores -- the faster
- * K1 when it runs alone (1.01 of the measured copy peak on 256 MiB).  Applies
- * to local, 16-byte aligned transfers without a fused digest; others in the
- * batch keep the register tile kernel.  FSX_FWD_VARIANT=5 makes it the
- * default for every call. */
+ * K1 when it runs alone (1.01 of the measured copy peak on 256 MiB).  Local
+ * or peer (NVLink) slabs; it applies when every transfer of the batch is
+ * 16-byte aligned without a fused digest, else the register tile kernel runs. */
 #define FSX_FWD_BULK 4u
-/* FSX_FWD_SHARE_SM: cap this launch at two K1 CTAs per SM (register tiles,
- * padded shared memory) so a consumer kernel running concurrently on the
- * same GPU (the colocated early-start merge) always finds a free slot on
- * every SM, whatever order the CTA dispatcher takes the two grids in. */
-#define FSX_FWD_SHARE_SM 8u
+/* FSX_FWD_PEER_GPU_COUNT: for peer (NVLink) destinations, count each tile
+ * into its chunk with a gpu-scope acq_rel atomic and let the tile that
+ * completes a chunk make the whole chunk visible to the consumer GPU with one
+ * fence.sc.sys before the system-scope flag store, instead of a system-scope
+ * acq_rel atomic per tile (the default).  No effect on local slabs. */
+#define FSX_FWD_PEER_GPU_COUNT 16u
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                    uint32_t options, void* stream);
@@ -308,6 +308,25 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream);
  * Counts as one forward of total_item_rows * row_bytes bytes and one merge. */
 int fsx_forward_place(fsx_fabric* f, int src_gpu, int dst_gpu, const fsx_merge_batch* b,
                       int64_t done_flag, uint64_t token, void* stream);
+
+/* The forward and the merge as ONE kernel (the tee).  When the producer's
+ * buffers are addressable from one device -- N = 1, producer and consumer on
+ * the same GPU -- the slab pass reads every item row once and stores it twice:
+ * into the item's slab segment with per-chunk flags, exactly as
+ * fsx_forward_batch would (t[i]: dst_gpu, dst_off, chunk_bytes, flag_base,
+ * token in/out), and into its placeholder row, exactly as fsx_merge would (b:
+ * the consumer's batch, whose d_item_src[i] must be t[i].d_src).  The payload
+ * crosses HBM three times instead of four (K1 writes the slab, K3 reads it
+ * back), in one launch per 64 items.  n == b->num_items, t[i].bytes == item i's
+ * rows * row_bytes, chunk_bytes whole rows (or <= 0: one chunk).  mode:
+ * FSX_MERGE_FULL (scan first, same stream) or FSX_MERGE_COPY_ONLY (positions and
+ * statuses from an earlier scan); no early-start or discard bits.  Options:
+ * FSX_FWD_HOST_NOTIFY, FSX_FWD_L2_KEEP, FSX_FWD_PEER_GPU_COUNT.  Items of a
+ * request that failed validation are still forwarded; its prompt rows are
+ * left untouched.  Runs on t[0].src_gpu's device; counts as n forwards and
+ * one merge. */
+int fsx_forward_merge(fsx_fabric* f, int32_t n, fsx_transfer* t, const fsx_merge_batch* b,
+                      uint32_t options, void* stream);
 
 /* ---- streaming channels (config C) ------------------------------------------
  * The small-message streams of the reference: thinker hidden states, one

@@ -37,7 +37,7 @@ NETWORK_STREAM = 1
 FWD_HOST_NOTIFY = 1
 FWD_L2_KEEP = 2
 FWD_BULK = 4
-FWD_SHARE_SM = 8
+FWD_PEER_GPU_COUNT = 16
 FWD_MAX_BATCH = 64  # FSX_FWD_MAX_BATCH: transfers per K1 launch
 
 MERGE_FULL = 0
@@ -162,6 +162,8 @@ _SIGS = {
     "fsx_merge": [C.c_void_p, C.c_int, C.POINTER(MergeBatch), C.c_void_p],
     "fsx_forward_place": [C.c_void_p, C.c_int, C.c_int, C.POINTER(MergeBatch), C.c_int64,
                           C.c_uint64, C.c_void_p],
+    "fsx_forward_merge": [C.c_void_p, C.c_int32, C.POINTER(Transfer), C.POINTER(MergeBatch),
+                          C.c_uint32, C.c_void_p],
     "fsx_channel_open": [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int32, C.POINTER(C.c_int32)],
     "fsx_channel_close": [C.c_void_p, C.c_int32],
     "fsx_channel_push": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],

@@ -1,13 +1,19 @@
 // fsx_kernels.cu -- sm_100a kernels of the sidecar data plane.
 //
-//   K0 synth_kernel      synth_payload_into (common.hpp:247-259) on the device
-//   K1 forward_kernel    payload placement of SidecarFabric::send/try_place_local
-//                        (sidecar.hpp:302-347, 465-483) as a chunked 16-byte push
-//                        into the consumer slab with per-chunk completion flags
-//   K3 merge_scan_kernel + merge_copy_kernel
-//                        the consumer-side multimodal merge (derived contract,
-//                        SURVEY.md 8a-8; record_replay.hpp:404-416 slot order)
-//   flag kernels         set / wait on chunk flags (release/acquire, sys scope)
+//   K0 synth_kernel         synth_payload_into (common.hpp:247-259) on the device
+//   K1 forward_tile_kernel  payload placement of SidecarFabric::send/try_place_local
+//      forward_tma_kernel   (sidecar.hpp:302-347, 465-483): a chunked push of the
+//                           producer's bytes into the consumer slab (HBM or NVLink
+//                           peer memory) with per-chunk completion flags; register
+//                           tiles or bulk-copy (cp.async.bulk) tiles
+//   K3 merge_scan_kernel    the consumer-side multimodal merge (derived contract,
+//      merge_copy_kernel    SURVEY.md 8a-8; record_replay.hpp:404-416 slot order):
+//      merge_follow_kernel  placeholder scan, then the row scatter -- stream
+//                           ordered, or following the producer's chunk flags
+//   K1+K3 merge_tee_kernel  the forward and the merge as one kernel: each item row
+//                           is read once and stored into its slab segment (with
+//                           the chunk flags) and into its placeholder row
+//   flags / digest / mailbox / channel kernels (see each)
 //
 // Everything here is integer byte movement: rows are opaque 16-byte vectors,
 // never converted through a floating-point type, so bf16 NaN/Inf patterns in the
@@ -16,28 +22,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <cstdlib>
-
 #include "fsx_kernels.cuh"
 
 namespace fsx {
 namespace kern {
 
-constexpr int kFwdThreads = 256;
-// L2 policy of the follow merge's prompt-row stores (l2_policy: 0 normal,
-// 1 evict_first, 2 evict_last); FSX_FOLLOW_OUT_POLICY selects at build time
-#ifndef FSX_FOLLOW_OUT_POLICY
-#define FSX_FOLLOW_OUT_POLICY 1
-#endif
-constexpr int kFollowOutPolicy = FSX_FOLLOW_OUT_POLICY;
-constexpr int kTmaTileBytes = 32768;  // K1 bulk-copy tile (forward_tma_kernel)
+constexpr int kTileThreads = 256;     // K1 register tiles: 256 threads x 8 x 16 B = 32 KiB
+constexpr int kTileVecs = 8;
+constexpr int kTmaTileBytes = 32768;  // K1 bulk-copy tile
 constexpr int kMaxDevices = 64;       // per-device launch attributes
-// K1 variants: <vectors per lane per batch, min CTAs per SM>.  0: 16 x 16 B
-// (8 KiB per warp batch, 2 CTAs/SM), 1: 8 x 16 B at 4 CTAs/SM (register cap 64).
-constexpr int kMergeThreads = 256;
-constexpr int kMergeUnroll = 16;  // 32 lanes x 16 x 16 B = 8 KiB of a row per batch
+constexpr int kMergeThreads = 256;    // K3: one warp per placeholder row, 8 rows per CTA
+constexpr int kMergeWarps = kMergeThreads / 32;
+constexpr int kMergeUnroll = 16;      // 32 lanes x 16 x 16 B = 8 KiB of a row per batch
 constexpr int kScanThreads = 1024;
-constexpr int kScanRounds = 16;  // 1024 threads x 16 = 16384 token ids per round
+constexpr int kScanRounds = 16;       // 1024 threads x 16 = 16384 token ids per round
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -50,8 +48,8 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
-// Coherent streaming load: used where the data may have been written by a
-// peer GPU during this kernel's lifetime (early-start merge).
+// Coherent streaming load: used where the data may have been written by
+// another kernel or a peer GPU during this kernel's lifetime (early start).
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -86,45 +84,6 @@ __device__ __forceinline__ void st_v4_pol(void* p, const uint4& v, uint64_t pol)
                : "memory");
 }
 
-// 32-byte vectors: sm_100 has 256-bit global loads/stores (LDG/STG .256).
-struct alignas(32) v8u32 {
-  uint4 lo, hi;
-};
-
-__device__ __forceinline__ v8u32 ld_nc_v8_pol(const void* p, uint64_t pol) {
-  v8u32 r;
-  asm volatile(
-      "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-      : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x), "=r"(r.hi.y),
-        "=r"(r.hi.z), "=r"(r.hi.w)
-      : "l"(p), "l"(pol));
-  return r;
-}
-
-__device__ __forceinline__ void st_v8_pol(void* p, const v8u32& v, uint64_t pol) {
-  asm volatile(
-      "st.global.L1::no_allocate.L2::cache_hint.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
-      "r"(v.lo.x), "r"(v.lo.y), "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z),
-      "r"(v.hi.w), "l"(pol)
-      : "memory");
-}
-
-// Loads/stores of one V-byte vector (V = 16 or 32) with L2 policies.
-template <int V>
-struct VecIO;
-template <>
-struct VecIO<16> {
-  using T = uint4;
-  static __device__ __forceinline__ T ld(const void* p, uint64_t pol) { return ld_nc_v4_pol(p, pol); }
-  static __device__ __forceinline__ void st(void* p, const T& v, uint64_t pol) { st_v4_pol(p, v, pol); }
-};
-template <>
-struct VecIO<32> {
-  using T = v8u32;
-  static __device__ __forceinline__ T ld(const void* p, uint64_t pol) { return ld_nc_v8_pol(p, pol); }
-  static __device__ __forceinline__ void st(void* p, const T& v, uint64_t pol) { st_v8_pol(p, v, pol); }
-};
-
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
@@ -143,9 +102,17 @@ __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -157,36 +124,29 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 
 // Device spin on a completion flag.  A flag that never arrives (a producer
 // that died, or a kernel the spinning CTAs keep from being scheduled) would
-// hang the GPU, so after FSX_SPIN_TIMEOUT_S seconds the kernel traps: the
-// launch fails with an error the host sees instead of a hang.
-// (set per device by the runtime from FSX_SPIN_TIMEOUT_S, default 30 s)
+// hang the GPU, so after the watchdog time the kernel traps: the launch fails
+// with an error the host sees instead of a hang.  Set per device by the
+// runtime from FSX_SPIN_TIMEOUT_S (default 30 s).
 __constant__ uint64_t c_spin_timeout_ns = 30ull * 1000000000ull;
 
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// gpu-scope wait: producer and consumer on the same GPU (colocated pass)
-__device__ __forceinline__ void spin_until_gpu(const uint64_t* flag, uint64_t token) {
-  if (ld_acquire_gpu(flag) == token) return;
+template <bool kSys>
+__device__ __forceinline__ void spin_until_scoped(const uint64_t* flag, uint64_t token) {
+  auto load = [&] { return kSys ? ld_acquire_sys(flag) : ld_acquire_gpu(flag); };
+  if (load() == token) return;
   const uint64_t t0 = globaltimer_ns();
   uint32_t n = 0;
-  while (ld_acquire_gpu(flag) != token) {
+  while (load() != token) {
     __nanosleep(64);
     if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
   }
 }
-
+// system scope: the producer is another GPU, another process or the host
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t token) {
-  if (ld_acquire_sys(flag) == token) return;
-  const uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (ld_acquire_sys(flag) != token) {
-    __nanosleep(64);
-    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
-  }
+  spin_until_scoped<true>(flag, token);
+}
+// gpu scope: producer and consumer on the same GPU (colocated early start)
+__device__ __forceinline__ void spin_until_gpu(const uint64_t* flag, uint64_t token) {
+  spin_until_scoped<false>(flag, token);
 }
 
 // splitmix64 finaliser (common.hpp:203-208): output k (1-based) of a stream
@@ -197,9 +157,6 @@ __device__ __forceinline__ uint64_t splitmix_word(uint64_t s0, uint64_t k) {
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
   return z ^ (z >> 31);
 }
-
-// ---------------------------------------------------------------------------
-// K1 forward
 
 // fsx integrity digest dg64 (replaces the serial checksum64 of
 // common.hpp:221-241 on the device hop): with w_k the k-th little-endian
@@ -238,74 +195,6 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
-__device__ __forceinline__ uint64_t dg_any(const uint4& v, uint64_t word) { return dg_vec(v, word); }
-__device__ __forceinline__ uint64_t dg_any(const v8u32& v, uint64_t word) {
-  return dg_vec(v.lo, word) + dg_vec(v.hi, word + 2);
-}
-
-// Copy [beg, end) of src into dst with one warp using V-byte vectors (src, dst
-// and beg are 16-byte aligned; V = 32 also needs 32-byte aligned src/dst).  All
-// loads of a batch are issued before its stores (U x V bytes per lane in
-// flight).  With `dig`, the lane also digests the words it moved (returned per
-// lane; lane 0 adds the unvectorised head/tail bytes).
-template <int U, int V>
-__device__ __forceinline__ uint64_t warp_copy_vec(const uint8_t* __restrict__ src,
-                                                  uint8_t* __restrict__ dst, int64_t beg, int64_t end,
-                                                  bool dig, int lane, uint64_t ld_pol, uint64_t st_pol) {
-  using IO = VecIO<V>;
-  using T = typename IO::T;
-  uint64_t acc = 0;
-  const int64_t vbeg = (beg + V - 1) & ~int64_t{V - 1};
-  const int64_t vend = end & ~int64_t{V - 1};
-  if (vbeg < vend) {
-    const int64_t nv = (vend - vbeg) / V;
-    const uint64_t w0 = (uint64_t)(vbeg >> 3);
-    for (int64_t base = 0; base < nv; base += 32 * U) {
-      T r[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int64_t i = base + k * 32 + lane;
-        if (i < nv) r[k] = IO::ld(src + vbeg + i * V, ld_pol);
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int64_t i = base + k * 32 + lane;
-        if (i < nv) IO::st(dst + vbeg + i * V, r[k], st_pol);
-      }
-      if (dig) {
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) acc += dg_any(r[k], w0 + (uint64_t)i * (V / 8));
-        }
-      }
-    }
-    for (int64_t i = beg + lane; i < vbeg; i += 32) dst[i] = src[i];
-    for (int64_t i = vend + lane; i < end; i += 32) dst[i] = src[i];
-    if (dig && lane == 0) {
-      if (beg < vbeg) acc += dg_bytes(src, beg, vbeg);
-      if (vend < end) acc += dg_bytes(src, vend, end);
-    }
-    return acc;
-  }
-  for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
-  if (dig && lane == 0) acc += dg_bytes(src, beg, end);  // unit smaller than a vector
-  return acc;
-}
-
-// `vec`: 0 = byte path (unaligned; the runtime digests the source
-// separately), otherwise the kernel's vector width V (16 or 32; the runtime
-// launches the V = 32 instance only when every transfer allows it).
-template <int U, int V>
-__device__ __forceinline__ uint64_t warp_copy_range(const uint8_t* __restrict__ src,
-                                                    uint8_t* __restrict__ dst, int64_t beg,
-                                                    int64_t end, int vec, bool dig, int lane,
-                                                    uint64_t ld_pol, uint64_t st_pol) {
-  if (vec) return warp_copy_vec<U, V>(src, dst, beg, end, dig, lane, ld_pol, st_pol);
-  for (int64_t i = beg + lane; i < end; i += 32) dst[i] = src[i];
-  return 0;
-}
-
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bool sys) {
   uint32_t old;
   if (sys)
@@ -315,94 +204,84 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v, bo
   return old;
 }
 
-// Work unit u (kFwdUnitBytes, one warp) covers slice s of chunk c; units are
-// chunk-major so chunks complete roughly in order and a consumer can start on
-// chunk 0 while later chunks are still in flight.  Warps stream independently
-// (no CTA barrier): after its unit a warp counts itself into the chunk counter
-// with an acq_rel atomic (release covers the warp's stores via __syncwarp; gpu
-// scope for a local slab, system scope when the slab is peer memory), and the
-// warp that completes the chunk fences at system scope and publishes the token
-// to the consumer-device flag and the host-mapped flag.
-template <int U, int MINB, int V>
-__global__ void __launch_bounds__(kFwdThreads, MINB) forward_kernel(const __grid_constant__ FwdBatch b) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kFwdThreads / 32);
-  const int64_t total = b.unit_off[b.n];
-  // The producer's source is read once (evict first); slab writes may be
-  // kept in L2 for a consumer that merges right after on this GPU.
-  const uint64_t ld_pol = l2_policy(1);
-  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
-  int i = 0;  // transfer of the current unit; units only grow per warp
-  for (int64_t gu = (int64_t)blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5); gu < total;
-       gu += warps) {
-    while (gu >= b.unit_off[i + 1]) ++i;
-    const FwdArgs& a = b.t[i];
-    const int64_t u = gu - b.unit_off[i];
-    const int64_t c = u / a.chunk_units;
-    const int64_t s = u - c * a.chunk_units;
-    const int64_t cbeg = c * a.chunk_bytes;
-    const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
-    const int64_t beg = cbeg + s * a.slice;
-    const int64_t end = min(beg + a.slice, cend);
-    const bool dig = a.digest != nullptr;
-    uint64_t acc = warp_copy_range<U, V>(a.src, a.dst, beg, end, a.vec, dig, lane, ld_pol, st_pol);
-    if (dig) {  // fused dg64: one atomic per unit, ordered before the counter release
-      acc = warp_sum_u64(acc);
-      if (lane == 0) {
-        if (u == 0) acc += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
-        atomicAdd(reinterpret_cast<unsigned long long*>(a.digest), (unsigned long long)acc);
-      }
-    }
-    __syncwarp();
-    if (a.counters == nullptr) continue;  // diagnostic only: no completion tracking
-    if (lane == 0) {
-      const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
-      const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
-      if (prev == units - 1) {
-        a.counters[c] = 0u;  // slot is clean for the next transfer that draws it
-        if (a.peer) {
-          // data sits in peer memory: publish at system scope
-          __threadfence_system();
-          st_release_sys(&a.dflags[c], a.token);
-          if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
-        } else {
-          // data sits in this GPU's memory: every counted warp released at gpu
-          // scope and the acq_rel bump acquired them, so a gpu-scope release
-          // publishes the chunk to device consumers; the host mirror is a
-          // posted store issued only after every unit of the chunk is in L2.
-          st_release_gpu(&a.dflags[c], a.token);
-          if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
-        }
-      }
-    }
+// ---------------------------------------------------------------------------
+// Chunk completion protocol (K1 and the tee kernel)
+//
+// A chunk is done when every piece of it (K1 tile, tee row) is stored.  The
+// thread that finished a piece -- after a CTA barrier (register stores) or a
+// bulk-group wait + proxy fence (bulk stores) has ordered the piece's stores
+// before it -- adds the piece count to the chunk's counter with an acq_rel
+// atomic; the arrival that completes the chunk resets the counter (the slot
+// is clean for the next transfer that draws it) and publishes the token:
+//   local slab     count at gpu scope, flag st.release.gpu (the counted
+//                  pieces' stores happen-before it through the atomics);
+//   peer slab,     count at system scope (every piece's stores are made
+//   sys counting   visible at system scope by its own release), flag after
+//                  fence.sc.sys with st.release.sys;
+//   peer slab,     count at gpu scope (cheaper per piece: no system-scope
+//   gpu counting   release per tile), and the completing thread makes every
+//                  counted piece visible to the consumer GPU with one
+//                  fence.sc.sys (cumulative over what its acquire observed)
+//                  before st.release.sys of the flag (FSX_FWD_PEER_GPU_COUNT).
+// The host mirror (hflags) is a posted store after the device flag.
+__device__ __forceinline__ void complete_pieces(uint32_t* counter, uint32_t add, uint32_t need,
+                                                bool peer, bool gpu_count, uint64_t* dflag,
+                                                uint64_t* hflag, uint64_t token) {
+  const uint32_t prev = atom_add_acq_rel(counter, add, peer && !gpu_count);
+  if (prev + add != need) return;
+  *counter = 0u;
+  if (peer) {
+    fence_sc_sys();
+    st_release_sys(dflag, token);
+  } else {
+    st_release_gpu(dflag, token);
   }
+  if (hflag) st_relaxed_sys(hflag, token);
 }
 
-// K1, tile form (default).  One CTA per tile of kTileThreads x U x 16 B, no
-// persistence: the hardware CTA scheduler hands tiles to SMs as earlier ones
-// retire, which on B200 sustains ~6.7 TB/s for a plain copy where a persistent
-// grid-stride loop tops out near 5.9-6.3 (scripts/probe_sm_copy.cu).  Tiles are
-// chunk-major in blockIdx order, so chunks complete roughly in order.  After
-// its loads and stores the CTA barriers, and one thread counts the tile into
-// the chunk counter with an acq_rel atomic (bar.sync makes every thread's
-// stores part of that release; gpu scope for a local slab, system scope for
-// peer memory); the CTA that completes the chunk publishes the token.
-constexpr int kTileThreads = 256;
+__device__ __forceinline__ void count_tile(const FwdArgs& a, int64_t c, bool gpu_count) {
+  const uint32_t need = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
+  complete_pieces(&a.counters[c], 1u, need, a.peer != 0, gpu_count, &a.dflags[c],
+                  a.hflags ? &a.hflags[c] : nullptr, a.token);
+}
 
-template <int U>
+// Tile gt of a forward batch: its transfer and byte range.
+struct TileRef {
+  int i;          // transfer
+  int64_t u;      // unit within the transfer
+  int64_t c;      // chunk
+  int64_t beg, end;
+};
+
+__device__ __forceinline__ TileRef tile_of(const FwdBatch& b, int64_t gt) {
+  TileRef t;
+  t.i = 0;
+  while (gt >= b.unit_off[t.i + 1]) ++t.i;
+  const FwdArgs& a = b.t[t.i];
+  t.u = gt - b.unit_off[t.i];
+  t.c = t.u / a.chunk_units;
+  const int64_t s = t.u - t.c * a.chunk_units;
+  const int64_t cbeg = t.c * a.chunk_bytes;
+  const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
+  t.beg = cbeg + s * a.slice;
+  t.end = min(t.beg + a.slice, cend);
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// K1, register tile form.  One CTA per 32 KiB tile, no persistence: the
+// hardware CTA scheduler hands tiles to SMs as earlier ones retire, which on
+// B200 sustains ~6.7 TB/s for a plain copy where a persistent grid-stride loop
+// tops out near 5.9-6.3 (scripts/probe_sm_copy.cu).  Tiles are chunk-major in
+// blockIdx order, so chunks complete roughly in order.  Each thread issues its
+// 8 x 16 B loads (the producer's source is read once: L2 evict_first), then
+// its stores; the CTA barriers and thread 0 counts the tile (protocol above).
+// Optional fused dg64 of the source bytes (one atomic per tile).
 __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid_constant__ FwdBatch b) {
   __shared__ uint64_t red[kTileThreads / 32];
-  const int64_t gt = blockIdx.x;
-  int i = 0;
-  while (gt >= b.unit_off[i + 1]) ++i;
-  const FwdArgs& a = b.t[i];
-  const int64_t u = gt - b.unit_off[i];
-  const int64_t c = u / a.chunk_units;
-  const int64_t s = u - c * a.chunk_units;
-  const int64_t cbeg = c * a.chunk_bytes;
-  const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
-  const int64_t beg = cbeg + s * a.slice;
-  const int64_t end = min(beg + a.slice, cend);
+  const TileRef tr = tile_of(b, blockIdx.x);
+  const FwdArgs& a = b.t[tr.i];
+  const int64_t beg = tr.beg, end = tr.end;
   const uint64_t ld_pol = l2_policy(1);
   const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
   const bool dig = a.digest != nullptr;
@@ -411,20 +290,20 @@ __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid
     // beg is 16-byte aligned (slices and chunks are multiples of 16)
     const int64_t vend = end & ~int64_t{15};
     const int64_t nv = (vend - beg) >> 4;
-    uint4 r[U];
+    uint4 r[kTileVecs];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
+    for (int k = 0; k < kTileVecs; ++k) {
       const int64_t v = k * kTileThreads + threadIdx.x;
       if (v < nv) r[k] = ld_nc_v4_pol(a.src + beg + v * 16, ld_pol);
     }
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
+    for (int k = 0; k < kTileVecs; ++k) {
       const int64_t v = k * kTileThreads + threadIdx.x;
       if (v < nv) st_v4_pol(a.dst + beg + v * 16, r[k], st_pol);
     }
     if (dig) {
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
+      for (int k = 0; k < kTileVecs; ++k) {
         const int64_t v = k * kTileThreads + threadIdx.x;
         if (v < nv) acc += dg_vec(r[k], (uint64_t)((beg >> 3) + 2 * v));
       }
@@ -439,25 +318,119 @@ __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   }
   __syncthreads();
-  if (threadIdx.x != 0 || a.counters == nullptr) return;
+  if (threadIdx.x != 0) return;
   if (dig) {
     uint64_t t = 0;
     for (int w = 0; w < kTileThreads / 32; ++w) t += red[w];
-    if (u == 0) t += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
+    if (tr.u == 0) t += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
     atomicAdd(reinterpret_cast<unsigned long long*>(a.digest), (unsigned long long)t);
   }
-  const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
-  const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
-  if (prev == units - 1) {
-    a.counters[c] = 0u;
-    if (a.peer) {
-      __threadfence_system();
-      st_release_sys(&a.dflags[c], a.token);
-    } else {
-      st_release_gpu(&a.dflags[c], a.token);
-    }
-    if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
+  count_tile(a, tr.c, b.peer_gpu_count != 0);
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA engine) helpers
+
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "FSX_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra FSX_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// bulk store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_store_hint(void* dst, uint32_t src_smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(src_smem), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+// bulk load with an L2 eviction-priority policy
+__device__ __forceinline__ void bulk_load_hint(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+}  // namespace tma
+
+// K1, bulk-copy tile form (FSX_FWD_BULK).  One 32-thread CTA per 32 KiB tile,
+// one elected thread: the tile's two 16 KiB halves are loaded global->shared by
+// the copy engine (mbarrier complete_tx), each half is stored shared->global
+// (cp.async.bulk, to this GPU's slab or to a peer's over NVLink) as soon as it
+// has landed; then the thread waits for the stores to complete, orders them
+// (async proxy) before its generic acq_rel count, and the tile is counted like
+// the register form.  Bytes in flight cost shared memory, not registers.
+__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b) {
+  extern __shared__ __align__(128) uint8_t tile_mem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x != 0) return;
+  const TileRef tr = tile_of(b, blockIdx.x);
+  const FwdArgs& a = b.t[tr.i];
+  const int64_t beg = tr.beg, end = tr.end;
+  const int64_t vend = beg + ((end - beg) & ~int64_t{15});  // beg is 16-byte aligned
+  const uint32_t sbase = tma::smem_u32(tile_mem);
+  const int64_t half = ((vend - beg) / 2 + 15) & ~int64_t{15};
+  const int64_t len0 = min(half, vend - beg), len1 = (vend - beg) - len0;
+  tma::mbar_init(tma::smem_u32(&bars[0]), 1);
+  tma::mbar_init(tma::smem_u32(&bars[1]), 1);
+  tma::mbar_fence_init();
+  const uint64_t ld_pol = l2_policy(1);
+  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
+  if (len0 > 0) {
+    tma::mbar_expect_tx(tma::smem_u32(&bars[0]), (uint32_t)len0);
+    tma::bulk_load_hint(sbase, a.src + beg, (uint32_t)len0, tma::smem_u32(&bars[0]), ld_pol);
   }
+  if (len1 > 0) {
+    tma::mbar_expect_tx(tma::smem_u32(&bars[1]), (uint32_t)len1);
+    tma::bulk_load_hint(sbase + (uint32_t)len0, a.src + beg + len0, (uint32_t)len1, tma::smem_u32(&bars[1]),
+                        ld_pol);
+  }
+  if (len0 > 0) {
+    tma::mbar_wait(tma::smem_u32(&bars[0]), 0);
+    tma::bulk_store_hint(a.dst + beg, sbase, (uint32_t)len0, st_pol);
+  }
+  if (len1 > 0) {
+    tma::mbar_wait(tma::smem_u32(&bars[1]), 0);
+    tma::bulk_store_hint(a.dst + beg + len0, sbase + (uint32_t)len0, (uint32_t)len1, st_pol);
+  }
+  tma::bulk_commit();
+  for (int64_t j = vend; j < end; ++j) a.dst[j] = a.src[j];  // sub-16-byte tail
+  tma::bulk_wait_all();
+  // the tile's bulk stores are complete: order them (async proxy) before the
+  // generic release that counts the tile
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  count_tile(a, tr.c, b.peer_gpu_count != 0);
 }
 
 // Stand-alone dg64 of n device bytes, accumulated into *out (zeroed by the
@@ -613,215 +586,198 @@ __device__ __forceinline__ int64_t upper_index(const int64_t* off, int64_t n, in
   return lo;
 }
 
-// K3 merge, phase 2: one warp per placeholder row.  Lane 0 resolves the row's
-// item (binary search over item row offsets) and request, then the warp moves
-// the row as 16-byte vectors, all loads of a batch issued before its stores.
+// Item and request of placeholder row g (zero-row items sharing an offset
+// are skipped).
+__device__ __forceinline__ void row_owner(const fsx_merge_batch& b, int64_t g, int64_t* item, int64_t* req) {
+  int64_t it = upper_index(b.d_item_row_off, b.num_items + 1, g);
+  while (b.d_item_row_off[it + 1] <= g) ++it;
+  int64_t rq = upper_index(b.d_req_item_off, b.num_requests + 1, it);
+  while (b.d_req_item_off[rq + 1] <= it) ++rq;
+  *item = it;
+  *req = rq;
+}
+
+// Store of one 16-byte vector with an optional L2 policy (pol < 0: plain).
+__device__ __forceinline__ void st_v4_maybe_pol(void* p, const uint4& v, int pol, uint64_t policy) {
+  if (pol < 0) st_v4(p, v);
+  else st_v4_pol(p, v, policy);
+}
+
+// One row moved by one warp: all loads of a batch of the row in flight before
+// its stores; `dst2` (optional) receives the same bytes (the tee kernel's slab
+// segment).  pol / pol2: L2 policy of each destination's stores (-1 plain,
+// else l2_policy's index).  Byte path when a row is not 16-byte aligned.
+template <int U = kMergeUnroll>
+__device__ __forceinline__ void warp_move_row(const uint8_t* src, uint8_t* dst, uint8_t* dst2, int64_t rb,
+                                              int lane, bool coherent, int pol, int pol2) {
+  const bool vec = ((rb & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                     reinterpret_cast<uintptr_t>(dst2)) & 15) == 0;
+  if (!vec) {
+    for (int64_t i = lane; i < rb; i += 32) {
+      const uint8_t v = src[i];
+      if (dst) dst[i] = v;
+      if (dst2) dst2[i] = v;
+    }
+    return;
+  }
+  const uint64_t policy = pol >= 0 ? l2_policy(pol) : 0;
+  const uint64_t policy2 = pol2 >= 0 ? l2_policy(pol2) : 0;
+  const int64_t nv = rb >> 4;
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  for (int64_t base = 0; base < nv; base += 32 * U) {
+    uint4 r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = base + k * 32 + lane;
+      if (i < nv) r[k] = coherent ? ld_v4(s + i) : ld_nc_v4(s + i);
+    }
+    if (dst) {
+      uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + k * 32 + lane;
+        if (i < nv) st_v4_maybe_pol(d + i, r[k], pol, policy);
+      }
+    }
+    if (dst2) {
+      uint4* d = reinterpret_cast<uint4*>(dst2);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t i = base + k * 32 + lane;
+        if (i < nv) st_v4_maybe_pol(d + i, r[k], pol2, policy2);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void discard_row(const uint8_t* src, int64_t rb, int lane) {
+  // drop a merged slab row's lines from L2 without writing them back (whole
+  // 128-byte lines only): the segment is dead until it is released
+  const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
+  for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
+
+// K3 merge, phase 2, stream-ordered: one warp per placeholder row over a full
+// (non-persistent) grid, 8 rows per CTA.  Lane 0 resolves the row's item and
+// request (binary searches over the row offsets), then the warp moves the row.
 __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_batch b) {
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
+  const int64_t g = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+  if (g >= b.total_item_rows) return;
+  int64_t item = 0, req = 0;
+  if (lane == 0) row_owner(b, g, &item, &req);
+  item = __shfl_sync(0xffffffffu, item, 0);
+  req = __shfl_sync(0xffffffffu, req, 0);
+  if (b.d_status[req] != 0) return;  // validation failed: request untouched
   const int64_t rb = b.row_bytes;
-  const bool vec_rows = (rb & 15) == 0;
-  // newest rows first (meant for L2 reuse of K1's tail; measured no effect on
-  // B200, DESIGN.md §3 -- kept, it costs nothing)
-  const bool newest_first = b.d_item_flag == nullptr;
-  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  for (int64_t k = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
-       k < b.total_item_rows; k += warps) {
-    const int64_t g = newest_first ? b.total_item_rows - 1 - k : k;
+  const int64_t j = g - b.d_item_row_off[item];
+  const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
+  uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * rb;
+  warp_move_row(src, dst, nullptr, rb, lane, /*coherent=*/true, -1, -1);
+  if (b.mode & FSX_MERGE_DISCARD) discard_row(src, rb, lane);
+}
+
+// K1 + K3 as one kernel (fsx_forward_merge): the tee.  Same grid as
+// merge_copy_kernel over the placeholder rows of items [i0, i0 + n); each warp
+// reads its item row ONCE from the producer's buffer and stores it twice --
+// into the item's slab segment (the forward) and into its placeholder row
+// (the merge; skipped for a request that failed validation, the forward still
+// happens).  Chunk completion: the CTA barriers, then thread 0 walks its 8
+// rows, groups consecutive rows of the same (item, chunk) and counts each
+// group into that chunk's counter in rows (protocol above); zero-row items
+// have their single flag published by CTA 0.
+// Three CTAs per SM with 8 x 16 B in flight per lane (77 registers): 0.2196 ms
+// per config-B pass against 0.240 for two CTAs per SM at 16 x 16 B, 0.222-0.226
+// at 4 CTAs per SM (profiles/tee_variants_r02.txt).
+constexpr int kTeeMinBlocks = 3;
+constexpr int kTeeUnroll = 8;
+__global__ void __launch_bounds__(kMergeThreads, kTeeMinBlocks) merge_tee_kernel(fsx_merge_batch b,
+                                                                  const __grid_constant__ TeeBatch tb) {
+  __shared__ int32_t s_item[kMergeWarps];
+  __shared__ int64_t s_chunk[kMergeWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t g = tb.g0 + (int64_t)blockIdx.x * kMergeWarps + warp;
+  int32_t key_item = -1;
+  int64_t key_chunk = 0;
+  if (g < tb.g1) {
     int64_t item = 0, req = 0;
-    if (lane == 0) {
-      item = upper_index(b.d_item_row_off, b.num_items + 1, g);
-      // skip zero-row items sharing the same offset
-      while (b.d_item_row_off[item + 1] <= g) ++item;
-      req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-      while (b.d_req_item_off[req + 1] <= item) ++req;
-    }
+    if (lane == 0) row_owner(b, g, &item, &req);
     item = __shfl_sync(0xffffffffu, item, 0);
     req = __shfl_sync(0xffffffffu, req, 0);
-    if (b.d_status[req] != 0) continue;  // validation failed: request untouched
+    const TeeItem& t = tb.t[item - tb.i0];
+    const int64_t rb = b.row_bytes;
     const int64_t j = g - b.d_item_row_off[item];
-    if (b.d_item_flag) {
-      if (lane == 0) {
-        const int64_t cr = b.d_item_chunk_rows[item];
-        spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
-      }
-      __syncwarp();
-    }
     const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
-    const int64_t t = b.d_req_row_off[req] + b.d_scratch[g];
-    uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + t * rb;
-    if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-      const int64_t nv = rb >> 4;
-      const uint4* s = reinterpret_cast<const uint4*>(src);
-      uint4* d = reinterpret_cast<uint4*>(dst);
-      for (int64_t base = 0; base < nv; base += 32 * kMergeUnroll) {
-        uint4 r[kMergeUnroll];
-#pragma unroll
-        for (int k = 0; k < kMergeUnroll; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) r[k] = ld_v4(s + i);
-        }
-#pragma unroll
-        for (int k = 0; k < kMergeUnroll; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4(d + i, r[k]);
-        }
-      }
-    } else {
-      for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
-    }
-    if (discard) {
-      // the row's values are in registers and stored: drop its slab lines
-      // from L2 without writing them back (whole 128-byte lines only)
-      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
-      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
-      for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-    }
+    uint8_t* dst = b.d_status[req] == 0
+                       ? static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * rb
+                       : nullptr;
+    // the prompt row is plain-stored; the slab copy keeps L2 priority when a
+    // consumer on this GPU reads it next (FSX_FWD_L2_KEEP)
+    warp_move_row<kTeeUnroll>(src, dst, t.dst + j * rb, rb, lane, /*coherent=*/false, -1, tb.l2_keep_dst ? 2 : -1);
+    key_item = (int32_t)(item - tb.i0);
+    key_chunk = j / t.chunk_rows;
   }
-}
-
-// K3 merge, phase 2, early-start form: rows are taken in arrival order in runs
-// of kStreamRun consecutive placeholder rows per warp.  The warp resolves the
-// run's first row once (binary searches), prefetches the run's placeholder
-// positions with one coalesced load (one lane per row), and walks the rows
-// keeping item- and request-level values in registers, re-reading them only
-// when the run crosses into the next item or request, and spinning on a chunk
-// flag only when the run enters a new chunk.  A persistent grid of these warps
-// follows the producer's K1 chunk by chunk with far less per-row latency than
-// resolving every row from scratch (merge_copy_kernel).
-constexpr int kStreamRun = 16;
-__global__ void __launch_bounds__(kMergeThreads) merge_stream_kernel(fsx_merge_batch b,
-                                                                     unsigned long long* work) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kMergeThreads / 32);
-  const int64_t rb = b.row_bytes;
-  const int64_t n = b.total_item_rows;
-  const int64_t runs = (n + kStreamRun - 1) / kStreamRun;
-  const bool vec_rows = (rb & 15) == 0;
-  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool early = b.d_item_flag != nullptr;
-  // runs are claimed from the work counter in arrival order (every warp works
-  // on the earliest rows whose chunk has landed), or statically without one
-  auto claim = [&](int64_t prev) -> int64_t {
-    if (!work) return prev < 0 ? (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5) : prev + warps;
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(work, 1ull);
-    return (int64_t)__shfl_sync(0xffffffffu, u, 0);
-  };
-  for (int64_t u = claim(-1); u < runs; u = claim(u)) {
-    const int64_t g0 = u * kStreamRun;
-    const int64_t g1 = min(g0 + kStreamRun, n);
-    const int32_t mypos = (g0 + lane < g1) ? b.d_scratch[g0 + lane] : 0;
-    // every lane runs the same (uniform) resolution: same addresses, broadcast loads
-    int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g0);
-    while (b.d_item_row_off[item + 1] <= g0) ++item;
-    int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-    while (b.d_req_item_off[req + 1] <= item) ++req;
-    int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
-    const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-    int64_t req_row = b.d_req_row_off[req];
-    int32_t req_ok = b.d_status[req] == 0;
-    int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
-    int64_t waited = -1;  // chunk of the current item already waited for
-    for (int64_t g = g0; g < g1; ++g) {
-      if (g >= item_end) {  // next item (skipping zero-row items), maybe next request
-        do {
-          ++item;
-        } while (b.d_item_row_off[item + 1] <= g);
-        item_beg = b.d_item_row_off[item];
-        item_end = b.d_item_row_off[item + 1];
-        item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-        if (b.d_req_item_off[req + 1] <= item) {
-          do {
-            ++req;
-          } while (b.d_req_item_off[req + 1] <= item);
-          req_row = b.d_req_row_off[req];
-          req_ok = b.d_status[req] == 0;
-        }
-        if (early) chunk_rows = b.d_item_chunk_rows[item];
-        waited = -1;
-      }
-      const int32_t pos = __shfl_sync(0xffffffffu, mypos, (int)(g - g0));
-      if (!req_ok) continue;  // validation failed: request untouched
-      const int64_t j = g - item_beg;
-      if (early) {
-        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
-        if (c != waited) {
-          if (lane == 0) spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
-          __syncwarp();
-          waited = c;
-        }
-      }
-      const uint8_t* src = item_src + j * rb;
-      uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb;
-      if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-        const int64_t nv = rb >> 4;
-        const uint4* sv = reinterpret_cast<const uint4*>(src);
-        uint4* dv = reinterpret_cast<uint4*>(dst);
-        for (int64_t base = 0; base < nv; base += 32 * kMergeUnroll) {
-          uint4 r[kMergeUnroll];
-#pragma unroll
-          for (int k = 0; k < kMergeUnroll; ++k) {
-            const int64_t i = base + k * 32 + lane;
-            if (i < nv) r[k] = ld_v4(sv + i);
-          }
-#pragma unroll
-          for (int k = 0; k < kMergeUnroll; ++k) {
-            const int64_t i = base + k * 32 + lane;
-            if (i < nv) st_v4(dv + i, r[k]);
-          }
-        }
+  if (lane == 0) {
+    s_item[warp] = key_item;
+    s_chunk[warp] = key_chunk;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 0; w < kMergeWarps;) {
+    const int32_t it = s_item[w];
+    if (it < 0) break;  // rows past g1 are at the end of the CTA
+    const int64_t c = s_chunk[w];
+    int run = 1;
+    while (w + run < kMergeWarps && s_item[w + run] == it && s_chunk[w + run] == c) ++run;
+    const TeeItem& t = tb.t[it];
+    const uint32_t need = (uint32_t)min(t.chunk_rows, t.rows - c * t.chunk_rows);
+    complete_pieces(&t.counters[c], (uint32_t)run, need, t.peer != 0, tb.peer_gpu_count != 0, &t.dflags[c],
+                    t.hflags ? &t.hflags[c] : nullptr, t.token);
+    w += run;
+  }
+  if (blockIdx.x == 0) {
+    for (int k = 0; k < tb.n; ++k) {
+      const TeeItem& t = tb.t[k];
+      if (t.rows != 0) continue;
+      if (t.peer) {
+        fence_sc_sys();
+        st_release_sys(t.dflags, t.token);
       } else {
-        for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
+        st_release_gpu(t.dflags, t.token);
       }
-      if (discard) {
-        const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
-        const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
-        for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-      }
+      if (t.hflags) st_relaxed_sys(t.hflags, t.token);
     }
   }
 }
 
-// K3 merge, phase 2, "follow" form for early start: warp w of W moves the
-// placeholder rows g = w, w + W, w + 2W, ... in increasing order, so at any
-// moment the whole grid works on a window of about W rows right behind the
-// producer (one chunk's worth for W ~ chunk rows) instead of some warps
-// holding runs many chunks ahead.  Behind K1 on the same GPU that window is
-// still in L2 when it is read, and with FSX_MERGE_DISCARD its lines are
-// dropped from L2 right after, so the slab never round-trips through HBM.
-// Item / request values are re-read only when the warp's row crosses into the
-// next item; the row's chunk flag is checked (lane 0, acquire) before its
-// loads; the position comes from the scan's scratch.
-template <int U>
+// K3 merge, phase 2, early start ("follow" form): the batch carries item chunk
+// flags, set by a producer still running (K1 on a peer GPU writing into this
+// GPU's slab over NVLink, or on this GPU for the colocated pass).  Warp w of W
+// moves the placeholder rows g = w, w + W, w + 2W, ... in increasing order, so
+// the whole grid works on a window of about W rows right behind the producer
+// instead of some warps holding rows many chunks ahead.  Item / request values
+// are re-read only when the warp's row crosses into the next item; lane 0
+// acquires the row's chunk flag (once per chunk) before the warp loads it.
+// FSX_MERGE_COLOCATED (producer on this GPU): gpu-scope acquires, and the
+// launcher caps the grid at one CTA per SM so spinning merge warps never take
+// every slot K1 needs.  FSX_MERGE_DISCARD drops merged slab lines from L2.
 __global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merge_batch b) {
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * (kMergeThreads / 32);
-  const int64_t w = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
+  const int64_t W = (int64_t)gridDim.x * kMergeWarps;
+  const int64_t w = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
   const int64_t rb = b.row_bytes;
   const int64_t n = b.total_item_rows;
   if (w >= n) return;
-  const bool vec_rows = (rb & 15) == 0;
   const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool early = b.d_item_flag != nullptr;
-  // the producer's K1 runs on this GPU: a gpu-scope acquire pairs with its
-  // gpu-scope release; across GPUs the wait is system scope
-#ifndef FSX_COLOCATED_GPU_SCOPE
-#define FSX_COLOCATED_GPU_SCOPE 1
-#endif
-  const bool colocated = FSX_COLOCATED_GPU_SCOPE && (b.mode & FSX_MERGE_COLOCATED) != 0;
-  // the prompt rows are written once and not re-read here: evict them from L2
-  // first, so they do not push out slab rows K1 has just written
-  const uint64_t out_pol = l2_policy(kFollowOutPolicy);
-  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, w);
-  while (b.d_item_row_off[item + 1] <= w) ++item;
-  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-  while (b.d_req_item_off[req + 1] <= item) ++req;
+  const bool colocated = (b.mode & FSX_MERGE_COLOCATED) != 0;
+  int64_t item = 0, req = 0;
+  row_owner(b, w, &item, &req);
   int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
   const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
+  int64_t chunk_rows = b.d_item_chunk_rows[item];
   int64_t req_row = b.d_req_row_off[req];
   bool req_ok = b.d_status[req] == 0;
   int64_t waited = -1;
@@ -833,7 +789,7 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merg
       item_beg = b.d_item_row_off[item];
       item_end = b.d_item_row_off[item + 1];
       item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-      if (early) chunk_rows = b.d_item_chunk_rows[item];
+      chunk_rows = b.d_item_chunk_rows[item];
       waited = -1;
       if (b.d_req_item_off[req + 1] <= item) {
         do {
@@ -846,177 +802,21 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merg
     if (!req_ok) continue;  // validation failed: request untouched
     const int64_t j = g - item_beg;
     const int32_t pos = b.d_scratch[g];
-    if (early) {
-      const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
-      if (c != waited) {
-        if (lane == 0) {
-          if (colocated) spin_until_gpu(b.d_item_flag[item] + c, b.d_item_token[item]);
-          else spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
-        }
-        __syncwarp();
-        waited = c;
-      }
-    }
-    const uint8_t* src = item_src + j * rb;
-    uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb;
-    if (vec_rows && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-      const int64_t nv = rb >> 4;
-      const uint4* sv = reinterpret_cast<const uint4*>(src);
-      uint4* dv = reinterpret_cast<uint4*>(dst);
-      for (int64_t base = 0; base < nv; base += 32 * U) {
-        uint4 r[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) r[k] = ld_v4(sv + i);
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
-        }
-      }
-    } else {
-      for (int64_t i = lane; i < rb; i += 32) dst[i] = src[i];
-    }
-    if (discard) {
-      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127) & ~uintptr_t{127};
-      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + rb) & ~uintptr_t{127};
-      for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-    }
-  }
-}
-
-// Follow kernel, software-pipelined (FSX_MERGE_STREAM=4): the same row order
-// as merge_follow_kernel, but while a row's loads are in flight the warp
-// already resolves its next row (placeholder position, source view) and lane 0
-// issues that row's chunk-flag acquire, so the flag and position latencies
-// overlap the data instead of preceding it.  lane 0's acquire plus the
-// __syncwarp before the next row's loads order them after the flag.
-struct FollowRow {
-  const uint8_t* src;
-  uint8_t* dst;
-  const uint64_t* flag;
-  uint64_t token;
-  bool valid, ok;
-};
-
-template <int U>
-__global__ void __launch_bounds__(kMergeThreads, 2) merge_follow2_kernel(fsx_merge_batch b) {
-  const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * (kMergeThreads / 32);
-  const int64_t w = (int64_t)blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5);
-  const int64_t rb = b.row_bytes;
-  const int64_t n = b.total_item_rows;
-  if (w >= n) return;
-  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool early = b.d_item_flag != nullptr;
-  const bool colocated = FSX_COLOCATED_GPU_SCOPE && (b.mode & FSX_MERGE_COLOCATED) != 0;
-  const bool vec_rows = (rb & 15) == 0;
-  const uint64_t out_pol = l2_policy(kFollowOutPolicy);
-  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, w);
-  while (b.d_item_row_off[item + 1] <= w) ++item;
-  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-  while (b.d_req_item_off[req + 1] <= item) ++req;
-  int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
-  const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
-  const uint64_t* item_flags = early ? b.d_item_flag[item] : nullptr;
-  uint64_t item_token = early ? b.d_item_token[item] : 0;
-  int64_t req_row = b.d_req_row_off[req];
-  bool req_ok = b.d_status[req] == 0;
-  auto resolve = [&](int64_t g, FollowRow& m) {
-    m.valid = g < n;
-    if (!m.valid) return;
-    if (g >= item_end) {
-      do {
-        ++item;
-      } while (b.d_item_row_off[item + 1] <= g);
-      item_beg = b.d_item_row_off[item];
-      item_end = b.d_item_row_off[item + 1];
-      item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-      if (early) {
-        chunk_rows = b.d_item_chunk_rows[item];
-        item_flags = b.d_item_flag[item];
-        item_token = b.d_item_token[item];
-      }
-      if (b.d_req_item_off[req + 1] <= item) {
-        do {
-          ++req;
-        } while (b.d_req_item_off[req + 1] <= item);
-        req_row = b.d_req_row_off[req];
-        req_ok = b.d_status[req] == 0;
-      }
-    }
-    m.ok = req_ok;
-    const int64_t j = g - item_beg;
-    m.src = item_src + j * rb;
-    m.dst = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[g]) * rb;
-    m.flag = early ? item_flags + (chunk_rows > 0 ? j / chunk_rows : 0) : nullptr;
-    m.token = item_token;
-  };
-  auto acquire = [&](const uint64_t* f) { return colocated ? ld_acquire_gpu(f) : ld_acquire_sys(f); };
-  FollowRow cur, nxt;
-  resolve(w, cur);
-  uint64_t seen = (early && lane == 0 && cur.ok) ? acquire(cur.flag) : 0;
-  for (int64_t g = w; cur.valid; g += W) {
-    if (early && cur.ok) {
-      if (lane == 0 && seen != cur.token) {  // not landed yet when prefetched: wait
-        const uint64_t t0 = globaltimer_ns();
-        uint32_t spins = 0;
-        while ((seen = acquire(cur.flag)) != cur.token) {
-          __nanosleep(64);
-          if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
-        }
+    const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
+    if (c != waited) {
+      if (lane == 0) {
+        if (colocated) spin_until_gpu(b.d_item_flag[item] + c, b.d_item_token[item]);
+        else spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
       }
       __syncwarp();
+      waited = c;
     }
-    const bool vec = vec_rows && ((reinterpret_cast<uintptr_t>(cur.src) | reinterpret_cast<uintptr_t>(cur.dst)) & 15) == 0;
-    const int64_t nv = vec ? rb >> 4 : 0;
-    const uint4* sv = reinterpret_cast<const uint4*>(cur.src);
-    uint4* dv = reinterpret_cast<uint4*>(cur.dst);
-    uint4 r[U];
-    if (cur.ok) {
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int64_t i = k * 32 + lane;
-        if (i < nv) r[k] = ld_v4(sv + i);
-      }
-    }
-    // the next row: position, view and flag acquire overlap this row's loads
-    resolve(g + W, nxt);
-    uint64_t nseen = 0;
-    if (early && lane == 0 && nxt.valid && nxt.ok) nseen = acquire(nxt.flag);
-    if (cur.ok) {
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int64_t i = k * 32 + lane;
-        if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
-      }
-      for (int64_t base = 32 * U; base < nv; base += 32 * U) {  // rows wider than one batch
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) r[k] = ld_v4(sv + i);
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int64_t i = base + k * 32 + lane;
-          if (i < nv) st_v4_pol(dv + i, r[k], out_pol);
-        }
-      }
-      if (!vec)
-        for (int64_t i = lane; i < rb; i += 32) cur.dst[i] = cur.src[i];
-      if (discard) {
-        const uintptr_t lo = (reinterpret_cast<uintptr_t>(cur.src) + 127) & ~uintptr_t{127};
-        const uintptr_t hi = (reinterpret_cast<uintptr_t>(cur.src) + rb) & ~uintptr_t{127};
-        for (uintptr_t a = lo + 128 * (uintptr_t)lane; a < hi; a += 128 * 32)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-      }
-    }
-    cur = nxt;
-    seen = nseen;
+    const uint8_t* src = item_src + j * rb;
+    // the prompt rows are written once and not re-read here: evict them from
+    // L2 first, so they do not push out slab rows the producer has just written
+    warp_move_row(src, static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb, nullptr, rb, lane,
+                  /*coherent=*/true, 1, -1);
+    if (discard) discard_row(src, rb, lane);
   }
 }
 
@@ -1043,135 +843,6 @@ __global__ void synth_kernel(uint64_t s0, uint8_t* __restrict__ dst, int64_t n) 
       for (int bt = 0; bt < 8 && w * 8 + bt < n; ++bt) dst[w * 8 + bt] = (uint8_t)(v >> (8 * bt));
     }
   }
-}
-
-}  // namespace kern
-
-using namespace kern;
-
-__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b);
-
-// ---------------------------------------------------------------------------
-// Launchers
-
-int forward_block_threads() { return kFwdThreads; }
-
-cudaError_t set_spin_timeout(uint64_t ns) {
-  return cudaMemcpyToSymbol(c_spin_timeout_ns, &ns, sizeof(ns));
-}
-int merge_copy_block_threads() { return kMergeThreads; }
-
-namespace {
-using FwdFn = void (*)(FwdBatch);
-// variant: 0 <16 x 16 B, 2 CTAs/SM>, 1 <8 x 16 B, 4 CTAs/SM>, 2 <8 x 16 B, 3 CTAs/SM>;
-// wide = 32-byte vectors with half the count (same bytes in flight).
-FwdFn forward_variant(int v, bool wide = false) {
-  switch (v) {
-    case 1: return wide ? forward_kernel<4, 4, 32> : forward_kernel<8, 4, 16>;
-    case 2: return wide ? forward_kernel<4, 3, 32> : forward_kernel<8, 3, 16>;
-    default: return wide ? forward_kernel<8, 2, 32> : forward_kernel<16, 2, 16>;
-  }
-}
-}  // namespace
-
-int forward_blocks_per_sm(int variant) {
-  int n = 0;
-  if (variant >= 3) variant = 2;  // tile kernels are not persistent: grid = tiles
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, forward_variant(variant), kFwdThreads, 0) !=
-      cudaSuccess)
-    return 1;
-  return n > 0 ? n : 1;
-}
-
-int merge_copy_blocks_per_sm() {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_copy_kernel, kMergeThreads, 0) !=
-      cudaSuccess)
-    return 1;
-  return n > 0 ? n : 1;
-}
-
-int forward_tile_bytes(int variant) {
-  if (variant == 5) return kTmaTileBytes;          // 32 KiB bulk-copy tiles
-  if (variant == 3) return kTileThreads * 4 * 16;  // 16 KiB tiles
-  if (variant == 4) return kTileThreads * 8 * 16;  // 32 KiB tiles
-  return 0;                                        // persistent warp kernels
-}
-
-cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s, bool share_sm) {
-  if (variant == 5) {
-    // bulk-copy tiles for local, 16-byte aligned transfers without a fused
-    // digest; anything else in the batch takes the register tile kernel
-    bool ok = true;
-    for (int k = 0; k < b.n; ++k) ok = ok && b.t[k].vec && !b.t[k].peer && !b.t[k].digest;
-    if (ok) {
-      const int64_t tiles = b.unit_off[b.n];
-      if (tiles <= 0) return cudaSuccess;
-      // FSX_FWD_BULK_SMEM pads the shared memory per CTA (bytes >= 32 KiB) to cap
-      // the resident K1 CTAs per SM, e.g. beside a concurrent merge
-      static const int smem = [] {
-        const char* e = std::getenv("FSX_FWD_BULK_SMEM");
-        const int v = e ? std::atoi(e) : kTmaTileBytes;
-        return v < kTmaTileBytes ? kTmaTileBytes : v;
-      }();
-      // the opt-in shared-memory limit is a per-device function attribute
-      static bool attr_set[kMaxDevices] = {};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (dev < kMaxDevices && !attr_set[dev]) {
-        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set[dev] = true;
-      }
-      forward_tma_kernel<<<(unsigned)tiles, 32, smem, s>>>(b);
-      return cudaGetLastError();
-    }
-    variant = 4;
-  }
-  if (forward_tile_bytes(variant)) {
-    // one CTA per tile: grid = total tiles of the batch (16-byte vectors)
-    FwdBatch bb = b;
-    for (int k = 0; k < bb.n; ++k)
-      if (bb.t[k].vec) bb.t[k].vec = 16;
-    const int64_t tiles = bb.unit_off[bb.n];
-    if (tiles <= 0) return cudaSuccess;
-    // share_sm: pad shared memory so at most two K1 CTAs fit per SM (the
-    // opt-in limit is a per-device function attribute)
-    static int pad[kMaxDevices] = {};
-    size_t smem = 0;
-    if (share_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (dev < kMaxDevices && pad[dev] == 0) {
-        int sm_smem = 0;
-        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-        pad[dev] = sm_smem / 2 - 8 * 1024;  // 2 x pad + reserved fits, 3 x pad does not
-        cudaFuncSetAttribute(forward_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad[dev]);
-        cudaFuncSetAttribute(forward_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad[dev]);
-      }
-      smem = dev < kMaxDevices ? (size_t)pad[dev] : 0;
-    }
-    if (variant == 3) forward_tile_kernel<4><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
-    else forward_tile_kernel<8><<<(unsigned)tiles, kTileThreads, smem, s>>>(bb);
-    return cudaGetLastError();
-  }
-  bool wide = true;  // every vectorised transfer allows 32-byte vectors
-  for (int k = 0; k < b.n; ++k) wide = wide && (b.t[k].vec == 32 || b.t[k].vec == 0);
-  FwdBatch bb = b;
-  if (!wide)
-    for (int k = 0; k < bb.n; ++k)
-      if (bb.t[k].vec == 32) bb.t[k].vec = 16;
-  forward_variant(variant, wide)<<<grid, kFwdThreads, 0, s>>>(bb);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s) {
-  set_flags_kernel<<<1, 32, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s) {
-  wait_flags_kernel<<<1, 32, 0, s>>>(dflags, n, token);
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -1248,462 +919,61 @@ __global__ void __launch_bounds__(32) chan_pull_kernel(const __grid_constant__ C
   if (lane == 0) st_release_sys(c.tail, seq + 1);  // slot free for the producer
 }
 
+}  // namespace kern
+
+using namespace kern;
+
 // ---------------------------------------------------------------------------
-// K3 merge, phase 2, TMA variant: rows staged through shared memory by the
-// bulk-copy engine (cp.async.bulk global->shared with mbarrier completion,
-// shared->global bulk_group stores).  One elected thread per CTA runs an
-// S-stage ring: loads run S-1 rows ahead, each row's store is committed as
-// its own bulk group, and a stage is refilled once `wait_group.read 1` says the
-// store that last used it has finished reading shared memory.  No register
-// staging, no per-lane address math: the copy engine moves the 7-8 KiB rows.
+// Launchers
 
-namespace tma {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+cudaError_t set_spin_timeout(uint64_t ns) {
+  return cudaMemcpyToSymbol(c_spin_timeout_ns, &ns, sizeof(ns));
 }
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+int merge_copy_blocks_per_sm() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_copy_kernel, kMergeThreads, 0) !=
+      cudaSuccess)
+    return 1;
+  return n > 0 ? n : 1;
 }
 
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
+int forward_tile_bytes() { return kTileThreads * kTileVecs * 16; }
 
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "FSX_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra FSX_WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes,
-                                          uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dst_smem),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(src_smem), "r"(bytes)
-               : "memory");
-}
-
-// bulk store with an L2 eviction-priority policy (createpolicy)
-__device__ __forceinline__ void bulk_store_hint(void* dst, uint32_t src_smem, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
-               "r"(src_smem), "r"(bytes), "l"(pol)
-               : "memory");
-}
-
-// bulk load with an L2 eviction-priority policy
-__device__ __forceinline__ void bulk_load_hint(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar,
-                                               uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          dst_smem),
-      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-}  // namespace tma
-
-struct RowRef {
-  const uint8_t* src;
-  uint8_t* dst;
-};
-
-// Resolve placeholder row g: source row in its item, destination prompt row;
-// src == nullptr when its request failed validation.
-__device__ __forceinline__ RowRef resolve_row(const fsx_merge_batch& b, int64_t g) {
-  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g);
-  while (b.d_item_row_off[item + 1] <= g) ++item;
-  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-  while (b.d_req_item_off[req + 1] <= item) ++req;
-  if (b.d_status[req] != 0) return RowRef{nullptr, nullptr};
-  const int64_t j = g - b.d_item_row_off[item];
-  if (b.d_item_flag) {
-    const int64_t cr = b.d_item_chunk_rows[item];
-    spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
-    // the row is read by the bulk-copy (async) proxy after a generic acquire
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-  const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * b.row_bytes;
-  uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * b.row_bytes;
-  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) {
-    for (int64_t i = 0; i < b.row_bytes; ++i) dst[i] = src[i];  // bulk copies need 16 B alignment
-    return RowRef{nullptr, nullptr};
-  }
-  return RowRef{src, dst};
-}
-
-template <int S>
-__global__ void __launch_bounds__(32) merge_copy_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];
-  __shared__ __align__(8) uint64_t bars[S];
-  if (threadIdx.x != 0) return;
-  const uint32_t sbase = tma::smem_u32(stage_mem);
-  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
-  tma::mbar_fence_init();
-  const uint32_t rb = (uint32_t)b.row_bytes;
-  const int64_t first = blockIdx.x, stride = gridDim.x, n = b.total_item_rows;
-  uint8_t* dst_of[S];
-  uint32_t parity = 0;  // bit s = phase parity expected next on stage s
-  // Newest rows first when the slab was filled before this launch (stream
-  // order): the tail of what K1 just wrote is still in the 126 MB L2, so
-  // walking the rows backwards turns part of the slab reads into L2 hits.
-  // With early start (flags) rows are taken in arrival order instead.
-  const bool newest_first = b.d_item_flag == nullptr;
-  auto issue = [&](int64_t k) {  // load this CTA's k-th row into stage k % S
-    const int s = (int)(k % S);
-    const int64_t idx = first + k * stride;
-    const RowRef r = resolve_row(b, newest_first ? n - 1 - idx : idx);
-    dst_of[s] = r.dst;
-    if (!r.src) return;
-    const uint32_t bar = tma::smem_u32(&bars[s]);
-    tma::mbar_expect_tx(bar, rb);
-    tma::bulk_load(sbase + s * stage_bytes, r.src, rb, bar);
-  };
-  for (int64_t k = 0; k < S - 1 && first + k * stride < n; ++k) issue(k);
-  for (int64_t k = 0; first + k * stride < n; ++k) {
-    const int s = (int)(k % S);
-    if (dst_of[s]) {
-      tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
-      parity ^= 1u << s;
-      tma::bulk_store(dst_of[s], sbase + s * stage_bytes, rb);
-    }
-    tma::bulk_commit();  // one group per row (possibly empty) keeps the count exact
-    tma::bulk_wait_read1();  // the store issued one row ago has left shared memory
-    if (first + (k + S - 1) * stride < n) issue(k + S - 1);
-  }
-  tma::bulk_wait_all();
-}
-
-constexpr int kTmaStages = 4;
-
-// K1, bulk-copy tile form (FSX_FWD_VARIANT=5; local slabs, no fused digest).
-// One 32-thread CTA per 32 KiB tile, one elected thread: two 16 KiB halves are
-// loaded global->shared by the copy engine (mbarrier complete_tx), each half
-// is stored shared->global as soon as it has landed, then the thread waits
-// for the stores, orders them (async proxy) before its generic acq_rel count
-// into the chunk counter, and the CTA completing the chunk publishes the flag
-// like forward_tile_kernel.  Bytes in flight cost shared memory, not
-// registers: 6 such CTAs per SM keep 192 KiB in flight with ~2 K registers,
-// which leaves the register file to a merge running next to K1.
-__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b) {
-  extern __shared__ __align__(128) uint8_t tile_mem[];
-  __shared__ __align__(8) uint64_t bars[2];
-  if (threadIdx.x != 0) return;
-  const int64_t gt = blockIdx.x;
-  int i = 0;
-  while (gt >= b.unit_off[i + 1]) ++i;
-  const FwdArgs& a = b.t[i];
-  const int64_t u = gt - b.unit_off[i];
-  const int64_t c = u / a.chunk_units;
-  const int64_t sl = u - c * a.chunk_units;
-  const int64_t cbeg = c * a.chunk_bytes;
-  const int64_t cend = min(cbeg + a.chunk_bytes, a.bytes);
-  const int64_t beg = cbeg + sl * a.slice;
-  const int64_t end = min(beg + a.slice, cend);
-  const int64_t vend = beg + ((end - beg) & ~int64_t{15});  // beg is 16-byte aligned
-  const uint32_t sbase = tma::smem_u32(tile_mem);
-  const int64_t half = ((vend - beg) / 2 + 15) & ~int64_t{15};
-  const int64_t len0 = min(half, vend - beg), len1 = (vend - beg) - len0;
-  tma::mbar_init(tma::smem_u32(&bars[0]), 1);
-  tma::mbar_init(tma::smem_u32(&bars[1]), 1);
-  tma::mbar_fence_init();
-  // the producer's source is read once (evict first); slab stores keep L2
-  // priority when the consumer merges right behind (FSX_FWD_L2_KEEP)
-  const uint64_t ld_pol = l2_policy(1);
-  const uint64_t st_pol = l2_policy(b.l2_keep_dst ? 2 : 0);
-  if (len0 > 0) {
-    tma::mbar_expect_tx(tma::smem_u32(&bars[0]), (uint32_t)len0);
-    tma::bulk_load_hint(sbase, a.src + beg, (uint32_t)len0, tma::smem_u32(&bars[0]), ld_pol);
-  }
-  if (len1 > 0) {
-    tma::mbar_expect_tx(tma::smem_u32(&bars[1]), (uint32_t)len1);
-    tma::bulk_load_hint(sbase + (uint32_t)len0, a.src + beg + len0, (uint32_t)len1, tma::smem_u32(&bars[1]),
-                        ld_pol);
-  }
-  if (len0 > 0) {
-    tma::mbar_wait(tma::smem_u32(&bars[0]), 0);
-    tma::bulk_store_hint(a.dst + beg, sbase, (uint32_t)len0, st_pol);
-  }
-  if (len1 > 0) {
-    tma::mbar_wait(tma::smem_u32(&bars[1]), 0);
-    tma::bulk_store_hint(a.dst + beg + len0, sbase + (uint32_t)len0, (uint32_t)len1, st_pol);
-  }
-  tma::bulk_commit();
-  for (int64_t j = vend; j < end; ++j) a.dst[j] = a.src[j];  // sub-16-byte tail
-  tma::bulk_wait_all();
-  // the tile's bulk stores are complete: order them (async proxy) before the
-  // generic release that counts the tile
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  if (a.counters == nullptr) return;
-  const uint32_t units = (c == a.n_chunks - 1) ? (uint32_t)a.last_units : (uint32_t)a.chunk_units;
-  const uint32_t prev = atom_add_acq_rel(&a.counters[c], 1u, a.peer != 0);
-  if (prev == units - 1) {
-    a.counters[c] = 0u;
-    if (a.peer) {
-      __threadfence_system();
-      st_release_sys(&a.dflags[c], a.token);
-    } else {
-      st_release_gpu(&a.dflags[c], a.token);
-    }
-    if (a.hflags) st_relaxed_sys(&a.hflags[c], a.token);
-  }
-}
-
-
-
-// K3 merge, phase 2, early-start form (default whenever the batch carries item
-// flags: the N>1 consumer following NVLink pushes, and the N=1 colocated
-// pipeline following K1 on the same GPU).  One elected thread per 32-thread
-// CTA claims runs of kTmaRun consecutive placeholder rows from a global work
-// counter, so every CTA works on the earliest rows whose chunk has landed
-// (dynamic, arrival order), and moves each row with the bulk-copy engine:
-// cp.async.bulk global->shared (mbarrier complete_tx) then shared->global,
-// an S-stage ring with S-1 rows in flight per CTA and no registers spent on
-// the bytes -- so the merge CTAs sit next to K1's CTAs on every SM without
-// taking the registers K1 needs.  Within a run the thread walks rows
-// incrementally (item / request values re-read only at boundaries, a chunk
-// flag spun on only when the run enters a new chunk).  With FSX_MERGE_DISCARD
-// a row's slab lines are discarded from L2 once its bulk load has completed.
-// Bulk-copy form of the follow kernel (FSX_MERGE_STREAM=3): CTA c of C (32
-// threads, one elected thread) moves rows g = c, c + C, ... in increasing
-// order through an S-stage shared-memory ring (S-1 rows in flight), so the
-// grid's window behind the producer stays about (S-1) x C rows wide while the
-// bytes in flight cost shared memory instead of registers.
-template <int S>
-__global__ void __launch_bounds__(32) merge_follow_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];
-  __shared__ __align__(8) uint64_t bars[S];
-  if (threadIdx.x != 0) return;
-  const uint32_t sbase = tma::smem_u32(stage_mem);
-  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
-  tma::mbar_fence_init();
-  const int64_t rb = b.row_bytes, n = b.total_item_rows, C = gridDim.x;
-  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool early = b.d_item_flag != nullptr;
-  int64_t g = blockIdx.x;
-  if (g >= n) return;
-  int64_t item = upper_index(b.d_item_row_off, b.num_items + 1, g);
-  while (b.d_item_row_off[item + 1] <= g) ++item;
-  int64_t req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-  while (b.d_req_item_off[req + 1] <= item) ++req;
-  int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
-  const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-  int64_t chunk_rows = early ? b.d_item_chunk_rows[item] : 0;
-  int64_t req_row = b.d_req_row_off[req];
-  bool req_ok = b.d_status[req] == 0;
-  int64_t waited = -1;
-  auto next = [&](uint8_t** dst, const uint8_t** src) -> bool {
-    for (; g < n; g += C) {
-      if (g >= item_end) {
-        do {
-          ++item;
-        } while (b.d_item_row_off[item + 1] <= g);
-        item_beg = b.d_item_row_off[item];
-        item_end = b.d_item_row_off[item + 1];
-        item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-        if (early) chunk_rows = b.d_item_chunk_rows[item];
-        waited = -1;
-        if (b.d_req_item_off[req + 1] <= item) {
-          do {
-            ++req;
-          } while (b.d_req_item_off[req + 1] <= item);
-          req_row = b.d_req_row_off[req];
-          req_ok = b.d_status[req] == 0;
-        }
+cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s) {
+  const int64_t tiles = b.unit_off[b.n];
+  if (tiles <= 0) return cudaSuccess;
+  if (bulk) {
+    // bulk-copy tiles need 16-byte aligned transfers and no fused digest;
+    // a batch with any other transfer takes the register tile kernel
+    bool ok = true;
+    for (int k = 0; k < b.n; ++k) ok = ok && b.t[k].vec && !b.t[k].digest;
+    if (ok) {
+      // the opt-in shared-memory limit is a per-device function attribute
+      static bool attr_set[kMaxDevices] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < kMaxDevices && !attr_set[dev]) {
+        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaTileBytes);
+        attr_set[dev] = true;
       }
-      if (!req_ok) continue;
-      const int64_t j = g - item_beg;
-      if (early) {
-        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
-        if (c != waited) {
-          spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          waited = c;
-        }
-      }
-      const uint8_t* sr = item_src + j * rb;
-      uint8_t* d = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[g]) * rb;
-      if ((reinterpret_cast<uintptr_t>(sr) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)rb) & 15) {
-        for (int64_t i = 0; i < rb; ++i) d[i] = sr[i];
-        continue;
-      }
-      *dst = d;
-      *src = sr;
-      g += C;
-      return true;
+      forward_tma_kernel<<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
+      return cudaGetLastError();
     }
-    return false;
-  };
-  uint8_t* dst_of[S];
-  const uint8_t* src_of[S];
-  auto issue = [&](int64_t k) -> bool {
-    const int s = (int)(k % S);
-    if (!next(&dst_of[s], &src_of[s])) return false;
-    const uint32_t bar = tma::smem_u32(&bars[s]);
-    tma::mbar_expect_tx(bar, (uint32_t)rb);
-    tma::bulk_load(sbase + s * stage_bytes, src_of[s], (uint32_t)rb, bar);
-    return true;
-  };
-  int64_t issued = 0;
-  while (issued < S - 1 && issue(issued)) ++issued;
-  uint32_t parity = 0;
-  for (int64_t k = 0; k < issued; ++k) {
-    const int s = (int)(k % S);
-    tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
-    parity ^= 1u << s;
-    tma::bulk_store(dst_of[s], sbase + s * stage_bytes, (uint32_t)rb);
-    tma::bulk_commit();
-    if (discard) {
-      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src_of[s]) + 127) & ~uintptr_t{127};
-      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src_of[s]) + rb) & ~uintptr_t{127};
-      for (uintptr_t a = lo; a < hi; a += 128) asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-    }
-    tma::bulk_wait_read1();
-    if (issue(issued)) ++issued;
   }
-  tma::bulk_wait_all();
+  forward_tile_kernel<<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
+  return cudaGetLastError();
 }
 
-constexpr int kTmaRun = 8;
-
-template <int S>
-__global__ void __launch_bounds__(32) merge_stream_tma_kernel(fsx_merge_batch b, uint32_t stage_bytes,
-                                                              unsigned long long* work) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];
-  __shared__ __align__(8) uint64_t bars[S];
-  if (threadIdx.x != 0) return;
-  const uint32_t sbase = tma::smem_u32(stage_mem);
-  for (int s = 0; s < S; ++s) tma::mbar_init(tma::smem_u32(&bars[s]), 1);
-  tma::mbar_fence_init();
-  const int64_t rb = b.row_bytes, n = b.total_item_rows;
-  const int64_t runs = (n + kTmaRun - 1) / kTmaRun;
-  const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool early = b.d_item_flag != nullptr;
-  // row generator state
-  int64_t g = 0, g_end = 0, item = 0, req = 0, item_beg = 0, item_end = 0, req_row = 0, chunk_rows = 0;
-  int64_t waited = -1;
-  bool req_ok = true, done = false;
-  const uint8_t* item_src = nullptr;
-  auto load_item = [&]() {
-    item_beg = b.d_item_row_off[item];
-    item_end = b.d_item_row_off[item + 1];
-    item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
-    if (early) chunk_rows = b.d_item_chunk_rows[item];
-    waited = -1;
-  };
-  auto load_req = [&]() {
-    req_row = b.d_req_row_off[req];
-    req_ok = b.d_status[req] == 0;
-  };
-  // next placeholder row to move: false once the work counter is exhausted
-  auto next = [&](uint8_t** dst, const uint8_t** src) -> bool {
-    for (;;) {
-      if (g >= g_end) {
-        if (done) return false;
-        const int64_t u = (int64_t)atomicAdd(work, 1ull);
-        if (u >= runs) {
-          done = true;
-          return false;
-        }
-        g = u * kTmaRun;
-        g_end = min(g + kTmaRun, n);
-        item = upper_index(b.d_item_row_off, b.num_items + 1, g);
-        while (b.d_item_row_off[item + 1] <= g) ++item;
-        req = upper_index(b.d_req_item_off, b.num_requests + 1, item);
-        while (b.d_req_item_off[req + 1] <= item) ++req;
-        load_item();
-        load_req();
-      } else if (g >= item_end) {
-        do {
-          ++item;
-        } while (b.d_item_row_off[item + 1] <= g);
-        load_item();
-        if (b.d_req_item_off[req + 1] <= item) {
-          do {
-            ++req;
-          } while (b.d_req_item_off[req + 1] <= item);
-          load_req();
-        }
-      }
-      const int64_t row = g++;
-      if (!req_ok) continue;  // validation failed: request untouched
-      const int64_t j = row - item_beg;
-      if (early) {
-        const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
-        if (c != waited) {
-          spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
-          // the row is read by the bulk-copy (async) proxy after a generic acquire
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          waited = c;
-        }
-      }
-      const uint8_t* s = item_src + j * rb;
-      uint8_t* d = static_cast<uint8_t*>(b.d_embeds) + (req_row + b.d_scratch[row]) * rb;
-      if ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)rb) & 15) {
-        for (int64_t i = 0; i < rb; ++i) d[i] = s[i];  // bulk copies need 16-byte alignment
-        continue;
-      }
-      *dst = d;
-      *src = s;
-      return true;
-    }
-  };
-  uint8_t* dst_of[S];
-  const uint8_t* src_of[S];
-  auto issue = [&](int64_t k) -> bool {
-    const int s = (int)(k % S);
-    if (!next(&dst_of[s], &src_of[s])) return false;
-    const uint32_t bar = tma::smem_u32(&bars[s]);
-    tma::mbar_expect_tx(bar, (uint32_t)rb);
-    tma::bulk_load(sbase + s * stage_bytes, src_of[s], (uint32_t)rb, bar);
-    return true;
-  };
-  int64_t issued = 0;
-  while (issued < S - 1 && issue(issued)) ++issued;
-  uint32_t parity = 0;
-  for (int64_t k = 0; k < issued; ++k) {
-    const int s = (int)(k % S);
-    tma::mbar_wait(tma::smem_u32(&bars[s]), (parity >> s) & 1u);
-    parity ^= 1u << s;
-    tma::bulk_store(dst_of[s], sbase + s * stage_bytes, (uint32_t)rb);
-    tma::bulk_commit();
-    if (discard) {  // the slab row has been read into shared memory: drop its L2 lines
-      const uintptr_t lo = (reinterpret_cast<uintptr_t>(src_of[s]) + 127) & ~uintptr_t{127};
-      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src_of[s]) + rb) & ~uintptr_t{127};
-      for (uintptr_t a = lo; a < hi; a += 128) asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-    }
-    tma::bulk_wait_read1();  // the store issued one row ago has left shared memory
-    if (issue(issued)) ++issued;
-  }
-  tma::bulk_wait_all();
+cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s) {
+  set_flags_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
-
+cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s) {
+  wait_flags_kernel<<<1, 32, 0, s>>>(dflags, n, token);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st) {
   if (m.n <= 0) return cudaSuccess;
@@ -1728,8 +998,7 @@ cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches,
-                         unsigned long long* work) {
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
   *launches = 0;
   if (b.num_requests <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
@@ -1741,100 +1010,29 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     *launches = 1;
   }
   if (base_mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
-  // Default: the LDG/STG warp-per-row kernel over a full (non-persistent)
-  // grid, 6.80 TB/s in the config-B step against 5.98 for the persistent TMA
-  // bulk-copy ring (profiles/merge_ab_r01c.jsonl, 3 alternating runs each);
-  // FSX_MERGE_TMA=1 selects the TMA kernel.
-  static const bool use_tma = [] {
-    const char* e = std::getenv("FSX_MERGE_TMA");
-    return e && e[0] == '1';
-  }();
-  const uint32_t stage = (uint32_t)((b.row_bytes + 127) & ~int64_t{127});
-  if (use_tma && !b.d_item_flag && !(b.mode & FSX_MERGE_DISCARD) && b.row_bytes % 16 == 0 &&
-      stage * kTmaStages <= 48 * 1024) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = (size_t)stage * kTmaStages;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_copy_tma_kernel<kTmaStages>, 32,
-                                                      smem) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-    const int64_t cap = (int64_t)sms * per_sm;
-    const int grid = (int)(b.total_item_rows < cap ? b.total_item_rows : cap);
-    merge_copy_tma_kernel<kTmaStages><<<grid, 32, smem, s>>>(b, stage);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) ++*launches;
-    return e;
-  }
+  const int64_t need = (b.total_item_rows + kMergeWarps - 1) / kMergeWarps;
   if (b.d_item_flag) {
+    // early start: a persistent grid (resident CTAs only -- warps spin on
+    // flags); one CTA per SM beside a producer on the same GPU
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // early-start kernel: 0 follow (default), 1 register runs, 2 bulk-copy runs
-    static const int stream_kind = [] {
-      const char* e = std::getenv("FSX_MERGE_STREAM");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (stream_kind == 4) {
-      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
-      const int64_t want = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-      merge_follow2_kernel<16><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
-    } else if (stream_kind == 0) {
-      // one CTA per SM beside K1 on the same GPU, else the copy grid
-      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
-      const int64_t want = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-      static const int unroll = [] {
-        const char* e = std::getenv("FSX_FOLLOW_UNROLL");
-        return e ? std::atoi(e) : 16;
-      }();
-      if (unroll == 8)
-        merge_follow_kernel<8><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
-      else
-        merge_follow_kernel<16><<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b);
-    } else if (stream_kind == 3 && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
-      static const int per_sm_env = [] {
-        const char* e = std::getenv("FSX_FOLLOW_TMA_PER_SM");
-        return e ? std::atoi(e) : 4;
-      }();
-      const size_t smem = (size_t)stage * kTmaStages;
-      const int64_t cap = (int64_t)sms * per_sm_env;
-      merge_follow_tma_kernel<kTmaStages>
-          <<<(unsigned)(b.total_item_rows < cap ? b.total_item_rows : cap), 32, smem, s>>>(b, stage);
-    } else if (stream_kind == 2 && work && b.row_bytes % 16 == 0 && stage * kTmaStages <= 48 * 1024) {
-      // early start: bulk-copy rows claimed in arrival order; colocated with
-      // K1: 4 CTAs per SM (registers stay with K1), else the occupancy limit
-      const size_t smem = (size_t)stage * kTmaStages;
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_stream_tma_kernel<kTmaStages>, 32,
-                                                        smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-      if ((b.mode & FSX_MERGE_COLOCATED) && per_sm > 4) per_sm = 4;
-      const int64_t runs = (b.total_item_rows + kTmaRun - 1) / kTmaRun;
-      const int64_t cap = (int64_t)sms * per_sm;
-      merge_stream_tma_kernel<kTmaStages><<<(unsigned)(runs < cap ? runs : cap), 32, smem, s>>>(b, stage, work);
-    } else {
-      // register form (FSX_MERGE_STREAM_LDG=1): static run assignment; one
-      // CTA per SM when the producer shares this GPU
-      const int64_t runs = (b.total_item_rows + kStreamRun - 1) / kStreamRun;
-      const int64_t want = (runs + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-      const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
-      merge_stream_kernel<<<(unsigned)(want < cap ? want : cap), kMergeThreads, 0, s>>>(b, work);
-    }
-    e = cudaGetLastError();
-    if (e == cudaSuccess) ++*launches;
-    return e;
+    const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
+    merge_follow_kernel<<<(unsigned)(need < cap ? need : cap), kMergeThreads, 0, s>>>(b);
+  } else {
+    merge_copy_kernel<<<(unsigned)need, kMergeThreads, 0, s>>>(b);
   }
-  const int64_t need = (b.total_item_rows + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-  // one warp per row and no persistence (full grid) unless FSX_MERGE_PERSIST=1
-  static const bool persist = [] {
-    const char* e = std::getenv("FSX_MERGE_PERSIST");
-    return e && e[0] == '1';
-  }();
-  const int grid = (int)((persist && need > copy_grid) ? copy_grid : need);
-  merge_copy_kernel<<<grid, kMergeThreads, 0, s>>>(b);
   e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;
   return e;
+}
+
+cudaError_t launch_merge_tee(const fsx_merge_batch& b, const TeeBatch& tb, cudaStream_t s) {
+  const int64_t rows = tb.g1 - tb.g0;
+  const int64_t grid = rows > 0 ? (rows + kMergeWarps - 1) / kMergeWarps : (tb.n > 0 ? 1 : 0);
+  if (grid <= 0) return cudaSuccess;
+  merge_tee_kernel<<<(unsigned)grid, kMergeThreads, 0, s>>>(b, tb);
+  return cudaGetLastError();
 }
 
 cudaError_t preload_kernels() {
@@ -1843,19 +1041,14 @@ cudaError_t preload_kernels() {
   // already running.  A consumer spinning on flags (early-start merge,
   // wait_flags, channel pull), launched before its producer's first-ever
   // launch, would then wait forever for a producer that cannot load.  The
-  // producers -- every K1 form, the flag stores, the channel push -- are
-  // loaded up front.  Only those: loading the merge kernels eagerly as well
-  // measured a slower colocated pass (0.30 vs 0.255 ms per config-B pass).
+  // producers -- both K1 forms, the tee, the flag stores, the channel push --
+  // are loaded up front.  (Loading the consumer kernels eagerly as well made
+  // the colocated early-start pass come up in its slow mode,
+  // profiles/colocated_bimodality_r01k.md.)
   const void* fns[] = {
       reinterpret_cast<const void*>(forward_tma_kernel),
-      reinterpret_cast<const void*>(forward_tile_kernel<4>),
-      reinterpret_cast<const void*>(forward_tile_kernel<8>),
-      reinterpret_cast<const void*>(forward_variant(0, false)),
-      reinterpret_cast<const void*>(forward_variant(1, false)),
-      reinterpret_cast<const void*>(forward_variant(2, false)),
-      reinterpret_cast<const void*>(forward_variant(0, true)),
-      reinterpret_cast<const void*>(forward_variant(1, true)),
-      reinterpret_cast<const void*>(forward_variant(2, true)),
+      reinterpret_cast<const void*>(forward_tile_kernel),
+      reinterpret_cast<const void*>(merge_tee_kernel),
       reinterpret_cast<const void*>(set_flags_kernel),
       reinterpret_cast<const void*>(chan_push_kernel),
   };
@@ -1863,28 +1056,6 @@ cudaError_t preload_kernels() {
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
-  }
-  // FSX_DIAG_PRELOAD_ALL=1 (diagnostics, profiles/colocated_bimodality_r01k.md):
-  // also load the consumer kernels, which brings out the colocated pass's slow mode
-  static const bool all = std::getenv("FSX_DIAG_PRELOAD_ALL") != nullptr;
-  if (all) {
-    const void* more[] = {
-        reinterpret_cast<const void*>(merge_scan_kernel),
-        reinterpret_cast<const void*>(merge_copy_kernel),
-        reinterpret_cast<const void*>(merge_follow_kernel<8>),
-        reinterpret_cast<const void*>(merge_follow_kernel<16>),
-        reinterpret_cast<const void*>(merge_copy_tma_kernel<kTmaStages>),
-        reinterpret_cast<const void*>(merge_follow2_kernel<16>),
-        reinterpret_cast<const void*>(merge_follow_tma_kernel<kTmaStages>),
-        reinterpret_cast<const void*>(merge_stream_tma_kernel<kTmaStages>),
-        reinterpret_cast<const void*>(merge_stream_kernel),
-        reinterpret_cast<const void*>(synth_kernel),
-        reinterpret_cast<const void*>(mailbox_kernel),
-        reinterpret_cast<const void*>(digest_kernel),
-        reinterpret_cast<const void*>(wait_flags_kernel),
-        reinterpret_cast<const void*>(chan_pull_kernel),
-    };
-    for (const void* f : more) cudaFuncGetAttributes(&a, f);
   }
   return cudaSuccess;
 }

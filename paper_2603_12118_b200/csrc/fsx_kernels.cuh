@@ -21,7 +21,7 @@ struct FwdArgs {
   int64_t total_units;
   int32_t n_chunks;
   int32_t vec;         // 16-byte path usable
-  int32_t peer;        // dst is peer (NVLink) memory: system-scope release per unit
+  int32_t peer;        // dst is peer (NVLink) memory: chunk flags published at system scope
   uint32_t* counters;  // [n_chunks] on the source device, zero on entry, self-resetting
   uint64_t* dflags;    // [n_chunks] consumer-device flags (may be peer memory)
   uint64_t* hflags;    // [n_chunks] mapped pinned host flags, or nullptr
@@ -36,9 +36,34 @@ struct FwdArgs {
 constexpr int kFwdMaxBatch = FSX_FWD_MAX_BATCH;
 struct FwdBatch {
   int32_t n;
-  int32_t l2_keep_dst;  // slab stores with L2 evict_last (consumer merges next)
+  int32_t l2_keep_dst;     // slab stores with L2 evict_last (consumer merges next)
+  int32_t peer_gpu_count;  // peer chunks: count tiles at gpu scope, publish once at sys scope
+  int32_t _pad;
   int64_t unit_off[kFwdMaxBatch + 1];
   FwdArgs t[kFwdMaxBatch];
+};
+
+// The tee (fsx_forward_merge): per item of one launch, where its slab copy goes
+// and how its chunks complete.  Pieces are rows: chunk c of an item holds rows
+// [c * chunk_rows, min((c + 1) * chunk_rows, rows)).
+struct TeeItem {
+  uint8_t* dst;        // slab segment (local or peer-mapped)
+  uint32_t* counters;  // [n_chunks] on the launching device, zero on entry, self-resetting
+  uint64_t* dflags;    // [n_chunks]
+  uint64_t* hflags;    // [n_chunks] or nullptr
+  uint64_t token;
+  int64_t chunk_rows;  // >= 1
+  int64_t rows;
+  int32_t n_chunks;
+  int32_t peer;
+};
+constexpr int kTeeMaxItems = 64;
+struct TeeBatch {
+  int32_t i0, n;           // items [i0, i0 + n) of the merge batch
+  int64_t g0, g1;          // their placeholder rows [g0, g1)
+  int32_t peer_gpu_count;  // as FwdBatch
+  int32_t l2_keep_dst;     // slab copy stored with L2 evict_last
+  TeeItem t[kTeeMaxItems];
 };
 
 struct FlagSetArgs {
@@ -90,26 +115,27 @@ cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, 
 cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st);
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
-cudaError_t launch_forward(const FwdBatch& b, int variant, int grid, cudaStream_t s, bool share_sm = false);
+// bulk: the bulk-copy tile kernel when every transfer allows it (16-byte
+// aligned, no fused digest), else the register tile kernel.
+cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
-// `work`: a zeroed device counter for the early-start (item flags) kernel.
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches,
-                         unsigned long long* work);
-// Load the producer kernels (K1 forms, flag stores, channel push) now instead
-// of at their first launch; called per device by fsx_open.
+// Scan and/or row copy per b.mode; `copy_grid` caps the early-start
+// (persistent) grid.
+cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);
+// The tee kernel over items [tb.i0, tb.i0 + tb.n) (positions / statuses from a
+// scan already ordered before it on `s`).
+cudaError_t launch_merge_tee(const fsx_merge_batch& b, const TeeBatch& tb, cudaStream_t s);
+// Load the producer kernels (K1 forms, the tee, flag stores, channel push)
+// now instead of at their first launch; called per device by fsx_open.
 cudaError_t preload_kernels();
 cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaStream_t s);
 
 // Device spin watchdog (spin_until traps after this long), current device.
 cudaError_t set_spin_timeout(uint64_t ns);
 
-// Occupancy helpers.
-int forward_block_threads();
-int forward_blocks_per_sm(int variant);
-// Tile size of the one-CTA-per-tile K1 variants (3, 4), 0 for the persistent ones.
-int forward_tile_bytes(int variant);
-int merge_copy_block_threads();
+// K1 tile bytes (one CTA per tile) and the merge copy kernel's occupancy.
+int forward_tile_bytes();
 int merge_copy_blocks_per_sm();
 
 }  // namespace fsx

@@ -54,28 +54,6 @@ int fail(int code, const std::string& msg) {
 constexpr int64_t kAlign = 64;             // sidecar.hpp:195
 constexpr int64_t kFlagRing = 1 << 18;     // flags per consumer slab (2 MiB)
 constexpr int64_t kCounterRing = 1 << 16;  // chunk counters per source device
-// K1 tuning: bytes per warp work unit (one release + counter bump per unit)
-// and the kernel variant (fsx_kernels.cu).  Overridable for sweeps with
-// FSX_FWD_UNIT / FSX_FWD_VARIANT.
-int64_t fwd_unit_bytes() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("FSX_FWD_UNIT");
-    if (!e) return int64_t{0};  // adaptive (see fsx_forward_ex)
-    return std::max<int64_t>(512, (std::atoll(e) + 511) & ~int64_t{511});
-  }();
-  return v;
-}
-
-int fwd_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("FSX_FWD_VARIANT");
-    // 4: one CTA per 32 KiB tile (non-persistent), 6.4 TB/s in the bench step;
-    // the persistent warp variants 0-2 top out near 5.7 (profiles/README.md)
-    return e ? std::atoi(e) : 4;
-  }();
-  return v;
-}
-
 // Address-ordered block list over [0, capacity).  First fit in offset order,
 // 64-byte units, coalescing on free: the allocation policy of the reference
 // NodeArena (sidecar.hpp:149-186), re-homed to a device slab.
@@ -206,7 +184,6 @@ struct Device {
   uint32_t* counters = nullptr;
   Ring counter_ring;
   int sms = 0;
-  int fwd_grid = 0;
   int merge_grid = 0;
   uint64_t* state = nullptr;  // channel head/tail counters (kStatePool u64)
   int64_t state_next = 0;
@@ -342,7 +319,6 @@ int device_state(fsx_fabric* f, int ordinal, Device** out) {
   FSX_CUDA(cudaMemset(d->counters, 0, kCounterRing * sizeof(uint32_t)));
   d->counter_ring.size = kCounterRing;
   FSX_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, ordinal));
-  d->fwd_grid = d->sms * fsx::forward_blocks_per_sm(fwd_variant());
   {
     // device spin watchdog: flags that never arrive trap instead of hanging
     const char* e = std::getenv("FSX_SPIN_TIMEOUT_S");
@@ -416,8 +392,7 @@ int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* dev
   for (int d : devs) {
     Device* st = nullptr;
     int rc = device_state(f.get(), d, &st);
-    static const bool no_preload = std::getenv("FSX_NO_PRELOAD") != nullptr;  // diagnostics
-    if (rc == FSX_OK && !no_preload) {
+    if (rc == FSX_OK) {
       // producer kernels loaded now, not at their first launch (fsx_kernels.cuh)
       cudaSetDevice(d);
       const cudaError_t e = fsx::preload_kernels();
@@ -741,7 +716,6 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
   int src_dev = 0;
   int rc = find_gpu(f, t[0].src_gpu, &src_dev);
   if (rc) return rc;
-  int64_t batch_bytes = 0;
   for (int32_t i = 0; i < n; ++i) {
     int d = 0;
     rc = find_gpu(f, t[i].src_gpu, &d);
@@ -750,7 +724,6 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     if (t[i].bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
     if (t[i].chunk_bytes > 0 && t[i].chunk_bytes < t[i].bytes && t[i].chunk_bytes % 16)
       return fail(FSX_E_VALIDATION, "chunk_bytes must be a multiple of 16");
-    batch_bytes += t[i].bytes;
   }
   Device* dev = nullptr;
   {
@@ -758,17 +731,8 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     rc = device_state(f, src_dev, &dev);
     if (rc) return rc;
   }
-  // Work unit: one warp, one release + counter bump.  Large enough to
-  // amortise the release, small enough that mid-size batches still spread
-  // over every resident warp (sweep3: 16 KiB >= 64 MiB, down to 4 KiB).
-  int64_t unit = fsx::forward_tile_bytes(fwd_variant());  // tile kernels: unit = tile
-  if (unit == 0) unit = fwd_unit_bytes();
-  if (unit == 0) {
-    const int64_t warps =
-        std::max<int64_t>(1, (int64_t)dev->fwd_grid * (fsx::forward_block_threads() / 32));
-    unit = 16384;
-    while (unit > 4096 && batch_bytes / unit < warps / 2) unit /= 2;
-  }
+  // one CTA per 32 KiB tile; a chunk is counted complete tile by tile
+  const int64_t unit = fsx::forward_tile_bytes();
   FSX_CUDA(cudaSetDevice(src_dev));
   cudaStream_t st = pick_stream(dev, stream);
   const bool graph = capturing(st);
@@ -777,6 +741,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     fsx::FwdBatch b{};
     b.n = cnt;
     b.l2_keep_dst = (options & FSX_FWD_L2_KEEP) ? 1 : 0;
+    b.peer_gpu_count = (options & FSX_FWD_PEER_GPU_COUNT) ? 1 : 0;
     for (int32_t k = 0; k < cnt; ++k) {
       fsx_transfer& x = t[first + k];
       fsx::FwdArgs& a = b.t[k];
@@ -798,10 +763,6 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
           s->flags.pin(x.flag_base, n_chunks);
         }
         a.counters = dev->counters + c0;
-        // FSX_DIAG_NO_FLAGS=1: measure the copy without completion tracking
-        // (no chunk flags are ever set: stream-ordered consumers only)
-        static const bool diag_no_flags = std::getenv("FSX_DIAG_NO_FLAGS") != nullptr;
-        if (diag_no_flags) a.counters = nullptr;
         a.dst = s->base + x.dst_off;
         a.dflags = s->dflags + x.flag_base;
         a.hflags = (s->hflags && (options & FSX_FWD_HOST_NOTIFY)) ? s->hflags + x.flag_base : nullptr;
@@ -817,16 +778,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       a.last_units = std::max<int64_t>(1, (last_len + a.slice - 1) / a.slice);
       a.total_units = (n_chunks - 1) * a.chunk_units + a.last_units;
       a.n_chunks = (int32_t)n_chunks;
-      {
-        // widest vector both ends allow: 32 B (LDG/STG.256 on sm_100), 16 B, or bytes
-        const uintptr_t al = reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst);
-        static const bool v32 = [] {
-          // 256-bit vectors measured no better than 16-byte ones (profiles/README.md)
-          const char* e = std::getenv("FSX_FWD_V32");
-          return e && e[0] == '1';
-        }();
-        a.vec = (v32 && (al & 31) == 0) ? 32 : ((al & 15) == 0 ? 16 : 0);
-      }
+      a.vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0 ? 16 : 0;
       if (x.token == 0) x.token = f->next_token.fetch_add(1);
       a.token = x.token;
       // the fused digest needs the 16-byte path; otherwise digest the source
@@ -836,18 +788,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       f->bytes_forwarded += x.bytes;
       f->forwards++;
     }
-    // Balanced persistent grid: every warp gets the same number of units
-    // (rounds), instead of a full first round and a half-empty last one.
-    const int64_t warps_per_cta = fsx::forward_block_threads() / 32;
-    const int64_t units = b.unit_off[cnt];
-    const int64_t max_warps = (int64_t)dev->fwd_grid * warps_per_cta;
-    const int64_t rounds = std::max<int64_t>(1, (units + max_warps - 1) / max_warps);
-    const int64_t warps = (units + rounds - 1) / rounds;
-    const int grid = (int)std::max<int64_t>(1, (warps + warps_per_cta - 1) / warps_per_cta);
-    const bool share = (options & FSX_FWD_SHARE_SM) != 0;
-    int variant = (options & FSX_FWD_BULK) ? 5 : fwd_variant();
-    if (share && variant != 3) variant = 4;  // the capped form is the register tile kernel
-    FSX_CUDA(fsx::launch_forward(b, variant, grid, st, share));
+    FSX_CUDA(fsx::launch_forward(b, (options & FSX_FWD_BULK) != 0, st));
     f->launches++;
     for (int32_t k = 0; k < cnt; ++k) {
       const fsx_transfer& x = t[first + k];
@@ -1240,17 +1181,7 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
   }
   FSX_CUDA(cudaSetDevice(ordinal));
   int launched = 0;
-  unsigned long long* work = nullptr;  // run counter of the early-start kernel
-  if (b->d_item_flag && base_mode != FSX_MERGE_SCAN_ONLY) {
-    std::lock_guard<std::mutex> lk(f->mu);
-    if (!dev->scratch) {
-      FSX_CUDA(cudaMalloc(&dev->scratch, kScratchRing * sizeof(uint64_t)));
-      dev->scratch_ring.size = kScratchRing;
-    }
-    work = reinterpret_cast<unsigned long long*>(dev->scratch + dev->scratch_ring.take(1));
-    FSX_CUDA(cudaMemsetAsync(work, 0, sizeof(uint64_t), pick_stream(dev, stream)));
-  }
-  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched, work);
+  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched);
   f->launches += launched;
   if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge launch: ") + cudaGetErrorString(e));
   if (base_mode != FSX_MERGE_SCAN_ONLY) {
@@ -1280,6 +1211,101 @@ int fsx_forward_place(fsx_fabric* f, int src_gpu, int dst_gpu, const fsx_merge_b
   f->forwards++;
   f->bytes_forwarded += b->total_item_rows * b->row_bytes;
   if (done_flag >= 0) return fsx_signal_flags(f, dst_gpu, done_flag, 1, token, src_gpu, stream);
+  return FSX_OK;
+}
+
+int fsx_forward_merge(fsx_fabric* f, int32_t n, fsx_transfer* t, const fsx_merge_batch* b,
+                      uint32_t options, void* stream) {
+  NvtxRange nvtx_range("fsx.forward_merge");
+  if (!b || n < 0 || n != b->num_items) return fail(FSX_E_VALIDATION, "forward_merge: one transfer per item");
+  const int base_mode = b->mode & FSX_MERGE_MODE_MASK;
+  if (base_mode == FSX_MERGE_SCAN_ONLY || (b->mode & ~FSX_MERGE_MODE_MASK) || b->d_item_flag)
+    return fail(FSX_E_VALIDATION,
+                "forward_merge takes FSX_MERGE_FULL or FSX_MERGE_COPY_ONLY, no early-start or discard bits");
+  if (b->row_bytes <= 0) return fail(FSX_E_VALIDATION, "bad row_bytes");
+  if (n == 0) return fsx_merge(f, 0, b, stream);  // nothing to forward: statuses only
+  int src_dev = 0;
+  int rc = find_gpu(f, t[0].src_gpu, &src_dev);
+  if (rc) return rc;
+  int64_t rows_total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int d = 0;
+    rc = find_gpu(f, t[i].src_gpu, &d);
+    if (rc) return rc;
+    if (d != src_dev) return fail(FSX_E_VALIDATION, "a forward batch must share one source device");
+    if (t[i].bytes < 0 || t[i].bytes % b->row_bytes)
+      return fail(FSX_E_VALIDATION, "forward_merge: item bytes must be whole rows");
+    if (t[i].chunk_bytes > 0 && t[i].chunk_bytes < t[i].bytes && t[i].chunk_bytes % b->row_bytes)
+      return fail(FSX_E_VALIDATION, "forward_merge: chunk_bytes must be whole rows");
+    if (t[i].d_digest) return fail(FSX_E_VALIDATION, "forward_merge has no fused digest");
+    rows_total += t[i].bytes / b->row_bytes;
+  }
+  if (rows_total != b->total_item_rows)
+    return fail(FSX_E_VALIDATION, "forward_merge: transfers do not cover the batch's item rows");
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, src_dev, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(src_dev));
+  cudaStream_t st = pick_stream(dev, stream);
+  if (base_mode == FSX_MERGE_FULL) {  // positions and statuses first, in stream order
+    fsx_merge_batch scan = *b;
+    scan.mode = FSX_MERGE_SCAN_ONLY;
+    int launched = 0;
+    const cudaError_t e = fsx::launch_merge(scan, dev->merge_grid, st, &launched);
+    if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge scan launch: ") + cudaGetErrorString(e));
+    f->launches += launched;
+  }
+  const bool graph = capturing(st);
+  int64_t g = 0;
+  for (int32_t first = 0; first < n; first += fsx::kTeeMaxItems) {
+    const int32_t cnt = std::min<int32_t>(n - first, fsx::kTeeMaxItems);
+    fsx::TeeBatch tb{};
+    tb.i0 = first;
+    tb.n = cnt;
+    tb.g0 = g;
+    tb.peer_gpu_count = (options & FSX_FWD_PEER_GPU_COUNT) ? 1 : 0;
+    tb.l2_keep_dst = (options & FSX_FWD_L2_KEEP) ? 1 : 0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      fsx_transfer& x = t[first + k];
+      fsx::TeeItem& a = tb.t[k];
+      a.rows = x.bytes / b->row_bytes;
+      a.chunk_rows = (x.chunk_bytes <= 0 || x.chunk_bytes >= x.bytes) ? std::max<int64_t>(a.rows, 1)
+                                                                       : x.chunk_bytes / b->row_bytes;
+      const int64_t n_chunks = a.rows == 0 ? 1 : (a.rows + a.chunk_rows - 1) / a.chunk_rows;
+      a.n_chunks = (int32_t)n_chunks;
+      std::lock_guard<std::mutex> lk(f->mu);
+      Slab* s = slab_of(f, x.dst_gpu);
+      if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(x.dst_gpu));
+      if (x.dst_off < 0 || x.dst_off + x.bytes > s->capacity)
+        return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
+      if (x.flag_base < 0 || x.flag_base + n_chunks > kFlagRing)
+        return fail(FSX_E_VALIDATION, "flag range out of the ring");
+      const int64_t c0 = dev->counter_ring.take(n_chunks);
+      if (c0 < 0) return fail(FSX_E_OOM, "chunk counter ring exhausted by graph-pinned ranges");
+      if (graph) {
+        dev->counter_ring.pin(c0, n_chunks);
+        s->flags.pin(x.flag_base, n_chunks);
+      }
+      a.counters = dev->counters + c0;
+      a.dst = s->base + x.dst_off;
+      a.dflags = s->dflags + x.flag_base;
+      a.hflags = (s->hflags && (options & FSX_FWD_HOST_NOTIFY)) ? s->hflags + x.flag_base : nullptr;
+      a.peer = (s->imported || s->device != src_dev) ? 1 : 0;
+      if (x.token == 0) x.token = f->next_token.fetch_add(1);
+      a.token = x.token;
+      g += a.rows;
+      f->bytes_forwarded += x.bytes;
+      f->forwards++;
+    }
+    tb.g1 = g;
+    FSX_CUDA(fsx::launch_merge_tee(*b, tb, st));
+    f->launches++;
+  }
+  f->merges++;
+  f->merged_rows += b->total_item_rows;
   return FSX_OK;
 }
 

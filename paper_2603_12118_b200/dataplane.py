@@ -16,6 +16,7 @@ torch provides device memory and streams only.
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import List, Optional
 
 import numpy as np
@@ -138,8 +139,8 @@ class DataPlaneBatch:
         return self.chunk_rows * self.rb
 
     def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False,
-                bulk: bool = False, share_sm: bool = False, flag_base0: Optional[int] = None,
-                tokens: Optional[np.ndarray] = None) -> int:
+                bulk: bool = False, flag_base0: Optional[int] = None,
+                tokens: Optional[np.ndarray] = None, peer_gpu_count: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
         one K1 launch per N.FWD_MAX_BATCH items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
@@ -148,18 +149,57 @@ class DataPlaneBatch:
         M = len(self.lay.items)
         if M == 0:
             return 0
-        fb0 = flag_base0 if flag_base0 is not None else \
-            self.fab.flags_alloc(self.dst_gpu, int(self.n_chunks.sum()))
-        self.flag_base[:] = fb0 + self.chunk_prefix
-        view = self._xview  # numpy view of the fsx_transfer array: no per-item Python
-        view["dst_off"] = self.slab_off
-        view["flag_base"] = self.flag_base
-        view["token"] = 0 if tokens is None else tokens  # 0: the fabric draws fresh tokens
+        self._prep_transfers(flag_base0, tokens)  # numpy view of the fsx_transfer array
+        view = self._xview
         opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0) | \
-            (N.FWD_BULK if bulk else 0) | (N.FWD_SHARE_SM if share_sm else 0)
+            (N.FWD_BULK if bulk else 0) | (N.FWD_PEER_GPU_COUNT if peer_gpu_count else 0)
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return -(-M // N.FWD_MAX_BATCH)
+
+    def _prep_transfers(self, flag_base0: Optional[int], tokens: Optional[np.ndarray]) -> None:
+        """Slab offsets, flag ranges and tokens of this pass into the
+        fsx_transfer array (no per-item Python); token 0 = drawn by the fabric."""
+        fb0 = flag_base0 if flag_base0 is not None else \
+            self.fab.flags_alloc(self.dst_gpu, int(self.n_chunks.sum()))
+        self.flag_base[:] = fb0 + self.chunk_prefix
+        view = self._xview
+        view["dst_off"] = self.slab_off
+        view["flag_base"] = self.flag_base
+        view["token"] = 0 if tokens is None else tokens
+
+    def tee(self, stream=None, mode: int = N.MERGE_COPY_ONLY, slot: int = 0,
+            host_notify: bool = False, l2_keep: bool = False, flag_base0: Optional[int] = None,
+            tokens: Optional[np.ndarray] = None) -> int:
+        """The forward and the merge as one kernel (fsx_forward_merge): every
+        item row is read once from the producer's buffer and stored into its
+        slab segment (chunk flags set as K1 would) and into its placeholder
+        row (as K3 would).  mode MERGE_COPY_ONLY uses the positions of a
+        scan(slot) ordered before it; MERGE_FULL scans first.  Returns the
+        launches of the copy (one per 64 items)."""
+        assert self.slab_off is not None, "alloc() first"
+        M = len(self.lay.items)
+        self._prep_transfers(flag_base0, tokens)
+        cache = self.__dict__.setdefault("_tee_cache", {})
+        b = cache.get((mode, slot))
+        if b is None:
+            b = self.merge_batch(False, mode, slot)
+            b.d_item_src = self._direct_src().data_ptr()
+            cache[(mode, slot)] = b
+        opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0)
+        N.call("fsx_forward_merge", self.fab._h, M, self._xfers, C.byref(b), opts,
+               _stream_ptr(stream))
+        self.tokens[:] = self._xview["token"]
+        return max(1, -(-M // N.FWD_MAX_BATCH))
+
+    def _direct_src(self) -> torch.Tensor:
+        """Device array of the producer's item pointers (direct placement and
+        the tee read the producer's buffers, not slab segments)."""
+        if not hasattr(self, "item_src_direct"):
+            sb = self.src_buf.data_ptr()
+            self.item_src_direct = torch.from_numpy(self.src_off + sb).to(self.dst_dev) \
+                if len(self.src_off) else torch.zeros(1, dtype=torch.int64, device=self.dst_dev)
+        return self.item_src_direct
 
     def forward_host(self, host_payload: List[np.ndarray], stream=None) -> None:
         """The host-span send path (sidecar.hpp:302): payload bytes from host
@@ -286,83 +326,34 @@ class DataPlaneBatch:
         cache = self.__dict__.setdefault("_place_cache", {})
         b = cache.get((mode, slot))
         if b is None:
-            if not hasattr(self, "item_src_direct"):
-                sb = self.src_buf.data_ptr()
-                self.item_src_direct = torch.from_numpy(self.src_off + sb).to(self.dst_dev) \
-                    if len(self.src_off) else torch.zeros(1, dtype=torch.int64, device=self.dst_dev)
             b = self.merge_batch(False, mode, slot)
-            b.d_item_src = self.item_src_direct.data_ptr()
+            b.d_item_src = self._direct_src().data_ptr()
             cache[(mode, slot)] = b
         self.fab.forward_place(self.src_gpu, self.dst_gpu, b, stream=stream)
 
-    # -- CUDA-graph form of the stream-ordered pass -----------------------------
-    def capture(self, stream, bulk: bool = True, l2_keep: bool = False) -> None:
-        """Record forward + merge (FULL) once as a CUDA graph for the current
-        slab offsets; run_graph() replays it.  For launch-bound batches (config
-        A): segment offsets, flag ranges and tokens are baked in -- first fit
-        returns the same offsets pass after pass and nothing in stream order
+    # -- CUDA-graph form of a pass ------------------------------------------------
+    def capture(self, stream, kind: str = "serial", bulk: bool = True, l2_keep: bool = False) -> None:
+        """Record one pass once as a CUDA graph for the current slab offsets;
+        run_graph() replays it.  kind "serial": K1 then the merge (FULL) in
+        stream order; "tee": the scan then the fused forward + merge.  For
+        launch-bound batches (config A): segment offsets, flag ranges and
+        tokens are baked in (the ranges are pinned by the fabric) -- first fit
+        returns the same offsets pass after pass, and nothing in stream order
         waits on the flags."""
         assert self.slab_off is not None, "alloc() first"
+        if kind == "tee" and not hasattr(self, "item_src_direct"):
+            self._direct_src()  # a device upload: not inside the capture
         g = torch.cuda.CUDAGraph()
         l0 = self.fab.stats()["kernel_launches"]
         with torch.cuda.graph(g, stream=stream):
-            self.forward(stream, host_notify=False, l2_keep=l2_keep, bulk=bulk)
-            self.merge(stream)
+            if kind == "tee":
+                self.tee(stream, mode=N.MERGE_FULL, l2_keep=l2_keep)
+            else:
+                self.forward(stream, host_notify=False, l2_keep=l2_keep, bulk=bulk)
+                self.merge(stream)
         self.graph_kernels = self.fab.stats()["kernel_launches"] - l0  # fsx kernels per replay
         self._graph = g
-        self._graph_key = (self.slab_off.tobytes(), bulk, l2_keep)
-
-    def capture_colocated(self, stream, mstream, token_base: int = 0x6A00000000,
-                          merge_first: bool = True) -> None:
-        """CUDA graph of the colocated pass (K1 || early-start merge, as
-        bench.py's step_pipelined) for launch-bound batches.  A graph bakes its
-        tokens, so every replay first resets this pass's chunk flags to 0 (one
-        set_flags launch); then the scan and the early-start merge (one CTA per
-        SM, FSX_MERGE_COLOCATED | FSX_MERGE_DISCARD) on `mstream` and K1 on
-        `stream` run concurrently and join.  run_graph() replays it."""
-        assert self.slab_off is not None, "alloc() first"
-        M = len(self.lay.items)
-        total = int(self.n_chunks.sum())
-        fb0 = self.fab.flags_alloc(self.dst_gpu, total)
-        toks = np.arange(token_base, token_base + M, dtype=np.uint64)
-        flag0 = self.fab.flag_ptr(self.dst_gpu, 0)
-        cr = [self.chunk_rows or it.rows for it in self.lay.items]
-        self.item_chunk_rows.copy_(torch.tensor(cr, dtype=torch.int64))
-        desc = np.stack([flag0 + 8 * (fb0 + self.chunk_prefix), toks.astype(np.int64)])
-        self._colo_desc = torch.from_numpy(desc).to(self.dst_dev)  # (flag ptr, token) per item
-        mb = self.merge_batch(False, N.MERGE_FULL | N.MERGE_COLOCATED | N.MERGE_DISCARD)
-        mb.d_item_flag = self._colo_desc[0].data_ptr()
-        mb.d_item_token = self._colo_desc[1].data_ptr()
-        mb.d_item_chunk_rows = self.item_chunk_rows.data_ptr()
-        torch.cuda.synchronize()
-        fork, join = torch.cuda.Event(), torch.cuda.Event()
-
-        def pass_(count=False):
-            self.fab.signal_flags(self.dst_gpu, fb0, total, 0, self.src_gpu, stream)  # reset
-            fork.record(stream)
-            mstream.wait_event(fork)
-            # the merge branch first, so its one CTA per SM is resident before
-            # K1's tiles fill the SMs (graph nodes carry no stream priority);
-            # safe in either order since fsx_open preloads every kernel
-            if merge_first:
-                self.fab.merge(self.dst_gpu, mb, mstream)  # scan, then the follow merge
-            self.forward(stream, host_notify=False, l2_keep=True, flag_base0=fb0, tokens=toks)
-            if not merge_first:
-                self.fab.merge(self.dst_gpu, mb, mstream)
-            join.record(mstream)
-            stream.wait_event(join)
-
-        # once eagerly: the fabric allocates its per-device scratch lazily,
-        # which must not happen inside the capture
-        pass_()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        l0 = self.fab.stats()["kernel_launches"]
-        with torch.cuda.graph(g, stream=stream):
-            pass_()
-        self.graph_kernels = self.fab.stats()["kernel_launches"] - l0
-        self._graph = g
-        self._graph_key = (self.slab_off.tobytes(), "colocated", mstream, merge_first)
+        self._graph_key = (self.slab_off.tobytes(), kind, bulk, l2_keep)
 
     def run_graph(self, stream) -> None:
         """Replay the captured pass (alloc() first; re-captured if the slab
@@ -370,10 +361,7 @@ class DataPlaneBatch:
         assert self.slab_off is not None, "alloc() first"
         key = (self.slab_off.tobytes(),) + self._graph_key[1:]
         if key != self._graph_key:
-            if self._graph_key[1] == "colocated":
-                self.capture_colocated(stream, self._graph_key[2], merge_first=self._graph_key[3])
-            else:
-                self.capture(stream, *self._graph_key[1:])
+            self.capture(stream, *self._graph_key[1:])
         with torch.cuda.stream(stream):
             self._graph.replay()
 

@@ -233,7 +233,11 @@ def _expected(oracle_mod, batch):
     return emb, st
 
 
-def _run_batch(fab, reqs, rules, chunk_rows=None, early=False, tok_override=None):
+def _run_batch(fab, reqs, rules, chunk_rows=None, path="serial", tok_override=None):
+    """One data-plane pass over `reqs` by `path`: "serial" (K1 register tiles,
+    then the merge), "bulk" (bulk-copy K1, then the merge), "early" (K1, then
+    the early-start merge following the chunk flags) or "tee" (the fused
+    forward + merge, fsx_forward_merge, with host-mirrored flags)."""
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
 
     torch = _torch()
@@ -242,30 +246,37 @@ def _run_batch(fab, reqs, rules, chunk_rows=None, early=False, tok_override=None
         tok_override(b)
     b.synth_inputs()
     assert b.alloc()
-    b.forward()
-    if early:
+    if path == "tee":
+        b.tee(mode=N.MERGE_FULL, host_notify=True)
+        b.wait_host()  # every chunk flag of every item published
+    elif path == "early":
+        b.forward()
         b.merge(early_start=True)
     else:
+        b.forward(bulk=path == "bulk")
         torch.cuda.synchronize()
         b.merge()
     torch.cuda.synchronize()
     return b
 
 
+@pytest.mark.parametrize("path", ["serial", "bulk", "tee"])
 @pytest.mark.parametrize("config,count,chunk_rows", [("A", 64, None), ("A", 5, 64), ("D", 24, 1024),
                                                      ("B", 1, 1024),
                                                      # the bench batches at full BASELINE size
                                                      ("B", 4, 1024), ("D", 32, 1024)])
-def test_merge_bit_exact(fab, oracle_mod, config, count, chunk_rows):
+def test_merge_bit_exact(fab, oracle_mod, config, count, chunk_rows, path):
     rules = {"A": T.RULES["A"], "B": T.RULES["B"], "D": T.RULES["D"]}[config]
     reqs = T.config_requests(config, count)
-    b = _run_batch(fab, reqs, rules, chunk_rows)
+    b = _run_batch(fab, reqs, rules, chunk_rows, path)
     want, st = _expected(oracle_mod, b)
     assert (b.status_host() == 0).all() and (st == 0).all()
     got = b.embeds_host()
     assert np.array_equal(got, want)
     # the forwarded slab bytes themselves (ChunkCallback delivery parity)
-    for i in range(min(3, len(b.lay.items))):
+    for i in sorted({0, 1, len(b.lay.items) // 2, len(b.lay.items) - 1}):
+        if not 0 <= i < len(b.lay.items):
+            continue
         it = b.lay.items[i]
         exp = oracle_mod.synth_payload(T.payload_seed(it.ref_id, 0), it.rows * b.rb)
         assert b.slab_item_host(i).tobytes() == exp
@@ -273,8 +284,9 @@ def test_merge_bit_exact(fab, oracle_mod, config, count, chunk_rows):
     assert fab.slab_usage(1)["segments_in_use"] == 0
 
 
+@pytest.mark.parametrize("path", ["serial", "tee"])
 @pytest.mark.parametrize("config", ["A", "B", "D"])
-def test_merge_matches_reference_derived_golden(fab, config):
+def test_merge_matches_reference_derived_golden(fab, config, path):
     """The GPU pass (K1 into the slab, K3 merge) produces exactly the prompt
     embeddings built from the bytes the REFERENCE SidecarFabric delivered,
     placed in the slot order the reference record() gives the consumer
@@ -286,7 +298,7 @@ def test_merge_matches_reference_derived_golden(fab, config):
     with open(os.path.join(os.path.dirname(__file__), "golden", "record_dispatch.json")) as fh:
         want = json.load(fh)["merged_sha256"][config]
     reqs = T.config_requests(config, want["requests"])
-    b = _run_batch(fab, reqs, T.RULES[config], 1024 if config != "A" else None)
+    b = _run_batch(fab, reqs, T.RULES[config], 1024 if config != "A" else None, path)
     assert (b.status_host() == 0).all()
     assert hashlib.sha256(b.embeds_host().tobytes()).hexdigest() == want["sha256"]
     b.release()
@@ -294,13 +306,16 @@ def test_merge_matches_reference_derived_golden(fab, config):
 
 def test_merge_early_start_flags(fab, oracle_mod):
     reqs = T.config_requests("D", 12)
-    b = _run_batch(fab, reqs, T.RULES["D"], chunk_rows=512, early=True)
+    b = _run_batch(fab, reqs, T.RULES["D"], chunk_rows=512, path="early")
     want, _ = _expected(oracle_mod, b)
     assert np.array_equal(b.embeds_host(), want)
     b.release()
 
 
-def test_merge_validation_leaves_request_untouched(fab, oracle_mod):
+@pytest.mark.parametrize("path", ["serial", "tee"])
+def test_merge_validation_leaves_request_untouched(fab, oracle_mod, path):
+    """A request whose placeholder count does not match its items keeps its
+    prompt rows (status validation); the tee still forwards its items."""
     reqs = T.config_requests("A", 10)
     bad = next(r for r, q in enumerate(reqs) if q.items)
 
@@ -311,31 +326,41 @@ def test_merge_validation_leaves_request_untouched(fab, oracle_mod):
         b.tok_host[idx] = 7
         b.tok[idx] = 7
 
-    b = _run_batch(fab, reqs, T.RULES["A"], tok_override=corrupt)
+    b = _run_batch(fab, reqs, T.RULES["A"], path=path, tok_override=corrupt)
     want, st = _expected(oracle_mod, b)
     got_st = b.status_host()
     assert got_st[bad] == N.E_VALIDATION and st[bad] == 1
     assert (np.delete(got_st, bad) == 0).all()
     assert np.array_equal(b.embeds_host(), want)
+    k = int(b.lay.req_item_off[bad])  # the failed request's first item reached its slab segment
+    it = b.lay.items[k]
+    assert b.slab_item_host(k).tobytes() == oracle_mod.synth_payload(T.payload_seed(it.ref_id, 0),
+                                                                     it.rows * b.rb)
     b.release()
 
 
-def test_merge_edge_cases(fab, oracle_mod):
+@pytest.mark.parametrize("path", ["serial", "tee"])
+def test_merge_edge_cases(fab, oracle_mod, path):
     rules = T.ShapeRules(hidden_dim=8, pixels_per_token=1, default_image_width=1,
                          default_image_height=3, tokens_per_audio_second=1, default_audio_seconds=1)
     reqs = [T.make_request(0, 0, ["image"], rules),              # placeholders only
             T.make_request(1, 4, [], rules),                     # text only
             T.make_request(2, 1, ["image", "audio", "image"], rules),
-            T.make_request(3, 37, ["audio"], rules)]
-    b = _run_batch(fab, reqs, rules)
-    want, st = _expected(oracle_mod, b)
-    assert (b.status_host() == 0).all()
-    assert np.array_equal(b.embeds_host(), want)
-    b.release()
+            T.make_request(3, 37, ["audio"], rules),
+            T.make_request(4, 5, ["text", "image", "text"], rules)]  # zero-row items
+    for chunk_rows in (None, 2):  # 2: chunks end mid-CTA and mid-item
+        b = _run_batch(fab, reqs, rules, chunk_rows, path)
+        want, st = _expected(oracle_mod, b)
+        assert (b.status_host() == 0).all()
+        assert np.array_equal(b.embeds_host(), want)
+        for i, it in enumerate(b.lay.items):
+            exp = oracle_mod.synth_payload(T.payload_seed(it.ref_id, 0), it.rows * b.rb)
+            assert b.slab_item_host(i).tobytes() == exp
+        b.release()
     # odd row width (row_bytes not a multiple of 16): byte path
     rules2 = T.ShapeRules(hidden_dim=5, pixels_per_token=4096 * 4096)
     reqs2 = [T.make_request(i, 3 + i, ["image"] * (i % 3), rules2) for i in range(6)]
-    b2 = _run_batch(fab, reqs2, rules2)
+    b2 = _run_batch(fab, reqs2, rules2, None, path)
     want2, _ = _expected(oracle_mod, b2)
     assert np.array_equal(b2.embeds_host(), want2)
     b2.release()
@@ -432,27 +457,67 @@ def test_pass_graph_replay_bit_exact(fab, oracle_mod):
 
 
 @pytest.mark.parametrize("config,count", [("A", 24), ("D", 8)])
-def test_colocated_pass_graph_bit_exact(fab, oracle_mod, config, count):
-    """The colocated pass (flag reset, K1 || scan + early-start merge) as one
-    CUDA graph (DataPlaneBatch.capture_colocated), replayed several times:
-    merged rows == the oracle, every request valid."""
+def test_tee_pass_graph_bit_exact(fab, oracle_mod, config, count):
+    """The fused forward + merge (scan, then fsx_forward_merge) captured once
+    as a CUDA graph and replayed several times: merged rows and slab segments
+    == the oracle, and the graph-baked counter / flag ranges are pinned (eager
+    forwards in between never reuse them)."""
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
 
     torch = _torch()
     reqs = T.config_requests(config, count)
-    b = DataPlaneBatch(fab, reqs, T.RULES[config], 0, 1,
-                       chunk_rows=512 if config == "D" else None)
+    b = DataPlaneBatch(fab, reqs, T.RULES[config], 0, 1, chunk_rows=512 if config == "D" else None)
     b.synth_inputs()
     s = torch.cuda.Stream()
-    ms = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
     assert b.alloc()
-    b.capture_colocated(s, ms)
-    for _ in range(4):
+    b.capture(s, kind="tee")
+    assert b.graph_kernels >= 2  # scan + tee
+    baked = b.flag_base.copy()
+    other = DataPlaneBatch(fab, T.config_requests("A", 4), T.RULES["A"], 0, 1)
+    other.synth_inputs()
+    for _ in range(3):
         b.run_graph(s)
+        assert other.alloc()  # eager traffic between replays draws fresh ranges
+        other.forward()
+        other.wait_host()
+        assert not set(other.flag_base.tolist()) & set(baked.tolist())
+        other.release()
     s.synchronize()
     want, _ = _expected(oracle_mod, b)
     assert (b.status_host() == 0).all()
     assert np.array_equal(b.embeds_host(), want)
+    for i in range(min(3, len(b.lay.items))):
+        it = b.lay.items[i]
+        assert b.slab_item_host(i).tobytes() == oracle_mod.synth_payload(T.payload_seed(it.ref_id, 0),
+                                                                         it.rows * b.rb)
+    b.release()
+
+
+def test_forward_merge_validation(fab):
+    """fsx_forward_merge rejects a transfer count that is not the item count,
+    item bytes that are not whole rows, chunks that are not whole rows, and
+    early-start / discard mode bits."""
+    import ctypes as C
+
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    b = DataPlaneBatch(fab, T.config_requests("B", 1), T.RULES["B"], 0, 1, chunk_rows=1024)
+    b.synth_inputs()
+    assert b.alloc()
+    b._prep_transfers(None, None)
+    mb = b.merge_batch(False, N.MERGE_FULL)
+    mb.d_item_src = b._direct_src().data_ptr()
+    with pytest.raises(N.FsxError) as e:
+        N.call("fsx_forward_merge", fab._h, 0, b._xfers, C.byref(mb), 0, None)
+    assert e.value.code == "validation"
+    b._xview["chunk_bytes"] = 1000 * 16  # not whole 7168-byte rows
+    with pytest.raises(N.FsxError):
+        N.call("fsx_forward_merge", fab._h, 1, b._xfers, C.byref(mb), 0, None)
+    b._xview["chunk_bytes"] = 1024 * b.rb
+    for bits in (N.MERGE_DISCARD, N.MERGE_SCAN_ONLY):
+        bad = b.merge_batch(False, N.MERGE_FULL | bits)
+        with pytest.raises(N.FsxError):
+            N.call("fsx_forward_merge", fab._h, 1, b._xfers, C.byref(bad), 0, None)
     b.release()
 
 
@@ -483,32 +548,6 @@ def test_forward_place_edge_cases(fab, oracle_mod):
 def test_stats_and_launch_count(fab):
     s = fab.stats()
     assert s["forwards"] > 0 and s["merges"] > 0 and s["kernel_launches"] > 0
-
-
-@pytest.mark.parametrize("env", [{"FSX_MERGE_TMA": "1", "FSX_FWD_VARIANT": "0"},
-                                 {"FSX_FWD_VARIANT": "3", "FSX_MERGE_PERSIST": "1"},
-                                 {"FSX_FWD_VARIANT": "2", "FSX_FWD_V32": "1"},
-                                 {"FSX_FWD_VARIANT": "5", "FSX_MERGE_STREAM": "2"},
-                                 {"FSX_MERGE_STREAM": "1", "FSX_FOLLOW_UNROLL": "8"},
-                                 {"FSX_MERGE_STREAM": "3"},
-                                 {"FSX_MERGE_STREAM": "4"}])
-def test_alternate_kernel_instances(gpu, env):
-    """The non-default K1 / K3 instances (persistent-warp K1 with 16- or
-    32-byte vectors, 16 KiB tiles, bulk-copy K1 for every call, TMA bulk-copy
-    merge, persistent LDG merge, the early-start run / bulk-copy run /
-    bulk-copy follow merges) are read from the environment once per process,
-    so the forward and merge parity cases (early start and the colocated pass
-    included) are re-run in a subprocess per combination."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
-                        os.path.join(root, "tests", "test_gpu_parity.py"),
-                        "-k", "(merge or forward or digest) and not alternate"],
-                       env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
-    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
 
 
 def test_small_put_batch_roundtrip(fab, oracle_mod):
@@ -564,7 +603,7 @@ def test_merge_colocated_pipeline_discard(fab, oracle_mod, config, count, chunk_
     mode = N.MERGE_FULL | N.MERGE_DISCARD | N.MERGE_COLOCATED
     for _ in range(3):
         assert b.alloc()
-        b.forward(s1, host_notify=False, l2_keep=True, share_sm=True)
+        b.forward(s1, host_notify=False, l2_keep=True)
         with torch.cuda.stream(s2):
             b.merge(s2, early_start=True, mode=mode)
         torch.cuda.synchronize()
