@@ -7,15 +7,20 @@ per producer->consumer pair vs 900 GB/s NVLink; merged req/s).
 Workload (BASELINE.json configs[1]): Qwen2.5-VL video->text,
 R = 4 requests per step, each one video of 16 frames x 1024 tokens x 3584-d
 bf16 (117,440,512 B) forwarded as 16 per-frame chunks of 7,340,032 B with a
-completion flag each, then merged into the placeholder rows of the
+completion flag each, and merged into the placeholder rows of the
 [1800 + 16384, 3584] prompt embedding.  A step = one data-plane pass over the
-batch: slab alloc -> K1 forward -> K3 merge -> release.
+batch: slab segments allocated, every item forwarded into its segment with
+per-chunk flags, merged into the prompt rows, segments released.
 
-  N = 1: producer and consumer are the same B200 (intra-device forward, HBM).
+  N = 1: producer and consumer are the same B200 (intra-device forward, HBM):
+         the forward and the merge run as ONE kernel (fsx_forward_merge, the
+         tee: each row read once, stored into the slab and into its prompt
+         row), with the placeholder scan pipelined one pass ahead.
   N > 1: one process per GPU; rank 2k produces into rank 2k+1's slab over
          NVLink (CUDA IPC), rank 2k+1 merges with in-kernel early start and
          acks; pairs are independent ("scaling": "weak", no collective on the
-         data path).
+         data path).  Without RANK/WORLD_SIZE in the environment, bench.py
+         --gpus N spawns the N ranks itself (127.0.0.1 rendezvous).
 
 Inputs are larger than L2 (470 MB payload + 521 MB prompt embeddings per
 step vs 126 MB L2), so no flush is needed between steps.
@@ -26,6 +31,7 @@ import argparse
 import datetime
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -48,13 +54,19 @@ CONFIGS = {
           "workload": "D: servegen-like mixed image/video/audio trace (seed 42), 3584-d bf16"},
 }
 METRIC = "forwarded GB/s per producer->consumer pair vs 900 GB/s NVLink; merged req/s"
-# N=1: the consumer merges right after K1 on the same GPU; storing the slab with
-# L2 evict_last priority (FSX_FWD_L2_KEEP) measured 1-3 % slower than normal
-# priority (profiles/README.md), so it is off unless FSX_BENCH_L2_KEEP=1.
-L2_KEEP = os.environ.get("FSX_BENCH_L2_KEEP", "0") == "1"
-# Colocated pipeline: K1's slab stores keep L2 priority until the merge has
-# read (and discarded) them; FSX_BENCH_L2_KEEP_PIPE=0 turns that off.
-L2_KEEP_PIPE = os.environ.get("FSX_BENCH_L2_KEEP_PIPE", "1") == "1"
+KERNELS = {
+    "tee": "fsx::kern::merge_tee_kernel (fsx_forward_merge: forward + merge in one kernel)",
+    "forward": "fsx::kern::forward_tma_kernel (K1, bulk-copy tiles, all items of the step in one launch)",
+    "merge": "fsx::kern::merge_copy_kernel (K3b, warp per placeholder row, stream-ordered)",
+    "follow": "fsx::kern::merge_follow_kernel (K3b early start, persistent grid)",
+    "scan": "fsx::kern::merge_scan_kernel (K3a placeholder scan)",
+}
+
+
+# N>1: the K1 forms for peer (NVLink) destinations (fsx_forward_batch options)
+K1_FORMS = {"tile": 0,          # register tiles, system-scope acq_rel count per tile
+            "gpucount": 16,     # register tiles, gpu-scope count, one fence.sc.sys + flag per chunk
+            "bulk": 4}          # bulk-copy (cp.async.bulk) tiles into the peer slab
 
 
 def parse():
@@ -67,30 +79,23 @@ def parse():
     p.add_argument("--requests", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--verify", action="store_true",
-                   help="N>1: consumers check the merged embeddings against a local pass")
-    p.add_argument("--serial", action="store_true",
-                   help="N=1: K1 then the merge in stream order (no colocated pipeline)")
+    p.add_argument("--no-verify", dest="verify", action="store_false",
+                   help="N>1: skip the consumers' bit-exactness check of the merged embeddings "
+                        "against a local pass (on by default)")
     p.add_argument("--profile", action="store_true",
                    help="short run for ncu: no clocks, no cpu baseline, no e2e")
+    p.add_argument("--k1", choices=["auto"] + sorted(K1_FORMS), default="auto",
+                   help="N>1: the K1 form pushing into peer slabs (auto: probe all, time the fastest)")
+    p.add_argument("--transfer", choices=["slab", "direct"], default="slab",
+                   help="N>1 pairs: K1 into the consumer slab + early-start merge (slab), or the "
+                        "producer placing rows straight into the consumer's prompt (direct)")
+    p.add_argument("--chunk-rows", type=int, default=None,
+                   help="rows per flagged chunk (default: the config's, one video frame for B/D)")
+    p.add_argument("--sets", type=int, default=2,
+                   help="N>1: slab segment sets per consumer (the next transfer overlaps the merge)")
+    p.add_argument("--pin-device", type=int, default=None,
+                   help="N>1 protocol runs on a 1-GPU box: every rank on this device, gloo for setup")
     return p.parse_args()
-
-
-def fwd_kernel_name() -> str:
-    """K1 instance libfsx launches (fwd_variant() in fsx_runtime.cu)."""
-    v = int(os.environ.get("FSX_FWD_VARIANT", "4"))
-    if v == 3:
-        return "fsx::kern::forward_tile_kernel<4> (one CTA per 16 KiB tile)"
-    if v == 4:
-        return "fsx::kern::forward_tile_kernel<8> (one CTA per 32 KiB tile)"
-    return f"fsx::kern::forward_kernel (persistent warps, variant {v})"
-
-
-def merge_kernel_name() -> str:
-    """K3 copy instance libfsx launches (launch_merge in fsx_kernels.cu)."""
-    if os.environ.get("FSX_MERGE_TMA", "0") == "1":
-        return "fsx::merge_copy_tma_kernel<4> (persistent TMA bulk-copy ring)"
-    return "fsx::kern::merge_copy_kernel (warp per placeholder row, full grid)"
 
 
 def load_peaks():
@@ -102,13 +107,21 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic():
-    """DRAM bytes per launch from the committed `ncu --set full` capture."""
+def load_traffic(config: str, kernel: str, alg_bytes: int):
+    """DRAM bytes per launch of `kernel` on `config` from the committed
+    `ncu --set full` capture (profiles/traffic_r02.json, written by
+    scripts/profile_round.sh), only when that capture is of the same kernel on
+    the same launch size; else (None, reason)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh)
+        with open(os.path.join(ROOT, "profiles", "traffic_r02.json")) as fh:
+            rec = json.load(fh).get(f"{config}:{kernel}")
     except Exception:
-        return {}
+        rec = None
+    if not rec:
+        return None, f"no ncu capture of {kernel} on config {config} committed"
+    if int(rec.get("alg_bytes", -1)) != int(alg_bytes):
+        return None, f"committed capture is of a {rec.get('alg_bytes')}-byte launch, not {alg_bytes}"
+    return int(rec["dram_bytes"]), rec.get("source")
 
 
 # ---------------------------------------------------------------------------
@@ -292,7 +305,10 @@ def run_reference(args, rank):
 # fsx arm, one GPU
 
 def run_single(args):
-    import numpy as np
+    """N = 1: producer and consumer share one B200.  The timed pass is the
+    tee (fsx_forward_merge); the other schedules of the same pass and each
+    kernel alone are measured in the same process for the line's
+    `schedules` / `kernels` objects."""
     import torch
 
     from paper_2603_12118_b200 import _native as N
@@ -308,286 +324,212 @@ def run_single(args):
     lay = T.layout(reqs, rules.row_bytes)
     fab.slab_register(1, max(1 << 30, 2 * lay.payload_bytes))
     stream = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)
+    mstream = torch.cuda.Stream(device=dev, priority=torch.cuda.Stream.priority_range()[1])
     batch = DataPlaneBatch(fab, reqs, rules, src_gpu=0, dst_gpu=1, chunk_rows=CHUNK_ROWS)
     with torch.cuda.stream(stream):
         batch.synth_inputs(stream)
     torch.cuda.synchronize()
     payload = lay.payload_bytes
-    n_items = len(lay.items)
-    fwd_launches = -(-n_items // N.FWD_MAX_BATCH)  # fsx_forward_batch: transfers per K1 launch
-    # merge_copy_kernel: read slab rows + write placeholder rows + read positions
-    # (2*sum(n)*D*2; the sum(T)*4 token read is the scan, which
-    # runs on a side stream under K1)
-    merge_bytes = 2 * payload + 4 * lay.total_item_rows
-    fwd_bytes = 2 * payload                           # intra-device: read + write
+    n_rows = lay.total_item_rows
+    # algorithmic bytes per launch: the tee reads every item row
+    # once and writes it twice (slab segment + prompt row) and reads one
+    # position per row; K1 reads + writes the payload; the merge reads the
+    # slab + writes the prompt rows + reads the positions.
+    tee_bytes = 3 * payload + 4 * n_rows
+    fwd_bytes = 2 * payload
+    merge_bytes = 2 * payload + 4 * n_rows
+    s8d_pass_bytes = fwd_bytes + merge_bytes  # forward + merge counted separately
 
-    ev = []
-    side = torch.cuda.Stream(device=dev)
-    # K3 phase 1 (placeholder scan) needs only the token ids, so it is
-    # software-pipelined one pass ahead on a side stream into a second scan
-    # slot: pass s merges with the positions scanned during pass s-1 and scans
-    # for pass s+1.  Every pass still runs exactly one scan, one K1 and one K3b.
+    # The placeholder scan only needs token ids, so every schedule runs it one
+    # pass ahead on a side stream into a second scan slot: pass s copies with
+    # the positions scanned during pass s-1 and scans for pass s+1.
     scanned = [torch.cuda.Event(), torch.cuda.Event()]
-    counter = [0]
-    host_s = []
-
-    def prologue():
-        batch.scan(side, slot=0)
-        scanned[0].record(side)
-
-    # Default N=1 pass (colocated pipeline): K1 on `stream` and the early-start
-    # merge on `mstream` run concurrently; the merge follows K1 chunk by chunk
-    # (per-chunk flags), one CTA per SM so K1 always keeps room, reads each
-    # slab row while K1's stores of it still sit in L2 and then discards the
-    # row's L2 lines (FSX_MERGE_DISCARD): the slab never round-trips through
-    # HBM.  --serial runs K1 then the merge in stream order instead.
-    # high priority: the block scheduler hands the merge's CTAs the first free
-    # slots while K1's thousands of CTAs are still queued (equal priority
-    # would leave the merge waiting for K1's last wave)
-    lo_pri, hi_pri = torch.cuda.Stream.priority_range()
-    mstream = torch.cuda.Stream(device=dev, priority=hi_pri)
     merged = [torch.cuda.Event(), torch.cuda.Event()]
-    # timing events, created once: (e0, e1, e2) per timed pass, reused per run
+    fork = torch.cuda.Event()
+    counter = [0]
+    graph_launched = [0]
+    ev = []
     ev_pool = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
                for _ in range(max(args.steps, 20) + 1)]
-    fork_ev = torch.cuda.Event()
 
-    def timing_events(record):
-        return ev_pool[len(ev)] if record else (None, None, None)
-    merge_mode = N.MERGE_COPY_ONLY | N.MERGE_COLOCATED
-    if os.environ.get("FSX_BENCH_NO_DISCARD") != "1":
-        merge_mode |= N.MERGE_DISCARD
-
-    def step_pipelined(record=False):
-        t_host = time.perf_counter()
+    def begin(record):
         s = counter[0]
         counter[0] += 1
         cur, nxt = s % 2, (s + 1) % 2
         assert batch.alloc()
-        e0, e1, e2 = timing_events(record)
         if s > 0:
-            stream.wait_event(merged[(s - 1) % 2])  # slab segments free: pass s-1 merged
-        if record:
-            e0.record(stream)
-        batch.forward(stream, host_notify=False, l2_keep=L2_KEEP_PIPE,
-                      bulk=os.environ.get("FSX_BENCH_PIPE_BULK") == "1",
-                      share_sm=os.environ.get("FSX_BENCH_SHARE_SM", "0") == "1")
-        if record:
-            e1.record(stream)
-        with torch.cuda.stream(mstream):
-            mstream.wait_event(scanned[cur])
-            batch.merge(mstream, early_start=True, mode=merge_mode, slot=cur)
-            merged[cur].record(mstream)
-        # The next pass's scan runs once this merge is done: the scan kernel
-        # needs a whole SM (1024 threads), and no kernel that cannot fit next
-        # to a resident merge CTA may become ready while the merge spins on
-        # K1's flags (the CTA dispatcher could stall on it ahead of K1).
-        side.wait_event(merged[cur])
+            stream.wait_event(merged[(s - 1) % 2])  # previous pass (any stream) done
+        fork.record(stream)
+        side.wait_event(fork)
         batch.scan(side, slot=nxt)
         scanned[nxt].record(side)
+        stream.wait_event(scanned[cur])
+        e = ev_pool[len(ev)] if record else (None, None, None)
         if record:
-            stream.wait_event(merged[cur])
-            e2.record(stream)
-            ev.append((e0, e1, e2))
+            e[0].record(stream)
+        return cur, e
+
+    def end(cur, e, record):
+        merged[cur].record(stream)
+        if record:
+            e[2].record(stream)
+            ev.append(e)
         batch.release()
-        host_s.append(time.perf_counter() - t_host)
 
-    def step_serial(record=False, bulk=True):
-        t_host = time.perf_counter()
-        s = counter[0]
-        counter[0] += 1
-        if s > 0:
-            stream.wait_event(merged[(s - 1) % 2])  # a colocated pass before this one is done
-        cur, nxt = s % 2, (s + 1) % 2
-        # slab segments for the batch (first fit: the same offsets every step)
-        assert batch.alloc()
-        e0, e1, e2 = timing_events(record)
-        fork = fork_ev
-        fork.record(stream)  # the previous pass (incl. its merge) is done past here
+    def step_tee(record=False):
+        cur, e = begin(record)
+        batch.tee(stream, mode=N.MERGE_COPY_ONLY, slot=cur)
         if record:
-            e0.record(stream)
-        # K1: 4 items x 16 flagged per-frame chunks; the consumer (K3) is
-        # stream-ordered on this GPU, so no host mirror of the flags
-        batch.forward(stream, host_notify=False, l2_keep=L2_KEEP, bulk=bulk)
+            e[1].record(stream)
+        end(cur, e, record)
+
+    def step_serial(record=False):
+        cur, e = begin(record)
+        batch.forward(stream, host_notify=False, bulk=True)
         if record:
-            e1.record(stream)
-        side.wait_event(fork)
-        batch.scan(side, slot=nxt)      # positions for the next pass
-        scanned[nxt].record(side)
-        stream.wait_event(scanned[cur])  # this pass's positions (scanned last pass)
-        batch.merge(stream, mode=N.MERGE_COPY_ONLY, slot=cur)  # K3b: the row moves
+            e[1].record(stream)
+        batch.merge(stream, mode=N.MERGE_COPY_ONLY, slot=cur)
+        end(cur, e, record)
+
+    def step_follow(record=False):
+        # K1, then the early-start merge in stream order (its flags are all
+        # set): the follow kernel's own rate at full occupancy
+        cur, e = begin(record)
+        batch.forward(stream, host_notify=False, bulk=True)
         if record:
-            e2.record(stream)
-            ev.append((e0, e1, e2))
-        batch.release()               # ack: segments back to the slab
-        host_s.append(time.perf_counter() - t_host)
+            e[1].record(stream)
+        batch.merge(stream, early_start=True, mode=N.MERGE_COPY_ONLY, slot=cur)
+        end(cur, e, record)
 
-    def timed(step, nsteps, prange=False):
-        """nsteps passes between two events on `stream` (max over the
-        streams involved); returns (ms per pass, per-pass events, launches)."""
-        ev.clear()
-        host_s.clear()
-        launches0 = fab.stats()["kernel_launches"] + graph_launched[0]
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        start.record(stream)
-        for i in range(nsteps):
-            if prange and i == nsteps - 1:  # ncu --replay-mode range: the last pass
-                torch.cuda.synchronize()
-                batch.es_device_idle = True  # no event waits on events outside the range
-                torch.cuda.cudart().cudaProfilerStart()
-            step(record=True)
-            batch.es_device_idle = False
-            if prange and i == nsteps - 1:
-                stream.wait_event(merged[(counter[0] - 1) % 2])
-                torch.cuda.synchronize()
-                torch.cuda.cudart().cudaProfilerStop()
-        stream.wait_event(scanned[counter[0] % 2])  # the look-ahead scan is timed too
-        stream.wait_event(merged[(counter[0] - 1) % 2])
-        end.record(stream)
-        torch.cuda.synchronize()
-        return (start.elapsed_time(end) / nsteps, list(ev),
-                fab.stats()["kernel_launches"] + graph_launched[0] - launches0)
+    def step_colocated(record=False):
+        # K1 (register tiles) and the early-start merge concurrently: the merge
+        # follows K1's chunk flags on a high-priority stream, one CTA per SM
+        cur, e = begin(record)
+        mstream.wait_event(scanned[cur])
+        batch.forward(stream, host_notify=False, l2_keep=True)
+        if record:
+            e[1].record(stream)
+        with torch.cuda.stream(mstream):
+            batch.merge(mstream, early_start=True, slot=cur,
+                        mode=N.MERGE_COPY_ONLY | N.MERGE_COLOCATED | N.MERGE_DISCARD)
+        join = torch.cuda.Event()
+        join.record(mstream)
+        stream.wait_event(join)
+        end(cur, e, record)
 
-    # The colocated pipeline pays off once a pass is long enough to hide its
-    # extra host work (early-start descriptors, two streams): config B / D
-    # passes of ~0.25 ms do; config A's 70 MB passes are host-bound and run
-    # faster stream-ordered.
-    if not args.serial and payload < (128 << 20):
-        args.serial = True
-    # launch-bound small passes (config A) are replayed as a CUDA graph of the
-    # stream-ordered pass when that is faster (probed like the colocated pass)
-    graph_pass = (args.serial and payload < (128 << 20) and not args.profile and
-                  os.environ.get("FSX_BENCH_GRAPH", "1") == "1")
-
-    graph_launched = [0]
-    graph_kind = "serial"
+    def step_place(record=False):
+        cur, e = begin(record)
+        batch.place(stream, mode=N.MERGE_COPY_ONLY, slot=cur)
+        if record:
+            e[1].record(stream)
+        end(cur, e, record)
 
     def step_graph(record=False):
-        t_host = time.perf_counter()
+        # the tee pass (scan + tee, FULL) as one CUDA graph launch
+        s = counter[0]
+        counter[0] += 1
         assert batch.alloc()
-        e0, e1, e2 = timing_events(record)
+        if s > 0:
+            stream.wait_event(merged[(s - 1) % 2])
+        e = ev_pool[len(ev)] if record else None
         if record:
-            e0.record(stream)
-        batch.run_graph(stream)       # K1 (bulk-copy tiles) + scan + merge, one graph launch
-        graph_launched[0] += batch.graph_kernels  # our kernels in the replay
+            e[0].record(stream)
+        batch.run_graph(stream)
+        graph_launched[0] += batch.graph_kernels
         if record:
-            e1.record(stream)
-            e2.record(stream)
-            ev.append((e0, e1, e2))
+            e[1].record(stream)
+        merged[s % 2].record(stream)
+        if record:
+            e[2].record(stream)
+            ev.append(e)
         batch.release()
-        host_s.append(time.perf_counter() - t_host)
 
-    step = step_serial if args.serial else step_pipelined
-    probe = None
-    with torch.cuda.stream(stream):
-        prologue()
-        for _ in range(args.warmup):
-            step()
+    def timed(step, n):
+        """n passes between two events on `stream` (which waits for the last
+        scan and the last pass); returns (ms per pass, per-pass events,
+        fsx kernel launches)."""
+        ev.clear()
+        l0 = fab.stats()["kernel_launches"] + graph_launched[0]
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        if os.environ.get("FSX_BENCH_COLD_READ") == "1":
-            # diagnostic only: the merge follows K1's chunk flags but reads an
-            # identical copy of the payload that K1 never touches, so none of
-            # its reads can hit lines K1 just wrote (is the colocated gain L2
-            # reuse or overlap?)
-            shadow = batch.src_buf.clone()
-            batch.item_src.copy_(torch.from_numpy(batch.src_off + shadow.data_ptr()))
-            torch.cuda.synchronize()
-        if graph_pass:
-            def capture(kind):
-                assert batch.alloc()
-                if kind == "colocated":
-                    batch.capture_colocated(stream, mstream,
-                                            merge_first=os.environ.get("FSX_GRAPH_MERGE_FIRST", "1") == "1")
-                else:
-                    batch.capture(stream, bulk=True, l2_keep=L2_KEEP)
-                batch.release()
-                for _ in range(3):
-                    step_graph()
-                return timed(step_graph, 10)[0]
-            # the colocated pass as a graph measured slower here (config A:
-            # 0.078 vs 0.062 ms per pass, profiles/README.md); probed on request
-            c_ms = capture("colocated") if os.environ.get("FSX_BENCH_GRAPH_COLO") == "1" else 1e9
-            g_ms = capture("serial")
-            s_ms, _, _ = timed(step_serial, 10)
-            probe = {"graph_ms": round(g_ms, 4), "serial_ms": round(s_ms, 4)}
-            if c_ms < 1e9:
-                probe["graph_colocated_ms"] = round(c_ms, 4)
-            graph_pass = min(g_ms, c_ms) < s_ms
-            graph_kind = "colocated" if c_ms < g_ms else "serial"
-            if graph_pass:
-                if graph_kind == "colocated":
-                    capture("colocated")
+        start.record(stream)
+        for _ in range(n):
+            step(record=True)
+        stream.wait_event(scanned[counter[0] % 2])
+        stop.record(stream)
+        torch.cuda.synchronize()
+        return (start.elapsed_time(stop) / n, list(ev),
+                fab.stats()["kernel_launches"] + graph_launched[0] - l0)
+
+    def span(evs, a, b):
+        return statistics.mean(x[a].elapsed_time(x[b]) for x in evs)
+
+    with torch.cuda.stream(stream):
+        batch.scan(side, slot=0)
+        scanned[0].record(side)
+        for _ in range(max(3, args.warmup)):
+            step_tee()
+        step = step_tee
+        probe = None
+        # launch-bound small passes (config A) may run faster as one CUDA
+        # graph launch per pass: probed, the faster form is timed
+        if payload < (128 << 20) and not args.profile:
+            eager_ms = timed(step_tee, 10)[0]
+            assert batch.alloc()
+            batch.capture(stream, kind="tee")
+            batch.release()
+            for _ in range(3):
+                step_graph()
+            graph_ms = timed(step_graph, 10)[0]
+            probe = {"eager_ms": round(eager_ms, 4), "graph_ms": round(graph_ms, 4)}
+            if graph_ms < eager_ms:
                 step = step_graph
-            for _ in range(3):
-                step()
-            torch.cuda.synchronize()
-        if not args.serial and not args.profile:
-            # schedule choice: a short probe of both full passes; the timed run
-            # uses the faster (the colocated pass normally; stream order if the
-            # concurrent pass came up slow on this box, which happens rarely)
-            # two alternating rounds, averaged: one 10-pass sample of a pass
-            # in its slow mode can read borderline (0.2745 vs 0.2895 ms once,
-            # then timed at 0.30)
-            p1, _, _ = timed(step_pipelined, 10)
-            s1, _, _ = timed(step_serial, 10)
-            p2, _, _ = timed(step_pipelined, 10)
-            s2, _, _ = timed(step_serial, 10)
-            p_ms, s_ms = (p1 + p2) / 2, (s1 + s2) / 2
-            probe = {"pipelined_ms": round(p_ms, 4), "serial_ms": round(s_ms, 4),
-                     "rounds": [[round(p1, 4), round(s1, 4)], [round(p2, 4), round(s2, 4)]]}
-            if s_ms < p_ms:
-                args.serial = True
-                step = step_serial
-            for _ in range(3):
-                step()
-            torch.cuda.synchronize()
+        for _ in range(3):
+            step()
         with ClockSampler(dev) as clk:
-            ms_step, ev_main, launches = timed(step, args.steps,
-                                               os.environ.get("FSX_PROFILER_RANGE") == "1")
-        # read the pass events now: the pooled events are re-recorded below
-        main_k1_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev_main)
-        main_tail_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_main)
-        host_us = statistics.median(host_s) * 1e6
-        # the same two kernels measured one after the other (K1 with the
-        # bulk-copy engine, then the merge): per-kernel rooflines
-        iso_steps = 0 if args.profile and not args.serial else max(5, min(args.steps, 20))
-        if args.serial and not graph_pass:
-            ev_iso = ev_main  # not re-recorded: no second timed phase
-        elif iso_steps:
+            ms_step, ev_main, launches = timed(step, args.steps)
+        tee_ms = span(ev_main, 0, 1)
+        schedules = {}
+        kernels = {}
+        if not args.profile:
+            iso = max(5, min(args.steps, 20))
             for _ in range(3):
                 step_serial()
-            _, ev_iso, _ = timed(step_serial, iso_steps)
-        else:
-            ev_iso = []
-        # Direct placement (fsx_forward_place): the forward fused with the
-        # merge -- the producer writes each row straight into the consumer's
-        # placeholder rows, no slab round trip.  Not the headline (the
-        # reference places payloads in the consumer's arena); reported beside it.
-        place_ms = None
-        if not args.profile and os.environ.get("FSX_BENCH_DIRECT", "1") == "1":
-            def step_place(record=False):
-                # the placeholder scan pipelined one pass ahead on the side
-                # stream, as in the stream-ordered pass; one copy-only launch
-                s = counter[0]
-                counter[0] += 1
-                if s > 0:
-                    stream.wait_event(merged[(s - 1) % 2])
-                cur, nxt = s % 2, (s + 1) % 2
-                fork_ev.record(stream)
-                side.wait_event(fork_ev)
-                batch.scan(side, slot=nxt)
-                scanned[nxt].record(side)
-                stream.wait_event(scanned[cur])
-                batch.place(stream, mode=N.MERGE_COPY_ONLY, slot=cur)
+            serial_ms, ev_s, _ = timed(step_serial, iso)
+            kernels["forward"] = (span(ev_s, 0, 1), fwd_bytes, "forward")
+            kernels["merge"] = (span(ev_s, 1, 2), merge_bytes, "merge")
+            for _ in range(2):
+                step_follow()
+            _, ev_f, _ = timed(step_follow, iso)
+            kernels["follow"] = (span(ev_f, 1, 2), merge_bytes, "follow")
             for _ in range(3):
                 step_place()
-            place_ms, _, place_launches = timed(step_place, max(5, min(args.steps, 20)))
-    # parity guard on the measured data: status all zero, and the merged
-    # embeddings of the timed passes equal a plain serial pass (K1, then the
-    # merge without early start or discard) of the same requests
-    for slot in (0, 1):  # both scan slots were used by the measured passes
+            place_ms, _, _ = timed(step_place, iso)
+            # the colocated pass, as a long-lived server would run it: five
+            # back-to-back 10-pass measurements in this one process
+            for _ in range(3):
+                step_colocated()
+            colo = [round(timed(step_colocated, 10)[0], 4) for _ in range(5)]
+            schedules = {
+                "tee": {"what": "scan one pass ahead || fsx_forward_merge (the timed pass)",
+                        "ms_per_step": round(ms_step, 4)},
+                "serial": {"what": "K1 (bulk-copy tiles) then the merge, stream order",
+                           "ms_per_step": round(serial_ms, 4)},
+                "colocated": {"what": "K1 || early-start merge on a high-priority stream",
+                              "runs_ms": colo, "first_ms": colo[0],
+                              "steady_median_ms": statistics.median(colo[1:])},
+                "direct_placement": {"what": "fsx_forward_place: rows straight into the prompt, "
+                                             "no slab segment (not the reference's semantics)",
+                                     "ms_per_step": round(place_ms, 4),
+                                     "payload_gbs": round(payload / (place_ms * 1e-3) / 1e9, 1)},
+            }
+            if probe:
+                schedules["tee"]["graph_probe"] = probe
+    # parity guard on the measured data: statuses all zero, and the merged
+    # embeddings of the timed passes equal a plain K1-then-merge pass
+    for slot in (0, 1):
         st = batch.status_host(slot)
         assert (st == 0).all(), st
     if not args.profile:
@@ -602,89 +544,37 @@ def run_single(args):
         del ref_b
 
     peak, peak_kind = load_peaks()
-    traffic = load_traffic()
-    kernels = {}
-    if ev_iso:
-        fwd_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev_iso)
-        mrg_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev_iso)
-        fwd_gbs = fwd_bytes / (fwd_ms * 1e-3) / 1e9
-        mrg_gbs = merge_bytes / (mrg_ms * 1e-3) / 1e9
-        kernels = {
-            "measured": ("the timed passes (--serial)" if args.serial and not graph_pass else
-                         f"{iso_steps} extra passes in the same run with K1 then the merge in "
-                         "stream order, each event-timed on its stream"),
-            "forward": {"kernel": "fsx::forward_tma_kernel (bulk-copy tiles, FSX_FWD_BULK; "
-                                  "batched: all items of the step)",
-                        "launches_per_step": fwd_launches,
-                        "ms_per_step": round(fwd_ms, 4),
-                        "algorithmic_bytes_per_launch": fwd_bytes // fwd_launches,
-                        "achieved_gbs": round(fwd_gbs, 1), "frac": round(fwd_gbs / peak, 4),
-                        "traffic": traffic.get("forward_kernel")},
-            "merge": {"kernel": merge_kernel_name() + " (merge_scan_kernel pipelined one pass "
-                                  "ahead on a side stream)",
-                      "launches_per_step": 1, "ms_per_step": round(mrg_ms, 4),
-                      "algorithmic_bytes_per_launch": merge_bytes,
-                      "achieved_gbs": round(mrg_gbs, 1), "frac": round(mrg_gbs / peak, 4),
-                      "traffic": traffic.get("merge")},
-        }
-    if args.serial:
-        dom = "merge" if kernels["merge"]["ms_per_step"] >= kernels["forward"]["ms_per_step"] else "forward"
-        k = kernels[dom]
-        roofline = {"bound": "hbm", "kernel": k["kernel"], "achieved": k["achieved_gbs"],
-                    "peak": peak, "peak_kind": f"{peak_kind} hbm_gbs (copy)", "unit": "GB/s",
-                    "frac": k["frac"], "traffic": k["traffic"],
-                    "algorithmic_bytes_per_launch": k["algorithmic_bytes_per_launch"],
-                    "frac_of_nominal_8000": round(k["achieved_gbs"] / 8000.0, 4)}
-    else:
-        # The pass: K1 (forward_tile_kernel<8>) and the early-start merge
-        # (merge_follow_kernel, one CTA per SM, FSX_MERGE_COLOCATED |
-        # FSX_MERGE_DISCARD) run concurrently; algorithmic bytes are both
-        # kernels' (2 x payload each).  Part of the slab round
-        # trip never reaches DRAM, so the rate can exceed the DRAM copy peak;
-        # the DRAM floor of the pass is src read + embedding write (2 x payload).
-        alg = fwd_bytes + merge_bytes
-        pass_gbs = alg / (ms_step * 1e-3) / 1e9
-        floor_gbs = (fwd_bytes // 2 + merge_bytes // 2) / (ms_step * 1e-3) / 1e9
-        roofline = {"bound": "hbm",
-                    "kernel": "pass: fsx::kern::forward_tile_kernel<8> || fsx::kern::merge_follow_kernel "
-                              "(colocated early start, slab lines discarded from L2 after the merge)",
-                    "achieved": round(pass_gbs, 1), "peak": peak,
-                    "peak_kind": f"{peak_kind} hbm_gbs (copy)", "unit": "GB/s",
-                    "frac": round(pass_gbs / peak, 4), "traffic": None,
-                    "traffic_note": "the two kernels overlap; ncu kernel replay serialises them and "
-                                    "under range replay the profiled merge lags K1 by ~0.95 ms, so no "
-                                    "DRAM count of the timed pass exists (per-kernel ncu traffic: "
-                                    "kernels.*; profiles/range_replay_r01i.md).  L2 reuse is shown "
-                                    "by a control instead: the merge reading a cold copy of the "
-                                    "payload (FSX_BENCH_COLD_READ=1) makes the pass ~0.06 ms slower "
-                                    "(profiles/l2_reuse_hot_cold_r01i.jsonl)",
-                    "algorithmic_bytes_per_launch": alg,
-                    "dram_floor_gbs": round(floor_gbs, 1),
-                    "dram_floor_frac": round(floor_gbs / peak, 4),
-                    "why_above_peak": "algorithmic bytes count the slab write (K1) and read (merge); "
-                                      "part of that round trip never reaches DRAM (merged rows are "
-                                      "discarded from L2 instead of written back, some reads hit "
-                                      "L2), so the pass moves fewer DRAM bytes than it counts"}
-        kernels["pipeline"] = {
-            "k1_ms": round(main_k1_ms, 4),
-            "merge_tail_after_k1_ms": round(main_tail_ms, 4),
-            "merge_stream_priority": "high"}
 
-    if place_ms:
-        place_bytes = merge_bytes + 4 * lay.total_rows  # SURVEY.md 8d merge bytes incl. the scan
-        place_gbs = place_bytes / (place_ms * 1e-3) / 1e9
-        kernels["direct_placement"] = {
-            "kernel": "fsx_forward_place: merge_scan_kernel + " + merge_kernel_name() +
-                      " reading the producer's buffers (copy-only; the scan pipelined "
-                      "one pass ahead on a side stream)",
-            "what": "the forward fused with the merge: producer rows straight into the consumer's "
-                    "placeholder rows, no slab segment (the payload crosses HBM once)",
-            "ms_per_step": round(place_ms, 4),
-            "payload_gbs": round(payload / (place_ms * 1e-3) / 1e9, 1),
-            "merged_req_per_s": round(len(reqs) / (place_ms * 1e-3), 1),
-            "launches_per_step": place_launches / max(5, min(args.steps, 20)),
-            "algorithmic_bytes_per_step": place_bytes,
-            "achieved_gbs": round(place_gbs, 1), "frac": round(place_gbs / peak, 4)}
+    def kernel_obj(name, ms, nbytes):
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        traffic, why = load_traffic(CONFIG, name, nbytes)
+        o = {"kernel": KERNELS[name], "ms_per_launch": round(ms, 4),
+             "algorithmic_bytes_per_launch": nbytes, "achieved_gbs": round(gbs, 1),
+             "frac": round(gbs / peak, 4), "traffic": traffic}
+        if traffic is None:
+            o["traffic_note"] = why
+        else:
+            o["traffic_source"] = why
+        return o
+
+    kern = {"tee": kernel_obj("tee", tee_ms, tee_bytes)}
+    for k, (ms, nb, name) in kernels.items():
+        kern[k] = kernel_obj(name, ms, nb)
+    t = kern["tee"]
+    roofline = {"bound": "hbm", "kernel": t["kernel"], "achieved": t["achieved_gbs"], "peak": peak,
+                "peak_kind": f"{peak_kind} hbm_gbs (copy, burst)", "unit": "GB/s", "frac": t["frac"],
+                "traffic": t["traffic"],
+                "algorithmic_bytes_per_launch": tee_bytes,
+                "bytes_formula": "3 x payload (item rows read once, written to the slab segment and "
+                                 "to the prompt row) + 4 B position per placeholder row",
+                "measured": "CUDA events around each tee launch on its stream, mean over the timed passes",
+                "frac_of_nominal_8000": round(t["achieved_gbs"] / 8000.0, 4),
+                "s8d_pass_bytes": s8d_pass_bytes,
+                "s8d_pass_gbs": round(s8d_pass_bytes / (ms_step * 1e-3) / 1e9, 1),
+                "s8d_note": "SURVEY 8d counts the intra-device forward (2 x payload) and the merge "
+                            "(2 x payload + positions) separately; the tee never reads the slab back"}
+    if t["traffic"] is None:
+        roofline["traffic_note"] = t["traffic_note"]
     value = payload / (ms_step * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
@@ -692,24 +582,20 @@ def run_single(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (reference synth_payload bytes, K0 on device)",
         "merged_req_per_s": round(len(reqs) / (ms_step * 1e-3), 1),
-        "config": {"workload": CONFIGS[CONFIG]["workload"] +
-                               ", intra-device forward (producer == consumer GPU) + merge" +
-                               ("" if args.serial else ", colocated pipeline (K1 || early-start merge)"),
+        "config": {"workload": CONFIGS[CONFIG]["workload"],
+                   "placement": "intra-device forward (producer == consumer GPU) + merge",
+                   "schedule": ("scan (side stream, one pass ahead) + fsx_forward_merge" +
+                                (" as one CUDA graph per pass" if step is step_graph else "")),
                    "requests_per_step": len(reqs), "payload_bytes_per_step": payload,
                    "chunk_bytes": (CHUNK_ROWS or 0) * rules.row_bytes or "single shot",
                    "prompt_rows_per_step": lay.total_rows,
                    "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush needed)"},
         "roofline": roofline,
-        "kernels": kernels,
-        "pass_schedule": {"used": (("colocated (K1 || early-start merge, flags reset per pass) "
-                                    "as one CUDA graph launch per pass" if graph_kind == "colocated"
-                                    else "stream-ordered (K1 then merge) as one CUDA graph launch per pass")
-                                   if graph_pass else "stream-ordered (K1 then merge)") if args.serial
-                          else "colocated (K1 || early-start merge)", "probe": probe},
+        "kernels": kern,
+        "schedules": schedules,
         "nvlink": {"applies": False, "why": "N=1: producer and consumer share one B200"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
-        "host_us_per_step": round(host_us, 1),
         "clocks": clk.summary(),
     }
     if not args.profile and not args.no_e2e:
@@ -732,8 +618,8 @@ def run_e2e(args, fab, reqs, rules, stream):
 
     # host->device copies per flagged chunk: 4 frames (28 MiB) -- every H2D copy
     # costs a fixed gap on the copy engine, and 7 MiB copies lose ~3 % of the
-    # PCIe rate (FSX_E2E_CHUNK_ROWS overrides; profiles/README.md)
-    e2e_chunk = int(os.environ.get("FSX_E2E_CHUNK_ROWS", "0")) or (4 * CHUNK_ROWS if CHUNK_ROWS else None)
+    # PCIe rate (profiles/e2e_chunk_sweep_r01g.jsonl)
+    e2e_chunk = 4 * CHUNK_ROWS if CHUNK_ROWS else None
     batch = DataPlaneBatch(fab, reqs, rules, src_gpu=0, dst_gpu=1, chunk_rows=e2e_chunk)
     with torch.cuda.stream(stream):
         batch.synth_inputs(stream)
@@ -754,20 +640,15 @@ def run_e2e(args, fab, reqs, rules, stream):
     # step costs the PCIe transfer plus the last chunk's merge
     from paper_2603_12118_b200 import _native as N
     mstream = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
-    overlap = os.environ.get("FSX_E2E_OVERLAP", "1") == "1"
 
     def step():
         assert batch.alloc()
         batch.forward_host(host, stream)
-        if overlap:
-            with torch.cuda.stream(mstream):
-                batch.merge(mstream, early_start=True,
-                            mode=N.MERGE_FULL | N.MERGE_COLOCATED | N.MERGE_DISCARD)
-                status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
-            mstream.synchronize()
-        else:
-            batch.merge(stream)
+        with torch.cuda.stream(mstream):
+            batch.merge(mstream, early_start=True,
+                        mode=N.MERGE_FULL | N.MERGE_COLOCATED | N.MERGE_DISCARD)
             status_h.copy_(batch.status[:len(reqs)], non_blocking=True)
+        mstream.synchronize()
         stream.synchronize()
         batch.release()
         if int(status_h.numpy().max()) != 0:
@@ -798,22 +679,49 @@ def run_e2e(args, fab, reqs, rules, stream):
             "steps": steps, "pcie_h2d_copy_gbs": round(h2d_peak, 2),
             "frac_of_pcie_h2d": round(h2d / dt / 1e9 / h2d_peak, 3),
             "path": "fsx_forward_host (pinned host -> consumer slab, per-frame chunks + flags) "
-                    "-> fsx_merge" + (" (early start on the copy's chunk flags)" if overlap else "") +
-                    " -> status D2H, wall clock per step"}
+                    "-> fsx_merge (early start on the copy's chunk flags) -> status D2H, wall clock "
+                    "per step",
+            "boundary": "per step the payload crosses PCIe host->device and the per-request merge "
+                        "status comes back; token ids, the prompt's text rows and the merge "
+                        "descriptors stay on the device across steps (the on-GPU LLM consumer owns "
+                        "them).  The reference executors send from pageable vectors: that path "
+                        "(through the drop-in C++ API) is profiles/bench_fabric_dropin_r02.jsonl"}
 
 
 # ---------------------------------------------------------------------------
 # fsx arm, N GPUs: independent producer->consumer pairs
 
+def _probe_k1(args, run_steps, red_dev, first):
+    """--k1 auto: every rank runs 5 steps with each K1 form (the consumers'
+    side is the same for all); the form with the lowest max-over-ranks
+    device time per step is used for the timed region.  Returns (form,
+    {form: ms per step}, next step number)."""
+    import torch
+    import torch.distributed as dist
+
+    if args.k1 != "auto":
+        return args.k1, {}, first
+    probe = {}
+    s = first
+    for form in K1_FORMS:
+        run_steps(form, s, 2)  # warm this form
+        s += 2
+        ms = torch.tensor([run_steps(form, s, 5)], dtype=torch.float64, device=red_dev)
+        s += 5
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        probe[form] = round(ms.item() / 5, 4)
+    return min(probe, key=probe.get), probe, s
+
+
 def run_pairs(args, rank, world):
     """One process per GPU: rank 2k pushes its encoder outputs into rank
     2k+1's receive slab over NVLink (K1 on the producer, CUDA IPC mapping);
     rank 2k+1 merges with in-kernel early start on the chunk flags (K3) and
-    acks the step into the producer's ack flag.  The consumer holds two sets
-    of slab segments (and two prompt batches) so step s+1's transfer never
+    acks the step into the producer's ack flag.  The consumer holds `--sets`
+    sets of slab segments (and prompt batches) so step s+1's transfer never
     waits for step s's merge and ack: the producer only waits for the ack of
-    step s-1 of the same set (FSX_PAIRS_SETS=1 turns that off).  No collective
-    on the data path; timing is the max over ranks of the device-timed region."""
+    step s-sets of the same set.  No collective on the data path; timing is
+    the max over ranks of the device-timed region."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -824,14 +732,14 @@ def run_pairs(args, rank, world):
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
     from paper_2603_12118_b200.fabric import DeviceFabric, _stream_ptr
 
-    local, pinned, red_dev = _rank_device(rank)
+    local, pinned, red_dev = _rank_device(args, rank)
     me = PR.role(rank, world)
     P, Cg = me.producer_gpu, me.consumer_gpu
     rules = T.RULES[CONFIG]
     reqs = T.config_requests(CONFIG, args.requests)
     lay = T.layout(reqs, rules.row_bytes)
     stream = torch.cuda.Stream(device=local)
-    sets = 1 if me.alone else max(1, int(os.environ.get("FSX_PAIRS_SETS", "2")))
+    sets = 1 if me.alone else max(1, args.sets)
     slab_bytes = max(1 << 30, sets * lay.payload_bytes + (64 << 20))
     # both logical gpus of the pair are bound to this process's device; the
     # peer's slab is imported (mapped over NVLink) under its logical id
@@ -865,12 +773,12 @@ def run_pairs(args, rank, world):
     chunk_rows = CHUNK_ROWS or max(1, max((it.rows for it in lay.items), default=1))
     chunks = [max(1, -(-it.rows // chunk_rows)) for it in lay.items]
     M = len(lay.items)
-    # Direct placement over NVLink (FSX_PAIRS_DIRECT=1): the producer writes
+    # Direct placement over NVLink (--transfer direct): the producer writes
     # each row straight into the consumer's prompt embedding and status
     # (CUDA IPC mappings of the consumer's tensors) with fsx_forward_place --
     # the forward and the merge as ONE kernel over peer memory -- and sets a
     # done flag in the consumer's ring; no slab segment, no consumer merge.
-    direct = (not me.alone) and os.environ.get("FSX_PAIRS_DIRECT") == "1"
+    direct = (not me.alone) and args.transfer == "direct"
     place_mb = []
     if direct:
         from torch.multiprocessing.reductions import reduce_tensor
@@ -892,6 +800,7 @@ def run_pairs(args, rank, world):
     for i, it in enumerate(lay.items):
         xfers[i] = N.Transfer(P, Cg, batch.src_buf.data_ptr() + int(batch.src_off[i]), 0,
                               it.rows * batch.rb, chunk_rows * batch.rb, 0, 0, None)
+    k1_opts = [0]
 
     def step(s):
         if me.alone:
@@ -916,7 +825,7 @@ def run_pairs(args, rank, world):
             view["dst_off"] = set_offs[k]
             view["flag_base"] = [fb for fb, _ in sched]
             view["token"] = [tok for _, tok in sched]
-            N.call("fsx_forward_batch", fab._h, M, xfers, 0, _stream_ptr(stream))  # one K1 launch
+            N.call("fsx_forward_batch", fab._h, M, xfers, k1_opts[0], _stream_ptr(stream))  # one K1 launch
         else:
             b = batches[k]
             for i in range(M):
@@ -926,9 +835,29 @@ def run_pairs(args, rank, world):
             b.merge(stream, early_start=True, mode=N.MERGE_FULL | N.MERGE_DISCARD)
             fab.signal_flags(P, k, 1, PR.ack_token(s), Cg, stream)
 
+    def run_steps(form, first, n):
+        k1_opts[0] = K1_FORMS[form]
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for s in range(first, first + n):
+            step(s)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
             step(s)
+        nxt = args.warmup
+        form, k1_probe = args.k1 if args.k1 != "auto" else "tile", {}
+        if not me.alone and not direct:
+            form, k1_probe, nxt = _probe_k1(args, run_steps, red_dev, nxt)
+        k1_opts[0] = K1_FORMS[form]
+        for s in range(nxt, nxt + 2):
+            step(s)
+        nxt += 2
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
@@ -936,16 +865,40 @@ def run_pairs(args, rank, world):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clk:
             start.record(stream)
-            for s in range(args.warmup, args.warmup + args.steps):
+            for s in range(nxt, nxt + args.steps):
                 step(s)
             end.record(stream)
             torch.cuda.synchronize()
         dist.barrier()
         launches = fab.stats()["kernel_launches"] - l0
+        nxt += args.steps
     e2e = _e2e_phase(args, step, stream, red_dev, PR.pairs_in(world) * lay.payload_bytes,
                      [batch.src_buf] if (me.producer or me.alone) else [],
                      (lambda s: batches[s % sets]) if consumer else None,
-                     first=args.warmup + args.steps, n_requests=PR.pairs_in(world) * len(reqs))
+                     first=nxt, n_requests=PR.pairs_in(world) * len(reqs))
+    # the copy-engine comparator: the producer copies the same items into the
+    # same peer slab segments with cudaMemcpyAsync (peer copy), event-timed
+    ce_ms = torch.zeros(1, dtype=torch.float64, device=red_dev)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if me.producer and not me.alone and not direct:
+        base = fab.slab_ptr(Cg, 0)
+        with torch.cuda.stream(stream):
+            def copies():
+                for i, it in enumerate(lay.items):
+                    N.call("fsx_copy_engine", fab._h, P, base + int(set_offs[0][i]),
+                           batch.src_buf.data_ptr() + int(batch.src_off[i]), it.rows * batch.rb,
+                           _stream_ptr(stream))
+            copies()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(5):
+                copies()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ce_ms[0] = a.elapsed_time(b) / 5
+    dist.all_reduce(ce_ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
     verified = None
     if consumer:
         for b in batches:
@@ -975,29 +928,40 @@ def run_pairs(args, rank, world):
     ms_step = ms.item() / args.steps
     if rank == 0:
         pair_gbs = lay.payload_bytes / (ms_step * 1e-3) / 1e9
+        ce = ce_ms.item()
         line = {
             "metric": METRIC, "value": round(payload_all / (ms.item() * 1e-3) / 1e9, 2),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "merged_req_per_s": round(n_pairs * len(reqs) / (ms_step * 1e-3), 1),
-            "config": {"workload": CONFIGS[CONFIG]["workload"] + ", encoder GPU 2k -> LLM GPU "
-                                   "2k+1 over NVLink (CUDA IPC slab), early-start merge on the consumer",
+            "config": {"workload": CONFIGS[CONFIG]["workload"],
+                       "placement": "encoder GPU 2k -> LLM GPU 2k+1 over NVLink (CUDA IPC slab), "
+                                    "early-start merge on the consumer",
                        "requests_per_step_per_pair": len(reqs), "pairs": n_pairs,
                        "chunk_bytes": chunk_rows * rules.row_bytes,
                        "slab_segment_sets": sets,
                        "transfer": ("direct placement: fsx_forward_place, producer rows straight "
                                     "into the consumer's prompt rows over NVLink (one kernel), "
                                     "done flag; no slab, no consumer merge") if direct else
-                                   "K1 into the consumer slab + early-start merge",
+                                   f"K1 ({form}) into the consumer slab + early-start merge",
                        "parallelism": f"{n_pairs} independent producer->consumer pairs"},
             "roofline": {"bound": "nvlink", "achieved": round(pair_gbs, 1), "peak": 770.0,
                          "unit": "GB/s", "frac": round(pair_gbs / 770.0, 4), "traffic": None,
+                         "traffic_note": "NVLink bytes: scripts/profile_round.sh nvl section "
+                                         "(nvltx__bytes / nvlrx__bytes, >= 2-GPU boxes)",
+                         "what": "payload per pair per step / max-over-ranks step time",
                          "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                          "frac_of_nominal_900": round(pair_gbs / 900.0, 4)},
+            "k1_forms": {"chosen": form, "probe_ms_per_step": k1_probe},
+            "copy_engine": ({"what": "cudaMemcpyAsync peer copies (copy engine) of the same items into "
+                                     "the same slab segments, no flags, event-timed on the producer",
+                             "ms_per_step": round(ce, 4),
+                             "pair_gbs": round(lay.payload_bytes / (ce * 1e-3) / 1e9, 1),
+                             "k1_over_copy_engine": round(ce / ms_step, 4)} if ce > 0 else None),
             "gpu_launches": int(tot_launch.item()),
             "e2e": e2e,
-            "verified": bool(args.verify),
+            "verified": bool(verified) if args.verify else False,
             "pinned_device": pinned,
             "clocks": clk.summary(),
         }
@@ -1007,18 +971,18 @@ def run_pairs(args, rank, world):
     dist.destroy_process_group()
 
 
-def _rank_device(rank):
+def _rank_device(args, rank):
     """(device, pinned, reduction device) for one rank: LOCAL_RANK's GPU with
-    NCCL for setup/timing, or every rank pinned to FSX_PAIRS_DEVICE with gloo
-    (the protocol tests on a 1-GPU box: CUDA IPC works between processes of
-    one device, NCCL does not allow that)."""
+    NCCL for setup/timing, or every rank pinned to --pin-device with gloo (the
+    protocol tests on a 1-GPU box: CUDA IPC works between processes of one
+    device, NCCL does not allow that)."""
     import torch
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", rank))
-    pinned = os.environ.get("FSX_PAIRS_DEVICE")
+    pinned = args.pin_device
     if pinned is not None:
-        local = int(pinned)
+        local = pinned
     torch.cuda.set_device(local)
     if pinned is None:
         # a rank that dies must not leave the others waiting for the default
@@ -1039,7 +1003,7 @@ def run_fanout(args, rank, world):
     it feeds (CUDA IPC) and pushes all its items of a step with one batched K1
     call over NVLink; each LLM merges with in-kernel early start and acks
     every encoder that fed it.  Every LLM holds two sets of slab segments
-    (FSX_PAIRS_SETS), so an encoder's next transfer does not wait for the
+    (--sets), so an encoder's next transfer does not wait for the
     current merge.  No collective on the data path."""
     import numpy as np
     import torch
@@ -1052,7 +1016,7 @@ def run_fanout(args, rank, world):
     from paper_2603_12118_b200.dataplane import DataPlaneBatch, _align
     from paper_2603_12118_b200.fabric import DeviceFabric, _stream_ptr
 
-    local, pinned, red_dev = _rank_device(rank)
+    local, pinned, red_dev = _rank_device(args, rank)
     rules = T.RULES[CONFIG]
     rb = rules.row_bytes
     n_prod = len(range(0, world, 2))
@@ -1063,7 +1027,7 @@ def run_fanout(args, rank, world):
     me = rank // 2  # encoder ordinal (even ranks) / LLM ordinal (odd ranks)
     stream = torch.cuda.Stream(device=local)
     fab = DeviceFabric({g: 0 for g in range(world)}, {g: local for g in range(world)})
-    sets = max(1, int(os.environ.get("FSX_PAIRS_SETS", "2")))
+    sets = max(1, args.sets)
     batch, batches = None, []
     if producer:
         fab.slab_register(rank, 1 << 20)  # ack flags: index = LLM ordinal x sets + set
@@ -1111,6 +1075,7 @@ def run_fanout(args, rank, world):
                 for k in range(sets)] if producer else []
     acks_from = pl.consumers_of(me) if producer else []
     acks_to = pl.producers_of(me) if not producer else []
+    k1_opts = [0]
 
     def step(s):
         k = s % sets
@@ -1123,7 +1088,7 @@ def run_fanout(args, rank, world):
                 view["dst_off"] = set_offs[k]
                 view["flag_base"] = [b for b, _ in sch]
                 view["token"] = [t for _, t in sch]
-                N.call("fsx_forward_batch", fab._h, len(items), xfers, 0, _stream_ptr(stream))
+                N.call("fsx_forward_batch", fab._h, len(items), xfers, k1_opts[0], _stream_ptr(stream))
         else:
             b = batches[k]
             for idx, (q, j) in enumerate(pl.consumer_items[me]):
@@ -1134,9 +1099,28 @@ def run_fanout(args, rank, world):
             for p in acks_to:
                 fab.signal_flags(pl.producers[p], me * sets + k, 1, PR.ack_token(s), rank, stream)
 
+    def run_steps(form, first, n):
+        k1_opts[0] = K1_FORMS[form]
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for s in range(first, first + n):
+            step(s)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
             step(s)
+        form, k1_probe, nxt = _probe_k1(args, run_steps, red_dev, args.warmup)
+        if args.k1 == "auto" and not k1_probe:
+            form = "tile"
+        k1_opts[0] = K1_FORMS[form]
+        for s in range(nxt, nxt + 2):
+            step(s)
+        nxt += 2
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
@@ -1144,17 +1128,18 @@ def run_fanout(args, rank, world):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clk:
             start.record(stream)
-            for s in range(args.warmup, args.warmup + args.steps):
+            for s in range(nxt, nxt + args.steps):
                 step(s)
             end.record(stream)
             torch.cuda.synchronize()
         dist.barrier()
         launches = fab.stats()["kernel_launches"] - l0
+        nxt += args.steps
     total_payload = sum(it.rows * rb for q in reqs for it in q.items)
     e2e = _e2e_phase(args, step, stream, red_dev, total_payload,
                      [src_buf] if producer else [],
                      (lambda s: batches[s % sets]) if not producer else None,
-                     first=args.warmup + args.steps, n_requests=len(reqs))
+                     first=nxt, n_requests=len(reqs))
     if not producer:
         for b in batches:
             st = b.status_host()
@@ -1191,9 +1176,10 @@ def run_fanout(args, rank, world):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "merged_req_per_s": round(len(reqs) / (ms_step * 1e-3), 1),
-            "config": {"workload": CONFIGS[CONFIG]["workload"] + ", encoders on even ranks -> LLM "
-                                   "replicas on odd ranks, reference select_replica placement "
-                                   "(fan-out / fan-in over NVLink), early-start merge",
+            "config": {"workload": CONFIGS[CONFIG]["workload"],
+                       "placement": "encoders on even ranks -> LLM replicas on odd ranks, reference "
+                                    "TaskDispatcher placement (fan-out / fan-in over NVLink), "
+                                    f"K1 ({form}), early-start merge",
                        "requests_per_step": len(reqs), "requests_per_encoder": args.requests,
                        "encoders": len(pl.producers), "llms": len(pl.consumers),
                        "fan_out": fan_out, "fan_in": fan_in,
@@ -1205,6 +1191,7 @@ def run_fanout(args, rank, world):
                          "what": "busiest GPU's NVLink direction (max encoder egress / LLM ingress)",
                          "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                          "frac_of_nominal_900": round(busiest / 900.0, 4)},
+            "k1_forms": {"chosen": form, "probe_ms_per_step": k1_probe},
             "gpu_launches": int(tot_launch.item()),
             "e2e": e2e,
             "verified": bool(args.verify),
@@ -1267,17 +1254,37 @@ def _e2e_phase(args, step, stream, red_dev, payload_all, src_bufs, recv_batch, f
                     "per step, max over ranks"}
 
 
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks of this
+    script with the torchrun environment (RANK, LOCAL_RANK, WORLD_SIZE,
+    MASTER_ADDR=127.0.0.1, MASTER_PORT) and wait for all; rank 0 prints the
+    line.  Returns the worst exit code."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
 def main():
     global CONFIG, REQUESTS, CHUNK_ROWS
     args = parse()
-    if os.environ.get("FSX_HANG_DUMP_S"):  # debugging aid: dump every thread's stack, exit
-        import faulthandler
-        faulthandler.dump_traceback_later(float(os.environ["FSX_HANG_DUMP_S"]), exit=True)
     CONFIG = args.config
     REQUESTS = CONFIGS[CONFIG]["requests"]
-    CHUNK_ROWS = CONFIGS[CONFIG]["chunk_rows"]
+    CHUNK_ROWS = args.chunk_rows or CONFIGS[CONFIG]["chunk_rows"]
     if args.requests is None:
         args.requests = REQUESTS
+    if args.gpus > 1 and "RANK" not in os.environ and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     if args.impl == "reference":

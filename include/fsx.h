@@ -383,6 +383,13 @@ int fsx_pointer_device(const void* p, int* device);
  * borrowed span, e.g. backlogged sends, sidecar.hpp:327). */
 int fsx_copy_to_host(void* h_dst, const void* d_src, int64_t n);
 
+/* The copy-engine comparator (BASELINE.json configs[4]: "vs cudaMemcpyPeer"):
+ * cudaMemcpyAsync(d_dst, d_src, n, cudaMemcpyDefault) on `stream` of src_gpu's
+ * device -- a peer copy over NVLink when d_dst is a peer or IPC-mapped slab.
+ * No chunk flags, no digest: timed beside K1 for the same bytes. */
+int fsx_copy_engine(fsx_fabric* f, int src_gpu, void* d_dst, const void* d_src, int64_t n,
+                    void* stream);
+
 /* ---- stats ----------------------------------------------------------------
  * SidecarStats (sidecar.hpp:209-217, 403-415) device-side counterparts plus
  * the number of fsx kernels launched (bench "gpu_launches"). */

@@ -1331,6 +1331,23 @@ int fsx_synth_payload(fsx_fabric* f, int gpu, uint64_t seed, void* d_dst, int64_
   return FSX_OK;
 }
 
+int fsx_copy_engine(fsx_fabric* f, int src_gpu, void* d_dst, const void* d_src, int64_t n,
+                    void* stream) {
+  int ordinal = 0;
+  int rc = find_gpu(f, src_gpu, &ordinal);
+  if (rc) return rc;
+  if (n < 0) return fail(FSX_E_VALIDATION, "negative byte count");
+  Device* dev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    rc = device_state(f, ordinal, &dev);
+    if (rc) return rc;
+  }
+  FSX_CUDA(cudaSetDevice(ordinal));
+  if (n) FSX_CUDA(cudaMemcpyAsync(d_dst, d_src, n, cudaMemcpyDefault, pick_stream(dev, stream)));
+  return FSX_OK;
+}
+
 int fsx_pointer_device(const void* p, int* device) {
   *device = -1;
   if (!p) return FSX_OK;
