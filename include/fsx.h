@@ -379,6 +379,13 @@ int fsx_read_u64(fsx_fabric* f, int gpu, const uint64_t* d, uint64_t* h, void* s
  * Lets the send(span) entry point (sidecar.hpp:302) take a producer tensor that
  * already lives on the GPU down the K1 path instead of the host copy path. */
 int fsx_pointer_device(const void* p, int* device);
+/* What a send() source span is: *kind = 0 pageable (or unknown) host memory,
+ * 1 pinned host memory (page-locked / registered: the DMA reads it
+ * asynchronously), 2 device or managed memory.  Never fails. */
+#define FSX_PTR_PAGEABLE 0
+#define FSX_PTR_PINNED 1
+#define FSX_PTR_DEVICE 2
+int fsx_pointer_kind(const void* p, int* kind);
 /* Synchronous device->host copy (owning a device payload that must outlive a
  * borrowed span, e.g. backlogged sends, sidecar.hpp:327). */
 int fsx_copy_to_host(void* h_dst, const void* d_src, int64_t n);

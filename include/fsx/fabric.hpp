@@ -72,6 +72,14 @@ struct SidecarConfig {
   // fsx additions
   int64_t device_chunk_bytes = int64_t{8} << 20;  // flag granularity of K1 pushes
   int64_t wait_timeout_us = 30'000'000;            // GPU completion watchdog
+  // send() borrows its span for the call only (sidecar.hpp:302, 327).  A
+  // pageable host span is fully copied out before the copy call returns, so
+  // send() then returns without waiting for the bytes to land; the delivery
+  // waits instead (if it comes first).  Device spans and pinned host spans
+  // are read by the GPU asynchronously, so send() waits for them -- unless
+  // the caller keeps them unchanged until the delivery (stream-ordered
+  // producers), which this flag declares.
+  bool async_borrowed_sources = false;
 
   double latency_ms(Transport t, int64_t bytes) const {
     const double mb = static_cast<double>(bytes) / (1024.0 * 1024.0);
@@ -203,6 +211,17 @@ class Fabric {
   using ChunkCallback = std::function<void(const Envelope&, std::vector<uint8_t>)>;
   using RefErrorCallback = std::function<void(const Error&)>;
   using RawChunkCallback = std::function<void(const Envelope&, int64_t)>;
+  // Early start (fsx addition): the segment's offset plus the chunk flags its
+  // bytes are landing under -- chunk c is in the slab once flag
+  // flag_base + c of the destination GPU equals token (fsx_stream_wait_flags,
+  // an early-start fsx_merge, fsx_wait, fsx_chunk_ready).
+  struct ChunkFlags {
+    int64_t flag_base = 0;
+    int32_t n_chunks = 0;  // 0: already landed (small message / staged network arrival)
+    uint64_t token = 0;
+    int64_t chunk_bytes = 0;
+  };
+  using EarlyChunkCallback = std::function<void(const Envelope&, int64_t offset, const ChunkFlags&)>;
   using FailureHandler = std::function<void(const std::string&, const std::string&, const Error&)>;
 
   // devices: logical gpu -> CUDA ordinal (missing -> gpu % device_count).
@@ -259,6 +278,27 @@ class Fabric {
     RefState& st = refs_[key_of(ref_id, gpu)];
     st.dst_gpu = gpu;
     st.raw_cb = std::move(on_chunk);
+    st.on_error = std::move(on_error);
+    st.has_interest = true;
+    drain(st);
+  }
+
+  // Early-start interest (no reference counterpart; SURVEY.md 7 "hard parts"):
+  // like register_interest_raw, but the callback runs when the payload is
+  // PLACED -- on the sender's event, before the bytes have landed and before
+  // the modeled delivery latency -- with the chunk flags that gate each
+  // chunk, so a device consumer (an early-start merge, a prefill gated by
+  // fsx_stream_wait_flags) can start on chunk 0 while later chunks are still
+  // in flight.  Chunks are handed over in placement order (env.seq tells the
+  // consumer where each goes); the consumer owns the segment until ack_raw.
+  void register_interest_early(int gpu, const std::string& ref_id, EarlyChunkCallback on_chunk,
+                               RefErrorCallback on_error = {}) {
+    node_of(gpu);
+    RefState& st = refs_[key_of(ref_id, gpu)];
+    st.dst_gpu = gpu;
+    st.early_cb = std::move(on_chunk);
+    st.on_chunk = nullptr;
+    st.raw_cb = nullptr;
     st.on_error = std::move(on_error);
     st.has_interest = true;
     drain(st);
@@ -431,11 +471,19 @@ class Fabric {
  private:
   // A delivered chunk waiting for its turn: envelope, slab offset, and the
   // small-message ticket (fsx_put_small) whose read-back it owns, or -1.
+  // Chunk flags of a placement still in flight (n_chunks 0: landed).
+  struct Landing {
+    int64_t flag_base = 0;
+    int32_t n_chunks = 0;
+    uint64_t token = 0;
+  };
+
   struct Parked {
     Envelope env;
     int64_t off = -1;
     int64_t ticket = -1;
     bool network = false;  // arrived as a network frame: verify the sender's checksum64
+    Landing landing;       // waited for before the bytes are handed over
   };
 
   struct RefState {
@@ -444,6 +492,7 @@ class Fabric {
     bool has_interest = false;
     ChunkCallback on_chunk;
     RawChunkCallback raw_cb;
+    EarlyChunkCallback early_cb;  // handed the segment at placement, before it lands
     RefErrorCallback on_error;
     int64_t next_seq = 0;
     std::map<int64_t, Parked> parked;  // by seq
@@ -571,18 +620,52 @@ class Fabric {
     int32_t n_chunks = 1;
     if (!start_copy(ps, &off, &token, &flag_base, &n_chunks, &ticket)) return false;
     // The source is borrowed (caller span) or owned by a Pending about to be
-    // dropped, so the copy completes before we return, exactly like the
-    // reference's memcpy into the arena (sidecar.hpp:470); a small message has
-    // been staged in the pinned mailbox instead and is waited for at delivery.
-    // The batched C ABI (fsx_forward on a stream) is the asynchronous path.
-    if (ticket < 0) wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    // dropped.  Where the GPU still reads it after the copy call -- a device
+    // span under K1, a pinned host span under DMA -- the copy completes before
+    // we return, like the reference's memcpy into the arena (sidecar.hpp:470).
+    // A pageable host span has been copied out of by then (fsx_forward_host
+    // stages it), and a small message sits in the pinned mailbox: send()
+    // returns at once and the delivery waits for the landing instead.
+    Landing landing{flag_base, ticket < 0 ? n_chunks : 0, token};
+    if (ticket < 0 && source_still_read(ps)) {
+      wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+      landing.n_chunks = 0;
+    }
     if (digest_slot_) check(fsx_read_u64(h_, ps.env.src_gpu, digest_slot_, &ps.env.checksum, nullptr));
     ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
     const double lat = config_.latency_ms(Transport::LocalBuffer, ps.env.chunk_bytes);
     added_latency_ms_ += lat;
+    if (hand_over_early(ps.env, off, ticket, landing)) return true;
     auto env = std::make_shared<Envelope>(ps.env);
     Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.deliver",
-                     [this, env, off, ticket] { deliver(*env, off, ticket); });
+                     [this, env, off, ticket, landing] { deliver(*env, off, ticket, false, landing); });
+    return true;
+  }
+
+  // Does the GPU read the sender's bytes after the copy call returned?
+  bool source_still_read(const Pending& ps) const {
+    if (config_.async_borrowed_sources || ps.env.chunk_bytes == 0) return false;
+    if (ps.src_is_device) return true;
+    if (ps.owned) return false;  // our own pageable copy (backlog / network)
+    int kind = 0;
+    return fsx_pointer_kind(ps.src, &kind) == FSX_OK && kind == 1;  // pinned: DMA reads it
+  }
+
+  // An early-start consumer takes the segment at placement (see
+  // register_interest_early); false when the ref has none.
+  bool hand_over_early(const Envelope& env, int64_t off, int64_t ticket, const Landing& landing) {
+    auto it = refs_.find(key_of(env.ref_id, env.dst_gpu));
+    if (it == refs_.end() || !it->second.early_cb) return false;
+    RefState& st = it->second;
+    if (st.request_id.empty()) st.request_id = env.request_id;
+    drop_ticket(ticket);  // a staged small message: in the slab once its batch ran
+    ChunkFlags cf{landing.flag_base, landing.n_chunks, landing.token,
+                  landing.n_chunks > 1 ? std::min<int64_t>(config_.device_chunk_bytes, env.chunk_bytes)
+                                       : env.chunk_bytes};
+    ++transfers_;
+    bytes_forwarded_ += env.chunk_bytes;
+    raw_held_.insert({env.dst_gpu, off});
+    st.early_cb(env, off, cf);
     return true;
   }
 
@@ -599,17 +682,19 @@ class Fabric {
   }
 
   // sidecar.hpp:498-525
-  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1, bool network = false) {
+  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1, bool network = false,
+               Landing landing = {}) {
     const std::string key = key_of(env.ref_id, env.dst_gpu);
     RefState& st = refs_[key];
     if (st.request_id.empty()) st.request_id = env.request_id;
     if (st.failed) {
       drop_ticket(ticket);
+      settle(landing, env.dst_gpu);  // no segment is reused while bytes still land in it
       release_segment(env.dst_gpu, off);
       place_backlog(env.dst_gpu);
       return;
     }
-    st.parked.emplace(env.seq, Parked{env, off, ticket, network});
+    st.parked.emplace(env.seq, Parked{env, off, ticket, network, landing});
     if (st.has_interest) {
       drain(st);
       return;
@@ -626,6 +711,7 @@ class Fabric {
     if (p == it->second.parked.end()) return;
     const int slab = p->second.env.dst_gpu;
     drop_ticket(p->second.ticket);
+    settle(p->second.landing, slab);
     release_segment(slab, p->second.off);
     it->second.parked.erase(p);
     ++orphan_reclaims_;
@@ -640,7 +726,22 @@ class Fabric {
       const int64_t off = it->second.off;
       const int64_t ticket = it->second.ticket;
       const bool network = it->second.network;
+      const Landing landing = it->second.landing;
       st.parked.erase(it);
+      if (st.early_cb) {  // early interest registered after the placement
+        drop_ticket(ticket);
+        ++transfers_;
+        bytes_forwarded_ += env.chunk_bytes;
+        ++st.next_seq;
+        raw_held_.insert({env.dst_gpu, off});
+        ChunkFlags cf{landing.flag_base, landing.n_chunks, landing.token,
+                      landing.n_chunks > 1 ? std::min<int64_t>(config_.device_chunk_bytes, env.chunk_bytes)
+                                           : env.chunk_bytes};
+        st.early_cb(env, off, cf);
+        continue;
+      }
+      // a send that returned before its bytes landed: the delivery waits
+      settle(landing, env.dst_gpu);
       if (st.raw_cb) {
         drop_ticket(ticket);  // waits until the bytes are in the slab
         ++transfers_;
@@ -696,9 +797,15 @@ class Fabric {
   void drop_parked(RefState& st) {
     for (auto& [seq, e] : st.parked) {
       drop_ticket(e.ticket);
+      settle(e.landing, e.env.dst_gpu);
       release_segment(e.env.dst_gpu, e.off);
     }
     st.parked.clear();
+  }
+
+  // Wait for a placement still in flight (send returned before it landed).
+  void settle(const Landing& l, int dst) {
+    if (l.n_chunks > 0) wait_landed(dst, l.flag_base, l.n_chunks, l.token);
   }
 
   // Wait for a small message's copy and read-back, then recycle its mailbox

@@ -174,6 +174,7 @@ _SIGS = {
     "fsx_u64_slot": [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_void_p],
     "fsx_read_u64": [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
     "fsx_pointer_device": [C.c_void_p, C.POINTER(C.c_int)],
+    "fsx_pointer_kind": [C.c_void_p, C.POINTER(C.c_int)],
     "fsx_copy_to_host": [C.c_void_p, C.c_void_p, C.c_int64],
     "fsx_copy_engine": [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_get_stats": [C.c_void_p, C.POINTER(Stats)],

@@ -253,7 +253,8 @@ struct TileRef {
   int64_t beg, end;
 };
 
-__device__ __forceinline__ TileRef tile_of(const FwdBatch& b, int64_t gt) {
+template <class Batch>
+__device__ __forceinline__ TileRef tile_of(const Batch& b, int64_t gt) {
   TileRef t;
   t.i = 0;
   while (gt >= b.unit_off[t.i + 1]) ++t.i;
@@ -277,7 +278,8 @@ __device__ __forceinline__ TileRef tile_of(const FwdBatch& b, int64_t gt) {
 // 8 x 16 B loads (the producer's source is read once: L2 evict_first), then
 // its stores; the CTA barriers and thread 0 counts the tile (protocol above).
 // Optional fused dg64 of the source bytes (one atomic per tile).
-__global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid_constant__ FwdBatch b) {
+template <int CAP>
+__global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid_constant__ FwdBatchT<CAP> b) {
   __shared__ uint64_t red[kTileThreads / 32];
   const TileRef tr = tile_of(b, blockIdx.x);
   const FwdArgs& a = b.t[tr.i];
@@ -391,7 +393,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // has landed; then the thread waits for the stores to complete, orders them
 // (async proxy) before its generic acq_rel count, and the tile is counted like
 // the register form.  Bytes in flight cost shared memory, not registers.
-__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatch b) {
+template <int CAP>
+__global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__ FwdBatchT<CAP> b) {
   extern __shared__ __align__(128) uint8_t tile_mem[];
   __shared__ __align__(8) uint64_t bars[2];
   if (threadIdx.x != 0) return;
@@ -764,7 +767,11 @@ __global__ void __launch_bounds__(kMergeThreads, kTeeMinBlocks) merge_tee_kernel
 // FSX_MERGE_COLOCATED (producer on this GPU): gpu-scope acquires, and the
 // launcher caps the grid at one CTA per SM so spinning merge warps never take
 // every slot K1 needs.  FSX_MERGE_DISCARD drops merged slab lines from L2.
-__global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merge_batch b) {
+// Three CTAs per SM with 8 x 16 B per lane in flight, like the tee (two CTAs
+// at 16 x 16 B: 0.161 ms alone on config B, 0.89 of the copy peak).
+constexpr int kFollowMinBlocks = 3;
+constexpr int kFollowUnroll = 8;
+__global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocks) merge_follow_kernel(fsx_merge_batch b) {
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kMergeWarps;
   const int64_t w = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
@@ -814,8 +821,8 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_follow_kernel(fsx_merg
     const uint8_t* src = item_src + j * rb;
     // the prompt rows are written once and not re-read here: evict them from
     // L2 first, so they do not push out slab rows the producer has just written
-    warp_move_row(src, static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb, nullptr, rb, lane,
-                  /*coherent=*/true, 1, -1);
+    warp_move_row<kFollowUnroll>(src, static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb, nullptr,
+                                 rb, lane, /*coherent=*/true, 1, -1);
     if (discard) discard_row(src, rb, lane);
   }
 }
@@ -930,9 +937,9 @@ cudaError_t set_spin_timeout(uint64_t ns) {
   return cudaMemcpyToSymbol(c_spin_timeout_ns, &ns, sizeof(ns));
 }
 
-int merge_copy_blocks_per_sm() {
+int merge_follow_blocks_per_sm() {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_copy_kernel, kMergeThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_follow_kernel, kMergeThreads, 0) !=
       cudaSuccess)
     return 1;
   return n > 0 ? n : 1;
@@ -940,7 +947,16 @@ int merge_copy_blocks_per_sm() {
 
 int forward_tile_bytes() { return kTileThreads * kTileVecs * 16; }
 
-cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s) {
+// One launch with the parameter block cut to CAP transfers.
+template <int CAP>
+cudaError_t launch_forward_cap(const FwdBatch& full, bool bulk, cudaStream_t s) {
+  FwdBatchT<CAP> b;
+  b.n = full.n;
+  b.l2_keep_dst = full.l2_keep_dst;
+  b.peer_gpu_count = full.peer_gpu_count;
+  b._pad = 0;
+  for (int k = 0; k <= full.n; ++k) b.unit_off[k] = full.unit_off[k];
+  for (int k = 0; k < full.n; ++k) b.t[k] = full.t[k];
   const int64_t tiles = b.unit_off[b.n];
   if (tiles <= 0) return cudaSuccess;
   if (bulk) {
@@ -954,15 +970,22 @@ cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s) {
       int dev = 0;
       cudaGetDevice(&dev);
       if (dev < kMaxDevices && !attr_set[dev]) {
-        cudaFuncSetAttribute(forward_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaTileBytes);
+        cudaFuncSetAttribute(forward_tma_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTmaTileBytes);
         attr_set[dev] = true;
       }
-      forward_tma_kernel<<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
+      forward_tma_kernel<CAP><<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
       return cudaGetLastError();
     }
   }
-  forward_tile_kernel<<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
+  forward_tile_kernel<CAP><<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
   return cudaGetLastError();
+}
+
+cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s) {
+  if (b.n <= 1) return launch_forward_cap<1>(b, bulk, s);
+  if (b.n <= 8) return launch_forward_cap<8>(b, bulk, s);
+  return launch_forward_cap<kFwdMaxBatch>(b, bulk, s);
 }
 
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s) {
@@ -998,7 +1021,7 @@ cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches) {
+cudaError_t launch_merge(const fsx_merge_batch& b, cudaStream_t s, int* launches) {
   *launches = 0;
   if (b.num_requests <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
@@ -1017,7 +1040,7 @@ cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : copy_grid;
+    const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : (int64_t)sms * merge_follow_blocks_per_sm();
     merge_follow_kernel<<<(unsigned)(need < cap ? need : cap), kMergeThreads, 0, s>>>(b);
   } else {
     merge_copy_kernel<<<(unsigned)need, kMergeThreads, 0, s>>>(b);
@@ -1046,8 +1069,12 @@ cudaError_t preload_kernels() {
   // the colocated early-start pass come up in its slow mode,
   // profiles/colocated_bimodality_r01k.md.)
   const void* fns[] = {
-      reinterpret_cast<const void*>(forward_tma_kernel),
-      reinterpret_cast<const void*>(forward_tile_kernel),
+      reinterpret_cast<const void*>(forward_tma_kernel<1>),
+      reinterpret_cast<const void*>(forward_tma_kernel<8>),
+      reinterpret_cast<const void*>(forward_tma_kernel<kFwdMaxBatch>),
+      reinterpret_cast<const void*>(forward_tile_kernel<1>),
+      reinterpret_cast<const void*>(forward_tile_kernel<8>),
+      reinterpret_cast<const void*>(forward_tile_kernel<kFwdMaxBatch>),
       reinterpret_cast<const void*>(merge_tee_kernel),
       reinterpret_cast<const void*>(set_flags_kernel),
       reinterpret_cast<const void*>(chan_push_kernel),

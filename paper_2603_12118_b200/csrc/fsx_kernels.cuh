@@ -33,15 +33,20 @@ struct FwdArgs {
 // parameter space: ~8.5 KB of the 32 KB sm_100 allows, so a 64-image batch is
 // one launch instead of four back-to-back launches with four tails): units
 // are laid out transfer-major, chunk-major.
+// The launch copies only a block sized to the batch (FwdBatchT<1 | 8 | 64>):
+// kernel parameters are copied per launch, and the full 64-transfer block
+// (~8.5 KB) alone cost ~1.5 us per K1 launch, the floor of small transfers.
 constexpr int kFwdMaxBatch = FSX_FWD_MAX_BATCH;
-struct FwdBatch {
+template <int CAP>
+struct FwdBatchT {
   int32_t n;
   int32_t l2_keep_dst;     // slab stores with L2 evict_last (consumer merges next)
   int32_t peer_gpu_count;  // peer chunks: count tiles at gpu scope, publish once at sys scope
   int32_t _pad;
-  int64_t unit_off[kFwdMaxBatch + 1];
-  FwdArgs t[kFwdMaxBatch];
+  int64_t unit_off[CAP + 1];
+  FwdArgs t[CAP];
 };
+using FwdBatch = FwdBatchT<kFwdMaxBatch>;
 
 // The tee (fsx_forward_merge): per item of one launch, where its slab copy goes
 // and how its chunks complete.  Pieces are rows: chunk c of an item holds rows
@@ -120,9 +125,8 @@ cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s);
 cudaError_t launch_set_flags(const FlagSetArgs& a, cudaStream_t s);
 cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token, cudaStream_t s);
-// Scan and/or row copy per b.mode; `copy_grid` caps the early-start
-// (persistent) grid.
-cudaError_t launch_merge(const fsx_merge_batch& b, int copy_grid, cudaStream_t s, int* launches);
+// Scan and/or row copy per b.mode.
+cudaError_t launch_merge(const fsx_merge_batch& b, cudaStream_t s, int* launches);
 // The tee kernel over items [tb.i0, tb.i0 + tb.n) (positions / statuses from a
 // scan already ordered before it on `s`).
 cudaError_t launch_merge_tee(const fsx_merge_batch& b, const TeeBatch& tb, cudaStream_t s);
@@ -134,8 +138,8 @@ cudaError_t launch_synth(uint64_t seed, uint8_t* dst, int64_t n, int grid, cudaS
 // Device spin watchdog (spin_until traps after this long), current device.
 cudaError_t set_spin_timeout(uint64_t ns);
 
-// K1 tile bytes (one CTA per tile) and the merge copy kernel's occupancy.
+// K1 tile bytes (one CTA per tile) and the early-start merge's occupancy.
 int forward_tile_bytes();
-int merge_copy_blocks_per_sm();
+int merge_follow_blocks_per_sm();
 
 }  // namespace fsx

@@ -184,7 +184,6 @@ struct Device {
   uint32_t* counters = nullptr;
   Ring counter_ring;
   int sms = 0;
-  int merge_grid = 0;
   uint64_t* state = nullptr;  // channel head/tail counters (kStatePool u64)
   int64_t state_next = 0;
   uint64_t* scratch = nullptr;  // short-lived u64 slots (digests), ring
@@ -325,7 +324,6 @@ int device_state(fsx_fabric* f, int ordinal, Device** out) {
     const double secs = e ? std::atof(e) : 30.0;
     FSX_CUDA(fsx::set_spin_timeout((uint64_t)(std::max(secs, 0.001) * 1e9)));
   }
-  d->merge_grid = d->sms * fsx::merge_copy_blocks_per_sm();
   *out = d.get();
   f->devices.emplace(ordinal, std::move(d));
   return FSX_OK;
@@ -1181,7 +1179,7 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
   }
   FSX_CUDA(cudaSetDevice(ordinal));
   int launched = 0;
-  cudaError_t e = fsx::launch_merge(*b, dev->merge_grid, pick_stream(dev, stream), &launched);
+  cudaError_t e = fsx::launch_merge(*b, pick_stream(dev, stream), &launched);
   f->launches += launched;
   if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge launch: ") + cudaGetErrorString(e));
   if (base_mode != FSX_MERGE_SCAN_ONLY) {
@@ -1254,7 +1252,7 @@ int fsx_forward_merge(fsx_fabric* f, int32_t n, fsx_transfer* t, const fsx_merge
     fsx_merge_batch scan = *b;
     scan.mode = FSX_MERGE_SCAN_ONLY;
     int launched = 0;
-    const cudaError_t e = fsx::launch_merge(scan, dev->merge_grid, st, &launched);
+    const cudaError_t e = fsx::launch_merge(scan, st, &launched);
     if (e != cudaSuccess) return fail(FSX_E_INTERNAL, std::string("merge scan launch: ") + cudaGetErrorString(e));
     f->launches += launched;
   }
@@ -1357,6 +1355,19 @@ int fsx_pointer_device(const void* p, int* device) {
     return FSX_OK;
   }
   if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) *device = a.device;
+  return FSX_OK;
+}
+
+int fsx_pointer_kind(const void* p, int* kind) {
+  *kind = FSX_PTR_PAGEABLE;
+  if (!p) return FSX_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return FSX_OK;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) *kind = FSX_PTR_DEVICE;
+  else if (a.type == cudaMemoryTypeHost) *kind = FSX_PTR_PINNED;
   return FSX_OK;
 }
 
