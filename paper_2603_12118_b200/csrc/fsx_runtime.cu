@@ -16,6 +16,8 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -213,22 +215,88 @@ bool is_pinned_host(const void* p) {
 
 // memcpy of a large piece on up to 4 threads (first-touched pageable source,
 // pinned destination: one core moves ~15 GB/s on the B200 hosts)
+// Persistent host copy workers for staging pageable spans (thread creation
+// per piece cost more than the copy of a 2 MiB part).  min(8, cores / 2)
+// threads; par_memcpy splits a piece across them and the calling thread.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  int workers() const { return static_cast<int>(threads_.size()); }
+  // Run fn(0..n-1) with part 0 on the caller; returns when all are done.
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> one(run_mu_);  // one job at a time (several devices may stage)
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &fn;
+      parts_ = n;
+      next_ = 1;
+      pending_ = n - 1;
+      ++epoch_;
+    }
+    cv_.notify_all();
+    fn(0);
+    for (;;) {  // help with parts not yet claimed
+      int k;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (next_ >= parts_) break;
+        k = next_++;
+      }
+      fn(k);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const int n = static_cast<int>(std::min(8u, hw / 2));
+    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
+    for (auto& t : threads_) t.detach();  // live for the process (static pool)
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return epoch_ != seen && job_ && next_ < parts_; });
+      seen = epoch_;
+      while (job_ && next_ < parts_) {
+        const int k = next_++;
+        const std::function<void(int)>* job = job_;
+        lk.unlock();
+        (*job)(k);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t epoch_ = 0;
+  std::vector<std::thread> threads_;
+};
+
 void par_memcpy(uint8_t* dst, const uint8_t* src, int64_t n) {
-  const int64_t parts = std::min<int64_t>(4, std::max<int64_t>(1, n / (int64_t{2} << 20)));
+  CopyPool& pool = CopyPool::get();
+  const int64_t parts = std::min<int64_t>(pool.workers() + 1, std::max<int64_t>(1, n / (int64_t{1} << 20)));
   if (parts < 2) {
     std::memcpy(dst, src, (size_t)n);
     return;
   }
   const int64_t per = (n / parts + 63) / 64 * 64;
-  std::thread th[3];
-  for (int64_t t = 1; t < parts; ++t) {
+  pool.run(static_cast<int>(parts), [=](int t) {
     const int64_t b = t * per, e = std::min(n, b + per);
-    th[t - 1] = std::thread([=] {
-      if (e > b) std::memcpy(dst + b, src + b, (size_t)(e - b));
-    });
-  }
-  std::memcpy(dst, src, (size_t)std::min(n, per));
-  for (int64_t t = 1; t < parts; ++t) th[t - 1].join();
+    if (e > b) std::memcpy(dst + b, src + b, (size_t)(e - b));
+  });
 }
 
 constexpr size_t kEventRing = 1024;

@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """K1 sweep on one B200 (intra-device forward, HBM-bound, 2 x payload bytes):
 chunk-size sweep of BASELINE config E plus the config-B video item, timed with
-CUDA events on the launching stream.  Tuning knobs come from the environment
-(FSX_FWD_VARIANT, FSX_FWD_UNIT).  Prints one JSON line per size; compares with
-cudaMemcpyAsync D2D (torch copy_) of the same bytes.
+CUDA events on the launching stream.  Prints one JSON line per size; compares
+with cudaMemcpyAsync D2D (torch copy_) of the same bytes.
 
   --graph   capture the repetitions of both arms in a CUDA graph and time the
             replay: kernel throughput without the per-call host path (which
-            dominates below ~16 MiB when each call goes through Python)."""
+            dominates below ~16 MiB when each call goes through Python).
+  --flush   (with --graph) write a 256 MiB buffer before every repetition so
+            each copy reads its source from HBM, not L2; the flush-only graph
+            is timed too and subtracted."""
 from __future__ import annotations
 
 import json
@@ -26,6 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--bulk", action="store_true", help="bulk-copy K1 tiles (FSX_FWD_BULK)")
+    ap.add_argument("--flush", action="store_true", help="L2 flush before every repetition (--graph)")
     ap.add_argument("--cpu-ref", action="store_true",
                     help="also time the reference CPU forward (oracle/_ref SidecarFabric, 1 thread) per size")
     args = ap.parse_args()
@@ -44,8 +47,7 @@ def main():
     src = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     fab.synth(0, 1234, src.data_ptr(), src.numel())
     ref = torch.empty_like(src)
-    variant = os.environ.get("FSX_FWD_VARIANT", "4")
-    unit = os.environ.get("FSX_FWD_UNIT", "32768")
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
     cases = [(n, 0) for n in sizes] + [(117_440_512, 7_340_032), (256 << 20, 1 << 20),
                                        (256 << 20, 64 << 10)]
     for n, chunk in cases:
@@ -61,14 +63,23 @@ def main():
             torch.cuda.synchronize()
             if args.graph:
                 fb = fab.flags_alloc(1, nch)
-                g, gc = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                g, gc, gf = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     for _ in range(reps):  # fixed flags/token: nobody waits on them here
+                        if flush_buf is not None:
+                            flush_buf.fill_(1)
                         fab.forward(0, src.data_ptr(), 1, off, n, chunk, fb, s, token=(1 << 40) + n,
                                     host_notify=False, bulk=args.bulk)
                 with torch.cuda.graph(gc, stream=s):
                     for _ in range(reps):
+                        if flush_buf is not None:
+                            flush_buf.fill_(1)
                         ref[:n].copy_(src[:n])
+                if flush_buf is not None:
+                    with torch.cuda.graph(gf, stream=s):
+                        for _ in range(reps):
+                            flush_buf.fill_(1)
+                    gf.replay()
                 g.replay()
                 gc.replay()
                 torch.cuda.synchronize()
@@ -93,6 +104,14 @@ def main():
             c1.record(s)
             c1.synchronize()
             cms = c0.elapsed_time(c1) / reps
+            if flush_buf is not None and args.graph:
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(s)
+                gf.replay()
+                f1.record(s)
+                f1.synchronize()
+                fms = f0.elapsed_time(f1) / reps
+                ms, cms = ms - fms, cms - fms
         fab.slab_free(1, off)
         cpu = {}
         if cref is not None and chunk == 0:
@@ -100,7 +119,8 @@ def main():
             secs = cref.ref_forward_bench(n, iters, 1)
             cpu = {"cpu_ref_us": round(secs / iters * 1e6, 1),
                    "cpu_ref_payload_gbs": round(n * iters / secs / 1e9, 3), "cpu_ref_threads": 1}
-        print(json.dumps({"variant": "bulk" if args.bulk else variant, "graph": args.graph, "bytes": n, **cpu, "chunk_bytes": chunk,
+        print(json.dumps({"k1": "bulk" if args.bulk else "tile", "graph": args.graph,
+                          "l2_flush": bool(args.flush and args.graph), "bytes": n, **cpu, "chunk_bytes": chunk,
                           "chunks": nch, "us": round(ms * 1e3, 2),
                           "hbm_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),
                           "memcpy_us": round(cms * 1e3, 2),

@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """Config E (BASELINE.json configs[4]): chunk-size sweep of the P2P forward at
 2 / 4 / 8 GPUs of one box -- disjoint producer->consumer pairs 0->1, 2->3, ...
-running concurrently, K1 pushing 16-byte stores over NVLink/NVSwitch into the
-peer's slab -- next to cudaMemcpyPeerAsync of the same bytes.  One process,
+running concurrently, K1 pushing into the peer's slab over NVLink/NVSwitch in
+each of its three peer forms (register tiles with a system-scope count per
+tile; register tiles counted at gpu scope with one system-scope publish per
+chunk; bulk-copy tiles) -- next to cudaMemcpyPeerAsync of the same bytes.  One process,
 one stream per pair, CUDA events per pair; reports per-pair GB/s against
 900 GB/s per direction (nominal) / 770 GB/s (measured peer copy,
 B200_PROFILING.md) and the aggregate.  Needs >= 2 GPUs; prints a note and
@@ -59,7 +61,8 @@ def main():
         chunk = min(args.chunk, size)
         offs = {c: fab.slab_alloc(c, size) for _, c in pairs}
         res = {}
-        for impl in ("fsx", "memcpy_peer"):
+        forms = {"fsx_tile": {}, "fsx_gpucount": {"peer_gpu_count": True}, "fsx_bulk": {"bulk": True}}
+        for impl in list(forms) + ["memcpy_peer"]:
             ev = {}
             for p, c in pairs:
                 s = streams[p]
@@ -69,10 +72,10 @@ def main():
                     for r in range(reps + 2):
                         if r == 2:
                             e0.record(s)
-                        if impl == "fsx":
+                        if impl in forms:
                             nch = -(-size // chunk)
                             fab.forward(p, src[p].data_ptr(), c, offs[c], size, chunk,
-                                        fab.flags_alloc(c, nch), s, host_notify=False)
+                                        fab.flags_alloc(c, nch), s, host_notify=False, **forms[impl])
                         else:
                             dstbuf[c][:size].copy_(src[p][:size], non_blocking=True)
                     e1.record(s)
