@@ -13,8 +13,11 @@
 //              prompt row (fsx_merge), stream-ordered after forward() or with
 //              early start on the chunk flags;
 //   release()  the segments go back to the slab (the ack, sidecar.hpp:287-290).
-// run_place() is the slab-free alternative: the forward fused with the merge
-// (fsx_forward_place), the producer's rows straight into the prompt rows.
+// run_tee() is the N = 1 pass as ONE kernel (fsx_forward_merge): each item row
+// is read once and stored into its slab segment (with the chunk flags) and
+// into its prompt row.  run_place() is the slab-free alternative: the forward
+// fused with the merge (fsx_forward_place), the producer's rows straight into
+// the prompt rows.
 // The batch's device arrays (prompt embedding, token ids, offsets, item
 // views, scratch, status) are allocated once; a pass costs a handful of C-ABI
 // calls and one small descriptor upload when segment offsets change.
@@ -218,18 +221,35 @@ class DataPlanePass {
     return true;
   }
 
+  // The tee pass (producer and consumer on the same device): alloc, then one
+  // fsx_forward_merge (scan + the fused forward/merge kernel, stream order),
+  // then release.  Same slab segments and chunk flags as run(), same merged
+  // rows, the payload crossing HBM three times instead of four.
+  bool run_tee(cudaStream_t st, uint32_t fwd_options = 0) {
+    if (!alloc()) return false;
+    ensure_place_src();
+    int64_t fb = 0;
+    if (!items_.empty()) check(fsx_flags_alloc(f_, dst_, static_cast<int32_t>(n_chunks_), &fb));
+    for (size_t i = 0; i < items_.size(); ++i) {
+      xfers_[i].dst_off = offs_[i];
+      xfers_[i].flag_base = fb;
+      xfers_[i].token = 0;
+      fb += chunks_[i];
+    }
+    fsx_merge_batch mb = b_;
+    mb.d_item_src = place_src_;
+    check(fsx_forward_merge(f_, static_cast<int32_t>(items_.size()), xfers_.data(), &mb, fwd_options, st));
+    release();
+    return true;
+  }
+
   // Direct placement (fsx_forward_place): the forward fused with the merge.
   // The producer writes every item row from its own buffer straight into the
   // consumer's placeholder rows (scan + row copy, one fsx call, stream order);
   // no slab segment is held and the payload crosses memory once.  Always
   // succeeds (nothing to allocate).
   bool run_place(cudaStream_t st) {
-    if (!place_src_) {
-      std::vector<const void*> src(items_.size());
-      for (size_t i = 0; i < items_.size(); ++i) src[i] = items_[i].d_src;
-      cuda(cudaSetDevice(dev_));
-      place_src_ = upload(src);
-    }
+    ensure_place_src();
     fsx_merge_batch mb = b_;
     mb.d_item_src = place_src_;
     check(fsx_forward_place(f_, src_, dst_, &mb, -1, 0, st));
@@ -283,6 +303,14 @@ class DataPlanePass {
   static void cuda(cudaError_t e) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + cudaGetErrorString(e));
   }
+  // Device array of the producer's item pointers (tee and direct placement).
+  void ensure_place_src() {
+    if (place_src_) return;
+    std::vector<const void*> src(items_.size());
+    for (size_t i = 0; i < items_.size(); ++i) src[i] = items_[i].d_src;
+    cuda(cudaSetDevice(dev_));
+    place_src_ = upload(src);
+  }
   template <class T>
   T* alloc_dev(int64_t n) {
     void* p = nullptr;
@@ -313,7 +341,7 @@ class DataPlanePass {
   int64_t *req_row_off_ = nullptr, *req_item_off_ = nullptr, *item_row_off_ = nullptr;
   int32_t *scratch_ = nullptr, *status_ = nullptr;
   const void** item_src_ = nullptr;
-  const void** place_src_ = nullptr;  // producer buffers, for run_place
+  const void** place_src_ = nullptr;  // producer buffers, for run_tee / run_place
   fsx_merge_batch b_{};
   // colocated pass state
   static constexpr int kStages = 4;

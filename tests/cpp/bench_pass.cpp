@@ -2,8 +2,9 @@
 // config B (4 Qwen2.5-VL videos, 16 x 1024 x 3584 bf16 each, 7 MiB flagged
 // chunks) and an A-like batch (64 requests x one 256 x 4096 bf16 image),
 // intra-device forward + merge per pass, stream-ordered or as the colocated
-// pass (K1 || early-start merge, DataPlanePass::run_colocated), or direct
-// placement (DataPlanePass::run_place: no slab).  Prints one JSON line
+// pass (K1 || early-start merge, DataPlanePass::run_colocated), as the tee
+// (DataPlanePass::run_tee: one kernel), or direct placement
+// (DataPlanePass::run_place: no slab).  Prints one JSON line
 // per batch: device time per pass, host time per pass, payload GB/s; then
 // checks the merged prompt embeddings byte for byte against the oracle
 // restatement (test infrastructure: inputs built and checked with
@@ -41,6 +42,7 @@ struct Case {
   bool colocated;  // K1 || early-start merge (DataPlanePass::run_colocated)
   bool graph = false;  // stream-ordered pass replayed as a CUDA graph (run_graph)
   bool place = false;  // direct placement, no slab (run_place)
+  bool tee = false;    // forward + merge as one kernel (run_tee)
 };
 
 int run_case(fsx_fabric* f, const Case& c, int passes) {
@@ -73,6 +75,7 @@ int run_case(fsx_fabric* f, const Case& c, int passes) {
   auto one = [&]() -> bool {
     if (c.graph) return pass.run_graph(st);
     if (c.place) return pass.run_place(st);
+    if (c.tee) return pass.run_tee(st);
     return c.colocated ? pass.run_colocated(st, mst) : pass.run(st);
   };
   // prompt rows pre-filled like the Python batch (synth_payload(fnv1a64(id + "/text")))
@@ -156,6 +159,10 @@ int main(int argc, char** argv) {
   }
   if (fsx_slab_register(f, 1, int64_t{1} << 30) != FSX_OK) return 2;
   int rc = 0;
+  rc |= run_case(f, Case{"B, tee (fsx_forward_merge: forward + merge in one kernel)", 4, 16384, 1800, 7168,
+                          1024, false, false, false, true},
+                 passes);
+  rc |= run_case(f, Case{"A-like, tee", 64, 256, 500, 8192, 0, false, false, false, true}, passes);
   rc |= run_case(f, Case{"B: Qwen2.5-VL video, 7 MiB chunks", 4, 16384, 1800, 7168, 1024, false}, passes);
   rc |= run_case(f, Case{"B, colocated pass", 4, 16384, 1800, 7168, 1024, true}, passes);
   rc |= run_case(f, Case{"A-like: 64 x one 256-row 4096-d image", 64, 256, 500, 8192, 0, false}, passes);
