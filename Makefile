@@ -32,7 +32,7 @@ oracle:
 FISSIM_REF_INCLUDE ?= /root/reference/proj/include
 FISSIM_REF_TESTS ?= /root/reference/proj/tests
 NLOHMANN_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
-CXXTEST := $(CXX) -std=c++20 -O2 -Wall -Wno-unused-parameter -Iinclude -Itests/cpp/catch2_shim \
+CXXTEST := $(CXX) -std=c++20 -O2 -g -rdynamic -Wall -Wno-unused-parameter -Iinclude -Itests/cpp/catch2_shim \
            -I/usr/local/cuda/include
 LINKFSX := -L$(PKG) -lfsx -L/usr/local/cuda/lib64 -lcudart -lpthread \
            -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
@@ -49,7 +49,7 @@ build/test_fabric: tests/cpp/test_fabric.cpp tests/cpp/shim_main.cpp include/fsx
 # the drop-in header (needs the reference tree: built here, run on the box).
 build/ref_test_sidecar: $(FISSIM_REF_TESTS)/test_sidecar.cpp tests/cpp/shim_main.cpp \
                         include/fsx/fabric.hpp include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ $(FISSIM_REF_TESTS)/test_sidecar.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 
@@ -59,14 +59,14 @@ build/ref_test_sidecar: $(FISSIM_REF_TESTS)/test_sidecar.cpp tests/cpp/shim_main
 build/ref_test_executors: $(FISSIM_REF_TESTS)/test_executor_sim.cpp $(FISSIM_REF_TESTS)/test_dispatcher.cpp \
                           tests/cpp/shim_main.cpp include/fsx/fabric.hpp \
                           include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) -o $@ \
 	    $(FISSIM_REF_TESTS)/test_executor_sim.cpp $(FISSIM_REF_TESTS)/test_dispatcher.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 
 build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp \
                          include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -o $@ tests/cpp/dropin_criterion4.cpp $(LINKFSX)
 
 # Multi-process executors: the worker executable and the
@@ -77,7 +77,7 @@ build/dropin_criterion4: tests/cpp/dropin_criterion4.cpp include/fsx/fabric.hpp 
 REFDATA := $(CURDIR)/build/refdata
 build/fsx_worker: tests/cpp/fsx_worker_main.cpp include/fsx/dropin/fissim/executor_worker.hpp \
                   include/fsx/dropin/fissim/sidecar.hpp include/fsx/fabric.hpp $(LIB) | build
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -o $@ tests/cpp/fsx_worker_main.cpp $(LINKFSX)
 
 build/refdata: | build
@@ -92,34 +92,34 @@ build/refdata: | build
 build/ref_acceptance: $(FISSIM_REF_TESTS)/acceptance_test.cpp build/fsx_worker \
                       include/fsx/dropin/fissim/sidecar.hpp include/fsx/dropin/fissim/executor_worker.hpp \
                       | build/refdata
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ $(FISSIM_REF_TESTS)/acceptance_test.cpp $(LINKFSX)
 
 build/ref_test_control_plane: $(FISSIM_REF_TESTS)/test_control_plane.cpp tests/cpp/shim_main.cpp \
                               build/fsx_worker include/fsx/dropin/fissim/sidecar.hpp | build/refdata
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) \
 	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ $(FISSIM_REF_TESTS)/test_control_plane.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
 build/ref_test_worker: $(FISSIM_REF_TESTS)/test_worker.cpp tests/cpp/shim_main.cpp build/fsx_worker \
                        include/fsx/dropin/fissim/executor_worker.hpp | build/refdata
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ $(FISSIM_REF_TESTS)/test_worker.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
 build/test_worker_ipc: tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp build/fsx_worker \
                        include/fsx/dropin/fissim/executor_worker.hpp | build/refdata
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
 	    -DFSX_REFDATA='"$(REFDATA)"' -DFSX_WORKER_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
 build/ref_test_bench: $(FISSIM_REF_TESTS)/test_bench.cpp tests/cpp/shim_main.cpp \
                       include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build/refdata
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(FISSIM_REF_TESTS) -I$(NLOHMANN_DIR) \
 	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ $(FISSIM_REF_TESTS)/test_bench.cpp tests/cpp/shim_main.cpp $(LINKFSX)
@@ -128,7 +128,7 @@ build/ref_test_bench: $(FISSIM_REF_TESTS)/test_bench.cpp tests/cpp/shim_main.cpp
 # envelope and its cost next to the reference JSON route.  CPU only.
 build/test_envelope_codec: tests/cpp/test_envelope_codec.cpp tests/cpp/shim_main.cpp \
                            include/fsx/envelope_codec.hpp include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build
-	$(CXX) -std=c++20 -O2 -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
+	$(CXX) -std=c++20 -O2 -g -rdynamic -w -Iinclude/fsx/dropin -Iinclude -Itests/cpp/catch2_shim \
 	    -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) -o $@ tests/cpp/test_envelope_codec.cpp \
 	    tests/cpp/shim_main.cpp $(LINKFSX)
 

@@ -58,7 +58,7 @@ KERNELS = {
     "tee": "fsx::kern::merge_tee_kernel (fsx_forward_merge: forward + merge in one kernel)",
     "forward": "fsx::kern::forward_tma_kernel (K1, bulk-copy tiles, all items of the step in one launch)",
     "merge": "fsx::kern::merge_copy_kernel (K3b, warp per placeholder row, stream-ordered)",
-    "follow": "fsx::kern::merge_follow_kernel (K3b early start, persistent grid)",
+    "follow": "fsx::kern::merge_follow_kernel (K3b early start: warp per placeholder row, chunk flag acquired per row)",
     "scan": "fsx::kern::merge_scan_kernel (K3a placeholder scan)",
 }
 

@@ -263,7 +263,9 @@ int fsx_signal_flags(fsx_fabric* f, int dst_gpu, int64_t flag_base, int32_t n, u
  *   back to HBM.  The segment must not be read again before it is rewritten.
  * FSX_MERGE_COLOCATED early start while the producer's K1 runs on this same
  *   GPU: at most one merge CTA per SM, so spinning merge warps can never take
- *   every slot K1 needs to make progress. */
+ *   every slot K1 needs to make progress.  Without it an early-start merge is
+ *   a full grid (warp per row, resident CTAs spin on their chunk flags): for
+ *   producers on another GPU or in another process. */
 #define FSX_MERGE_DISCARD 0x100
 #define FSX_MERGE_COLOCATED 0x200
 #define FSX_MERGE_MODE_MASK 0xff
@@ -279,7 +281,8 @@ typedef struct fsx_merge_batch {
   const int64_t* d_req_item_off;     /* [R + 1] */
   const void* const* d_item_src;     /* [M] device pointers (slab views) */
   const int64_t* d_item_row_off;     /* [M + 1] prefix sums of item rows */
-  int32_t* d_scratch;                /* [sum item rows] scratch */
+  int32_t* d_scratch;                /* [sum item rows] scratch (the scan's prompt row
+                                        per placeholder row; total_rows < 2^31) */
   int32_t* d_status;                 /* [R] out */
   const uint64_t* const* d_item_flag; /* optional [M] */
   const uint64_t* d_item_token;      /* optional [M] */

@@ -9,7 +9,8 @@
 //   K3 merge_scan_kernel    the consumer-side multimodal merge (derived contract,
 //      merge_copy_kernel    SURVEY.md 8a-8; record_replay.hpp:404-416 slot order):
 //      merge_follow_kernel  placeholder scan, then the row scatter -- stream
-//                           ordered, or following the producer's chunk flags
+//      merge_colocated_kernel  ordered, or following the producer's chunk flags
+//                           (producer on another GPU / beside it on this GPU)
 //   K1+K3 merge_tee_kernel  the forward and the merge as one kernel: each item row
 //                           is read once and stored into its slab segment (with
 //                           the chunk flags) and into its placeholder row
@@ -521,8 +522,9 @@ __global__ void wait_flags_kernel(const uint64_t* dflags, int32_t n, uint64_t to
 // token ids with coalesced loads (round j, lane l -> token base_w + 32 j + l),
 // ballots the placeholder mask of each round, and the CTA scans the per-warp
 // totals once in shared memory.  The k-th placeholder row of the request gets
-// its row offset inside the request written to
-// scratch[item_row_off[first item] + k].
+// its prompt row (index into d_embeds) written to
+// scratch[item_row_off[first item] + k]; a request that fails validation gets
+// -1 in all of its entries.  The copy kernels then need no request lookup.
 __global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batch b) {
   __shared__ int32_t warp_excl[kScanThreads / 32];
   __shared__ int32_t tile_total;
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batc
     for (int j = 0; j < kScanRounds; ++j) {
       if ((m[j] >> lane) & 1u) {
         const int64_t kk = k + __popc(m[j] & lt_mask);
-        if (kk < want) b.d_scratch[kbase + kk] = (int32_t)(wbase + 32 * j - t0);
+        if (kk < want) b.d_scratch[kbase + kk] = (int32_t)(wbase + 32 * j);
       }
       k += __popc(m[j]);
     }
@@ -575,29 +577,35 @@ __global__ void __launch_bounds__(kScanThreads) merge_scan_kernel(fsx_merge_batc
     if (threadIdx.x == 0) running += tile_total;
     __syncthreads();
   }
+  // (every thread has read `running` after the last barrier)
+  if (running != want) {
+    // validation failed: the request's rows are marked -1, so the copy
+    // kernels leave its prompt untouched without looking the request up
+    for (int64_t k = threadIdx.x; k < want; k += kScanThreads) b.d_scratch[kbase + k] = -1;
+  }
   if (threadIdx.x == 0) b.d_status[r] = (running == want) ? 0 : FSX_E_VALIDATION;
 }
 
-__device__ __forceinline__ int64_t upper_index(const int64_t* off, int64_t n, int64_t x) {
-  // largest i in [0, n) with off[i] <= x  (off is non-decreasing, off[0] == 0)
-  int64_t lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= x) lo = mid;
-    else hi = mid - 1;
+// Item of placeholder row g, searched by the whole warp: the largest item i
+// in [0, M) with item_row_off[i] <= g (zero-row items share an offset with
+// the next item and are skipped by taking the largest).  Each round the 32
+// lanes probe 32 evenly spaced offsets of the remaining range [lo, hi) and a
+// ballot picks the sub-range, so M <= 32 items take one round of loads and
+// M <= 1024 two -- where a binary search (and the request search after it)
+// cost ~12 dependent loads per row, most of a warp's life on small rows.
+// Invariant: off[lo] <= g < off[hi] (off[M] = total rows > g).
+__device__ __forceinline__ int64_t warp_item_of(const int64_t* off, int64_t m, int64_t g, int lane) {
+  int64_t lo = 0, hi = m;
+  while (hi - lo > 1) {
+    const int64_t span = hi - lo;
+    const int64_t idx = lo + (span * lane) / 32;  // lane 0 probes lo
+    const uint32_t le = __ballot_sync(0xffffffffu, off[idx] <= g);
+    const int top = 31 - __clz(le);  // offsets are non-decreasing: le is a prefix of lanes
+    const int64_t nlo = lo + (span * top) / 32;
+    hi = top == 31 ? hi : lo + (span * (top + 1)) / 32;
+    lo = nlo;
   }
   return lo;
-}
-
-// Item and request of placeholder row g (zero-row items sharing an offset
-// are skipped).
-__device__ __forceinline__ void row_owner(const fsx_merge_batch& b, int64_t g, int64_t* item, int64_t* req) {
-  int64_t it = upper_index(b.d_item_row_off, b.num_items + 1, g);
-  while (b.d_item_row_off[it + 1] <= g) ++it;
-  int64_t rq = upper_index(b.d_req_item_off, b.num_requests + 1, it);
-  while (b.d_req_item_off[rq + 1] <= it) ++rq;
-  *item = it;
-  *req = rq;
 }
 
 // Store of one 16-byte vector with an optional L2 policy (pol < 0: plain).
@@ -663,24 +671,47 @@ __device__ __forceinline__ void discard_row(const uint8_t* src, int64_t rb, int 
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
 }
 
-// K3 merge, phase 2, stream-ordered: one warp per placeholder row over a full
-// (non-persistent) grid, 8 rows per CTA.  Lane 0 resolves the row's item and
-// request (binary searches over the row offsets), then the warp moves the row.
-__global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_batch b) {
+// K3 merge, phase 2: one warp per placeholder row over a full (non-persistent)
+// grid, 8 rows per CTA.  Lane 0 resolves the row's item and request (binary
+// searches over the row offsets), then the warp moves the row with all of its
+// 16-byte loads in flight.  kGated (early start, producer on another GPU or in
+// another process): lane 0 first acquires the flag of the chunk the row sits
+// in.  The hardware hands out CTAs in blockIdx (row) order and the producer
+// completes chunks in the same order, so the resident CTAs are the ones right
+// behind the producer; with every flag already set the gated form runs at the
+// stream-ordered form's rate (the persistent grid-stride form it replaces
+// reached 0.88 of the copy peak alone, bench r02b `kernels.follow`).
+template <bool kGated>
+__device__ __forceinline__ void merge_row(const fsx_merge_batch& b) {
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
   if (g >= b.total_item_rows) return;
-  int64_t item = 0, req = 0;
-  if (lane == 0) row_owner(b, g, &item, &req);
-  item = __shfl_sync(0xffffffffu, item, 0);
-  req = __shfl_sync(0xffffffffu, req, 0);
-  if (b.d_status[req] != 0) return;  // validation failed: request untouched
+  const int32_t row = b.d_scratch[g];  // prompt row, -1: request failed validation
+  const int64_t item = warp_item_of(b.d_item_row_off, b.num_items, g, lane);
+  if (row < 0) return;  // validation failed: request untouched
   const int64_t rb = b.row_bytes;
   const int64_t j = g - b.d_item_row_off[item];
+  if (kGated) {
+    if (lane == 0) {
+      const int64_t cr = b.d_item_chunk_rows[item];
+      spin_until(b.d_item_flag[item] + (cr > 0 ? j / cr : 0), b.d_item_token[item]);
+    }
+    __syncwarp();
+  }
   const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
-  uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * rb;
+  uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (int64_t)row * rb;
   warp_move_row(src, dst, nullptr, rb, lane, /*coherent=*/true, -1, -1);
   if (b.mode & FSX_MERGE_DISCARD) discard_row(src, rb, lane);
+}
+
+// stream-ordered: the slab segments are complete when the kernel starts
+__global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_batch b) {
+  merge_row<false>(b);
+}
+
+// early start behind a producer on another GPU / in another process
+__global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_batch b) {
+  merge_row<true>(b);
 }
 
 // K1 + K3 as one kernel (fsx_forward_merge): the tee.  Same grid as
@@ -706,17 +737,13 @@ __global__ void __launch_bounds__(kMergeThreads, kTeeMinBlocks) merge_tee_kernel
   int32_t key_item = -1;
   int64_t key_chunk = 0;
   if (g < tb.g1) {
-    int64_t item = 0, req = 0;
-    if (lane == 0) row_owner(b, g, &item, &req);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    req = __shfl_sync(0xffffffffu, req, 0);
+    const int32_t row = b.d_scratch[g];  // prompt row, -1: request failed validation
+    const int64_t item = warp_item_of(b.d_item_row_off, b.num_items, g, lane);
     const TeeItem& t = tb.t[item - tb.i0];
     const int64_t rb = b.row_bytes;
     const int64_t j = g - b.d_item_row_off[item];
     const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
-    uint8_t* dst = b.d_status[req] == 0
-                       ? static_cast<uint8_t*>(b.d_embeds) + (b.d_req_row_off[req] + b.d_scratch[g]) * rb
-                       : nullptr;
+    uint8_t* dst = row >= 0 ? static_cast<uint8_t*>(b.d_embeds) + (int64_t)row * rb : nullptr;
     // the prompt row is plain-stored; the slab copy keeps L2 priority when a
     // consumer on this GPU reads it next (FSX_FWD_L2_KEEP)
     warp_move_row<kTeeUnroll>(src, dst, t.dst + j * rb, rb, lane, /*coherent=*/false, -1, tb.l2_keep_dst ? 2 : -1);
@@ -756,22 +783,17 @@ __global__ void __launch_bounds__(kMergeThreads, kTeeMinBlocks) merge_tee_kernel
   }
 }
 
-// K3 merge, phase 2, early start ("follow" form): the batch carries item chunk
-// flags, set by a producer still running (K1 on a peer GPU writing into this
-// GPU's slab over NVLink, or on this GPU for the colocated pass).  Warp w of W
+// K3 merge, phase 2, early start beside a producer on THIS GPU (the colocated
+// pass, FSX_MERGE_COLOCATED): a persistent grid of one CTA per SM, so spinning
+// merge warps never take every slot the producer's K1 needs.  Warp w of W
 // moves the placeholder rows g = w, w + W, w + 2W, ... in increasing order, so
-// the whole grid works on a window of about W rows right behind the producer
-// instead of some warps holding rows many chunks ahead.  Item / request values
-// are re-read only when the warp's row crosses into the next item; lane 0
-// acquires the row's chunk flag (once per chunk) before the warp loads it.
-// FSX_MERGE_COLOCATED (producer on this GPU): gpu-scope acquires, and the
-// launcher caps the grid at one CTA per SM so spinning merge warps never take
-// every slot K1 needs.  FSX_MERGE_DISCARD drops merged slab lines from L2.
-// Three CTAs per SM with 8 x 16 B per lane in flight, like the tee (two CTAs
-// at 16 x 16 B: 0.161 ms alone on config B, 0.89 of the copy peak).
+// the grid works on a window of about W rows right behind the producer.
+// Item / request values are re-read only when the warp's row crosses into the
+// next item; lane 0 acquires the row's chunk flag (gpu scope, once per chunk)
+// before the warp loads it.  FSX_MERGE_DISCARD drops merged slab lines from L2.
 constexpr int kFollowMinBlocks = 3;
 constexpr int kFollowUnroll = 8;
-__global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocks) merge_follow_kernel(fsx_merge_batch b) {
+__global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocks) merge_colocated_kernel(fsx_merge_batch b) {
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kMergeWarps;
   const int64_t w = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
@@ -779,14 +801,10 @@ __global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocks) merge_follow_
   const int64_t n = b.total_item_rows;
   if (w >= n) return;
   const bool discard = (b.mode & FSX_MERGE_DISCARD) != 0;
-  const bool colocated = (b.mode & FSX_MERGE_COLOCATED) != 0;
-  int64_t item = 0, req = 0;
-  row_owner(b, w, &item, &req);
+  int64_t item = warp_item_of(b.d_item_row_off, b.num_items, w, lane);
   int64_t item_beg = b.d_item_row_off[item], item_end = b.d_item_row_off[item + 1];
   const uint8_t* item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
   int64_t chunk_rows = b.d_item_chunk_rows[item];
-  int64_t req_row = b.d_req_row_off[req];
-  bool req_ok = b.d_status[req] == 0;
   int64_t waited = -1;
   for (int64_t g = w; g < n; g += W) {
     if (g >= item_end) {
@@ -798,31 +816,21 @@ __global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocks) merge_follow_
       item_src = static_cast<const uint8_t*>(b.d_item_src[item]);
       chunk_rows = b.d_item_chunk_rows[item];
       waited = -1;
-      if (b.d_req_item_off[req + 1] <= item) {
-        do {
-          ++req;
-        } while (b.d_req_item_off[req + 1] <= item);
-        req_row = b.d_req_row_off[req];
-        req_ok = b.d_status[req] == 0;
-      }
     }
-    if (!req_ok) continue;  // validation failed: request untouched
+    const int32_t row = b.d_scratch[g];
+    if (row < 0) continue;  // validation failed: request untouched
     const int64_t j = g - item_beg;
-    const int32_t pos = b.d_scratch[g];
     const int64_t c = chunk_rows > 0 ? j / chunk_rows : 0;
     if (c != waited) {
-      if (lane == 0) {
-        if (colocated) spin_until_gpu(b.d_item_flag[item] + c, b.d_item_token[item]);
-        else spin_until(b.d_item_flag[item] + c, b.d_item_token[item]);
-      }
+      if (lane == 0) spin_until_gpu(b.d_item_flag[item] + c, b.d_item_token[item]);
       __syncwarp();
       waited = c;
     }
     const uint8_t* src = item_src + j * rb;
     // the prompt rows are written once and not re-read here: evict them from
     // L2 first, so they do not push out slab rows the producer has just written
-    warp_move_row<kFollowUnroll>(src, static_cast<uint8_t*>(b.d_embeds) + (req_row + pos) * rb, nullptr,
-                                 rb, lane, /*coherent=*/true, 1, -1);
+    warp_move_row<kFollowUnroll>(src, static_cast<uint8_t*>(b.d_embeds) + (int64_t)row * rb, nullptr, rb, lane,
+                                 /*coherent=*/true, 1, -1);
     if (discard) discard_row(src, rb, lane);
   }
 }
@@ -937,14 +945,6 @@ cudaError_t set_spin_timeout(uint64_t ns) {
   return cudaMemcpyToSymbol(c_spin_timeout_ns, &ns, sizeof(ns));
 }
 
-int merge_follow_blocks_per_sm() {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_follow_kernel, kMergeThreads, 0) !=
-      cudaSuccess)
-    return 1;
-  return n > 0 ? n : 1;
-}
-
 int forward_tile_bytes() { return kTileThreads * kTileVecs * 16; }
 
 // One launch with the parameter block cut to CAP transfers.
@@ -1034,14 +1034,14 @@ cudaError_t launch_merge(const fsx_merge_batch& b, cudaStream_t s, int* launches
   }
   if (base_mode == FSX_MERGE_SCAN_ONLY || b.total_item_rows <= 0) return cudaSuccess;
   const int64_t need = (b.total_item_rows + kMergeWarps - 1) / kMergeWarps;
-  if (b.d_item_flag) {
-    // early start: a persistent grid (resident CTAs only -- warps spin on
-    // flags); one CTA per SM beside a producer on the same GPU
+  if (b.d_item_flag && (b.mode & FSX_MERGE_COLOCATED)) {
+    // early start beside a producer on this GPU: one resident CTA per SM
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t cap = (b.mode & FSX_MERGE_COLOCATED) ? sms : (int64_t)sms * merge_follow_blocks_per_sm();
-    merge_follow_kernel<<<(unsigned)(need < cap ? need : cap), kMergeThreads, 0, s>>>(b);
+    merge_colocated_kernel<<<(unsigned)(need < sms ? need : sms), kMergeThreads, 0, s>>>(b);
+  } else if (b.d_item_flag) {
+    merge_follow_kernel<<<(unsigned)need, kMergeThreads, 0, s>>>(b);
   } else {
     merge_copy_kernel<<<(unsigned)need, kMergeThreads, 0, s>>>(b);
   }

@@ -140,6 +140,5 @@ cudaError_t set_spin_timeout(uint64_t ns);
 
 // K1 tile bytes (one CTA per tile) and the early-start merge's occupancy.
 int forward_tile_bytes();
-int merge_follow_blocks_per_sm();
 
 }  // namespace fsx

@@ -221,8 +221,11 @@ bool is_pinned_host(const void* p) {
 class CopyPool {
  public:
   static CopyPool& get() {
-    static CopyPool pool;
-    return pool;
+    // never destroyed: the workers block on cv_ for the life of the process,
+    // and destroying a condition variable with waiters at exit hangs in
+    // pthread_cond_destroy (every C++ test binary hung after its last case)
+    static CopyPool* pool = new CopyPool;
+    return *pool;
   }
   int workers() const { return static_cast<int>(threads_.size()); }
   // Run fn(0..n-1) with part 0 on the caller; returns when all are done.
@@ -1233,6 +1236,8 @@ int fsx_merge(fsx_fabric* f, int gpu, const fsx_merge_batch* b, void* stream) {
     return fail(FSX_E_VALIDATION, "merge batch is missing a device array");
   if (b->d_item_flag && (!b->d_item_token || !b->d_item_chunk_rows))
     return fail(FSX_E_VALIDATION, "early-start merge needs tokens and chunk rows");
+  if (b->total_rows > INT32_MAX)  // d_scratch holds int32 prompt row indices
+    return fail(FSX_E_VALIDATION, "merge batch has more than 2^31 - 1 prompt rows");
   const int base_mode = b->mode & FSX_MERGE_MODE_MASK;
   if (base_mode > FSX_MERGE_COPY_ONLY ||
       (b->mode & ~(FSX_MERGE_MODE_MASK | FSX_MERGE_DISCARD | FSX_MERGE_COLOCATED)))
@@ -1289,6 +1294,8 @@ int fsx_forward_merge(fsx_fabric* f, int32_t n, fsx_transfer* t, const fsx_merge
     return fail(FSX_E_VALIDATION,
                 "forward_merge takes FSX_MERGE_FULL or FSX_MERGE_COPY_ONLY, no early-start or discard bits");
   if (b->row_bytes <= 0) return fail(FSX_E_VALIDATION, "bad row_bytes");
+  if (b->total_rows > INT32_MAX)  // d_scratch holds int32 prompt row indices
+    return fail(FSX_E_VALIDATION, "merge batch has more than 2^31 - 1 prompt rows");
   if (n == 0) return fsx_merge(f, 0, b, stream);  // nothing to forward: statuses only
   int src_dev = 0;
   int rc = find_gpu(f, t[0].src_gpu, &src_dev);

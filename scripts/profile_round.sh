@@ -16,7 +16,7 @@ mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv \
     --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --profile > $OUT/launches_$TAG.log 2>&1
-for C in B A; do
+for C in B A D; do
   ncu --set full --clock-control none --import-source on --profile-from-start off \
       -o $OUT/full_${TAG}_$C python scripts/profile_kernels.py $C > $OUT/full_${TAG}_$C.log 2>&1
   tail -1 $OUT/full_${TAG}_$C.log

@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 def _run(binary: str, timeout: int = 600):
     path = os.path.join(ROOT, "build", binary)
     assert os.path.exists(path), f"{path} not built: run `make cpptests` (part of build())"
-    p = subprocess.run([path], capture_output=True, text=True, timeout=timeout)
+    p = subprocess.run([path], capture_output=True, text=True, timeout=timeout,
+                       env={**os.environ, "FSX_CASE_TIMEOUT_S": "120"})
     return p.returncode, p.stdout + p.stderr
 
 

@@ -6,6 +6,8 @@ bf16 NaN/Inf bit patterns.
 """
 import hashlib
 
+import time
+
 import numpy as np
 import pytest
 
@@ -260,7 +262,7 @@ def _run_batch(fab, reqs, rules, chunk_rows=None, path="serial", tok_override=No
     return b
 
 
-@pytest.mark.parametrize("path", ["serial", "bulk", "tee"])
+@pytest.mark.parametrize("path", ["serial", "bulk", "tee", "early"])
 @pytest.mark.parametrize("config,count,chunk_rows", [("A", 64, None), ("A", 5, 64), ("D", 24, 1024),
                                                      ("B", 1, 1024),
                                                      # the bench batches at full BASELINE size
@@ -304,6 +306,39 @@ def test_merge_matches_reference_derived_golden(fab, config, path):
     b.release()
 
 
+def test_follow_merge_waits_for_late_flags(fab, oracle_mod):
+    """The early-start merge (merge_follow_kernel, full grid, one chunk-flag
+    acquire per row) launched before its flags are set: it must not finish
+    until they are, and then merge byte-exact.  The flags are published late
+    from the host side with fresh tokens (fsx_signal_flags), standing in for
+    a producer on another GPU."""
+    from paper_2603_12118_b200.dataplane import DataPlaneBatch
+
+    torch = _torch()
+    reqs = T.config_requests("A", 8)  # a grid small enough to be resident at once
+    b = DataPlaneBatch(fab, reqs, T.RULES["A"], 0, 1, chunk_rows=64)
+    b.synth_inputs()
+    assert b.alloc()
+    b.forward()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    b.tokens[:] = (1 << 44) + rng.integers(1, 1 << 30, size=len(b.tokens))  # nobody set these yet
+    s2 = torch.cuda.Stream()
+    done = torch.cuda.Event()
+    with torch.cuda.stream(s2):
+        b.merge(s2, early_start=True)
+        done.record(s2)
+    time.sleep(0.05)
+    assert not done.query(), "early-start merge finished before its chunk flags were set"
+    for i in range(len(b.lay.items)):
+        fab.signal_flags(1, int(b.flag_base[i]), int(b.n_chunks[i]), int(b.tokens[i]), 0)
+    done.synchronize()
+    want, st = _expected(oracle_mod, b)
+    assert (b.status_host() == 0).all() and (st == 0).all()
+    assert np.array_equal(b.embeds_host(), want)
+    b.release()
+
+
 def test_merge_early_start_flags(fab, oracle_mod):
     reqs = T.config_requests("D", 12)
     b = _run_batch(fab, reqs, T.RULES["D"], chunk_rows=512, path="early")
@@ -312,7 +347,7 @@ def test_merge_early_start_flags(fab, oracle_mod):
     b.release()
 
 
-@pytest.mark.parametrize("path", ["serial", "tee"])
+@pytest.mark.parametrize("path", ["serial", "tee", "early"])
 def test_merge_validation_leaves_request_untouched(fab, oracle_mod, path):
     """A request whose placeholder count does not match its items keeps its
     prompt rows (status validation); the tee still forwards its items."""
@@ -339,7 +374,7 @@ def test_merge_validation_leaves_request_untouched(fab, oracle_mod, path):
     b.release()
 
 
-@pytest.mark.parametrize("path", ["serial", "tee"])
+@pytest.mark.parametrize("path", ["serial", "tee", "early"])
 def test_merge_edge_cases(fab, oracle_mod, path):
     rules = T.ShapeRules(hidden_dim=8, pixels_per_token=1, default_image_width=1,
                          default_image_height=3, tokens_per_audio_second=1, default_audio_seconds=1)
