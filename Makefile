@@ -142,7 +142,10 @@ build/bench_pass: tests/cpp/bench_pass.cpp include/fsx/dataplane.hpp build/fsx_o
 build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
 
-cpptests: build/test_fabric build/bench_fabric build/bench_pass build/test_host_digest
+build/probe_small_path: tests/cpp/probe_small_path.cpp include/fsx/fabric.hpp $(LIB) | build
+	$(CXXTEST) -o $@ tests/cpp/probe_small_path.cpp $(LINKFSX)
+
+cpptests: build/test_fabric build/bench_fabric build/probe_small_path build/bench_pass build/test_host_digest
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \

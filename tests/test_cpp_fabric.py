@@ -130,12 +130,13 @@ def test_reference_bench_harness_tests_on_dropin(gpu):
 
 def test_cpp_dataplane_pass_bit_exact(gpu):
     """The native pass runner (include/fsx/dataplane.hpp): config B and an
-    A-like batch forwarded + merged from C++ (stream order, colocated, graph,
-    direct placement), merged prompt embeddings equal
+    A-like batch forwarded + merged from C++ (tee, stream order, colocated,
+    graph, direct placement), merged prompt embeddings equal
     to the oracle restatement byte for byte (tests/cpp/bench_pass.cpp)."""
     import json
 
     rc, out = _run("bench_pass", timeout=600)
     assert rc == 0, out[-4000:]
     lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
-    assert len(lines) == 8 and all(l["bit_exact_vs_oracle"] for l in lines), out[-2000:]
+    assert len(lines) == 10 and all(l["bit_exact_vs_oracle"] for l in lines), out[-2000:]
+    assert sum("tee" in l["batch"] for l in lines) == 2, out[-2000:]
