@@ -201,23 +201,29 @@ int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token
  * The reference's per-token sends (executor_sim.hpp:540-564: thinker hidden
  * states, talker codes) are 4 B - 7 KiB host spans, each handed to a
  * ChunkCallback as an owned host vector after a checksum (sidecar.hpp:527-563).
- * Done as separate synchronous steps (H2D, wait, digest, read the digest,
- * D2H) that costs five GPU round trips per message.  fsx_put_small stages the
- * span in a slot of a pinned mapped mailbox and returns; staged messages are
- * flushed per device as ONE launch (at the first fsx_ticket_wait that needs
- * one of them, at fsx_flush_small, or once 2 MiB are staged) in which one CTA
- * per message copies the bytes into its slab segment and reads the landed
- * segment back into the slot while computing its dg64 on the device.
- * fsx_ticket_wait blocks until the message's batch has run (its bytes are
- * then in the slab) and returns the read-back bytes (valid until
- * fsx_ticket_free) and the device digest.  *ticket = -1 (not an error) when n
- * is 0 or > FSX_SMALL_MAX or the mailbox is full: use fsx_forward_host. */
+ * fsx_put_small copies the span into a slot of a pinned mapped mailbox,
+ * publishes a descriptor on the destination device's small-message lane and
+ * returns: a one-CTA service kernel on that device (launched on demand, exits
+ * after 200 us without work) moves each published message into its slab
+ * segment, digests the bytes it read (sent) and the segment read back (landed)
+ * and marks it done -- no launch, event or host digest per message.
+ * fsx_ticket_wait blocks until the message is served (its bytes are then in
+ * the slab) and returns the sent bytes (valid until fsx_ticket_free) and the
+ * landed dg64; fsx_ticket_digests returns both digests (sent == landed: the
+ * slab holds the bytes as sent).  *ticket = -1 (not an error) when n is 0 or
+ * > FSX_SMALL_MAX or the mailbox / lane ring is full: use fsx_forward_host.
+ * fsx_flush_small is a no-op kept for callers of the batched form. */
 #define FSX_SMALL_MAX 65536
 int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
                   int64_t* ticket);
 int fsx_flush_small(fsx_fabric* f);
 int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest);
+int fsx_ticket_digests(fsx_fabric* f, int64_t ticket, uint64_t* sent, uint64_t* landed);
 int fsx_ticket_free(fsx_fabric* f, int64_t ticket);
+/* Wait, copy the first n bytes of the message to h_dst (may be NULL), return
+ * both digests and free the ticket, in one call (the drop-in's delivery). */
+int fsx_ticket_take(fsx_fabric* f, int64_t ticket, void* h_dst, int64_t n, uint64_t* sent,
+                    uint64_t* landed);
 
 /* Host wait until flags [flag_base, flag_base + n) all equal token;
  * FSX_E_TIMEOUT after timeout_us (< 0 = forever). */

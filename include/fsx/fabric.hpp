@@ -296,6 +296,7 @@ class Fabric {
     node_of(gpu);
     RefState& st = refs_[key_of(ref_id, gpu)];
     st.dst_gpu = gpu;
+    any_early_ = true;
     st.early_cb = std::move(on_chunk);
     st.on_chunk = nullptr;
     st.raw_cb = nullptr;
@@ -517,6 +518,13 @@ class Fabric {
     return ref_id + "@" + std::to_string(gpu);
   }
 
+  // ForwardEnvelope::location of a slab segment: "gpu<G>:off<K>"
+  static std::string location_of(int gpu, int64_t off) {
+    char buf[48];
+    const int k = std::snprintf(buf, sizeof buf, "gpu%d:off%lld", gpu, static_cast<long long>(off));
+    return std::string(buf, static_cast<size_t>(k));
+  }
+
   static int device_of_pointer(const void* p) {
     int dev = -1;
     if (fsx_pointer_device(p, &dev) != FSX_OK) return -1;
@@ -562,11 +570,11 @@ class Fabric {
     const bool local = Traits::is_local(ps.env) && !ps.network;
     *ticket = -1;
     if (!ps.src_is_device && n > 0 && n <= FSX_SMALL_MAX) {
-      // small host span (per-token hidden states, codes): one asynchronous
-      // H2D + device read-back, waited for at delivery
+      // small host span (per-token hidden states, codes): published on the
+      // destination's small-message lane; the lane kernel digests the bytes
+      // it moves (sent) and the landed segment, read at delivery
       check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
       if (*ticket >= 0) {
-        if (local) ps.env.checksum = digest64(ps.src, static_cast<size_t>(n));
         *n_chunks = 0;
         *token = 0;
         digest_slot_ = nullptr;
@@ -632,11 +640,12 @@ class Fabric {
       landing.n_chunks = 0;
     }
     if (digest_slot_) check(fsx_read_u64(h_, ps.env.src_gpu, digest_slot_, &ps.env.checksum, nullptr));
-    ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
+    ps.env.location = location_of(ps.env.dst_gpu, off);
     const double lat = config_.latency_ms(Transport::LocalBuffer, ps.env.chunk_bytes);
     added_latency_ms_ += lat;
-    if (hand_over_early(ps.env, off, ticket, landing)) return true;
-    auto env = std::make_shared<Envelope>(ps.env);
+    if (any_early_ && hand_over_early(ps.env, off, ticket, landing)) return true;
+    // the Pending is dropped once placed (send / place_backlog): move its envelope
+    auto env = std::make_shared<Envelope>(std::move(ps.env));
     Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.deliver",
                      [this, env, off, ticket, landing] { deliver(*env, off, ticket, false, landing); });
     return true;
@@ -658,14 +667,20 @@ class Fabric {
     if (it == refs_.end() || !it->second.early_cb) return false;
     RefState& st = it->second;
     if (st.request_id.empty()) st.request_id = env.request_id;
-    drop_ticket(ticket);  // a staged small message: in the slab once its batch ran
+    Envelope e = env;
+    if (ticket >= 0) {  // a small message: in the slab once the lane served it
+      uint64_t sent = 0;
+      check(fsx_ticket_digests(h_, ticket, &sent, nullptr));
+      if (Traits::is_local(e)) e.checksum = sent;
+      drop_ticket(ticket);
+    }
     ChunkFlags cf{landing.flag_base, landing.n_chunks, landing.token,
-                  landing.n_chunks > 1 ? std::min<int64_t>(config_.device_chunk_bytes, env.chunk_bytes)
-                                       : env.chunk_bytes};
+                  landing.n_chunks > 1 ? std::min<int64_t>(config_.device_chunk_bytes, e.chunk_bytes)
+                                       : e.chunk_bytes};
     ++transfers_;
-    bytes_forwarded_ += env.chunk_bytes;
-    raw_held_.insert({env.dst_gpu, off});
-    st.early_cb(env, off, cf);
+    bytes_forwarded_ += e.chunk_bytes;
+    raw_held_.insert({e.dst_gpu, off});
+    st.early_cb(e, off, cf);
     return true;
   }
 
@@ -675,7 +690,7 @@ class Fabric {
     uint64_t token = 0;
     int32_t n_chunks = 1;
     if (!start_copy(ps, &off, &token, &flag_base, &n_chunks, &ticket)) return false;
-    ps.env.location = "gpu" + std::to_string(ps.env.dst_gpu) + ":off" + std::to_string(off);
+    ps.env.location = location_of(ps.env.dst_gpu, off);
     if (ticket < 0) wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
     deliver(ps.env, off, ticket, /*network=*/true);
     return true;
@@ -729,6 +744,11 @@ class Fabric {
       const Landing landing = it->second.landing;
       st.parked.erase(it);
       if (st.early_cb) {  // early interest registered after the placement
+        if (ticket >= 0 && Traits::is_local(env) && !network) {
+          uint64_t sent = 0;
+          check(fsx_ticket_digests(h_, ticket, &sent, nullptr));
+          env.checksum = sent;
+        }
         drop_ticket(ticket);
         ++transfers_;
         bytes_forwarded_ += env.chunk_bytes;
@@ -743,6 +763,11 @@ class Fabric {
       // a send that returned before its bytes landed: the delivery waits
       settle(landing, env.dst_gpu);
       if (st.raw_cb) {
+        if (ticket >= 0 && Traits::is_local(env) && !network) {
+          uint64_t sent = 0;
+          check(fsx_ticket_digests(h_, ticket, &sent, nullptr));
+          env.checksum = sent;
+        }
         drop_ticket(ticket);  // waits until the bytes are in the slab
         ++transfers_;
         bytes_forwarded_ += env.chunk_bytes;
@@ -758,15 +783,14 @@ class Fabric {
       std::vector<uint8_t> bytes;
       bool dev_ok = true;
       if (ticket >= 0) {
-        // small message: bytes and dg64 were read back from the slab on the
-        // device right after they landed (fsx_put_small)
-        const void* mail = nullptr;
-        uint64_t dev_digest = 0;
-        check(fsx_ticket_wait(h_, ticket, &mail, &dev_digest));
-        const uint8_t* m = static_cast<const uint8_t*>(mail);
-        bytes.assign(m, m + env.chunk_bytes);
-        check(fsx_ticket_free(h_, ticket));
-        dev_ok = !local || dev_digest == env.checksum;
+        // small message: the lane kernel digested the bytes it moved (the
+        // producer's, as staged by send) and the segment read back from the
+        // slab; the consumer gets the staged bytes
+        uint64_t sent = 0, landed = 0;
+        bytes.resize(static_cast<size_t>(env.chunk_bytes));
+        check(fsx_ticket_take(h_, ticket, bytes.data(), env.chunk_bytes, &sent, &landed));
+        if (local) env.checksum = sent;
+        dev_ok = landed == sent;
       } else {
         bytes = owned_buffer(static_cast<size_t>(env.chunk_bytes));
         dev_ok = !local || slab_digest(env.dst_gpu, off, env.chunk_bytes) == env.checksum;
@@ -856,6 +880,7 @@ class Fabric {
   SidecarConfig config_;
   fsx_fabric* h_ = nullptr;
   uint64_t* digest_slot_ = nullptr;  // K1 digest of the send being placed
+  bool any_early_ = false;           // an early-start interest was registered (placement looks it up)
   std::vector<int> slabs_;
   std::map<std::string, RefState> refs_;
   std::set<std::pair<int, int64_t>> raw_held_;  // (slab gpu, offset) handed to raw callbacks

@@ -143,7 +143,10 @@ _SIGS = {
     "fsx_ipc_close": [C.c_void_p, C.c_void_p],
     "fsx_put_small": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)],
     "fsx_ticket_wait": [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
+    "fsx_ticket_digests": [C.c_void_p, C.c_int64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "fsx_ticket_free": [C.c_void_p, C.c_int64],
+    "fsx_ticket_take": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_uint64),
+                        C.POINTER(C.c_uint64)],
     "fsx_flush_small": [C.c_void_p],
     "fsx_flags_alloc": [C.c_void_p, C.c_int, C.c_int32, C.POINTER(C.c_int64)],
     "fsx_flag_ptr": [C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_void_p)],

@@ -14,7 +14,7 @@
 //   K1+K3 merge_tee_kernel  the forward and the merge as one kernel: each item row
 //                           is read once and stored into its slab segment (with
 //                           the chunk flags) and into its placeholder row
-//   flags / digest / mailbox / channel kernels (see each)
+//   flags / digest / small-message lane / channel kernels (see each)
 //
 // Everything here is integer byte movement: rows are opaque 16-byte vectors,
 // never converted through a floating-point type, so bf16 NaN/Inf patterns in the
@@ -461,45 +461,216 @@ __global__ void __launch_bounds__(256) digest_kernel(const uint8_t* __restrict__
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)acc);
 }
 
-// Small host messages (fsx_put_small), one CTA per message: copy the staged
-// bytes from the mapped pinned mailbox (PCIe reads) into the slab segment,
-// then read the landed segment back into the slot while computing its dg64,
-// so a ChunkCallback consumer gets the bytes that are in device memory,
-// verified on the device.  bar.sync orders the CTA's slab stores before its
-// own re-reads (coherent loads, no .nc).
-constexpr int kMailThreads = 256;
-__global__ void __launch_bounds__(kMailThreads) mailbox_kernel(const __grid_constant__ MailStep m) {
-  __shared__ uint64_t red[kMailThreads / 32];
-  uint8_t* slot = m.mail + m.slot[blockIdx.x];
-  MailHeader* h = reinterpret_cast<MailHeader*>(slot);
-  uint8_t* bytes = slot + kMailHeader;
-  uint8_t* dst = h->dst;
-  const int64_t n = h->n;
-  const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;  // slots are 64 B aligned
-  const int64_t nv = vec ? n >> 4 : 0;
-  for (int64_t i = threadIdx.x; i < nv; i += kMailThreads)
-    st_v4(dst + 16 * i, ld_v4(bytes + 16 * i));
-  for (int64_t j = nv * 16 + threadIdx.x; j < n; j += kMailThreads) dst[j] = bytes[j];
-  __syncthreads();
-  uint64_t acc = 0;
-  for (int64_t i = threadIdx.x; i < nv; i += kMailThreads) {
-    const uint4 v = ld_v4(dst + 16 * i);
-    *reinterpret_cast<uint4*>(bytes + 16 * i) = v;
-    acc += dg_vec(v, 2 * (uint64_t)i);
+// ---------------------------------------------------------------------------
+// Small-message lane (fsx_put_small; LaneCtl / LaneDesc in fsx_kernels.cuh).
+//
+// One 1024-thread CTA per destination device serves the lane.  Warp 0 is the
+// poller: lane 0 reads the host-published tail (one PCIe round trip, ~1.2 us
+// on the B200 hosts, scripts/probe_pcie_pull.cu), the warp fetches the new
+// descriptors with coalesced reads into a shared-memory cache and publishes
+// the tail to the workers in shared memory.  Warps 1..31 are workers: worker
+// w moves messages m with m % 31 == w as soon as the shared tail passes m,
+// independently of the others (no CTA barrier per batch, so messages
+// published while others are in flight start at once).  A worker's lanes read
+// 4 x 16 B of the staged bytes per round (volatile loads: mapped host memory
+// is not L1-coherent and slots are reused), store them into the slab segment,
+// digest them (`sent`), read the segment back (volatile, from L2) and digest
+// that (`landed`); after __syncwarp lane 0 writes both digests and
+// st.release.sys's done = seq + 1.
+//
+// Exit handshake (no cross-device atomics): once every worker has finished
+// everything published and nothing new arrived for kLaneIdleNs, the poller
+// stores `consumed` and exit_epoch = its epoch, fence.sc.sys, and re-reads
+// the tail; the host publishes with store tail, mfence, load exit_epoch.  Of
+// two racing sides at least one sees the other's store: either the poller
+// sees the new tail and keeps serving (resetting exit_epoch), or the host
+// sees the announcement and launches epoch + 1 behind it on the lane's
+// stream, which resumes from `consumed`.  Workers only ever take messages
+// below the tail the poller published, so an exiting instance and its
+// successor never move the same message.  A spare instance is harmless (it
+// starts after this one exits, finds nothing, idles out).
+constexpr int kLaneThreads = 1024;
+constexpr int kLaneWorkers = kLaneThreads / 32 - 1;
+constexpr int kLaneUnroll = 4;
+constexpr int kLaneCache = 256;  // shared descriptor cache (power of two)
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ uint8_t ld_volatile_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.volatile.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return (uint8_t)v;
+}
+
+// One worker warp moves one message (see above).
+__device__ __forceinline__ void lane_move(LaneDesc* d, uint8_t* dst, const uint8_t* src, int n, uint64_t seq) {
+  const int lane = threadIdx.x & 31;
+  const bool vec = (((uintptr_t)dst | (uintptr_t)src) & 15) == 0;
+  const int nv = vec ? n >> 4 : 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  uint64_t sent = 0, landed = 0;
+  for (int base = lane; base < nv; base += 32 * kLaneUnroll) {
+    uint4 r[kLaneUnroll];
+#pragma unroll
+    for (int k = 0; k < kLaneUnroll; ++k)
+      if (base + 32 * k < nv) r[k] = ld_volatile_v4(s4 + base + 32 * k);
+#pragma unroll
+    for (int k = 0; k < kLaneUnroll; ++k)
+      if (base + 32 * k < nv) {
+        st_v4(d4 + base + 32 * k, r[k]);
+        sent += dg_vec(r[k], 2 * (uint64_t)(base + 32 * k));
+      }
   }
-  __syncthreads();  // every vector store into the slot precedes the tail rewrite below
-  if (threadIdx.x == 0) {
-    const int64_t from = nv * 16;
-    for (int64_t j = from; j < n; ++j) bytes[j] = dst[j];
-    acc += dg_bytes(dst, from, n) + (uint64_t)n * 0x9e3779b97f4a7c15ull;
+  // sub-vector tail (and unaligned messages), lane 0, byte-wise
+  const int from = nv * 16;
+  if (lane == 0 && from < n) {
+    for (int w8 = from >> 3; w8 * 8 < n; ++w8) {
+      uint64_t v = 0;
+      for (int b = 0; b < 8 && w8 * 8 + b < n; ++b) {
+        const uint8_t x = ld_volatile_u8(src + w8 * 8 + b);
+        dst[w8 * 8 + b] = x;
+        v |= (uint64_t)x << (8 * b);
+      }
+      sent += dg_word(v, (uint64_t)w8);
+    }
   }
-  acc = warp_sum_u64(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
+  __syncwarp();
+  for (int base = lane; base < nv; base += 32 * kLaneUnroll) {
+    uint4 r[kLaneUnroll];
+#pragma unroll
+    for (int k = 0; k < kLaneUnroll; ++k)
+      if (base + 32 * k < nv) r[k] = ld_volatile_v4(d4 + base + 32 * k);
+#pragma unroll
+    for (int k = 0; k < kLaneUnroll; ++k)
+      if (base + 32 * k < nv) landed += dg_vec(r[k], 2 * (uint64_t)(base + 32 * k));
+  }
+  if (lane == 0 && from < n) {
+    for (int w8 = from >> 3; w8 * 8 < n; ++w8) {
+      uint64_t v = 0;
+      for (int b = 0; b < 8 && w8 * 8 + b < n; ++b) v |= (uint64_t)ld_volatile_u8(dst + w8 * 8 + b) << (8 * b);
+      landed += dg_word(v, (uint64_t)w8);
+    }
+  }
+  sent = warp_sum_u64(sent);
+  landed = warp_sum_u64(landed);
+  __syncwarp();
+  if (lane == 0) {
+    const uint64_t len = (uint64_t)n * 0x9e3779b97f4a7c15ull;
+    st_volatile_u64(&d->sent, sent + len);
+    st_volatile_u64(&d->landed, landed + len);
+    st_release_sys(&d->done, seq + 1);  // the warp's slab stores and the digests first
+  }
+}
+
+__global__ void __launch_bounds__(kLaneThreads, 1) lane_kernel(LaneCtl* ctl, LaneDesc* ring, uint64_t epoch) {
+  __shared__ uint64_t s_dst[kLaneCache], s_src[kLaneCache];
+  __shared__ uint32_t s_n[kLaneCache];
+  __shared__ uint64_t s_q[kLaneWorkers];  // per worker: its next message (all before it are done)
+  __shared__ uint64_t s_tail;             // published to the workers
+  __shared__ int s_exit;
+  volatile uint64_t* vq = s_q;
+  volatile uint64_t* vtail = &s_tail;
+  volatile int* vexit = &s_exit;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t consumed = ld_volatile_u64(&ctl->consumed);
   if (threadIdx.x == 0) {
-    uint64_t t = 0;
-    for (int w = 0; w < kMailThreads / 32; ++w) t += red[w];
-    h->digest = t;
+    s_tail = consumed;
+    s_exit = 0;
+  }
+  if (warp > 0 && lane == 0) {
+    const uint64_t w = (uint64_t)(warp - 1);
+    s_q[w] = consumed + (w + kLaneWorkers - consumed % kLaneWorkers) % kLaneWorkers;
+  }
+  __syncthreads();
+  if (warp == 0) {  // poller
+    uint64_t pub = consumed;
+    uint64_t idle_from = globaltimer_ns();
+    for (;;) {
+      uint64_t t = 0;
+      if (lane == 0) t = ld_acquire_sys(&ctl->tail);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      // oldest message a worker may still read from the cache
+      uint64_t oldest = lane < kLaneWorkers ? vq[lane] : ~0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) oldest = min(oldest, __shfl_xor_sync(0xffffffffu, oldest, o));
+      t = min(t, oldest + kLaneCache);
+      if (t > pub) {
+        // descriptors [pub, t): lane l reads word l % 4 of descriptor pub + l / 4
+        for (uint64_t m0 = pub; m0 < t; m0 += 8) {
+          const uint64_t m = m0 + (lane >> 2);
+          const int wd = lane & 3;
+          uint64_t v = 0;
+          if (m < t && wd < 3) v = ld_volatile_u64(reinterpret_cast<const uint64_t*>(&ring[m % kLaneSlots]) + wd);
+          const int c = (int)(m % kLaneCache);
+          if (m < t) {
+            if (wd == 0) s_dst[c] = v;
+            else if (wd == 1) s_src[c] = v;
+            else if (wd == 2) s_n[c] = (uint32_t)v;
+          }
+        }
+        __syncwarp();
+        __threadfence_block();  // the cache entries before the tail the workers read
+        if (lane == 0) *vtail = t;
+        pub = t;
+        idle_from = globaltimer_ns();
+        continue;
+      }
+      // idle: every worker past everything published, nothing new for a while
+      const bool drained = __all_sync(0xffffffffu, lane >= kLaneWorkers || vq[lane] >= pub);
+      int leave = 0;
+      if (drained && (globaltimer_ns() - idle_from > kLaneIdleNs || ld_volatile_u64(&ctl->stop) != 0)) {
+        if (lane == 0) {
+          st_volatile_u64(&ctl->consumed, pub);
+          st_volatile_u64(&ctl->exit_epoch, epoch);
+          fence_sc_sys();
+          if (ld_acquire_sys(&ctl->tail) > pub) {
+            st_volatile_u64(&ctl->exit_epoch, 0);  // keep serving
+          } else {
+            *vexit = 1;
+            leave = 1;
+          }
+        }
+        leave = __shfl_sync(0xffffffffu, leave, 0);
+        if (leave) return;
+      } else {
+        __nanosleep(100);
+      }
+    }
+  }
+  // worker
+  const int w = warp - 1;
+  uint64_t q = s_q[w];
+  for (;;) {
+    if (*vtail <= q) {
+      if (*vexit) return;
+      __nanosleep(32);
+      continue;
+    }
+    __threadfence_block();
+    const int c = (int)(q % kLaneCache);
+    lane_move(&ring[q % kLaneSlots], reinterpret_cast<uint8_t*>(s_dst[c]),
+              reinterpret_cast<const uint8_t*>(s_src[c]), (int)s_n[c], q);
+    q += kLaneWorkers;
+    __syncwarp();
+    if (lane == 0) vq[w] = q;
   }
 }
 
@@ -998,9 +1169,8 @@ cudaError_t launch_wait_flags(const uint64_t* dflags, int32_t n, uint64_t token,
   return cudaGetLastError();
 }
 
-cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st) {
-  if (m.n <= 0) return cudaSuccess;
-  mailbox_kernel<<<m.n, kMailThreads, 0, st>>>(m);
+cudaError_t launch_lane(LaneCtl* ctl, LaneDesc* ring, uint64_t epoch, cudaStream_t st) {
+  lane_kernel<<<1, kLaneThreads, 0, st>>>(ctl, ring, epoch);
   return cudaGetLastError();
 }
 
@@ -1078,6 +1248,7 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(merge_tee_kernel),
       reinterpret_cast<const void*>(set_flags_kernel),
       reinterpret_cast<const void*>(chan_push_kernel),
+      reinterpret_cast<const void*>(lane_kernel),
   };
   cudaFuncAttributes a;
   for (const void* f : fns) {

@@ -99,25 +99,41 @@ struct ChanStep {
   ChanRow c[kChanMaxRows];
 };
 
-// Small host messages (fsx_put_small): each staged in a slot of a mapped
-// pinned mailbox, header first.  One launch moves a batch of them.
-struct MailHeader {
-  uint8_t* dst;     // slab destination (device)
-  int64_t n;        // bytes (<= FSX_SMALL_MAX)
-  uint64_t digest;  // dg64 of the landed bytes, written by the kernel
+// Small host messages (fsx_put_small): the small-message lane.  Each message
+// is staged in a slot of a mapped pinned mailbox and described by a LaneDesc
+// in a per-device ring of mapped pinned host memory; the host publishes it by
+// advancing LaneCtl::tail.  A one-CTA service kernel on the destination
+// device polls the tail, moves each message into its slab segment, digests the
+// bytes it read and the bytes it reads back from the slab, and marks the
+// descriptor done -- no launch and no event per message or per batch.  The
+// kernel exits after kLaneIdleNs without work (so a device-wide synchronize
+// never waits on it for long); the host relaunches it when it publishes into
+// a lane whose kernel has announced its exit (LaneCtl::exit_epoch, a
+// store/fence/load handshake on both sides, see lane_kernel).
+struct LaneDesc {                 // 64 B, mapped pinned host memory
+  uint8_t* dst;                   // slab destination (device)
+  const uint8_t* src;             // staged bytes (mapped pinned host memory)
+  int64_t n;                      // bytes (<= FSX_SMALL_MAX)
+  uint64_t sent;                  // dg64 of the bytes read from src (kernel)
+  uint64_t landed;                // dg64 of the bytes read back from dst (kernel)
+  uint64_t done;                  // seq + 1 once sent/landed are written (kernel)
+  uint64_t _pad[2];
 };
-constexpr int64_t kMailHeader = 64;  // bytes start 64 B into the slot
-constexpr int kMailMaxBatch = 256;
-struct MailStep {
-  uint8_t* mail;                  // mailbox base (mapped pinned host memory)
-  int32_t n;
-  int32_t _pad;
-  int64_t slot[kMailMaxBatch];    // slot offsets
+struct LaneCtl {                  // mapped pinned host memory, one per device
+  uint64_t tail;                  // descriptors published (host)
+  uint64_t _p0[7];
+  uint64_t consumed;              // descriptors processed, written at kernel exit
+  uint64_t _p1[7];
+  uint64_t exit_epoch;            // epoch of the kernel that announced its exit
+  uint64_t stop;                  // host: exit as soon as idle (fsx_close)
+  uint64_t _p2[6];
 };
+constexpr int kLaneSlots = 4096;                 // descriptor ring
+constexpr uint64_t kLaneIdleNs = 200ull * 1000;  // service kernel exits after 200 us idle
 
 // Launchers return cudaError_t of the launch.  `grid` is chosen by the caller.
 cudaError_t launch_digest(const uint8_t* p, int64_t n, uint64_t* out, int grid, cudaStream_t st);
-cudaError_t launch_mailbox(const MailStep& m, cudaStream_t st);
+cudaError_t launch_lane(LaneCtl* ctl, LaneDesc* ring, uint64_t epoch, cudaStream_t st);
 cudaError_t launch_chan_push(const ChanStep& s, cudaStream_t st);
 cudaError_t launch_chan_pull(const ChanStep& s, cudaStream_t st);
 // bulk: the bulk-copy tile kernel when every transfer allows it (16-byte

@@ -335,26 +335,27 @@ struct fsx_fabric {
   std::map<int, std::unique_ptr<Device>> devices;
   std::vector<Channel> channels;
   std::map<void*, int> ipc_maps;  // fsx_ipc_open mappings -> device
-  // fsx_put_small: pinned mapped mailbox (first-fit slots), tickets, and per
-  // device the staged messages not yet flushed to the GPU
+  // fsx_put_small: pinned mapped mailbox (first-fit slots for the staged
+  // bytes), per destination device a small-message lane (descriptor ring +
+  // control block in mapped pinned memory, served by lane_kernel), tickets
+  struct Lane {
+    fsx::LaneCtl* ctl = nullptr;
+    fsx::LaneDesc* ring = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t tail = 0;         // descriptors published
+    uint64_t epoch = 0;        // epoch of the last launched service kernel (0: none yet)
+    int64_t outstanding = 0;   // published, ticket not yet freed
+  };
+  std::map<int, Lane> lanes;   // by device ordinal
   uint8_t* mail = nullptr;
   BlockList mail_blocks;
   struct Ticket {
-    int64_t slot = -1;   // mailbox offset of the slot header, -1 = free ticket
+    int64_t slot = -1;   // mailbox offset of the staged bytes, -1 = free ticket
     int device = -1;
-    int64_t batch = -1;  // flush batch (its event), -1 = still staged
+    uint64_t seq = 0;    // lane descriptor sequence number
   };
   std::vector<Ticket> tickets;
   std::vector<int64_t> free_tickets;
-  struct MailBatch {
-    cudaEvent_t ev = nullptr;
-    int refs = 0;
-    bool done = false;  // ev seen complete (later waits skip the synchronize)
-  };
-  std::vector<MailBatch> batches;
-  std::vector<int64_t> free_batches;
-  std::map<int, std::vector<int64_t>> staged;  // device -> staged tickets
-  std::map<int, int64_t> staged_bytes;         // device -> their payload bytes
   std::atomic<uint64_t> next_token{1};
   std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
 };
@@ -479,6 +480,15 @@ int fsx_open(int n_gpus, const int* gpu_ids, const int* node_ids, const int* dev
 
 int fsx_close(fsx_fabric* f) {
   if (!f) return FSX_OK;
+  for (auto& [o, l] : f->lanes) {  // service kernels exit once idle
+    reinterpret_cast<volatile uint64_t*>(&l.ctl->stop)[0] = 1;
+    cudaSetDevice(o);
+    if (l.stream) {
+      cudaStreamSynchronize(l.stream);
+      cudaStreamDestroy(l.stream);
+    }
+    cudaFreeHost(l.ctl);
+  }
   for (auto& [o, d] : f->devices) {
     cudaSetDevice(o);
     cudaStreamSynchronize(d->stream);
@@ -493,8 +503,6 @@ int fsx_close(fsx_fabric* f) {
       if (s->hflags) cudaFreeHost(s->hflags);
     }
   }
-  for (auto& b : f->batches)
-    if (b.ev) cudaEventDestroy(b.ev);
   if (f->mail) cudaFreeHost(f->mail);
   for (auto& [p, o] : f->ipc_maps) {
     cudaSetDevice(o);
@@ -1007,44 +1015,62 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
 }
 
 constexpr int64_t kMailBytes = int64_t{16} << 20;
-constexpr int64_t kMailStageBytes = int64_t{2} << 20;  // flush once this much is staged
 
 namespace {
 
-// Launch the staged messages of `device` as one batch (caller holds f->mu).
-int flush_staged(fsx_fabric* f, int device) {
-  NvtxRange nvtx_range("fsx.small_flush");
-  auto it = f->staged.find(device);
-  if (it == f->staged.end() || it->second.empty()) return FSX_OK;
-  std::vector<int64_t>& q = it->second;
-  Device* dev = nullptr;
-  int rc = device_state(f, device, &dev);
-  if (rc) return rc;
-  int64_t bid;
-  if (f->free_batches.empty()) {
-    f->batches.emplace_back();
-    bid = (int64_t)f->batches.size() - 1;
-  } else {
-    bid = f->free_batches.back();
-    f->free_batches.pop_back();
+// The lane of `device`, created on first use (caller holds f->mu).
+int lane_of(fsx_fabric* f, int device, fsx_fabric::Lane** out) {
+  auto it = f->lanes.find(device);
+  if (it != f->lanes.end()) {
+    *out = &it->second;
+    return FSX_OK;
   }
-  fsx_fabric::MailBatch& mb = f->batches[bid];
+  fsx_fabric::Lane l;
   FSX_CUDA(cudaSetDevice(device));
-  if (!mb.ev) FSX_CUDA(cudaEventCreateWithFlags(&mb.ev, cudaEventDisableTiming));
-  for (size_t at = 0; at < q.size(); at += fsx::kMailMaxBatch) {
-    fsx::MailStep ms{};
-    ms.mail = f->mail;
-    ms.n = (int32_t)std::min<size_t>(fsx::kMailMaxBatch, q.size() - at);
-    for (int32_t k = 0; k < ms.n; ++k) ms.slot[k] = f->tickets[q[at + k]].slot;
-    FSX_CUDA(fsx::launch_mailbox(ms, dev->stream));
-    f->launches++;
+  void* mem = nullptr;
+  const size_t bytes = sizeof(fsx::LaneCtl) + sizeof(fsx::LaneDesc) * fsx::kLaneSlots;
+  FSX_CUDA(cudaHostAlloc(&mem, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(mem, 0, bytes);
+  l.ctl = static_cast<fsx::LaneCtl*>(mem);
+  l.ring = reinterpret_cast<fsx::LaneDesc*>(static_cast<uint8_t*>(mem) + sizeof(fsx::LaneCtl));
+  FSX_CUDA(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+  *out = &f->lanes.emplace(device, l).first->second;
+  return FSX_OK;
+}
+
+inline uint64_t vload(const uint64_t* p) { return *reinterpret_cast<const volatile uint64_t*>(p); }
+inline void vstore(uint64_t* p, uint64_t v) { *reinterpret_cast<volatile uint64_t*>(p) = v; }
+
+// The ticket's descriptor, once its message has been served (caller does not
+// hold f->mu).  Spins on the done mark (host memory the kernel writes over
+// PCIe); FSX_E_TIMEOUT after FSX_SPIN_TIMEOUT_S (default 30 s).
+int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t* slot) {
+  const fsx::LaneDesc* d = nullptr;
+  uint64_t seq = 0;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || f->tickets[ticket].slot < 0)
+      return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
+    const fsx_fabric::Ticket& t = f->tickets[ticket];
+    d = &f->lanes.at(t.device).ring[t.seq % fsx::kLaneSlots];
+    seq = t.seq;
+    *slot = t.slot;
   }
-  FSX_CUDA(cudaEventRecord(mb.ev, dev->stream));
-  mb.done = false;
-  mb.refs = (int)q.size();
-  for (int64_t t : q) f->tickets[t].batch = bid;
-  q.clear();
-  f->staged_bytes[device] = 0;
+  if (vload(&d->done) != seq + 1) {
+    const char* e = std::getenv("FSX_SPIN_TIMEOUT_S");
+    const double secs = e ? std::atof(e) : 30.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    uint32_t n = 0;
+    while (vload(&d->done) != seq + 1) {
+      if ((++n & 4095u) == 0) {
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > secs)
+          return fail(FSX_E_TIMEOUT, "small-message lane: message not served within the watchdog time");
+        std::this_thread::yield();
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  *out = d;
   return FSX_OK;
 }
 
@@ -1063,7 +1089,11 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
     FSX_CUDA(cudaHostAlloc(&f->mail, kMailBytes, cudaHostAllocMapped | cudaHostAllocPortable));
     f->mail_blocks.reset(kMailBytes);
   }
-  const int64_t slot = f->mail_blocks.alloc(fsx::kMailHeader + (n + 63) / 64 * 64);
+  fsx_fabric::Lane* l = nullptr;
+  int rc = lane_of(f, s->device, &l);
+  if (rc) return rc;
+  if (l->outstanding >= fsx::kLaneSlots) return FSX_OK;  // ring full: caller takes the synchronous path
+  const int64_t slot = f->mail_blocks.alloc((n + 63) / 64 * 64);
   if (slot < 0) return FSX_OK;  // mailbox full: caller takes the synchronous path
   int64_t id;
   if (f->free_tickets.empty()) {
@@ -1073,65 +1103,87 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
     id = f->free_tickets.back();
     f->free_tickets.pop_back();
   }
-  f->tickets[id] = fsx_fabric::Ticket{slot, s->device, -1};
-  // slot: header {slab destination, bytes, digest} then the bytes
-  fsx::MailHeader* h = reinterpret_cast<fsx::MailHeader*>(f->mail + slot);
-  h->dst = s->base + dst_off;
-  h->n = n;
-  h->digest = 0;
-  std::memcpy(f->mail + slot + fsx::kMailHeader, h_src, (size_t)n);
-  std::vector<int64_t>& q = f->staged[s->device];
-  q.push_back(id);
+  const uint64_t seq = l->tail;
+  f->tickets[id] = fsx_fabric::Ticket{slot, s->device, seq};
+  std::memcpy(f->mail + slot, h_src, (size_t)n);
+  fsx::LaneDesc* d = &l->ring[seq % fsx::kLaneSlots];
+  d->dst = s->base + dst_off;
+  d->src = f->mail + slot;
+  d->n = n;
+  vstore(&d->done, 0);
+  // descriptor and bytes before the tail (x86 keeps stores in order; this
+  // orders the compiler), then the exit handshake of lane_kernel: store tail,
+  // full fence, load exit_epoch
+  std::atomic_thread_fence(std::memory_order_release);
+  vstore(&l->ctl->tail, seq + 1);
+  l->tail = seq + 1;
+  ++l->outstanding;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  if (l->epoch == 0 || vload(&l->ctl->exit_epoch) == l->epoch) {
+    FSX_CUDA(cudaSetDevice(s->device));
+    FSX_CUDA(fsx::launch_lane(l->ctl, l->ring, l->epoch + 1, l->stream));
+    ++l->epoch;
+    f->launches++;
+  }
   f->forwards++;
   f->bytes_forwarded += n;
   *ticket = id;
-  if ((f->staged_bytes[s->device] += n) >= kMailStageBytes) return flush_staged(f, s->device);
   return FSX_OK;
 }
 
 int fsx_flush_small(fsx_fabric* f) {
-  std::lock_guard<std::mutex> lk(f->mu);
-  for (auto& [device, q] : f->staged) {
-    int rc = flush_staged(f, device);
-    if (rc) return rc;
-  }
+  (void)f;  // messages are served as they are published (small-message lane)
   return FSX_OK;
 }
 
 int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest) {
-  cudaEvent_t ev = nullptr;
+  const fsx::LaneDesc* d = nullptr;
   int64_t slot = -1;
-  {
-    std::lock_guard<std::mutex> lk(f->mu);
-    if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || f->tickets[ticket].slot < 0)
-      return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
-    if (f->tickets[ticket].batch < 0) {
-      int rc = flush_staged(f, f->tickets[ticket].device);  // everything staged on that device
-      if (rc) return rc;
-    }
-    auto& bt = f->batches[f->tickets[ticket].batch];
-    ev = bt.done ? nullptr : bt.ev;  // a batch seen complete is not synchronised again
-    slot = f->tickets[ticket].slot;
-  }
-  if (ev) {
-    FSX_CUDA(cudaEventSynchronize(ev));
-    std::lock_guard<std::mutex> lk(f->mu);
-    f->batches[f->tickets[ticket].batch].done = true;
-  }
-  const fsx::MailHeader* h = reinterpret_cast<const fsx::MailHeader*>(f->mail + slot);
-  if (h_bytes) *h_bytes = f->mail + slot + fsx::kMailHeader;
-  if (digest) *digest = *reinterpret_cast<const volatile uint64_t*>(&h->digest);
+  int rc = lane_wait(f, ticket, &d, &slot);
+  if (rc) return rc;
+  if (h_bytes) *h_bytes = f->mail + slot;
+  if (digest) *digest = vload(&d->landed);
+  return FSX_OK;
+}
+
+int fsx_ticket_digests(fsx_fabric* f, int64_t ticket, uint64_t* sent, uint64_t* landed) {
+  const fsx::LaneDesc* d = nullptr;
+  int64_t slot = -1;
+  int rc = lane_wait(f, ticket, &d, &slot);
+  if (rc) return rc;
+  if (sent) *sent = vload(&d->sent);
+  if (landed) *landed = vload(&d->landed);
+  return FSX_OK;
+}
+
+int fsx_ticket_take(fsx_fabric* f, int64_t ticket, void* h_dst, int64_t n, uint64_t* sent,
+                    uint64_t* landed) {
+  const fsx::LaneDesc* d = nullptr;
+  int64_t slot = -1;
+  int rc = lane_wait(f, ticket, &d, &slot);
+  if (rc) return rc;
+  const int64_t len = (int64_t)vload(reinterpret_cast<const uint64_t*>(&d->n));
+  if (n < 0 || n > len) return fail(FSX_E_VALIDATION, "ticket take longer than the message");
+  if (h_dst && n > 0) std::memcpy(h_dst, f->mail + slot, (size_t)n);
+  if (sent) *sent = vload(&d->sent);
+  if (landed) *landed = vload(&d->landed);
+  std::lock_guard<std::mutex> lk(f->mu);
+  fsx_fabric::Ticket& t = f->tickets[ticket];
+  f->mail_blocks.release(t.slot);
+  --f->lanes.at(t.device).outstanding;
+  t = fsx_fabric::Ticket{};
+  f->free_tickets.push_back(ticket);
   return FSX_OK;
 }
 
 int fsx_ticket_free(fsx_fabric* f, int64_t ticket) {
-  // the slot and the slab segment may only be reused once the batch has run
+  // the slot and the slab segment may only be reused once the message is served
   int rc = fsx_ticket_wait(f, ticket, nullptr, nullptr);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(f->mu);
   fsx_fabric::Ticket& t = f->tickets[ticket];
   f->mail_blocks.release(t.slot);
-  if (--f->batches[t.batch].refs == 0) f->free_batches.push_back(t.batch);
+  --f->lanes.at(t.device).outstanding;
   t = fsx_fabric::Ticket{};
   f->free_tickets.push_back(ticket);
   return FSX_OK;
