@@ -445,6 +445,8 @@ def run_single(args):
             ev.append(e)
         batch.release()
 
+    host_issue = [0.0]  # host microseconds to issue one pass (last timed())
+
     def timed(step, n, record=True):
         """n passes between two events on `stream` (which waits for the last
         scan and the last pass); returns (ms per pass, per-pass events,
@@ -455,8 +457,10 @@ def run_single(args):
         stop = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         start.record(stream)
+        h0 = time.perf_counter()
         for _ in range(n):
             step(record=record)
+        host_issue[0] = (time.perf_counter() - h0) / n * 1e6
         stream.wait_event(scanned[counter[0] % 2])
         stop.record(stream)
         torch.cuda.synchronize()
@@ -491,6 +495,7 @@ def run_single(args):
         # the timed region: K passes, no per-pass events in between
         with ClockSampler(dev) as clk:
             ms_step, _, launches = timed(step, args.steps, record=False)
+        host_us_step = host_issue[0]
         # the same passes again with events around each tee launch: its
         # in-pass kernel time for the roofline
         for _ in range(2):
@@ -604,6 +609,7 @@ def run_single(args):
         "nvlink": {"applies": False, "why": "N=1: producer and consumer share one B200"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
+        "host_us_per_step": round(host_us_step, 1),
         "clocks": clk.summary(),
     }
     if not args.profile and not args.no_e2e:

@@ -808,8 +808,14 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     rc = device_state(f, src_dev, &dev);
     if (rc) return rc;
   }
-  // one CTA per 32 KiB tile; a chunk is counted complete tile by tile
-  const int64_t unit = fsx::forward_tile_bytes();
+  // one CTA per tile; a chunk is counted complete tile by tile.  Tiles are
+  // 32 KiB, or 4 KiB when the whole batch is at most 2 MiB: a small transfer
+  // is latency-bound, and 8x more CTAs with one vector per thread finish it
+  // sooner (64 KiB: 2.0 vs 2.5 us, 1 MiB: 2.4 vs 2.7 us; 4 MiB is faster with
+  // 32 KiB tiles; profiles/launch_floor_r02c.jsonl)
+  int64_t batch_bytes = 0;
+  for (int32_t i = 0; i < n; ++i) batch_bytes += t[i].bytes;
+  const int64_t unit = batch_bytes <= (int64_t{2} << 20) ? 4096 : fsx::forward_tile_bytes();
   FSX_CUDA(cudaSetDevice(src_dev));
   cudaStream_t st = pick_stream(dev, stream);
   const bool graph = capturing(st);

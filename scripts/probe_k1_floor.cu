@@ -1,0 +1,88 @@
+// Probe: the product K1 (fsx::launch_forward, linked from build/fsx_kernels.o)
+// for one small transfer, 200 launches back to back in a CUDA graph, next to
+// cudaMemcpyAsync D2D of the same bytes -- the same harness as
+// scripts/probe_launch_floor.cu, so the two files' numbers compare directly.
+// Diagnostic only.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -Ipaper_2603_12118_b200/csrc \
+//        -o build/probe_k1_floor scripts/probe_k1_floor.cu build/fsx_kernels.o
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "fsx_kernels.cuh"
+
+int main() {
+  const int reps = 200;
+  uint8_t *s = nullptr, *d = nullptr;
+  uint32_t* c = nullptr;
+  uint64_t* f = nullptr;
+  cudaMalloc(&s, 64 << 20);
+  cudaMalloc(&d, 64 << 20);
+  cudaMalloc(&c, 1 << 20);
+  cudaMalloc(&f, 1 << 20);
+  cudaMemset(s, 1, 64 << 20);
+  cudaMemset(c, 0, 1 << 20);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fsx::preload_kernels();
+  auto time_graph = [&](auto&& body) -> double {
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal) != cudaSuccess) return -1;
+    for (int i = 0; i < reps; ++i) body(i);
+    if (cudaStreamEndCapture(st, &g) != cudaSuccess) return -2;
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) return -3;
+    double best = 1e30;
+    for (int t = 0; t < 5; ++t) {
+      cudaGraphLaunch(ge, st);
+      cudaEventRecord(e0, st);
+      cudaGraphLaunch(ge, st);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    if (cudaGetLastError() != cudaSuccess) return -4;
+    return best * 1e3 / reps;
+  };
+  for (int64_t n : {int64_t{64} << 10, int64_t{256} << 10, int64_t{1} << 20, int64_t{4} << 20}) {
+    auto k1 = [&](int64_t unit, bool bulk) {
+      return time_graph([&](int i) {
+        fsx::FwdBatch b{};
+        b.n = 1;
+        fsx::FwdArgs& a = b.t[0];
+        a.src = s;
+        a.dst = d;
+        a.bytes = n;
+        a.chunk_bytes = n;
+        a.slice = unit;
+        a.chunk_units = (n + unit - 1) / unit;
+        a.last_units = a.chunk_units;
+        a.total_units = a.chunk_units;
+        a.n_chunks = 1;
+        a.vec = 16;
+        a.peer = 0;
+        a.counters = c + i;
+        a.dflags = f + i;
+        a.hflags = nullptr;
+        a.token = 1000 + i;
+        a.digest = nullptr;
+        b.unit_off[1] = a.total_units;
+        fsx::launch_forward(b, bulk, st);
+      });
+    };
+    const double t4 = k1(4096, false), t32 = k1(32768, false), b4 = k1(4096, true), b32 = k1(32768, true);
+    const double mc = time_graph([&](int) { cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st); });
+    std::printf("{\"bytes\": %lld, \"k1_tile_4k_us\": %.3f, \"k1_tile_32k_us\": %.3f, \"k1_bulk_4k_us\": %.3f, "
+                "\"k1_bulk_32k_us\": %.3f, \"memcpy_us\": %.3f}\n",
+                (long long)n, t4, t32, b4, b32, mc);
+  }
+  return 0;
+}
