@@ -858,7 +858,7 @@ __device__ __forceinline__ void discard_row(const uint8_t* src, int64_t rb, int 
 // behind the producer; with every flag already set the gated form runs at the
 // stream-ordered form's rate (the persistent grid-stride form it replaces
 // reached 0.88 of the copy peak alone, bench r02b `kernels.follow`).
-template <bool kGated>
+template <bool kGated, int U = kMergeUnroll>
 __device__ __forceinline__ void merge_row(const fsx_merge_batch& b) {
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
@@ -877,7 +877,7 @@ __device__ __forceinline__ void merge_row(const fsx_merge_batch& b) {
   }
   const uint8_t* src = static_cast<const uint8_t*>(b.d_item_src[item]) + j * rb;
   uint8_t* dst = static_cast<uint8_t*>(b.d_embeds) + (int64_t)row * rb;
-  warp_move_row(src, dst, nullptr, rb, lane, /*coherent=*/true, -1, -1);
+  warp_move_row<U>(src, dst, nullptr, rb, lane, /*coherent=*/true, -1, -1);
   if (b.mode & FSX_MERGE_DISCARD) discard_row(src, rb, lane);
 }
 
@@ -886,9 +886,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_copy_kernel(fsx_merge_bat
   merge_row<false>(b);
 }
 
-// early start behind a producer on another GPU / in another process
-__global__ void __launch_bounds__(kMergeThreads) merge_follow_kernel(fsx_merge_batch b) {
-  merge_row<true>(b);
+// early start behind a producer on another GPU / in another process.  Each
+// warp's flag acquire is one more dependent round trip before its loads, so
+// the gated form keeps more rows in flight: 3 CTAs per SM at 8 x 16 B per lane
+constexpr int kFollowMinBlocksGated = 3;
+__global__ void __launch_bounds__(kMergeThreads, kFollowMinBlocksGated) merge_follow_kernel(fsx_merge_batch b) {
+  merge_row<true, 8>(b);
 }
 
 // K1 + K3 as one kernel (fsx_forward_merge): the tee.  Same grid as
