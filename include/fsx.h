@@ -195,6 +195,14 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
 int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
                      int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                      void* stream);
+/* fsx_forward_host that also returns the dg64 of the source bytes as sent:
+ * computed in the same pass that stages a pageable source (copy and digest
+ * fused on the host copy threads), or alongside the DMA of a pinned one.  The
+ * drop-in's host-span sends (sidecar.hpp:302-347) use it for the envelope's
+ * checksum. */
+int fsx_forward_host_digest(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
+                            int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                            void* stream, uint64_t* digest);
 /* Non-blocking readiness of one chunk (host mirror of the flag). */
 int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token, int* ready);
 /* ---- small host messages ----------------------------------------------------

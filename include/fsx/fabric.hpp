@@ -597,9 +597,12 @@ class Fabric {
       *token = t.token;
       digest_slot_ = t.d_digest;
     } else {
-      // the H2D copy is in flight while the host digests the same span
-      check(fsx_forward_host(h_, ps.src, dst, *off, n, cb, *flag_base, token, nullptr));
-      if (local) ps.env.checksum = digest64_par(ps.src, static_cast<size_t>(n));
+      // host span: staged (pageable) or DMA'd (pinned) into the slab; its
+      // dg64 is computed in the same pass that stages it
+      uint64_t dg = 0;
+      check(fsx_forward_host_digest(h_, ps.src, dst, *off, n, cb, *flag_base, token, nullptr,
+                                    local ? &dg : nullptr));
+      if (local) ps.env.checksum = dg;
       digest_slot_ = nullptr;
     }
     return true;

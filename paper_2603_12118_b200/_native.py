@@ -157,6 +157,8 @@ _SIGS = {
     "fsx_forward_batch": [C.c_void_p, C.c_int32, C.POINTER(Transfer), C.c_uint32, C.c_void_p],
     "fsx_forward_host": [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                          C.c_int64, C.POINTER(C.c_uint64), C.c_void_p],
+    "fsx_forward_host_digest": [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                C.c_int64, C.POINTER(C.c_uint64), C.c_void_p, C.POINTER(C.c_uint64)],
     "fsx_chunk_ready": [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.POINTER(C.c_int)],
     "fsx_wait": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_int64],
     "fsx_stream_wait_flags": [C.c_void_p, C.c_int, C.c_int64, C.c_int32, C.c_uint64, C.c_void_p],

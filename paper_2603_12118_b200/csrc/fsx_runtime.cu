@@ -288,6 +288,55 @@ class CopyPool {
   std::vector<std::thread> threads_;
 };
 
+// dg64 word terms (include/fsx.h, fsx_kernels.cu dg_word) of src[0, n), whose
+// word 0 is word `word0` of the whole span, copying the bytes to dst on the
+// way when dst is not null: one pass over the source for a staged host send
+// (copy and digest were two passes, 6.4 ms per 112 MiB span).  n must be a
+// multiple of 8 unless this piece ends the span (zero-padded last word).
+uint64_t copy_digest(uint8_t* dst, const uint8_t* src, int64_t n, uint64_t word0) {
+  constexpr uint64_t C1 = 0xbf58476d1ce4e5b9ull, C2 = 0x94d049bb133111ebull;
+  uint64_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+  const int64_t words = n / 8;
+  uint64_t c = (word0 + 1) * C1;
+  int64_t k = 0;
+  for (; k + 4 <= words; k += 4, c += 4 * C1) {
+    uint64_t w[4];
+    std::memcpy(w, src + k * 8, 32);
+    if (dst) std::memcpy(dst + k * 8, w, 32);
+    const uint64_t y0 = (w[0] ^ c) * C2, y1 = (w[1] ^ (c + C1)) * C2;
+    const uint64_t y2 = (w[2] ^ (c + 2 * C1)) * C2, y3 = (w[3] ^ (c + 3 * C1)) * C2;
+    h0 += y0 ^ (y0 >> 29);
+    h1 += y1 ^ (y1 >> 29);
+    h2 += y2 ^ (y2 >> 29);
+    h3 += y3 ^ (y3 >> 29);
+  }
+  for (; k * 8 < n; ++k, c += C1) {
+    uint64_t w = 0;
+    const int64_t take = std::min<int64_t>(8, n - k * 8);
+    std::memcpy(&w, src + k * 8, (size_t)take);
+    if (dst) std::memcpy(dst + k * 8, &w, (size_t)take);
+    const uint64_t y = (w ^ c) * C2;
+    h0 += y ^ (y >> 29);
+  }
+  return h0 + h1 + h2 + h3;
+}
+
+// copy_digest split across the copy pool (parts at 64-byte boundaries).
+uint64_t par_copy_digest(uint8_t* dst, const uint8_t* src, int64_t n, uint64_t word0) {
+  CopyPool& pool = CopyPool::get();
+  const int64_t parts = std::min<int64_t>(pool.workers() + 1, std::max<int64_t>(1, n / (int64_t{1} << 20)));
+  if (parts < 2) return copy_digest(dst, src, n, word0);
+  const int64_t per = ((n + parts - 1) / parts + 63) / 64 * 64;  // parts * per >= n
+  std::vector<uint64_t> part(parts, 0);
+  pool.run(static_cast<int>(parts), [&](int t) {
+    const int64_t b = t * per, e = std::min(n, b + per);
+    if (e > b) part[t] = copy_digest(dst ? dst + b : nullptr, src + b, e - b, word0 + b / 8);
+  });
+  uint64_t h = 0;
+  for (uint64_t v : part) h += v;
+  return h;
+}
+
 void par_memcpy(uint8_t* dst, const uint8_t* src, int64_t n) {
   CopyPool& pool = CopyPool::get();
   const int64_t parts = std::min<int64_t>(pool.workers() + 1, std::max<int64_t>(1, n / (int64_t{1} << 20)));
@@ -295,7 +344,7 @@ void par_memcpy(uint8_t* dst, const uint8_t* src, int64_t n) {
     std::memcpy(dst, src, (size_t)n);
     return;
   }
-  const int64_t per = (n / parts + 63) / 64 * 64;
+  const int64_t per = ((n + parts - 1) / parts + 63) / 64 * 64;  // parts * per >= n
   pool.run(static_cast<int>(parts), [=](int t) {
     const int64_t b = t * per, e = std::min(n, b + per);
     if (e > b) std::memcpy(dst + b, src + b, (size_t)(e - b));
@@ -657,8 +706,34 @@ int fsx_slab_read(fsx_fabric* f, int gpu, int64_t off, void* h_dst, int64_t n, v
   if (n == 0) return FSX_OK;
   FSX_CUDA(cudaSetDevice(s->device));
   cudaStream_t st = pick_stream(dev, stream);
-  FSX_CUDA(cudaMemcpyAsync(h_dst, s->base + off, n, cudaMemcpyDeviceToHost, st));
-  FSX_CUDA(cudaStreamSynchronize(st));
+  if (n < kStageMin || is_pinned_host(h_dst)) {
+    FSX_CUDA(cudaMemcpyAsync(h_dst, s->base + off, n, cudaMemcpyDeviceToHost, st));
+    FSX_CUDA(cudaStreamSynchronize(st));
+    return FSX_OK;
+  }
+  // pageable destination (a ChunkCallback's fresh std::vector, sidecar.hpp:
+  // 543-561): D2H into the pinned staging ring, three pieces in flight, each
+  // landed piece copied out by the copy threads (which also take the
+  // destination's first-touch page faults in parallel)
+  std::lock_guard<std::mutex> stage_lk(dev->stage_mu);
+  for (int k = 0; k < 3; ++k) {
+    if (!dev->stage[k]) FSX_CUDA(cudaHostAlloc(&dev->stage[k], kStagePiece, cudaHostAllocDefault));
+    if (!dev->stage_ev[k]) FSX_CUDA(cudaEventCreateWithFlags(&dev->stage_ev[k], cudaEventDisableTiming));
+    FSX_CUDA(cudaEventSynchronize(dev->stage_ev[k]));  // a host->device staging copy still reading it
+  }
+  const int64_t pieces = (n + kStagePiece - 1) / kStagePiece;
+  auto issue = [&](int64_t i) -> cudaError_t {
+    const int64_t beg = i * kStagePiece, len = std::min(kStagePiece, n - beg);
+    cudaError_t e = cudaMemcpyAsync(dev->stage[i % 3], s->base + off + beg, len, cudaMemcpyDeviceToHost, st);
+    return e != cudaSuccess ? e : cudaEventRecord(dev->stage_ev[i % 3], st);
+  };
+  for (int64_t i = 0; i < std::min<int64_t>(3, pieces); ++i) FSX_CUDA(issue(i));
+  for (int64_t i = 0; i < pieces; ++i) {
+    const int64_t beg = i * kStagePiece, len = std::min(kStagePiece, n - beg);
+    FSX_CUDA(cudaEventSynchronize(dev->stage_ev[i % 3]));
+    par_memcpy(static_cast<uint8_t*>(h_dst) + beg, dev->stage[i % 3], len);
+    if (i + 3 < pieces) FSX_CUDA(issue(i + 3));
+  }
   return FSX_OK;
 }
 
@@ -950,6 +1025,13 @@ int fsx_read_u64(fsx_fabric* f, int gpu, const uint64_t* d, uint64_t* h, void* s
 int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
                      int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                      void* stream) {
+  return fsx_forward_host_digest(f, h_src, dst_gpu, dst_off, bytes, chunk_bytes, flag_base, token, stream,
+                                 nullptr);
+}
+
+int fsx_forward_host_digest(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_off,
+                            int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
+                            void* stream, uint64_t* digest) {
   NvtxRange nvtx_range("fsx.forward_host");
   if (bytes < 0) return fail(FSX_E_VALIDATION, "negative byte count");
   if (chunk_bytes <= 0 || chunk_bytes >= bytes) chunk_bytes = std::max<int64_t>(bytes, 1);
@@ -991,6 +1073,7 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
       if (!dev->stage_ev[k]) FSX_CUDA(cudaEventCreateWithFlags(&dev->stage_ev[k], cudaEventDisableTiming));
     }
   }
+  uint64_t dg = 0;  // dg64 word terms of the source (digest != nullptr)
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int64_t beg = c * chunk_bytes, len = std::min(chunk_bytes, bytes - beg);
     if (len > 0 && staged) {
@@ -998,7 +1081,10 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
         const int64_t pl = std::min(kStagePiece, beg + len - p);
         const int k = (int)(dev->stage_next++ % 3);
         FSX_CUDA(cudaEventSynchronize(dev->stage_ev[k]));  // its previous copy has run
-        par_memcpy(dev->stage[k], static_cast<const uint8_t*>(h_src) + p, pl);
+        if (digest)
+          dg += par_copy_digest(dev->stage[k], static_cast<const uint8_t*>(h_src) + p, pl, (uint64_t)p / 8);
+        else
+          par_memcpy(dev->stage[k], static_cast<const uint8_t*>(h_src) + p, pl);
         FSX_CUDA(cudaMemcpyAsync(s->base + dst_off + p, dev->stage[k], pl, cudaMemcpyHostToDevice, st));
         FSX_CUDA(cudaEventRecord(dev->stage_ev[k], st));
       }
@@ -1014,6 +1100,9 @@ int fsx_forward_host(fsx_fabric* f, const void* h_src, int dst_gpu, int64_t dst_
     FSX_CUDA(fsx::launch_set_flags(fa, dev->notify));
     f->launches++;
   }
+  // unstaged (pinned / small) source: digested while the DMA reads it
+  if (digest && !staged) dg = par_copy_digest(nullptr, static_cast<const uint8_t*>(h_src), bytes, 0);
+  if (digest) *digest = (uint64_t)bytes * 0x9e3779b97f4a7c15ull + dg;
   f->forwards++;
   f->bytes_forwarded += bytes;
   if (token) *token = tok;

@@ -196,6 +196,39 @@ def test_forward_host_span_path(fab, oracle_mod):
         fab.slab_free(1, off)
 
 
+def test_forward_host_digest_matches_oracle(fab, oracle_mod):
+    """fsx_forward_host_digest (the drop-in's host-span send): the bytes land
+    byte-exact and the returned dg64 -- fused into the staging copy for a
+    pageable source >= 4 MiB, computed alongside the DMA otherwise (small
+    pageable, pinned) -- equals the oracle's, for unaligned lengths and
+    chunked copies."""
+    import ctypes as C
+
+    torch = _torch()
+    cases = [(1, 0, False), (4097, 0, False), (5 << 20, 0, False), ((17 << 20) + 13, 3 << 20, False),
+             ((6 << 20) + 5, 0, True), ((6 << 20) + 5, 0, False), (40 << 20, 7 << 20, False)]
+    # (6 MiB + 5 splits into 6 copy-thread parts whose 64-byte-rounded size
+    # once left the last 5 bytes uncopied)
+    for n, chunk, pinned in cases:
+        data = oracle_mod.synth_payload(n + 77, n)
+        if pinned:
+            buf = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            buf.numpy()[:] = np.frombuffer(data, np.uint8)
+            ptr = buf.data_ptr()
+        else:
+            arr = np.frombuffer(data, np.uint8).copy()
+            ptr = arr.ctypes.data
+        off = fab.slab_alloc(1, n)
+        nchunks = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
+        fb = fab.flags_alloc(1, nchunks)
+        tok, dg = C.c_uint64(0), C.c_uint64(0)
+        N.call("fsx_forward_host_digest", fab._h, ptr, 1, off, n, chunk, fb, C.byref(tok), None, C.byref(dg))
+        fab.wait(1, fb, nchunks, tok.value, timeout_us=20_000_000)
+        assert dg.value == oracle_mod.C.or_digest64(data, n), (n, chunk, pinned)
+        assert fab.slab_read(1, off, n) == data
+        fab.slab_free(1, off)
+
+
 def test_slab_allocator_replays_reference_nodearena(fab, kat):
     # NodeArena op trace produced by the reference (sidecar.hpp:106-205)
     from paper_2603_12118_b200.fabric import DeviceFabric
@@ -644,7 +677,6 @@ def test_small_lane_idle_exit_and_relaunch(fab, oracle_mod):
                 N.call("fsx_ticket_wait", fab._h, tickets[i - 4], None, None)
         for i, (m, off, t) in enumerate(zip(msgs, offs, tickets)):
             sent, landed = C.c_uint64(), C.c_uint64()
-            assert fab.slab_read(2, off, len(m)) == m
             if i % 2:  # wait + copy out + digests + free in one call (the drop-in's delivery)
                 out = C.create_string_buffer(len(m))
                 N.call("fsx_ticket_take", fab._h, t, out, len(m), C.byref(sent), C.byref(landed))
@@ -653,6 +685,7 @@ def test_small_lane_idle_exit_and_relaunch(fab, oracle_mod):
                 N.call("fsx_ticket_digests", fab._h, t, C.byref(sent), C.byref(landed))
                 N.call("fsx_ticket_free", fab._h, t)
             assert sent.value == landed.value == oracle_mod.C.or_digest64(m, len(m))
+            assert fab.slab_read(2, off, len(m)) == m  # served: the bytes are in the slab
             fab.slab_free(2, off)
         with pytest.raises(N.FsxError):
             N.call("fsx_ticket_take", fab._h, tickets[1], None, 0, None, None)  # already taken
