@@ -145,7 +145,19 @@ build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_
 build/probe_small_path: tests/cpp/probe_small_path.cpp include/fsx/fabric.hpp $(LIB) | build
 	$(CXXTEST) -o $@ tests/cpp/probe_small_path.cpp $(LINKFSX)
 
-cpptests: build/test_fabric build/bench_fabric build/probe_small_path build/bench_pass build/test_host_digest
+# Diagnostic probes (scripts/probe_*.cu|cpp; numbers in profiles/).
+build/probe_launch_floor: scripts/probe_launch_floor.cu | build
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+build/probe_pcie_pull: scripts/probe_pcie_pull.cu | build
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+build/probe_k1_floor: scripts/probe_k1_floor.cu build/fsx_kernels.o | build
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -I$(CSRC) -o $@ $< build/fsx_kernels.o
+build/probe_host_copy: scripts/probe_host_copy.cpp | build
+	$(CXX) -O2 -std=c++17 -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart -lpthread
+
+probes: build/probe_launch_floor build/probe_pcie_pull build/probe_k1_floor build/probe_host_copy
+
+cpptests: probes build/test_fabric build/bench_fabric build/probe_small_path build/bench_pass build/test_host_digest
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \

@@ -21,6 +21,10 @@ timeout 600 python scripts/sweep_forward.py --graph --cpu-ref > $O/k1_sweep_conf
 timeout 600 python scripts/sweep_forward.py --graph --flush > $O/k1_sweep_flush_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 python scripts/sweep_forward.py --graph --flush --bulk > $O/k1_sweep_flush_bulk_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 build/bench_fabric 4 > $O/bench_fabric_dropin_$TAG.jsonl 2>> $O/bench_${TAG}.err
+timeout 120 build/probe_small_path 7168 > $O/small_path_phases_$TAG.jsonl 2>> $O/bench_${TAG}.err
+[ -x build/probe_k1_floor ] && timeout 120 build/probe_k1_floor > $O/k1_floor_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 build/bench_pass 50 > $O/bench_pass_cpp_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 python scripts/bench_stream.py > $O/stream_configC_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 1800 bash scripts/profile_round.sh $TAG
+rm -f $O/sanitize_summary.txt
+timeout 3000 bash scripts/sanitize.sh
