@@ -282,7 +282,6 @@ __device__ __forceinline__ TileRef tile_of(const Batch& b, int64_t gt) {
 template <int CAP>
 __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid_constant__ FwdBatchT<CAP> b) {
   __shared__ uint64_t red[kTileThreads / 32];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL (launch_pdl)
   const TileRef tr = tile_of(b, blockIdx.x);
   const FwdArgs& a = b.t[tr.i];
   const int64_t beg = tr.beg, end = tr.end;
@@ -317,9 +316,6 @@ __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid
   } else {
     for (int64_t j = beg + threadIdx.x; j < end; j += kTileThreads) a.dst[j] = a.src[j];
   }
-  // the stream's next PDL launch may start its CTAs (they still wait for
-  // this grid's completion in griddepcontrol.wait)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (dig) {  // block-reduce the digest, one atomic per tile
     acc = warp_sum_u64(acc);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -403,7 +399,6 @@ __global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__
   extern __shared__ __align__(128) uint8_t tile_mem[];
   __shared__ __align__(8) uint64_t bars[2];
   if (threadIdx.x != 0) return;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched with PDL (launch_pdl)
   const TileRef tr = tile_of(b, blockIdx.x);
   const FwdArgs& a = b.t[tr.i];
   const int64_t beg = tr.beg, end = tr.end;
@@ -435,7 +430,6 @@ __global__ void __launch_bounds__(32) forward_tma_kernel(const __grid_constant__
   }
   tma::bulk_commit();
   for (int64_t j = vend; j < end; ++j) a.dst[j] = a.src[j];  // sub-16-byte tail
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tma::bulk_wait_all();
   // the tile's bulk stores are complete: order them (async proxy) before the
   // generic release that counts the tile
@@ -1128,28 +1122,6 @@ cudaError_t set_spin_timeout(uint64_t ns) {
 int forward_tile_bytes() { return kTileThreads * kTileVecs * 16; }
 
 // One launch with the parameter block cut to CAP transfers.
-// Programmatic dependent launch: the grid may be scheduled before the
-// previous kernel on the stream has finished (its launch and CTA setup
-// overlap that kernel's tail); the kernel itself waits with
-// griddepcontrol.wait before its first memory access, which returns once the
-// previous grid has completed and its writes are visible.  Saves ~0.15 us per
-// small K1 (profiles/launch_floor_r02c.jsonl).
-template <class Args>
-cudaError_t launch_pdl(void (*kernel)(Args), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
-                       const Args& args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args);
-}
-
 template <int CAP>
 cudaError_t launch_forward_cap(const FwdBatch& full, bool bulk, cudaStream_t s) {
   FwdBatchT<CAP> b;
@@ -1176,15 +1148,15 @@ cudaError_t launch_forward_cap(const FwdBatch& full, bool bulk, cudaStream_t s) 
                              kTmaTileBytes);
         attr_set[dev] = true;
       }
-      return launch_pdl(forward_tma_kernel<CAP>, (unsigned)tiles, 32, kTmaTileBytes, s, b);
+      forward_tma_kernel<CAP><<<(unsigned)tiles, 32, kTmaTileBytes, s>>>(b);
+      return cudaGetLastError();
     }
   }
-  return launch_pdl(forward_tile_kernel<CAP>, (unsigned)tiles, kTileThreads, 0, s, b);
+  forward_tile_kernel<CAP><<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_forward(const FwdBatch& b, bool bulk, cudaStream_t s) {
-  // (launch_pdl: K1 may be scheduled while the stream's previous kernel
-  // drains; its CTAs wait in griddepcontrol.wait before touching memory)
   if (b.n <= 1) return launch_forward_cap<1>(b, bulk, s);
   if (b.n <= 8) return launch_forward_cap<8>(b, bulk, s);
   return launch_forward_cap<kFwdMaxBatch>(b, bulk, s);
