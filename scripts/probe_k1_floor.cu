@@ -12,6 +12,21 @@
 
 #include "fsx_kernels.cuh"
 
+// the lean probe kernel of scripts/probe_launch_floor.cu (4 KiB tiles, count +
+// release), here with a distinct counter and flag per launch like the product
+__global__ void __launch_bounds__(256) lean_tiles(const uint4* __restrict__ s, uint4* __restrict__ d, int64_t nv,
+                                                  uint32_t* counter, uint64_t* flag, uint32_t need, uint64_t token) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i < nv) d[i] = __ldg(s + i);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(counter), "r"(1u) : "memory");
+  if (old + 1 != need) return;
+  *counter = 0;
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag), "l"(token) : "memory");
+}
+
 int main() {
   const int reps = 200;
   uint8_t *s = nullptr, *d = nullptr;
@@ -79,6 +94,17 @@ int main() {
       });
     };
     const double t4 = k1(4096, false), t32 = k1(32768, false), b4 = k1(4096, true), b32 = k1(32768, true);
+    const unsigned g4 = (unsigned)((n / 16 + 255) / 256);
+    const double lean_same = time_graph([&](int i) {
+      lean_tiles<<<g4, 256, 0, st>>>(reinterpret_cast<const uint4*>(s), reinterpret_cast<uint4*>(d), n / 16, c, f,
+                                     g4, 1000 + i);
+    });
+    const double lean_distinct = time_graph([&](int i) {
+      lean_tiles<<<g4, 256, 0, st>>>(reinterpret_cast<const uint4*>(s), reinterpret_cast<uint4*>(d), n / 16, c + 64 * i,
+                                     f + 64 * i, g4, 1000 + i);
+    });
+    std::printf("{\"bytes\": %lld, \"lean_4k_same_counter_us\": %.3f, \"lean_4k_distinct_counters_us\": %.3f}\n",
+                (long long)n, lean_same, lean_distinct);
     const double mc = time_graph([&](int) { cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st); });
     std::printf("{\"bytes\": %lld, \"k1_tile_4k_us\": %.3f, \"k1_tile_32k_us\": %.3f, \"k1_bulk_4k_us\": %.3f, "
                 "\"k1_bulk_32k_us\": %.3f, \"memcpy_us\": %.3f}\n",
