@@ -426,7 +426,7 @@ def run_single(args):
         end(cur, e, record)
 
     def step_graph(record=False):
-        # the tee pass (scan + tee, FULL) as one CUDA graph launch
+        # the tee pass as one CUDA graph launch: the tee || the next pass's scan
         s = counter[0]
         counter[0] += 1
         assert batch.alloc()
@@ -482,7 +482,9 @@ def run_single(args):
         if payload < (128 << 20) and not args.profile:
             eager_ms = timed(step_tee, 10)[0]
             assert batch.alloc()
-            batch.capture(stream, kind="tee")
+            # one graph per pass: the tee of this pass || the scan of the next
+            batch.capture(stream, kind="tee_pipelined")
+            batch.scan(stream, slot=0)
             batch.release()
             for _ in range(3):
                 step_graph()
@@ -598,7 +600,8 @@ def run_single(args):
         "config": {"workload": CONFIGS[CONFIG]["workload"],
                    "placement": "intra-device forward (producer == consumer GPU) + merge",
                    "schedule": ("scan (side stream, one pass ahead) + fsx_forward_merge" +
-                                (" as one CUDA graph per pass" if step is step_graph else "")),
+                                (" as one CUDA graph per pass (the tee || the next pass's scan)"
+                                 if step is step_graph else "")),
                    "requests_per_step": len(reqs), "payload_bytes_per_step": payload,
                    "chunk_bytes": (CHUNK_ROWS or 0) * rules.row_bytes or "single shot",
                    "prompt_rows_per_step": lay.total_rows,

@@ -341,18 +341,41 @@ class DataPlaneBatch:
         returns the same offsets pass after pass, and nothing in stream order
         waits on the flags."""
         assert self.slab_off is not None, "alloc() first"
-        if kind == "tee" and not hasattr(self, "item_src_direct"):
+        if kind in ("tee", "tee_pipelined") and not hasattr(self, "item_src_direct"):
             self._direct_src()  # a device upload: not inside the capture
-        g = torch.cuda.CUDAGraph()
-        l0 = self.fab.stats()["kernel_launches"]
-        with torch.cuda.graph(g, stream=stream):
-            if kind == "tee":
-                self.tee(stream, mode=N.MERGE_FULL, l2_keep=l2_keep)
-            else:
-                self.forward(stream, host_notify=False, l2_keep=l2_keep, bulk=bulk)
-                self.merge(stream)
-        self.graph_kernels = self.fab.stats()["kernel_launches"] - l0  # fsx kernels per replay
-        self._graph = g
+        if kind == "tee_pipelined":
+            # two graphs, one per scan slot k: the tee of this pass reads the
+            # positions of slot k (scanned by the previous replay) while a
+            # forked branch scans slot 1 - k for the next pass -- the eager
+            # schedule's one-pass-ahead scan, inside the graph.  The caller
+            # scans slot 0 once before the first replay.
+            side = torch.cuda.Stream(device=stream.device)
+            graphs = []
+            l0 = self.fab.stats()["kernel_launches"]
+            for k in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    side.wait_stream(stream)
+                    self.scan(side, slot=1 - k)
+                    self.tee(stream, mode=N.MERGE_COPY_ONLY, slot=k, l2_keep=l2_keep)
+                    stream.wait_stream(side)
+                graphs.append(g)
+            self.graph_kernels = (self.fab.stats()["kernel_launches"] - l0) // 2
+            self._graphs = graphs
+            self._graph = graphs[0]
+            self._replays = 0
+        else:
+            g = torch.cuda.CUDAGraph()
+            l0 = self.fab.stats()["kernel_launches"]
+            with torch.cuda.graph(g, stream=stream):
+                if kind == "tee":
+                    self.tee(stream, mode=N.MERGE_FULL, l2_keep=l2_keep)
+                else:
+                    self.forward(stream, host_notify=False, l2_keep=l2_keep, bulk=bulk)
+                    self.merge(stream)
+            self.graph_kernels = self.fab.stats()["kernel_launches"] - l0  # fsx kernels per replay
+            self._graph = g
+            self._graphs = None
         self._graph_key = (self.slab_off.tobytes(), kind, bulk, l2_keep)
 
     def run_graph(self, stream) -> None:
@@ -363,7 +386,11 @@ class DataPlaneBatch:
         if key != self._graph_key:
             self.capture(stream, *self._graph_key[1:])
         with torch.cuda.stream(stream):
-            self._graph.replay()
+            if self._graphs:  # tee_pipelined: alternate the scan slots
+                self._graphs[self._replays % 2].replay()
+                self._replays += 1
+            else:
+                self._graph.replay()
 
     def scan(self, stream=None, slot: int = 0) -> None:
         """Phase 1 of K3 only: needs just the token ids, so it can run while

@@ -524,12 +524,14 @@ def test_pass_graph_replay_bit_exact(fab, oracle_mod):
     fab.slab_free(1, hold)
 
 
+@pytest.mark.parametrize("kind", ["tee", "tee_pipelined"])
 @pytest.mark.parametrize("config,count", [("A", 24), ("D", 8)])
-def test_tee_pass_graph_bit_exact(fab, oracle_mod, config, count):
+def test_tee_pass_graph_bit_exact(fab, oracle_mod, config, count, kind):
     """The fused forward + merge (scan, then fsx_forward_merge) captured once
     as a CUDA graph and replayed several times: merged rows and slab segments
     == the oracle, and the graph-baked counter / flag ranges are pinned (eager
-    forwards in between never reuse them)."""
+    forwards in between never reuse them).  tee_pipelined: two graphs, each
+    the tee of one scan slot || the scan of the other (the bench's form)."""
     from paper_2603_12118_b200.dataplane import DataPlaneBatch
 
     torch = _torch()
@@ -538,8 +540,10 @@ def test_tee_pass_graph_bit_exact(fab, oracle_mod, config, count):
     b.synth_inputs()
     s = torch.cuda.Stream()
     assert b.alloc()
-    b.capture(s, kind="tee")
+    b.capture(s, kind=kind)
     assert b.graph_kernels >= 2  # scan + tee
+    if kind == "tee_pipelined":
+        b.scan(s, slot=0)
     baked = b.flag_base.copy()
     other = DataPlaneBatch(fab, T.config_requests("A", 4), T.RULES["A"], 0, 1)
     other.synth_inputs()
@@ -710,6 +714,41 @@ def test_small_lane_idle_exit_and_relaunch(fab, oracle_mod):
         deadline = time.perf_counter() + float(rng.uniform(150e-6, 260e-6))
         while time.perf_counter() < deadline:
             pass
+    fab.slab_free(2, off)
+
+
+def test_small_lane_ring_full_declines(fab, oracle_mod):
+    """4,096 descriptors per lane: with that many messages outstanding (not
+    yet freed) the next put declines (ticket -1, the caller takes the
+    synchronous path) instead of overwriting a live descriptor; freeing one
+    makes room again, and every message is still served byte-exact."""
+    import ctypes as C
+
+    n_ring = 4096
+    off = fab.slab_alloc(2, 64 * (n_ring + 8))
+    tickets = []
+    for i in range(n_ring + 3):
+        m = (i % 251).to_bytes(1, "little") * 48
+        t = C.c_int64(-2)
+        N.call("fsx_put_small", fab._h, 2, off + 64 * i, m, len(m), C.byref(t))
+        if i < n_ring:
+            assert t.value >= 0, i
+            tickets.append(t.value)
+        else:
+            assert t.value == -1, i
+    N.call("fsx_ticket_free", fab._h, tickets[0])
+    t = C.c_int64(-2)
+    N.call("fsx_put_small", fab._h, 2, off + 64 * n_ring, b"z" * 48, 48, C.byref(t))
+    assert t.value >= 0
+    tickets = tickets[1:] + [t.value]
+    for t in tickets:
+        sent, landed = C.c_uint64(), C.c_uint64()
+        N.call("fsx_ticket_take", fab._h, t, None, 0, C.byref(sent), C.byref(landed))
+        assert sent.value == landed.value
+    got = fab.slab_read(2, off + 64, 64 * (n_ring - 1))
+    for i in range(1, n_ring):
+        assert got[64 * (i - 1):64 * (i - 1) + 48] == (i % 251).to_bytes(1, "little") * 48
+    assert fab.slab_read(2, off + 64 * n_ring, 48) == b"z" * 48
     fab.slab_free(2, off)
 
 
