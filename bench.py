@@ -79,6 +79,9 @@ def parse():
     p.add_argument("--requests", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--colocated", action="store_true",
+                   help="also time the colocated schedule (K1 || early-start merge on one GPU, "
+                        "round 1's headline): two kernels spinning on each other's progress")
     p.add_argument("--no-verify", dest="verify", action="store_false",
                    help="N>1: skip the consumers' bit-exactness check of the merged embeddings "
                         "against a local pass (on by default)")
@@ -520,19 +523,24 @@ def run_single(args):
             for _ in range(3):
                 step_place()
             place_ms, _, _ = timed(step_place, iso)
-            # the colocated pass, as a long-lived server would run it: five
-            # back-to-back 10-pass measurements in this one process
-            for _ in range(3):
-                step_colocated()
-            colo = [round(timed(step_colocated, 10)[0], 4) for _ in range(5)]
+            colo = None
+            if args.colocated:
+                # the colocated pass, as a long-lived server would run it: five
+                # back-to-back 10-pass measurements in this one process
+                for _ in range(3):
+                    step_colocated()
+                colo = [round(timed(step_colocated, 10)[0], 4) for _ in range(5)]
             schedules = {
                 "tee": {"what": "scan one pass ahead || fsx_forward_merge (the timed pass)",
                         "ms_per_step": round(ms_step, 4)},
                 "serial": {"what": "K1 (bulk-copy tiles) then the merge, stream order",
                            "ms_per_step": round(serial_ms, 4)},
-                "colocated": {"what": "K1 || early-start merge on a high-priority stream",
-                              "runs_ms": colo, "first_ms": colo[0],
-                              "steady_median_ms": statistics.median(colo[1:])},
+                "colocated": ({"what": "K1 || early-start merge on a high-priority stream",
+                               "runs_ms": colo, "first_ms": colo[0],
+                               "steady_median_ms": statistics.median(colo[1:])} if colo else
+                              {"what": "K1 || early-start merge on a high-priority stream (round 1's "
+                                       "headline; opt-in: --colocated)",
+                               "last_measured": "0.290 ms steady median, profiles/bench_r02i_full.json"}),
                 "direct_placement": {"what": "fsx_forward_place: rows straight into the prompt, "
                                              "no slab segment (not the reference's semantics)",
                                      "ms_per_step": round(place_ms, 4),

@@ -97,8 +97,8 @@ def test_bench_single_gpu_line(gpu):
     the timed kernel (the tee) with an event-timed rate, the other schedules
     and kernels measured beside it, and config.workload identical to the
     reference arm's (the driver compares them)."""
-    d = _run(["--steps", "5", "--warmup", "3", "--config", "A", "--no-cpu-baseline", "--no-e2e"],
-             launcher="self")
+    d = _run(["--steps", "5", "--warmup", "3", "--config", "A", "--no-cpu-baseline", "--no-e2e",
+              "--colocated"], launcher="self")
     import importlib.util
 
     spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
