@@ -53,7 +53,7 @@ CONFIGS = {
     "D": {"requests": 32, "chunk_rows": 1024,
           "workload": "D: servegen-like mixed image/video/audio trace (seed 42), 3584-d bf16"},
 }
-METRIC = "forwarded GB/s per producer->consumer pair vs 900 GB/s NVLink; merged req/s"
+METRIC = "forwarded GB/s per producer\u2192consumer pair vs 900 GB/s NVLink; merged req/s"  # BASELINE.json
 KERNELS = {
     "tee": "fsx::kern::merge_tee_kernel (fsx_forward_merge: forward + merge in one kernel)",
     "forward": "fsx::kern::forward_tma_kernel (K1, bulk-copy tiles, all items of the step in one launch)",

@@ -89,3 +89,13 @@ def test_bench_clock_summary_and_sample():
     b.CONFIG, b.REQUESTS = "A", 64
     sample = b.cpu_sample(T)  # the whole 64-request batch is < 100 MiB
     assert len(sample) == 64
+
+
+def test_bench_metric_is_baselines():
+    """The driver compares the bench line's metric with BASELINE.json's: the
+    same string (unicode arrow included), for both arms."""
+    import json
+
+    b = _bench()
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        assert b.METRIC == json.load(fh)["metric"]
