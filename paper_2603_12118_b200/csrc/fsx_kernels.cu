@@ -331,6 +331,57 @@ __global__ void __launch_bounds__(kTileThreads) forward_tile_kernel(const __grid
   count_tile(a, tr.c, b.peer_gpu_count != 0);
 }
 
+// K1, small-batch form: when the whole batch is <= 2 MiB a transfer is
+// latency-bound, so tiles are 4 KiB -- one 16-byte vector per thread of a
+// 256-thread CTA, one load round trip -- and the tile lookup is 32-bit (no
+// 64-bit division on the path to the first load).  Same completion protocol
+// and fused digest as the tile kernel; the runtime picks it (FwdBatch.small).
+constexpr int kSmallTile = kTileThreads * 16;
+template <int CAP>
+__global__ void __launch_bounds__(kTileThreads) forward_small_kernel(const __grid_constant__ FwdBatchT<CAP> b) {
+  __shared__ uint64_t red[kTileThreads / 32];
+  const uint32_t gt = blockIdx.x;
+  int i = 0;
+  while (gt >= (uint32_t)b.unit_off[i + 1]) ++i;
+  const FwdArgs& a = b.t[i];
+  const uint32_t u = gt - (uint32_t)b.unit_off[i];
+  const uint32_t cu = (uint32_t)a.chunk_units;
+  const uint32_t c = u / cu;
+  const uint32_t cbeg = c * (uint32_t)a.chunk_bytes;
+  const uint32_t cend = min(cbeg + (uint32_t)a.chunk_bytes, (uint32_t)a.bytes);
+  const uint32_t beg = cbeg + (u - c * cu) * (uint32_t)a.slice;  // slice <= kSmallTile
+  const uint32_t end = min(beg + (uint32_t)a.slice, cend);
+  uint64_t acc = 0;
+  if (a.vec) {
+    const uint32_t vend = end & ~15u;  // beg is 16-byte aligned
+    const uint32_t at = beg + 16 * threadIdx.x;
+    if (at < vend) {
+      const uint4 r = __ldg(reinterpret_cast<const uint4*>(a.src + at));
+      *reinterpret_cast<uint4*>(a.dst + at) = r;
+      if (a.digest) acc = dg_vec(r, (uint64_t)(at >> 3));
+    }
+    if (threadIdx.x == 0 && vend < end) {
+      for (uint32_t j = vend; j < end; ++j) a.dst[j] = a.src[j];
+      if (a.digest) acc += dg_bytes(a.src, vend, end);
+    }
+  } else {
+    for (uint32_t j = beg + threadIdx.x; j < end; j += kTileThreads) a.dst[j] = a.src[j];
+  }
+  if (a.digest) {
+    acc = warp_sum_u64(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (a.digest) {
+    uint64_t t = 0;
+    for (int w = 0; w < kTileThreads / 32; ++w) t += red[w];
+    if (u == 0) t += (uint64_t)a.bytes * 0x9e3779b97f4a7c15ull;
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.digest), (unsigned long long)t);
+  }
+  count_tile(a, c, b.peer_gpu_count != 0);
+}
+
 // ---------------------------------------------------------------------------
 // Bulk-copy (TMA engine) helpers
 
@@ -1128,7 +1179,7 @@ cudaError_t launch_forward_cap(const FwdBatch& full, bool bulk, cudaStream_t s) 
   b.n = full.n;
   b.l2_keep_dst = full.l2_keep_dst;
   b.peer_gpu_count = full.peer_gpu_count;
-  b._pad = 0;
+  b.small = full.small;
   for (int k = 0; k <= full.n; ++k) b.unit_off[k] = full.unit_off[k];
   for (int k = 0; k < full.n; ++k) b.t[k] = full.t[k];
   const int64_t tiles = b.unit_off[b.n];
@@ -1152,7 +1203,10 @@ cudaError_t launch_forward_cap(const FwdBatch& full, bool bulk, cudaStream_t s) 
       return cudaGetLastError();
     }
   }
-  forward_tile_kernel<CAP><<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
+  if (b.small)
+    forward_small_kernel<CAP><<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
+  else
+    forward_tile_kernel<CAP><<<(unsigned)tiles, kTileThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 
@@ -1248,6 +1302,9 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(forward_tile_kernel<1>),
       reinterpret_cast<const void*>(forward_tile_kernel<8>),
       reinterpret_cast<const void*>(forward_tile_kernel<kFwdMaxBatch>),
+      reinterpret_cast<const void*>(forward_small_kernel<1>),
+      reinterpret_cast<const void*>(forward_small_kernel<8>),
+      reinterpret_cast<const void*>(forward_small_kernel<kFwdMaxBatch>),
       reinterpret_cast<const void*>(merge_tee_kernel),
       reinterpret_cast<const void*>(set_flags_kernel),
       reinterpret_cast<const void*>(chan_push_kernel),

@@ -42,7 +42,7 @@ struct FwdBatchT {
   int32_t n;
   int32_t l2_keep_dst;     // slab stores with L2 evict_last (consumer merges next)
   int32_t peer_gpu_count;  // peer chunks: count tiles at gpu scope, publish once at sys scope
-  int32_t _pad;
+  int32_t small;           // 4 KiB tiles (batch <= 2 MiB): the latency form of K1
   int64_t unit_off[CAP + 1];
   FwdArgs t[CAP];
 };

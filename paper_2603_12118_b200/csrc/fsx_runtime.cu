@@ -900,6 +900,7 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
     b.n = cnt;
     b.l2_keep_dst = (options & FSX_FWD_L2_KEEP) ? 1 : 0;
     b.peer_gpu_count = (options & FSX_FWD_PEER_GPU_COUNT) ? 1 : 0;
+    b.small = unit == 4096 ? 1 : 0;
     for (int32_t k = 0; k < cnt; ++k) {
       fsx_transfer& x = t[first + k];
       fsx::FwdArgs& a = b.t[k];

@@ -90,6 +90,7 @@ int main() {
         a.token = 1000 + i;
         a.digest = nullptr;
         b.unit_off[1] = a.total_units;
+        b.small = unit == 4096 ? 1 : 0;  // as fsx_forward_batch picks it (batch <= 2 MiB)
         fsx::launch_forward(b, bulk, st);
       });
     };
