@@ -142,6 +142,9 @@ build/bench_pass: tests/cpp/bench_pass.cpp include/fsx/dataplane.hpp build/fsx_o
 build/bench_fabric: tests/cpp/bench_fabric.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
 	$(CXXTEST) -Ioracle -o $@ tests/cpp/bench_fabric.cpp build/fsx_oracle_test.o $(LINKFSX)
 
+build/probe_send_phases: tests/cpp/probe_send_phases.cpp include/fsx/fabric.hpp build/fsx_oracle_test.o $(LIB) | build
+	$(CXXTEST) -Ioracle -o $@ tests/cpp/probe_send_phases.cpp build/fsx_oracle_test.o $(LINKFSX)
+
 build/probe_small_path: tests/cpp/probe_small_path.cpp include/fsx/fabric.hpp $(LIB) | build
 	$(CXXTEST) -o $@ tests/cpp/probe_small_path.cpp $(LINKFSX)
 
@@ -157,7 +160,7 @@ build/probe_host_copy: scripts/probe_host_copy.cpp | build
 
 probes: build/probe_launch_floor build/probe_pcie_pull build/probe_k1_floor build/probe_host_copy
 
-cpptests: probes build/test_fabric build/bench_fabric build/probe_small_path build/bench_pass build/test_host_digest
+cpptests: probes build/test_fabric build/bench_fabric build/probe_small_path build/probe_send_phases build/bench_pass build/test_host_digest
 	@if [ -f $(FISSIM_REF_TESTS)/test_sidecar.cpp ]; then \
 	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \

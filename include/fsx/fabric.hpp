@@ -50,6 +50,12 @@
 
 #include "fsx.h"
 
+// Phase hooks for host-overhead probes (tests/cpp/probe_send_phases.cpp
+// defines it before including this header); compiled out otherwise.
+#ifndef FSX_PHASE
+#define FSX_PHASE(i) ((void)0)
+#endif
+
 namespace fsx {
 
 enum class Transport { LocalBuffer, NetworkStream };
@@ -340,6 +346,7 @@ class Fabric {
   // HBM).  The span is borrowed for the duration of the call only.
   void send(const std::string& request_id, const Ref& ref, int src_gpu, int dst_gpu,
             std::span<const uint8_t> payload, int64_t seq, bool final_chunk) {
+    FSX_PHASE(14);
     const int64_t n = static_cast<int64_t>(payload.size());
     if (!Traits::streaming(ref) && n != Traits::total_bytes(ref))
       Traits::raise(status::kProtocol, "payload length " + std::to_string(n) +
@@ -360,7 +367,9 @@ class Fabric {
     ps.env.dst_gpu = dst_gpu;
     ps.deadline = Traits::now(kernel_) + config_.send_timeout_ms;
     ps.src = payload.data();
+    FSX_PHASE(0);
     ps.src_is_device = n > 0 && device_of_pointer(payload.data()) >= 0;
+    FSX_PHASE(1);
 
     if (t == Transport::NetworkStream) {
       // Cross-node: envelope and bytes travel together (sidecar.hpp:337-346),
@@ -561,7 +570,9 @@ class Fabric {
                   int64_t* ticket) {
     const int dst = ps.env.dst_gpu;
     ensure_slab(dst);
+    FSX_PHASE(2);
     check(fsx_slab_alloc(h_, dst, std::max<int64_t>(ps.env.chunk_bytes, 1), off));
+    FSX_PHASE(3);
     if (*off < 0) return false;
     const int64_t n = ps.env.chunk_bytes;
     // The envelope's checksum is the producer's: dg64 set here for local
@@ -574,6 +585,7 @@ class Fabric {
       // destination's small-message lane; the lane kernel digests the bytes
       // it moves (sent) and the landed segment, read at delivery
       check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
+      FSX_PHASE(4);
       if (*ticket >= 0) {
         *n_chunks = 0;
         *token = 0;
@@ -648,9 +660,11 @@ class Fabric {
     added_latency_ms_ += lat;
     if (any_early_ && hand_over_early(ps.env, off, ticket, landing)) return true;
     // the Pending is dropped once placed (send / place_backlog): move its envelope
+    FSX_PHASE(5);
     auto env = std::make_shared<Envelope>(std::move(ps.env));
     Traits::schedule(kernel_, Traits::now(kernel_) + lat, "sidecar.deliver",
-                     [this, env, off, ticket, landing] { deliver(*env, off, ticket, false, landing); });
+                     [this, env, off, ticket, landing] { deliver(std::move(*env), off, ticket, false, landing); });
+    FSX_PHASE(6);
     return true;
   }
 
@@ -700,10 +714,12 @@ class Fabric {
   }
 
   // sidecar.hpp:498-525
-  void deliver(const Envelope& env, int64_t off, int64_t ticket = -1, bool network = false,
+  void deliver(Envelope env, int64_t off, int64_t ticket = -1, bool network = false,
                Landing landing = {}) {
+    FSX_PHASE(8);
     const std::string key = key_of(env.ref_id, env.dst_gpu);
     RefState& st = refs_[key];
+    FSX_PHASE(9);
     if (st.request_id.empty()) st.request_id = env.request_id;
     if (st.failed) {
       drop_ticket(ticket);
@@ -712,12 +728,12 @@ class Fabric {
       place_backlog(env.dst_gpu);
       return;
     }
-    st.parked.emplace(env.seq, Parked{env, off, ticket, network, landing});
+    const int64_t seq = env.seq;
+    st.parked.emplace(seq, Parked{std::move(env), off, ticket, network, landing});
     if (st.has_interest) {
       drain(st);
       return;
     }
-    const int64_t seq = env.seq;
     Traits::schedule(kernel_, Traits::now(kernel_) + config_.orphan_timeout_ms, "sidecar.orphan",
                      [this, key, seq] { reclaim_orphan(key, seq); });
   }
@@ -740,7 +756,7 @@ class Fabric {
   void drain(RefState& st) {
     for (auto it = st.parked.find(st.next_seq); it != st.parked.end();
          it = st.parked.find(st.next_seq)) {
-      Envelope env = it->second.env;
+      Envelope env = std::move(it->second.env);  // erased next
       const int64_t off = it->second.off;
       const int64_t ticket = it->second.ticket;
       const bool network = it->second.network;
@@ -791,7 +807,9 @@ class Fabric {
         // slab; the consumer gets the staged bytes
         uint64_t sent = 0, landed = 0;
         bytes.resize(static_cast<size_t>(env.chunk_bytes));
+        FSX_PHASE(10);
         check(fsx_ticket_take(h_, ticket, bytes.data(), env.chunk_bytes, &sent, &landed));
+        FSX_PHASE(11);
         if (local) env.checksum = sent;
         dev_ok = landed == sent;
       } else {
@@ -815,7 +833,9 @@ class Fabric {
       ++transfers_;
       bytes_forwarded_ += env.chunk_bytes;
       ++st.next_seq;
+      FSX_PHASE(12);
       if (st.on_chunk) st.on_chunk(env, std::move(bytes));
+      FSX_PHASE(13);
     }
   }
 

@@ -63,20 +63,30 @@ class BlockList {
  public:
   void reset(int64_t capacity) {
     blocks_.clear();
+    free_.clear();
     blocks_[0] = Block{capacity, true};
+    free_[0] = capacity;
     used_segments_ = 0;
     used_bytes_ = 0;
     peak_ = 0;
   }
 
+  // First fit in offset order, as NodeArena::allocate (sidecar.hpp:149-170);
+  // the scan visits only free blocks (free_ mirrors the free entries of
+  // blocks_), so its cost does not grow with the live segments.
   int64_t alloc(int64_t len) {
     const int64_t need = (std::max<int64_t>(len, 1) + kAlign - 1) & ~(kAlign - 1);
-    for (auto it = blocks_.begin(); it != blocks_.end(); ++it) {
-      if (!it->second.free || it->second.len < need) continue;
-      const int64_t off = it->first;
-      const int64_t rest = it->second.len - need;
+    for (auto fit = free_.begin(); fit != free_.end(); ++fit) {
+      if (fit->second < need) continue;
+      const int64_t off = fit->first;
+      const int64_t rest = fit->second - need;
+      auto it = blocks_.find(off);
       it->second = Block{need, false};
-      if (rest > 0) blocks_.emplace_hint(std::next(it), off + need, Block{rest, true});
+      free_.erase(fit);
+      if (rest > 0) {
+        blocks_.emplace_hint(std::next(it), off + need, Block{rest, true});
+        free_.emplace(off + need, rest);
+      }
       ++used_segments_;
       used_bytes_ += need;
       peak_ = std::max(peak_, used_bytes_);
@@ -85,6 +95,7 @@ class BlockList {
     return -1;
   }
 
+  // Free with coalescing of both neighbours (sidecar.hpp:172-186).
   bool release(int64_t off) {
     auto it = blocks_.find(off);
     if (it == blocks_.end() || it->second.free) return false;
@@ -94,6 +105,7 @@ class BlockList {
     auto nx = std::next(it);
     if (nx != blocks_.end() && nx->second.free) {
       it->second.len += nx->second.len;
+      free_.erase(nx->first);
       blocks_.erase(nx);
     }
     if (it != blocks_.begin()) {
@@ -101,8 +113,11 @@ class BlockList {
       if (pv->second.free) {
         pv->second.len += it->second.len;
         blocks_.erase(it);
+        free_[pv->first] = pv->second.len;
+        return true;
       }
     }
+    free_[it->first] = it->second.len;
     return true;
   }
 
@@ -115,7 +130,8 @@ class BlockList {
     int64_t len;
     bool free;
   };
-  std::map<int64_t, Block> blocks_;
+  std::map<int64_t, Block> blocks_;  // every block by offset
+  std::map<int64_t, int64_t> free_;  // the free ones: offset -> len
   int64_t used_segments_ = 0, used_bytes_ = 0, peak_ = 0;
 };
 
@@ -1201,8 +1217,13 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
   }
   const uint64_t seq = l->tail;
   f->tickets[id] = fsx_fabric::Ticket{slot, s->device, seq};
-  std::memcpy(f->mail + slot, h_src, (size_t)n);
   fsx::LaneDesc* d = &l->ring[seq % fsx::kLaneSlots];
+  // the descriptor lines were last written by the device (a PCIe write drops
+  // them from the host caches): fetch this one and the next for writing while
+  // the bytes are copied
+  __builtin_prefetch(d, 1);
+  __builtin_prefetch(&l->ring[(seq + 1) % fsx::kLaneSlots], 1);
+  std::memcpy(f->mail + slot, h_src, (size_t)n);
   d->dst = s->base + dst_off;
   d->src = f->mail + slot;
   d->n = n;
