@@ -224,6 +224,13 @@ int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token
 #define FSX_SMALL_MAX 65536
 int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
                   int64_t* ticket);
+/* The same for a DEVICE source (a thinker's hidden-state row on its GPU, this
+ * device's memory or a peer's): no host staging, the lane kernel reads the
+ * row in place, so the source must stay unchanged until the ticket is served
+ * (fsx_ticket_wait).  fsx_ticket_wait returns no host bytes for it
+ * (*h_bytes = NULL); fsx_ticket_take copies the landed segment out. */
+int fsx_put_small_device(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* d_src, int64_t n,
+                         int64_t* ticket);
 int fsx_flush_small(fsx_fabric* f);
 int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest);
 int fsx_ticket_digests(fsx_fabric* f, int64_t ticket, uint64_t* sent, uint64_t* landed);

@@ -580,11 +580,15 @@ class Fabric {
     // transport tag says (sidecar.hpp:351-364 verifies the frame as sent).
     const bool local = Traits::is_local(ps.env) && !ps.network;
     *ticket = -1;
-    if (!ps.src_is_device && n > 0 && n <= FSX_SMALL_MAX) {
-      // small host span (per-token hidden states, codes): published on the
-      // destination's small-message lane; the lane kernel digests the bytes
-      // it moves (sent) and the landed segment, read at delivery
-      check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
+    if (n > 0 && n <= FSX_SMALL_MAX) {
+      // small span (per-token hidden states, codes): published on the
+      // destination's small-message lane -- a host span staged, a device span
+      // read in place; the lane kernel digests the bytes it moves (sent) and
+      // the landed segment, read at delivery
+      if (ps.src_is_device)
+        check(fsx_put_small_device(h_, dst, *off, ps.src, n, ticket));
+      else
+        check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
       FSX_PHASE(4);
       if (*ticket >= 0) {
         *n_chunks = 0;
@@ -650,8 +654,15 @@ class Fabric {
     // stages it), and a small message sits in the pinned mailbox: send()
     // returns at once and the delivery waits for the landing instead.
     Landing landing{flag_base, ticket < 0 ? n_chunks : 0, token};
-    if (ticket < 0 && source_still_read(ps)) {
-      wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
+    // a staged small host span is copied out already; a small device span is
+    // read by the lane kernel after this call
+    const bool still_read = ticket >= 0 ? ps.src_is_device && !config_.async_borrowed_sources
+                                        : source_still_read(ps);
+    if (still_read) {
+      if (ticket >= 0)
+        check(fsx_ticket_wait(h_, ticket, nullptr, nullptr));  // the lane has read the device span
+      else
+        wait_landed(ps.env.dst_gpu, flag_base, n_chunks, token);
       landing.n_chunks = 0;
     }
     if (digest_slot_) check(fsx_read_u64(h_, ps.env.src_gpu, digest_slot_, &ps.env.checksum, nullptr));

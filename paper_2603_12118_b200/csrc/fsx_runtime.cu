@@ -415,7 +415,8 @@ struct fsx_fabric {
   uint8_t* mail = nullptr;
   BlockList mail_blocks;
   struct Ticket {
-    int64_t slot = -1;   // mailbox offset of the staged bytes, -1 = free ticket
+    bool used = false;
+    int64_t slot = -1;   // mailbox offset of the staged bytes; -1: device source (no staging)
     int device = -1;
     uint64_t seq = 0;    // lane descriptor sequence number
   };
@@ -1161,7 +1162,7 @@ int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t*
   uint64_t seq = 0;
   {
     std::lock_guard<std::mutex> lk(f->mu);
-    if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || f->tickets[ticket].slot < 0)
+    if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || !f->tickets[ticket].used)
       return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
     const fsx_fabric::Ticket& t = f->tickets[ticket];
     d = &f->lanes.at(t.device).ring[t.seq % fsx::kLaneSlots];
@@ -1188,8 +1189,13 @@ int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t*
 
 }  // namespace
 
-int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
-                  int64_t* ticket) {
+namespace {
+
+// Publish one message on the destination device's lane: host bytes are
+// staged in a mailbox slot; a device source (this GPU's memory or a peer's,
+// peer access is enabled at fsx_open) is read by the lane kernel in place.
+int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src, int64_t n, bool device,
+                   int64_t* ticket) {
   *ticket = -1;
   if (n <= 0 || n > FSX_SMALL_MAX) return FSX_OK;
   std::lock_guard<std::mutex> lk(f->mu);
@@ -1197,7 +1203,7 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
   if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
   if (dst_off < 0 || dst_off + n > s->capacity)
     return fail(FSX_E_VALIDATION, "small put overruns the destination slab");
-  if (!f->mail) {
+  if (!device && !f->mail) {
     FSX_CUDA(cudaHostAlloc(&f->mail, kMailBytes, cudaHostAllocMapped | cudaHostAllocPortable));
     f->mail_blocks.reset(kMailBytes);
   }
@@ -1205,8 +1211,11 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
   int rc = lane_of(f, s->device, &l);
   if (rc) return rc;
   if (l->outstanding >= fsx::kLaneSlots) return FSX_OK;  // ring full: caller takes the synchronous path
-  const int64_t slot = f->mail_blocks.alloc((n + 63) / 64 * 64);
-  if (slot < 0) return FSX_OK;  // mailbox full: caller takes the synchronous path
+  int64_t slot = -1;
+  if (!device) {
+    slot = f->mail_blocks.alloc((n + 63) / 64 * 64);
+    if (slot < 0) return FSX_OK;  // mailbox full: caller takes the synchronous path
+  }
   int64_t id;
   if (f->free_tickets.empty()) {
     f->tickets.emplace_back();
@@ -1216,16 +1225,16 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
     f->free_tickets.pop_back();
   }
   const uint64_t seq = l->tail;
-  f->tickets[id] = fsx_fabric::Ticket{slot, s->device, seq};
+  f->tickets[id] = fsx_fabric::Ticket{true, slot, s->device, seq};
   fsx::LaneDesc* d = &l->ring[seq % fsx::kLaneSlots];
   // the descriptor lines were last written by the device (a PCIe write drops
   // them from the host caches): fetch this one and the next for writing while
   // the bytes are copied
   __builtin_prefetch(d, 1);
   __builtin_prefetch(&l->ring[(seq + 1) % fsx::kLaneSlots], 1);
-  std::memcpy(f->mail + slot, h_src, (size_t)n);
+  if (!device) std::memcpy(f->mail + slot, src, (size_t)n);
   d->dst = s->base + dst_off;
-  d->src = f->mail + slot;
+  d->src = device ? static_cast<const uint8_t*>(src) : f->mail + slot;
   d->n = n;
   vstore(&d->done, 0);
   // descriptor and bytes before the tail (x86 keeps stores in order; this
@@ -1248,6 +1257,18 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
   return FSX_OK;
 }
 
+}  // namespace
+
+int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
+                  int64_t* ticket) {
+  return put_small_impl(f, dst_gpu, dst_off, h_src, n, false, ticket);
+}
+
+int fsx_put_small_device(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* d_src, int64_t n,
+                         int64_t* ticket) {
+  return put_small_impl(f, dst_gpu, dst_off, d_src, n, true, ticket);
+}
+
 int fsx_flush_small(fsx_fabric* f) {
   (void)f;  // messages are served as they are published (small-message lane)
   return FSX_OK;
@@ -1258,7 +1279,7 @@ int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_
   int64_t slot = -1;
   int rc = lane_wait(f, ticket, &d, &slot);
   if (rc) return rc;
-  if (h_bytes) *h_bytes = f->mail + slot;
+  if (h_bytes) *h_bytes = slot >= 0 ? f->mail + slot : nullptr;  // device source: no host copy
   if (digest) *digest = vload(&d->landed);
   return FSX_OK;
 }
@@ -1281,12 +1302,19 @@ int fsx_ticket_take(fsx_fabric* f, int64_t ticket, void* h_dst, int64_t n, uint6
   if (rc) return rc;
   const int64_t len = (int64_t)vload(reinterpret_cast<const uint64_t*>(&d->n));
   if (n < 0 || n > len) return fail(FSX_E_VALIDATION, "ticket take longer than the message");
-  if (h_dst && n > 0) std::memcpy(h_dst, f->mail + slot, (size_t)n);
+  if (h_dst && n > 0) {
+    if (slot >= 0) {
+      std::memcpy(h_dst, f->mail + slot, (size_t)n);
+    } else {  // device source: the landed segment
+      const void* seg = reinterpret_cast<const void*>(vload(reinterpret_cast<const uint64_t*>(&d->dst)));
+      FSX_CUDA(cudaMemcpy(h_dst, seg, (size_t)n, cudaMemcpyDeviceToHost));
+    }
+  }
   if (sent) *sent = vload(&d->sent);
   if (landed) *landed = vload(&d->landed);
   std::lock_guard<std::mutex> lk(f->mu);
   fsx_fabric::Ticket& t = f->tickets[ticket];
-  f->mail_blocks.release(t.slot);
+  if (t.slot >= 0) f->mail_blocks.release(t.slot);
   --f->lanes.at(t.device).outstanding;
   t = fsx_fabric::Ticket{};
   f->free_tickets.push_back(ticket);
@@ -1299,7 +1327,7 @@ int fsx_ticket_free(fsx_fabric* f, int64_t ticket) {
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(f->mu);
   fsx_fabric::Ticket& t = f->tickets[ticket];
-  f->mail_blocks.release(t.slot);
+  if (t.slot >= 0) f->mail_blocks.release(t.slot);
   --f->lanes.at(t.device).outstanding;
   t = fsx_fabric::Ticket{};
   f->free_tickets.push_back(ticket);

@@ -92,23 +92,44 @@ int main(int argc, char** argv) {
   // thinker sends one hidden-state row (host span, streaming ref, seq = step)
   // and the talker's ChunkCallback receives it (executor_sim.hpp:370-381,
   // 556-562).  Reported as microseconds per step and messages per second.
-  for (int row : {7168, 2048}) {
+  // device mode: the thinker's rows already on its GPU (the real deployment),
+  // sent from device memory to raw (zero-copy) talker consumers, the producer
+  // keeping each step's rows until delivery (async_borrowed_sources)
+  for (int mode = 0; mode < 3; ++mode) {
+    const int row = mode == 1 ? 2048 : 7168;
+    const bool device = mode == 2;
     const int batch = 32, steps = 200;
     EventLoop k;
     SidecarConfig cfg;
+    cfg.async_borrowed_sources = device;
     SidecarFabric f(k, topo, cfg);
+    void* drow = nullptr;
+    if (device && cudaMalloc(&drow, (size_t)row * batch) != cudaSuccess) return 2;
     std::vector<uint8_t> rowbuf(row);
     or_synth_payload_into(7, rowbuf.data(), row);
+    for (int r = 0; r < batch && device; ++r)
+      cudaMemcpy(static_cast<uint8_t*>(drow) + (size_t)r * row, rowbuf.data(), row, cudaMemcpyHostToDevice);
     int64_t got = 0;
-    for (int r = 0; r < batch; ++r)
-      f.register_interest(1, "req-" + std::to_string(r) + "/r0001",
-                          [&](const ForwardEnvelope&, std::vector<uint8_t> b) { got += (int64_t)b.size(); });
+    for (int r = 0; r < batch; ++r) {
+      if (device)
+        f.register_interest_raw(1, "req-" + std::to_string(r) + "/r0001",
+                                [&](const ForwardEnvelope& env, int64_t off) {
+                                  got += env.chunk_bytes;
+                                  f.ack_raw(1, off);
+                                });
+      else
+        f.register_interest(1, "req-" + std::to_string(r) + "/r0001",
+                            [&](const ForwardEnvelope&, std::vector<uint8_t> b) { got += (int64_t)b.size(); });
+    }
     double send_s = 0, deliver_s = 0;  // host time split: the sends, then the deliveries
     auto step = [&](int s) {
       const auto a = std::chrono::steady_clock::now();
       for (int r = 0; r < batch; ++r)
         f.send("req-" + std::to_string(r), DataRef{"req-" + std::to_string(r) + "/r0001", 0, true}, 0, 1,
-               std::span<const uint8_t>(rowbuf.data(), row), s, false);
+               std::span<const uint8_t>(device ? static_cast<const uint8_t*>(drow) + (size_t)r * row
+                                               : rowbuf.data(),
+                                        row),
+               s, false);
       const auto b = std::chrono::steady_clock::now();
       k.run_until_idle();
       send_s += std::chrono::duration<double>(b - a).count();
@@ -120,12 +141,14 @@ int main(int argc, char** argv) {
     const auto t0 = std::chrono::steady_clock::now();
     for (int s = 10; s < 10 + steps; ++s) step(s);
     const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    std::printf("{\"mode\": \"stream_host_span_chunk_callback\", \"rows_per_step\": %d, \"row_bytes\": %d, "
+    std::printf("{\"mode\": \"%s\", \"rows_per_step\": %d, \"row_bytes\": %d, "
                 "\"us_per_step\": %.1f, \"send_us_per_step\": %.1f, \"deliver_us_per_step\": %.1f, "
                 "\"msgs_per_s\": %.0f, \"bytes_ok\": %s}\n",
-                batch, row, sec / steps * 1e6, send_s / steps * 1e6, deliver_s / steps * 1e6,
+                device ? "stream_device_rows_raw_interest" : "stream_host_span_chunk_callback", batch, row,
+                sec / steps * 1e6, send_s / steps * 1e6, deliver_s / steps * 1e6,
                 batch * steps / sec,
                 got == (int64_t)batch * steps * row ? "true" : "false");
+    if (drow) cudaFree(drow);
   }
   return 0;
 }

@@ -118,7 +118,7 @@ TEST_CASE("host spans land byte-exact in device slabs on both transports") {
   CHECK(s.transfers == 16);
 }
 
-TEST_CASE("device payloads take the K1 path and land byte-exact") {
+TEST_CASE("device payloads land byte-exact (small ones on the lane, large ones by K1)") {
   EventLoop k;
   SidecarConfig cfg;
   cfg.arena_bytes = 256 << 20;
@@ -149,9 +149,10 @@ TEST_CASE("local envelopes carry the dg64 digest of the payload") {
   }
   EventLoop k;
   SidecarFabric f(k, two_nodes());
-  for (bool device : {false, true}) {
-    const size_t n = 777777;
-    const std::string id = std::string("req-d/r") + (device ? "1" : "0");
+  for (int c = 0; c < 4; ++c) {
+    const bool device = c % 2 == 1;
+    const size_t n = c < 2 ? 777777 : 5001;  // K1 / host staging, then the small-message lane
+    const std::string id = std::string("req-d/r") + std::to_string(c);
     auto payload = synth(seed_of(id), n);
     DeviceBuffer d(n);
     REQUIRE(cudaMemcpy(d.p, payload.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
@@ -529,4 +530,61 @@ TEST_CASE("host-span sends return before landing; the borrowed span may die at o
   });
   k.run_until_idle();
   CHECK(f.stats().segments_in_use == 0);
+}
+
+TEST_CASE("streamed device rows ride the small-message lane, in seq order, borrowed or not") {
+  // config C with the thinker's hidden states on its GPU: per decode step one
+  // 7 KiB row per request (executor_sim.hpp:556-562) sent from device memory.
+  // Borrowed (default): send waits until the lane has read the row, so the
+  // producer may overwrite it at once.  async_borrowed_sources: send returns
+  // at once and the producer keeps the row until delivery.
+  for (bool async_src : {false, true}) {
+    EventLoop k;
+    SidecarConfig cfg;
+    cfg.async_borrowed_sources = async_src;
+    SidecarFabric f(k, two_nodes(), cfg);
+    const int reqs = 6, steps = 5;
+    const size_t row = 7168;
+    DeviceBuffer d(row * reqs * (async_src ? steps : 1));
+    std::vector<std::vector<std::vector<uint8_t>>> want(reqs);
+    std::vector<Got> got(reqs);
+    std::vector<std::vector<int64_t>> raw_seq(reqs);
+    for (int r = 0; r < reqs; ++r) {
+      const std::string id = "req-c" + std::to_string(r) + "/r1";
+      if (r % 2 == 0) {
+        collect(f, 1, id, got[r]);
+      } else {  // zero-copy consumer: reads the slab in place, acks
+        f.register_interest_raw(1, id, [&, r](const ForwardEnvelope& env, int64_t off) {
+          std::vector<uint8_t> b(env.chunk_bytes);
+          REQUIRE(cudaMemcpy(b.data(), f.slab_ptr(1, off), b.size(), cudaMemcpyDeviceToHost) == cudaSuccess);
+          got[r].chunks.push_back(std::move(b));
+          raw_seq[r].push_back(env.seq);
+          f.ack_raw(1, off);
+        });
+      }
+    }
+    for (int s = 0; s < steps; ++s) {
+      k.post("step", [&, s] {
+        for (int r = 0; r < reqs; ++r) {
+          const std::string id = "req-c" + std::to_string(r) + "/r1";
+          auto bytes = synth(seed_of(id) ^ (uint64_t)(s + 1), row);
+          want[r].push_back(bytes);
+          uint8_t* slot = static_cast<uint8_t*>(d.p) + row * (async_src ? (size_t)(s * reqs + r) : (size_t)r);
+          REQUIRE(cudaMemcpy(slot, bytes.data(), row, cudaMemcpyHostToDevice) == cudaSuccess);
+          DataRef ref{id, 0, true};
+          f.send("req-c" + std::to_string(r), ref, 0, 1, std::span<const uint8_t>(slot, row), s, s == steps - 1);
+        }
+      });
+      if (!async_src) k.run_until_idle();  // borrowed rows are reused by the next step
+    }
+    k.run_until_idle();
+    for (int r = 0; r < reqs; ++r) {
+      REQUIRE(got[r].chunks.size() == (size_t)steps);
+      for (int s = 0; s < steps; ++s) CHECK(got[r].chunks[s] == want[r][s]);
+      if (r % 2 == 0) CHECK(got[r].seqs == std::vector<int64_t>({0, 1, 2, 3, 4}));
+      else CHECK(raw_seq[r] == std::vector<int64_t>({0, 1, 2, 3, 4}));
+    }
+    CHECK(f.stats().segments_in_use == 0);
+    CHECK(f.stats().integrity_errors == 0);
+  }
 }

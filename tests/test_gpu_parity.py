@@ -717,6 +717,39 @@ def test_small_lane_idle_exit_and_relaunch(fab, oracle_mod):
     fab.slab_free(2, off)
 
 
+def test_small_lane_device_source(fab, oracle_mod):
+    """fsx_put_small_device: a row already on the GPU is moved by the lane
+    kernel straight from device memory (no host staging): slab bytes, sent and
+    landed digests equal the oracle's; no host bytes from fsx_ticket_wait;
+    fsx_ticket_take copies the landed segment out."""
+    import ctypes as C
+
+    torch = _torch()
+    sizes = [4, 17, 2048, 7168, 4099, 65536]
+    msgs = [oracle_mod.synth_payload(7000 + i, n) for i, n in enumerate(sizes)]
+    dev = [torch.frombuffer(bytearray(m), dtype=torch.uint8).cuda() for m in msgs]
+    torch.cuda.synchronize()
+    offs, tickets = [], []
+    for m, d in zip(msgs, dev):
+        off = fab.slab_alloc(2, len(m))
+        t = C.c_int64(-2)
+        N.call("fsx_put_small_device", fab._h, 2, off, d.data_ptr(), len(m), C.byref(t))
+        assert t.value >= 0
+        offs.append(off)
+        tickets.append(t.value)
+    for i, (m, off, t) in enumerate(zip(msgs, offs, tickets)):
+        p, dg = C.c_void_p(1), C.c_uint64()
+        N.call("fsx_ticket_wait", fab._h, t, C.byref(p), C.byref(dg))
+        assert not p.value  # device source: nothing staged on the host
+        sent, landed = C.c_uint64(), C.c_uint64()
+        out = C.create_string_buffer(len(m))
+        N.call("fsx_ticket_take", fab._h, t, out, len(m), C.byref(sent), C.byref(landed))
+        assert out.raw == m
+        assert sent.value == landed.value == dg.value == oracle_mod.C.or_digest64(m, len(m))
+        assert fab.slab_read(2, off, len(m)) == m
+        fab.slab_free(2, off)
+
+
 def test_small_lane_ring_full_declines(fab, oracle_mod):
     """4,096 descriptors per lane: with that many messages outstanding (not
     yet freed) the next put declines (ticket -1, the caller takes the
