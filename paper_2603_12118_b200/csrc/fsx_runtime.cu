@@ -410,6 +410,7 @@ struct fsx_fabric {
     uint64_t tail = 0;         // descriptors published
     uint64_t epoch = 0;        // epoch of the last launched service kernel (0: none yet)
     int64_t outstanding = 0;   // published, ticket not yet freed
+    std::vector<int64_t> slot_ticket;  // ring slot -> ticket whose descriptor it holds (-1: none)
   };
   std::map<int, Lane> lanes;   // by device ordinal
   uint8_t* mail = nullptr;
@@ -419,6 +420,12 @@ struct fsx_fabric {
     int64_t slot = -1;   // mailbox offset of the staged bytes; -1: device source (no staging)
     int device = -1;
     uint64_t seq = 0;    // lane descriptor sequence number
+    int64_t n = 0;       // message bytes
+    uint8_t* dst = nullptr;  // its slab segment (device)
+    // a ticket held across a full turn of the ring (an orphaned or parked
+    // message) has its served descriptor copied here before the slot is reused
+    bool harvested = false;
+    uint64_t sent = 0, landed = 0;
   };
   std::vector<Ticket> tickets;
   std::vector<int64_t> free_tickets;
@@ -1147,17 +1154,29 @@ int lane_of(fsx_fabric* f, int device, fsx_fabric::Lane** out) {
   l.ctl = static_cast<fsx::LaneCtl*>(mem);
   l.ring = reinterpret_cast<fsx::LaneDesc*>(static_cast<uint8_t*>(mem) + sizeof(fsx::LaneCtl));
   FSX_CUDA(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
-  *out = &f->lanes.emplace(device, l).first->second;
+  l.slot_ticket.assign(fsx::kLaneSlots, -1);
+  *out = &f->lanes.emplace(device, std::move(l)).first->second;
   return FSX_OK;
 }
 
 inline uint64_t vload(const uint64_t* p) { return *reinterpret_cast<const volatile uint64_t*>(p); }
 inline void vstore(uint64_t* p, uint64_t v) { *reinterpret_cast<volatile uint64_t*>(p) = v; }
 
-// The ticket's descriptor, once its message has been served (caller does not
-// hold f->mu).  Spins on the done mark (host memory the kernel writes over
-// PCIe); FSX_E_TIMEOUT after FSX_SPIN_TIMEOUT_S (default 30 s).
-int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t* slot) {
+// A served message: its mailbox slot (-1: device source), bytes, slab
+// segment and both device digests.
+struct Served {
+  int64_t slot = -1, n = 0;
+  uint8_t* dst = nullptr;
+  uint64_t sent = 0, landed = 0;
+};
+
+// Wait until the ticket's message has been served (caller does not hold
+// f->mu).  Spins on the descriptor's done mark (host memory the kernel
+// writes over PCIe); FSX_E_TIMEOUT after FSX_SPIN_TIMEOUT_S (default 30 s).
+// The digests come from the descriptor, or from the ticket if a publisher
+// harvested them before reusing the slot (checked again after the read, so a
+// slot reused between the done mark and the read is never trusted).
+int lane_wait(fsx_fabric* f, int64_t ticket, Served* out) {
   const fsx::LaneDesc* d = nullptr;
   uint64_t seq = 0;
   {
@@ -1165,9 +1184,10 @@ int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t*
     if (ticket < 0 || ticket >= (int64_t)f->tickets.size() || !f->tickets[ticket].used)
       return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
     const fsx_fabric::Ticket& t = f->tickets[ticket];
+    *out = Served{t.slot, t.n, t.dst, t.sent, t.landed};
+    if (t.harvested) return FSX_OK;
     d = &f->lanes.at(t.device).ring[t.seq % fsx::kLaneSlots];
     seq = t.seq;
-    *slot = t.slot;
   }
   if (vload(&d->done) != seq + 1) {
     const char* e = std::getenv("FSX_SPIN_TIMEOUT_S");
@@ -1176,6 +1196,15 @@ int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t*
     uint32_t n = 0;
     while (vload(&d->done) != seq + 1) {
       if ((++n & 4095u) == 0) {
+        {
+          std::lock_guard<std::mutex> lk(f->mu);
+          const fsx_fabric::Ticket& t = f->tickets[ticket];
+          if (t.harvested) {
+            out->sent = t.sent;
+            out->landed = t.landed;
+            return FSX_OK;
+          }
+        }
         if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > secs)
           return fail(FSX_E_TIMEOUT, "small-message lane: message not served within the watchdog time");
         std::this_thread::yield();
@@ -1183,8 +1212,27 @@ int lane_wait(fsx_fabric* f, int64_t ticket, const fsx::LaneDesc** out, int64_t*
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
-  *out = d;
+  out->sent = vload(&d->sent);
+  out->landed = vload(&d->landed);
+  std::lock_guard<std::mutex> lk(f->mu);
+  const fsx_fabric::Ticket& t = f->tickets[ticket];
+  if (t.harvested) {  // the slot was reused after the done mark was read
+    out->sent = t.sent;
+    out->landed = t.landed;
+  }
   return FSX_OK;
+}
+
+// Release a waited ticket's mailbox slot and ring-slot claim (holds f->mu).
+void ticket_release(fsx_fabric* f, int64_t ticket) {
+  fsx_fabric::Ticket& t = f->tickets[ticket];
+  if (t.slot >= 0) f->mail_blocks.release(t.slot);
+  fsx_fabric::Lane& l = f->lanes.at(t.device);
+  --l.outstanding;
+  int64_t& claim = l.slot_ticket[t.seq % fsx::kLaneSlots];
+  if (claim == ticket) claim = -1;
+  t = fsx_fabric::Ticket{};
+  f->free_tickets.push_back(ticket);
 }
 
 }  // namespace
@@ -1210,7 +1258,6 @@ int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src,
   fsx_fabric::Lane* l = nullptr;
   int rc = lane_of(f, s->device, &l);
   if (rc) return rc;
-  if (l->outstanding >= fsx::kLaneSlots) return FSX_OK;  // ring full: caller takes the synchronous path
   int64_t slot = -1;
   if (!device) {
     slot = f->mail_blocks.alloc((n + 63) / 64 * 64);
@@ -1225,8 +1272,29 @@ int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src,
     f->free_tickets.pop_back();
   }
   const uint64_t seq = l->tail;
-  f->tickets[id] = fsx_fabric::Ticket{true, slot, s->device, seq};
   fsx::LaneDesc* d = &l->ring[seq % fsx::kLaneSlots];
+  int64_t& claim = l->slot_ticket[seq % fsx::kLaneSlots];
+  if (claim >= 0) {
+    // the ticket published one turn of the ring ago is still held (parked /
+    // orphaned message): its message was served long since (the lane is
+    // FIFO); keep its digests with the ticket before the slot is rewritten
+    fsx_fabric::Ticket& old = f->tickets[claim];
+    if (old.used && !old.harvested) {
+      const auto t0 = std::chrono::steady_clock::now();
+      while (vload(&d->done) != old.seq + 1) {
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 30.0)
+          return fail(FSX_E_TIMEOUT, "small-message lane: a ring slot was never served");
+        std::this_thread::yield();
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      old.sent = vload(&d->sent);
+      old.landed = vload(&d->landed);
+      old.harvested = true;
+    }
+  }
+  fsx_fabric::Ticket& tk = f->tickets[id];
+  tk = fsx_fabric::Ticket{true, slot, s->device, seq, n, s->base + dst_off};
+  claim = id;
   // the descriptor lines were last written by the device (a PCIe write drops
   // them from the host caches): fetch this one and the next for writing while
   // the bytes are copied
@@ -1275,62 +1343,49 @@ int fsx_flush_small(fsx_fabric* f) {
 }
 
 int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest) {
-  const fsx::LaneDesc* d = nullptr;
-  int64_t slot = -1;
-  int rc = lane_wait(f, ticket, &d, &slot);
+  Served sv;
+  int rc = lane_wait(f, ticket, &sv);
   if (rc) return rc;
-  if (h_bytes) *h_bytes = slot >= 0 ? f->mail + slot : nullptr;  // device source: no host copy
-  if (digest) *digest = vload(&d->landed);
+  if (h_bytes) *h_bytes = sv.slot >= 0 ? f->mail + sv.slot : nullptr;  // device source: no host copy
+  if (digest) *digest = sv.landed;
   return FSX_OK;
 }
 
 int fsx_ticket_digests(fsx_fabric* f, int64_t ticket, uint64_t* sent, uint64_t* landed) {
-  const fsx::LaneDesc* d = nullptr;
-  int64_t slot = -1;
-  int rc = lane_wait(f, ticket, &d, &slot);
+  Served sv;
+  int rc = lane_wait(f, ticket, &sv);
   if (rc) return rc;
-  if (sent) *sent = vload(&d->sent);
-  if (landed) *landed = vload(&d->landed);
+  if (sent) *sent = sv.sent;
+  if (landed) *landed = sv.landed;
   return FSX_OK;
 }
 
 int fsx_ticket_take(fsx_fabric* f, int64_t ticket, void* h_dst, int64_t n, uint64_t* sent,
                     uint64_t* landed) {
-  const fsx::LaneDesc* d = nullptr;
-  int64_t slot = -1;
-  int rc = lane_wait(f, ticket, &d, &slot);
+  Served sv;
+  int rc = lane_wait(f, ticket, &sv);
   if (rc) return rc;
-  const int64_t len = (int64_t)vload(reinterpret_cast<const uint64_t*>(&d->n));
-  if (n < 0 || n > len) return fail(FSX_E_VALIDATION, "ticket take longer than the message");
+  if (n < 0 || n > sv.n) return fail(FSX_E_VALIDATION, "ticket take longer than the message");
   if (h_dst && n > 0) {
-    if (slot >= 0) {
-      std::memcpy(h_dst, f->mail + slot, (size_t)n);
-    } else {  // device source: the landed segment
-      const void* seg = reinterpret_cast<const void*>(vload(reinterpret_cast<const uint64_t*>(&d->dst)));
-      FSX_CUDA(cudaMemcpy(h_dst, seg, (size_t)n, cudaMemcpyDeviceToHost));
-    }
+    if (sv.slot >= 0)
+      std::memcpy(h_dst, f->mail + sv.slot, (size_t)n);
+    else  // device source: the landed segment
+      FSX_CUDA(cudaMemcpy(h_dst, sv.dst, (size_t)n, cudaMemcpyDeviceToHost));
   }
-  if (sent) *sent = vload(&d->sent);
-  if (landed) *landed = vload(&d->landed);
+  if (sent) *sent = sv.sent;
+  if (landed) *landed = sv.landed;
   std::lock_guard<std::mutex> lk(f->mu);
-  fsx_fabric::Ticket& t = f->tickets[ticket];
-  if (t.slot >= 0) f->mail_blocks.release(t.slot);
-  --f->lanes.at(t.device).outstanding;
-  t = fsx_fabric::Ticket{};
-  f->free_tickets.push_back(ticket);
+  ticket_release(f, ticket);
   return FSX_OK;
 }
 
 int fsx_ticket_free(fsx_fabric* f, int64_t ticket) {
   // the slot and the slab segment may only be reused once the message is served
-  int rc = fsx_ticket_wait(f, ticket, nullptr, nullptr);
+  Served sv;
+  int rc = lane_wait(f, ticket, &sv);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(f->mu);
-  fsx_fabric::Ticket& t = f->tickets[ticket];
-  if (t.slot >= 0) f->mail_blocks.release(t.slot);
-  --f->lanes.at(t.device).outstanding;
-  t = fsx_fabric::Ticket{};
-  f->free_tickets.push_back(ticket);
+  ticket_release(f, ticket);
   return FSX_OK;
 }
 

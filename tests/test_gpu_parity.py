@@ -750,39 +750,55 @@ def test_small_lane_device_source(fab, oracle_mod):
         fab.slab_free(2, off)
 
 
-def test_small_lane_ring_full_declines(fab, oracle_mod):
-    """4,096 descriptors per lane: with that many messages outstanding (not
-    yet freed) the next put declines (ticket -1, the caller takes the
-    synchronous path) instead of overwriting a live descriptor; freeing one
-    makes room again, and every message is still served byte-exact."""
+def test_small_lane_ticket_held_across_ring_turns(fab, oracle_mod):
+    """The lane's descriptor ring has 4,096 slots; a ticket held while more
+    than a full turn of messages is published after it (an orphaned or parked
+    message) keeps its digests -- the publisher that reuses its slot copies
+    them into the ticket first -- and everything published meanwhile is served
+    byte-exact.  Also 4,100 tickets outstanding at once."""
     import ctypes as C
 
-    n_ring = 4096
-    off = fab.slab_alloc(2, 64 * (n_ring + 8))
+    held_msg = oracle_mod.synth_payload(4242, 7000)
+    held_off = fab.slab_alloc(2, len(held_msg))
+    held = C.c_int64(-2)
+    N.call("fsx_put_small", fab._h, 2, held_off, held_msg, len(held_msg), C.byref(held))
+    assert held.value >= 0
+    off = fab.slab_alloc(2, 64 * 4200)
+    for turn in range(2):  # two full turns, freed as they go
+        pending = []
+        for i in range(4100):
+            m = ((i + turn) % 251).to_bytes(1, "little") * 48
+            t = C.c_int64(-2)
+            N.call("fsx_put_small", fab._h, 2, off + 64 * i, m, len(m), C.byref(t))
+            assert t.value >= 0
+            pending.append(t.value)
+            if len(pending) > 64:
+                N.call("fsx_ticket_free", fab._h, pending.pop(0))
+        for t in pending:
+            N.call("fsx_ticket_free", fab._h, t)
+    got = fab.slab_read(2, off, 64 * 4100)
+    for i in range(4100):
+        assert got[64 * i:64 * i + 48] == ((i + 1) % 251).to_bytes(1, "little") * 48
+    sent, landed = C.c_uint64(), C.c_uint64()
+    out = C.create_string_buffer(len(held_msg))
+    N.call("fsx_ticket_take", fab._h, held.value, out, len(held_msg), C.byref(sent), C.byref(landed))
+    assert out.raw == held_msg
+    assert sent.value == landed.value == oracle_mod.C.or_digest64(held_msg, len(held_msg))
+    assert fab.slab_read(2, held_off, len(held_msg)) == held_msg
+    # 4,100 tickets outstanding at once (more than the ring): all served
     tickets = []
-    for i in range(n_ring + 3):
+    for i in range(4100):
         m = (i % 251).to_bytes(1, "little") * 48
         t = C.c_int64(-2)
         N.call("fsx_put_small", fab._h, 2, off + 64 * i, m, len(m), C.byref(t))
-        if i < n_ring:
-            assert t.value >= 0, i
-            tickets.append(t.value)
-        else:
-            assert t.value == -1, i
-    N.call("fsx_ticket_free", fab._h, tickets[0])
-    t = C.c_int64(-2)
-    N.call("fsx_put_small", fab._h, 2, off + 64 * n_ring, b"z" * 48, 48, C.byref(t))
-    assert t.value >= 0
-    tickets = tickets[1:] + [t.value]
-    for t in tickets:
-        sent, landed = C.c_uint64(), C.c_uint64()
+        assert t.value >= 0
+        tickets.append(t.value)
+    for i, t in enumerate(tickets):
         N.call("fsx_ticket_take", fab._h, t, None, 0, C.byref(sent), C.byref(landed))
-        assert sent.value == landed.value
-    got = fab.slab_read(2, off + 64, 64 * (n_ring - 1))
-    for i in range(1, n_ring):
-        assert got[64 * (i - 1):64 * (i - 1) + 48] == (i % 251).to_bytes(1, "little") * 48
-    assert fab.slab_read(2, off + 64 * n_ring, 48) == b"z" * 48
+        m = (i % 251).to_bytes(1, "little") * 48
+        assert sent.value == landed.value == oracle_mod.C.or_digest64(m, len(m))
     fab.slab_free(2, off)
+    fab.slab_free(2, held_off)
 
 
 @pytest.mark.parametrize("config,count,chunk_rows", [("B", 2, 1024), ("D", 16, 512), ("A", 12, 64)])
