@@ -588,3 +588,39 @@ TEST_CASE("streamed device rows ride the small-message lane, in seq order, borro
     CHECK(f.stats().integrity_errors == 0);
   }
 }
+
+TEST_CASE("a parked small message survives more than a ring turn of later messages") {
+  // the small-message lane's descriptor ring has 4,096 slots: a message parked
+  // without interest while 5,000 others are sent (all before any delivery, so
+  // more than a ring turn of tickets is outstanding) is still delivered
+  // intact, its digest verified, when its consumer registers later (before
+  // the orphan timeout)
+  EventLoop k;
+  SidecarFabric f(k, two_nodes());
+  const size_t n = 3000;
+  auto parked = synth(seed_of("req-o/r0"), n);
+  k.post("send-parked", [&] { f.send_payload("req-o", ref_of("req-o/r0", n), 0, 1, parked); });
+  Got flow;
+  collect(f, 1, "req-f/r0", flow);
+  const int msgs = 5000;
+  for (int s = 0; s < msgs; s += 100) {
+    k.post("flow", [&, s] {
+      for (int i = s; i < s + 100; ++i) {
+        std::vector<uint8_t> b(64, static_cast<uint8_t>(i));
+        DataRef ref{"req-f/r0", 0, true};
+        f.send("req-f", ref, 0, 1, b, i, i == msgs - 1);
+      }
+    });
+  }
+  Got late;
+  k.schedule(1000.0, "late-interest", [&] { collect(f, 1, "req-o/r0", late); });
+  k.run_until_idle();
+  REQUIRE(flow.chunks.size() == (size_t)msgs);
+  CHECK(flow.chunks[4321] == std::vector<uint8_t>(64, static_cast<uint8_t>(4321)));
+  REQUIRE(late.chunks.size() == 1);
+  CHECK(late.chunks[0] == parked);
+  CHECK(!late.error);
+  CHECK(f.stats().integrity_errors == 0);
+  CHECK(f.stats().orphan_reclaims == 0);
+  CHECK(f.stats().segments_in_use == 0);
+}
