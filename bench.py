@@ -247,12 +247,14 @@ def cpu_baseline(min_seconds=12.0, max_passes=80):
             "merged_req_per_s": round(n * len(reqs) / total_s, 3)}
 
 
-def cpu_sample(T):
+def cpu_sample(T, scale: int = 1):
     """Bounded CPU sample of the workload: the first requests of the batch
     whose embeddings add up to >= 100 MiB, and at least one request per host
-    thread while the batch has them (config B: the whole 4-video batch)."""
+    thread while the batch has them (config B: the whole 4-video batch).
+    scale: the fsx arm at N > 1 moves N/2 pairs' (or encoders') batches per
+    step, so the reference arm draws from that many requests."""
     rules = T.RULES[CONFIG]
-    full = T.config_requests(CONFIG, REQUESTS)
+    full = T.config_requests(CONFIG, REQUESTS * max(1, scale))
     want = min(len(full), os.cpu_count() or 1)
     out, acc = [], 0
     for q in full:
@@ -273,7 +275,9 @@ def run_reference(args, rank):
 
     rules = T.RULES[CONFIG]
     threads = os.cpu_count() or 1
-    reqs = cpu_sample(T)  # bounded sample per step (one request for config B)
+    # the same per-step workload as the fsx arm at this N: N/2 pairs (A/B) or
+    # N/2 encoders (D) each with a batch of REQUESTS requests
+    reqs = cpu_sample(T, max(1, args.gpus // 2))
     for _ in range(args.warmup):
         cpu_reference_pass(reqs, rules, threads)
     secs, nbytes, kind = 0.0, 0, "reference"
