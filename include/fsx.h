@@ -231,6 +231,12 @@ int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src
  * (*h_bytes = NULL); fsx_ticket_take copies the landed segment out. */
 int fsx_put_small_device(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* d_src, int64_t n,
                          int64_t* ticket);
+/* Allocate the slab segment (NodeArena first fit, as fsx_slab_alloc) and
+ * publish the message on the lane in one call: *dst_off = -1 when the slab is
+ * full (the reference parks the send, sidecar.hpp:329-334); *ticket = -1 when
+ * the lane declines (the segment stays allocated for the caller's own copy). */
+int fsx_put_small_alloc(fsx_fabric* f, int dst_gpu, const void* src, int64_t n, int src_is_device,
+                        int64_t* dst_off, int64_t* ticket);
 int fsx_flush_small(fsx_fabric* f);
 int fsx_ticket_wait(fsx_fabric* f, int64_t ticket, const void** h_bytes, uint64_t* digest);
 int fsx_ticket_digests(fsx_fabric* f, int64_t ticket, uint64_t* sent, uint64_t* landed);

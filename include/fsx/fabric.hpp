@@ -42,6 +42,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #if defined(__linux__)
@@ -570,33 +571,33 @@ class Fabric {
                   int64_t* ticket) {
     const int dst = ps.env.dst_gpu;
     ensure_slab(dst);
-    FSX_PHASE(2);
-    check(fsx_slab_alloc(h_, dst, std::max<int64_t>(ps.env.chunk_bytes, 1), off));
-    FSX_PHASE(3);
-    if (*off < 0) return false;
     const int64_t n = ps.env.chunk_bytes;
-    // The envelope's checksum is the producer's: dg64 set here for local
-    // sends; a network arrival keeps the sender's checksum64 whatever its
-    // transport tag says (sidecar.hpp:351-364 verifies the frame as sent).
-    const bool local = Traits::is_local(ps.env) && !ps.network;
     *ticket = -1;
+    FSX_PHASE(2);
     if (n > 0 && n <= FSX_SMALL_MAX) {
-      // small span (per-token hidden states, codes): published on the
-      // destination's small-message lane -- a host span staged, a device span
-      // read in place; the lane kernel digests the bytes it moves (sent) and
-      // the landed segment, read at delivery
-      if (ps.src_is_device)
-        check(fsx_put_small_device(h_, dst, *off, ps.src, n, ticket));
-      else
-        check(fsx_put_small(h_, dst, *off, ps.src, n, ticket));
+      // small span (per-token hidden states, codes): segment allocated and
+      // the message published on the destination's small-message lane in one
+      // call -- a host span staged, a device span read in place; the lane
+      // kernel digests the bytes it moves (sent) and the landed segment,
+      // read at delivery
+      check(fsx_put_small_alloc(h_, dst, ps.src, n, ps.src_is_device ? 1 : 0, off, ticket));
       FSX_PHASE(4);
+      if (*off < 0) return false;
       if (*ticket >= 0) {
         *n_chunks = 0;
         *token = 0;
         digest_slot_ = nullptr;
         return true;
       }
+    } else {
+      check(fsx_slab_alloc(h_, dst, std::max<int64_t>(n, 1), off));
+      FSX_PHASE(3);
+      if (*off < 0) return false;
     }
+    // The envelope's checksum is the producer's: dg64 set here for local
+    // sends; a network arrival keeps the sender's checksum64 whatever its
+    // transport tag says (sidecar.hpp:351-364 verifies the frame as sent).
+    const bool local = Traits::is_local(ps.env) && !ps.network;
     int64_t cb = config_.device_chunk_bytes;
     // host spans cross PCIe: every copy costs a fixed copy-engine gap, so
     // they go in chunks of at least 32 MiB (send() waits for all of it anyway)
@@ -917,7 +918,12 @@ class Fabric {
   bool any_early_ = false;           // an early-start interest was registered (placement looks it up)
   std::vector<int> slabs_;
   std::map<std::string, RefState> refs_;
-  std::set<std::pair<int, int64_t>> raw_held_;  // (slab gpu, offset) handed to raw callbacks
+  struct SegHash {
+    size_t operator()(const std::pair<int, int64_t>& k) const {
+      return std::hash<int64_t>()(k.second * 64 + k.first);
+    }
+  };
+  std::unordered_set<std::pair<int, int64_t>, SegHash> raw_held_;  // (slab gpu, offset) handed to raw callbacks
   std::map<int, std::deque<Pending>> backlog_;
   FailureHandler failure_handler_;
   int64_t transfers_ = 0, bytes_forwarded_ = 0, integrity_errors_ = 0, orphan_reclaims_ = 0;

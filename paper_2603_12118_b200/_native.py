@@ -146,6 +146,8 @@ _SIGS = {
     "fsx_ticket_digests": [C.c_void_p, C.c_int64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "fsx_ticket_free": [C.c_void_p, C.c_int64],
     "fsx_put_small_device": [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)],
+    "fsx_put_small_alloc": [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.POINTER(C.c_int64),
+                            C.POINTER(C.c_int64)],
     "fsx_ticket_take": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_uint64),
                         C.POINTER(C.c_uint64)],
     "fsx_flush_small": [C.c_void_p],

@@ -1162,6 +1162,18 @@ int lane_of(fsx_fabric* f, int device, fsx_fabric::Lane** out) {
 inline uint64_t vload(const uint64_t* p) { return *reinterpret_cast<const volatile uint64_t*>(p); }
 inline void vstore(uint64_t* p, uint64_t v) { *reinterpret_cast<volatile uint64_t*>(p) = v; }
 
+// Release a waited ticket's mailbox slot and ring-slot claim (holds f->mu).
+void ticket_release(fsx_fabric* f, int64_t ticket) {
+  fsx_fabric::Ticket& t = f->tickets[ticket];
+  if (t.slot >= 0) f->mail_blocks.release(t.slot);
+  fsx_fabric::Lane& l = f->lanes.at(t.device);
+  --l.outstanding;
+  int64_t& claim = l.slot_ticket[t.seq % fsx::kLaneSlots];
+  if (claim == ticket) claim = -1;
+  t = fsx_fabric::Ticket{};
+  f->free_tickets.push_back(ticket);
+}
+
 // A served message: its mailbox slot (-1: device source), bytes, slab
 // segment and both device digests.
 struct Served {
@@ -1176,7 +1188,7 @@ struct Served {
 // The digests come from the descriptor, or from the ticket if a publisher
 // harvested them before reusing the slot (checked again after the read, so a
 // slot reused between the done mark and the read is never trusted).
-int lane_wait(fsx_fabric* f, int64_t ticket, Served* out) {
+int lane_wait(fsx_fabric* f, int64_t ticket, Served* out, bool release = false) {
   const fsx::LaneDesc* d = nullptr;
   uint64_t seq = 0;
   {
@@ -1185,7 +1197,10 @@ int lane_wait(fsx_fabric* f, int64_t ticket, Served* out) {
       return fail(FSX_E_NOT_FOUND, "unknown small-message ticket");
     const fsx_fabric::Ticket& t = f->tickets[ticket];
     *out = Served{t.slot, t.n, t.dst, t.sent, t.landed};
-    if (t.harvested) return FSX_OK;
+    if (t.harvested) {
+      if (release) ticket_release(f, ticket);
+      return FSX_OK;
+    }
     d = &f->lanes.at(t.device).ring[t.seq % fsx::kLaneSlots];
     seq = t.seq;
   }
@@ -1202,6 +1217,7 @@ int lane_wait(fsx_fabric* f, int64_t ticket, Served* out) {
           if (t.harvested) {
             out->sent = t.sent;
             out->landed = t.landed;
+            if (release) ticket_release(f, ticket);
             return FSX_OK;
           }
         }
@@ -1220,19 +1236,8 @@ int lane_wait(fsx_fabric* f, int64_t ticket, Served* out) {
     out->sent = t.sent;
     out->landed = t.landed;
   }
+  if (release) ticket_release(f, ticket);
   return FSX_OK;
-}
-
-// Release a waited ticket's mailbox slot and ring-slot claim (holds f->mu).
-void ticket_release(fsx_fabric* f, int64_t ticket) {
-  fsx_fabric::Ticket& t = f->tickets[ticket];
-  if (t.slot >= 0) f->mail_blocks.release(t.slot);
-  fsx_fabric::Lane& l = f->lanes.at(t.device);
-  --l.outstanding;
-  int64_t& claim = l.slot_ticket[t.seq % fsx::kLaneSlots];
-  if (claim == ticket) claim = -1;
-  t = fsx_fabric::Ticket{};
-  f->free_tickets.push_back(ticket);
 }
 
 }  // namespace
@@ -1242,11 +1247,10 @@ namespace {
 // Publish one message on the destination device's lane: host bytes are
 // staged in a mailbox slot; a device source (this GPU's memory or a peer's,
 // peer access is enabled at fsx_open) is read by the lane kernel in place.
-int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src, int64_t n, bool device,
-                   int64_t* ticket) {
+int put_small_locked(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src, int64_t n, bool device,
+                     int64_t* ticket) {  // caller holds f->mu
   *ticket = -1;
   if (n <= 0 || n > FSX_SMALL_MAX) return FSX_OK;
-  std::lock_guard<std::mutex> lk(f->mu);
   Slab* s = slab_of(f, dst_gpu);
   if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
   if (dst_off < 0 || dst_off + n > s->capacity)
@@ -1325,11 +1329,30 @@ int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src,
   return FSX_OK;
 }
 
+int put_small_impl(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* src, int64_t n, bool device,
+                   int64_t* ticket) {
+  std::lock_guard<std::mutex> lk(f->mu);
+  return put_small_locked(f, dst_gpu, dst_off, src, n, device, ticket);
+}
+
 }  // namespace
 
 int fsx_put_small(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* h_src, int64_t n,
                   int64_t* ticket) {
   return put_small_impl(f, dst_gpu, dst_off, h_src, n, false, ticket);
+}
+
+int fsx_put_small_alloc(fsx_fabric* f, int dst_gpu, const void* src, int64_t n, int src_is_device,
+                        int64_t* dst_off, int64_t* ticket) {
+  *dst_off = -1;
+  *ticket = -1;
+  std::lock_guard<std::mutex> lk(f->mu);
+  Slab* s = slab_of(f, dst_gpu);
+  if (!s) return fail(FSX_E_NOT_FOUND, "no slab registered for gpu " + std::to_string(dst_gpu));
+  if (s->imported) return fail(FSX_E_CONFIG, "imported slabs are allocated by their owner");
+  *dst_off = s->blocks.alloc(std::max<int64_t>(n, 1));
+  if (*dst_off < 0) return FSX_OK;  // slab full: the caller parks the send (backlog)
+  return put_small_locked(f, dst_gpu, *dst_off, src, n, src_is_device != 0, ticket);
 }
 
 int fsx_put_small_device(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* d_src, int64_t n,
@@ -1382,11 +1405,7 @@ int fsx_ticket_take(fsx_fabric* f, int64_t ticket, void* h_dst, int64_t n, uint6
 int fsx_ticket_free(fsx_fabric* f, int64_t ticket) {
   // the slot and the slab segment may only be reused once the message is served
   Served sv;
-  int rc = lane_wait(f, ticket, &sv);
-  if (rc) return rc;
-  std::lock_guard<std::mutex> lk(f->mu);
-  ticket_release(f, ticket);
-  return FSX_OK;
+  return lane_wait(f, ticket, &sv, /*release=*/true);
 }
 
 int fsx_chunk_ready(fsx_fabric* f, int dst_gpu, int64_t flag_idx, uint64_t token, int* ready) {

@@ -750,6 +750,48 @@ def test_small_lane_device_source(fab, oracle_mod):
         fab.slab_free(2, off)
 
 
+def test_small_lane_alloc_and_publish(fab, oracle_mod):
+    """fsx_put_small_alloc: the slab segment (NodeArena first fit, as
+    fsx_slab_alloc) and the lane publish in one call, host and device
+    sources; the offsets are the allocator's, the bytes land, declines keep
+    the segment; a full slab returns -1 without publishing."""
+    import ctypes as C
+
+    torch = _torch()
+    msgs = [oracle_mod.synth_payload(8100 + i, 1000 + 700 * i) for i in range(6)]
+    placed = []
+    for i, m in enumerate(msgs):
+        off, t = C.c_int64(-2), C.c_int64(-2)
+        if i % 2:
+            d = torch.frombuffer(bytearray(m), dtype=torch.uint8).cuda()
+            torch.cuda.synchronize()
+            N.call("fsx_put_small_alloc", fab._h, 2, d.data_ptr(), len(m), 1, C.byref(off), C.byref(t))
+            placed.append((m, off.value, t.value, d))
+        else:
+            N.call("fsx_put_small_alloc", fab._h, 2, m, len(m), 0, C.byref(off), C.byref(t))
+            placed.append((m, off.value, t.value, None))
+        assert off.value >= 0 and t.value >= 0
+    offs = [p[1] for p in placed]
+    assert len(set(offs)) == len(offs)
+    for m, off, t, _ in placed:
+        sent, landed = C.c_uint64(), C.c_uint64()
+        N.call("fsx_ticket_take", fab._h, t, None, 0, C.byref(sent), C.byref(landed))
+        assert sent.value == landed.value == oracle_mod.C.or_digest64(m, len(m))
+        assert fab.slab_read(2, off, len(m)) == m
+        fab.slab_free(2, off)
+    # a segment the slab cannot hold: nothing allocated, nothing published
+    before = fab.slab_usage(2)
+    hog = fab.slab_alloc(2, (64 << 20) - 4096)
+    if hog >= 0:  # the fixture slab (64 MiB) is empty between tests
+        off, t = C.c_int64(-2), C.c_int64(-2)
+        N.call("fsx_put_small_alloc", fab._h, 2, b"x" * 8192, 8192, 0, C.byref(off), C.byref(t))
+        assert off.value == -1 and t.value == -1
+        fab.slab_free(2, hog)
+        after = fab.slab_usage(2)
+        assert {k: after[k] for k in ("segments_in_use", "bytes_in_use")} == \
+            {k: before[k] for k in ("segments_in_use", "bytes_in_use")}
+
+
 def test_small_lane_ticket_held_across_ring_turns(fab, oracle_mod):
     """The lane's descriptor ring has 4,096 slots; a ticket held while more
     than a full turn of messages is published after it (an orphaned or parked
