@@ -658,6 +658,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_kernel(LaneCtl* ctl, Lan
       uint64_t t = 0;
       if (lane == 0) t = ld_acquire_sys(&ctl->tail);
       t = __shfl_sync(0xffffffffu, t, 0);
+      __syncwarp();  // lane 0's acquire before the other lanes' descriptor reads
       // oldest message a worker may still read from the cache
       uint64_t oldest = lane < kLaneWorkers ? vq[lane] : ~0ull;
 #pragma unroll

@@ -1283,7 +1283,7 @@ int put_small_locked(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* sr
     // orphaned message): its message was served long since (the lane is
     // FIFO); keep its digests with the ticket before the slot is rewritten
     fsx_fabric::Ticket& old = f->tickets[claim];
-    if (old.used && !old.harvested) {
+    if (old.used && !old.harvested && old.seq % fsx::kLaneSlots == seq % fsx::kLaneSlots) {
       const auto t0 = std::chrono::steady_clock::now();
       while (vload(&d->done) != old.seq + 1) {
         if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 30.0)
