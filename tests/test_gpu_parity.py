@@ -45,13 +45,15 @@ def test_route_and_topology(fab):
     assert e.value.code == "not_found"
 
 
-@pytest.mark.parametrize("n", [0, 1, 7, 8, 15, 16, 17, 31, 4096, 4099, 65536 + 5, (1 << 20) + 3,
-                               117_440_512])
-@pytest.mark.parametrize("shift", [0, 8, 3])
+_SYNTH_SIZES = [0, 1, 7, 8, 15, 16, 17, 31, 4096, 4099, 65536 + 5, (1 << 20) + 3]
+
+
+# every small size at every alignment; the 112 MiB video aligned, and a
+# 16 MiB + 3 span through the unaligned path
+@pytest.mark.parametrize("n,shift", [(n, sh) for n in _SYNTH_SIZES for sh in (0, 8, 3)] +
+                         [(117_440_512, 0), ((16 << 20) + 3, 3), ((16 << 20) + 3, 8)])
 def test_synth_matches_reference_stream(fab, oracle_mod, n, shift):
     torch = _torch()
-    if n > (8 << 20) and shift:
-        pytest.skip("large size checked aligned only")
     seed = T.payload_seed("req-000000/r0000", 0)
     buf = torch.zeros(n + 32, dtype=torch.uint8, device="cuda")
     fab.synth(0, seed, buf.data_ptr() + shift, n)
