@@ -232,7 +232,7 @@ bool is_pinned_host(const void* p) {
 // memcpy of a large piece on up to 4 threads (first-touched pageable source,
 // pinned destination: one core moves ~15 GB/s on the B200 hosts)
 // Persistent host copy workers for staging pageable spans (thread creation
-// per piece cost more than the copy of a 2 MiB part).  min(8, cores / 2)
+// per piece cost more than the copy of a 2 MiB part).  min(15, cores - 1)
 // threads; par_memcpy splits a piece across them and the calling thread.
 class CopyPool {
  public:
@@ -276,7 +276,7 @@ class CopyPool {
  private:
   CopyPool() {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    const int n = static_cast<int>(std::min(8u, hw / 2));
+    const int n = static_cast<int>(std::min(15u, hw - 1));
     for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
     for (auto& t : threads_) t.detach();  // live for the process (static pool)
   }
