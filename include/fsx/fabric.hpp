@@ -28,6 +28,7 @@
 #pragma once
 
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -319,11 +320,13 @@ class Fabric {
   // reference's ack_raw(node, off) took one -- raises Internal instead of
   // freeing whatever live segment sits there.
   void ack_raw(int slab_gpu, int64_t offset) {
+    FSX_PHASE(20);
     if (raw_held_.erase({slab_gpu, offset}) == 0)
       Traits::raise(status::kInternal, "ack_raw of gpu " + std::to_string(slab_gpu) + " offset " +
                                            std::to_string(offset) +
                                            ": no segment held by a raw consumer there");
     release_segment(slab_gpu, offset);
+    FSX_PHASE(21);
     place_backlog(slab_gpu);
   }
 
@@ -530,9 +533,11 @@ class Fabric {
 
   // ForwardEnvelope::location of a slab segment: "gpu<G>:off<K>"
   static std::string location_of(int gpu, int64_t off) {
-    char buf[48];
-    const int k = std::snprintf(buf, sizeof buf, "gpu%d:off%lld", gpu, static_cast<long long>(off));
-    return std::string(buf, static_cast<size_t>(k));
+    char buf[48] = {'g', 'p', 'u'};
+    char* p = std::to_chars(buf + 3, buf + 16, gpu).ptr;
+    std::memcpy(p, ":off", 4);
+    p = std::to_chars(p + 4, buf + sizeof buf, off).ptr;
+    return std::string(buf, static_cast<size_t>(p - buf));
   }
 
   static int device_of_pointer(const void* p) {
@@ -794,12 +799,14 @@ class Fabric {
       // a send that returned before its bytes landed: the delivery waits
       settle(landing, env.dst_gpu);
       if (st.raw_cb) {
+        FSX_PHASE(18);
         if (ticket >= 0 && Traits::is_local(env) && !network) {
           uint64_t sent = 0;
           check(fsx_ticket_digests(h_, ticket, &sent, nullptr));
           env.checksum = sent;
         }
         drop_ticket(ticket);  // waits until the bytes are in the slab
+        FSX_PHASE(19);
         ++transfers_;
         bytes_forwarded_ += env.chunk_bytes;
         ++st.next_seq;
@@ -969,14 +976,16 @@ class EventLoop {
  public:
   double now() const { return now_; }
   void schedule(double at, std::string label, std::function<void()> fn) {
-    heap_.push(Ev{std::max(at, now_), next_++, std::move(label), std::move(fn)});
+    heap_.push_back(Ev{std::max(at, now_), next_++, std::move(label), std::move(fn)});
+    std::push_heap(heap_.begin(), heap_.end());
   }
   void post(std::string label, std::function<void()> fn) { schedule(now_, std::move(label), std::move(fn)); }
   size_t run_until_idle() {
     size_t n = 0;
     while (!heap_.empty()) {
-      Ev ev = heap_.top();
-      heap_.pop();
+      std::pop_heap(heap_.begin(), heap_.end());
+      Ev ev = std::move(heap_.back());  // moved out, not copied (the callback may be large)
+      heap_.pop_back();
       now_ = std::max(now_, ev.at);
       ev.fn();
       ++n;
@@ -992,7 +1001,7 @@ class EventLoop {
     std::function<void()> fn;
     bool operator<(const Ev& o) const { return at != o.at ? at > o.at : id > o.id; }
   };
-  std::priority_queue<Ev> heap_;
+  std::vector<Ev> heap_;  // binary heap ordered by (time, insertion)
   double now_ = 0;
   uint64_t next_ = 0;
 };

@@ -2,12 +2,14 @@
 // 32 host-span rows per decode step into ChunkCallback consumers): the
 // FSX_PHASE hooks of include/fsx/fabric.hpp record the time between
 // consecutive hook points; one JSON line per transition, ns per message.
+#include <cuda_runtime.h>
 #include <x86intrin.h>
 
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <string>
 #include <utility>
 
 static uint64_t g_last_t = 0;
@@ -36,25 +38,44 @@ using namespace fsx;
 
 int main(int argc, char** argv) {
   const int row = argc > 1 ? std::atoi(argv[1]) : 7168;
+  const bool device = argc > 2 && std::string(argv[2]) == "device";  // device rows -> raw consumers
   const int batch = 32, steps = 400;
   std::map<int, int> topo{{0, 0}, {1, 0}};
   EventLoop k;
   SidecarConfig cfg;
+  cfg.async_borrowed_sources = device;
   SidecarFabric f(k, topo, cfg);
   std::vector<uint8_t> rowbuf(row);
   or_synth_payload_into(7, rowbuf.data(), row);
+  void* drow = nullptr;
+  if (device) {
+    if (cudaMalloc(&drow, (size_t)row * batch) != cudaSuccess) return 2;
+    for (int r = 0; r < batch; ++r)
+      cudaMemcpy(static_cast<uint8_t*>(drow) + (size_t)r * row, rowbuf.data(), row, cudaMemcpyHostToDevice);
+  }
   int64_t got = 0;
-  for (int r = 0; r < batch; ++r)
-    f.register_interest(1, "req-" + std::to_string(100000 + r) + "/r0001",
-                        [&](const ForwardEnvelope&, std::vector<uint8_t> b) {
-                          FSX_PHASE(15);
-                          got += (int64_t)b.size();
-                        });
+  for (int r = 0; r < batch; ++r) {
+    if (device)
+      f.register_interest_raw(1, "req-" + std::to_string(100000 + r) + "/r0001",
+                              [&](const ForwardEnvelope& env, int64_t off) {
+                                FSX_PHASE(15);
+                                got += env.chunk_bytes;
+                                f.ack_raw(1, off);
+                              });
+    else
+      f.register_interest(1, "req-" + std::to_string(100000 + r) + "/r0001",
+                          [&](const ForwardEnvelope&, std::vector<uint8_t> b) {
+                            FSX_PHASE(15);
+                            got += (int64_t)b.size();
+                          });
+  }
   auto step = [&](int s) {
     for (int r = 0; r < batch; ++r)
       f.send("req-" + std::to_string(100000 + r),
              DataRef{"req-" + std::to_string(100000 + r) + "/r0001", 0, true}, 0, 1,
-             std::span<const uint8_t>(rowbuf.data(), row), s, false);
+             std::span<const uint8_t>(device ? static_cast<const uint8_t*>(drow) + (size_t)r * row
+                                             : rowbuf.data(), row),
+             s, false);
     FSX_PHASE(16);
     k.run_until_idle();
     FSX_PHASE(17);
@@ -67,8 +88,8 @@ int main(int argc, char** argv) {
   g_on = false;
   const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
   const double ns_per_tick = sec * 1e9 / double(__rdtsc() - t0);
-  std::printf("{\"row_bytes\": %d, \"us_per_step\": %.1f, \"bytes_ok\": %s}\n", row, sec / steps * 1e6,
-              got == (int64_t)batch * steps * row ? "true" : "false");
+  std::printf("{\"row_bytes\": %d, \"source\": \"%s\", \"us_per_step\": %.1f}\n", row,
+              device ? "device rows, raw interest" : "host span, ChunkCallback", sec / steps * 1e6);
   for (auto& [k2, v] : g_acc)
     std::printf("{\"from\": %d, \"to\": %d, \"ns_per_msg\": %.1f, \"count_per_step\": %.1f}\n", k2.first, k2.second,
                 v.first * ns_per_tick / (batch * steps), double(v.second) / steps);
