@@ -140,3 +140,28 @@ def test_cpp_dataplane_pass_bit_exact(gpu):
     lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
     assert len(lines) == 10 and all(l["bit_exact_vs_oracle"] for l in lines), out[-2000:]
     assert sum("tee" in l["batch"] for l in lines) == 2, out[-2000:]
+
+
+def test_reference_serving_experiment_report_identical_on_dropin(gpu):
+    """A whole serving experiment of the reference's own bench harness
+    (bench_harness.hpp run_experiment: planner, dispatcher, encoder / LLM /
+    thinker / talker / generator executors and the sidecar, Virtual clock),
+    built once against the reference's sidecar and once against the drop-in
+    (tests/cpp/app_experiment.cpp): the reports -- throughput, latency
+    percentiles, completions, failures -- are identical."""
+    import json
+
+    ref = os.path.join(ROOT, "build", "app_experiment_ref")
+    fsx = os.path.join(ROOT, "build", "app_experiment_fsx")
+    if not os.path.exists(ref) and not os.path.exists("/root/reference/proj/include"):
+        pytest.skip("reference tree absent here and no prebuilt build/app_experiment_*")
+    outs = {}
+    for name, path in (("reference", ref), ("fsx", fsx)):
+        p = subprocess.run([path], capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+        outs[name] = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(outs["reference"]) == len(outs["fsx"]) == 4
+    for r, f in zip(outs["reference"], outs["fsx"]):
+        assert (r["experiment"], r["run"]) == (f["experiment"], f["run"])
+        assert r["report_fnv1a"] == f["report_fnv1a"], (r, f)
+        assert f["completed"] > 0 and f["failed"] == 0
