@@ -117,14 +117,9 @@ build/test_worker_ipc: tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp bui
 	    -DFSX_REFDATA='"$(REFDATA)"' -DFSX_WORKER_BIN='"$(CURDIR)/build/fsx_worker"' \
 	    -o $@ tests/cpp/test_worker_ipc.cpp tests/cpp/shim_main.cpp $(LINKFSX)
 
-# Whole serving experiments of the reference's bench harness, built once
-# against the reference's own sidecar (reference headers, unmodified) and once
-# against the drop-in: same report, wall time of each (tests/cpp/app_experiment.cpp).
-build/app_experiment_ref: tests/cpp/app_experiment.cpp | build/refdata
-	$(CXX) -std=c++20 -O2 -g -w -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
-	    -DFISSIM_REPO_ROOT='"$(REFDATA)"' -DFISSIM_CLI_BIN='"$(CURDIR)/build/fsx_worker"' \
-	    -o $@ tests/cpp/app_experiment.cpp -lpthread
-
+# Whole serving experiments of the reference's bench harness against the
+# drop-in (tests/cpp/app_experiment.cpp); the same file built against the
+# reference's own sidecar is oracle/_ref/app_experiment_ref (oracle/Makefile).
 build/app_experiment_fsx: tests/cpp/app_experiment.cpp include/fsx/fabric.hpp \
                           include/fsx/dropin/fissim/sidecar.hpp $(LIB) | build/refdata
 	$(CXX) -std=c++20 -O2 -g -w -DFSX_DROPIN -Iinclude/fsx/dropin -Iinclude -I$(FISSIM_REF_INCLUDE) -I$(NLOHMANN_DIR) \
@@ -179,7 +174,7 @@ cpptests: probes build/test_fabric build/bench_fabric build/probe_small_path bui
 	    $(MAKE) -s -j8 build/ref_test_sidecar build/dropin_criterion4 build/ref_test_executors \
 	        build/fsx_worker build/ref_test_worker build/test_worker_ipc \
 	        build/ref_acceptance build/ref_test_control_plane build/ref_test_bench \
-	        build/test_envelope_codec build/app_experiment_ref build/app_experiment_fsx; fi
+	        build/test_envelope_codec build/app_experiment_fsx; fi
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libfsx.sass.txt

@@ -146,12 +146,13 @@ def test_reference_serving_experiment_report_identical_on_dropin(gpu):
     """A whole serving experiment of the reference's own bench harness
     (bench_harness.hpp run_experiment: planner, dispatcher, encoder / LLM /
     thinker / talker / generator executors and the sidecar, Virtual clock),
-    built once against the reference's sidecar and once against the drop-in
-    (tests/cpp/app_experiment.cpp): the reports -- throughput, latency
+    built once against the reference's sidecar (oracle/_ref/app_experiment_ref)
+    and once against the drop-in (build/app_experiment_fsx), both from
+    tests/cpp/app_experiment.cpp: the reports -- throughput, latency
     percentiles, completions, failures -- are identical."""
     import json
 
-    ref = os.path.join(ROOT, "build", "app_experiment_ref")
+    ref = os.path.join(ROOT, "oracle", "_ref", "app_experiment_ref")  # the reference sidecar (checker)
     fsx = os.path.join(ROOT, "build", "app_experiment_fsx")
     if not os.path.exists(ref) and not os.path.exists("/root/reference/proj/include"):
         pytest.skip("reference tree absent here and no prebuilt build/app_experiment_*")
