@@ -13,7 +13,7 @@ timeout 2400 python -m pytest tests -m gpu -q > $O/gpu_tests_$TAG.txt 2>&1; echo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_$TAG.txt 2>&1
 timeout 600 python bench.py > $O/bench_${TAG}_full.json 2> $O/bench_${TAG}.err
 timeout 600 python bench.py --impl reference > $O/bench_${TAG}_reference_arm.json 2>> $O/bench_${TAG}.err
-for C in A D; do
+for C in A C D; do
   timeout 600 python bench.py --config $C >> $O/bench_configs_AD_$TAG.jsonl 2>> $O/bench_${TAG}.err
   timeout 600 python bench.py --config $C --impl reference >> $O/bench_reference_arm_AD_$TAG.jsonl 2>> $O/bench_${TAG}.err
 done

@@ -110,3 +110,21 @@ def test_bench_single_gpu_line(gpu):
     assert set(d["schedules"]) >= {"tee", "serial", "colocated", "direct_placement"}
     assert len(d["schedules"]["colocated"]["runs_ms"]) == 5
     assert d["gpu_launches"] >= 5
+
+
+def test_bench_config_c_line(gpu):
+    """bench.py --config C: the Qwen2.5-Omni decode step (32 hidden rows + 16
+    codes through the streaming channels as one CUDA graph) prints one line
+    with the BASELINE metric, a device per-step time, an e2e from host memory
+    and the reference arm's workload name (the rows are checked byte-exact
+    inside bench.py)."""
+    d = _run(["--config", "C", "--steps", "20", "--warmup", "3", "--no-cpu-baseline"], launcher="self")
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert d["config"]["workload"] == b.CONFIGS["C"]["workload"] and d["metric"] == b.METRIC
+    assert d["value"] > 0 and 0 < d["us_per_step"] < 1000
+    assert d["e2e"]["h2d_bytes_per_step"] == 32 * 7168 + 16 * 4 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] == 4 * 20
