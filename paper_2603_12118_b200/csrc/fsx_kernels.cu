@@ -516,10 +516,11 @@ __global__ void __launch_bounds__(256) digest_kernel(const uint8_t* __restrict__
 // Small-message lane (fsx_put_small; LaneCtl / LaneDesc in fsx_kernels.cuh).
 //
 // One 1024-thread CTA per destination device serves the lane.  Warp 0 is the
-// poller: lane 0 reads the host-published tail (one PCIe round trip, ~1.2 us
-// on the B200 hosts, scripts/probe_pcie_pull.cu), the warp fetches the new
-// descriptors with coalesced reads into a shared-memory cache and publishes
-// the tail to the workers in shared memory.  Warps 1..31 are workers: worker
+// poller: it reads the next 8 descriptors (fields + publication mark, one
+// PCIe round trip, ~1.2 us on the B200 hosts, scripts/probe_pcie_pull.cu),
+// takes the ones whose mark matches their fields as published, copies them
+// into a shared-memory cache and publishes the new tail to the workers in
+// shared memory (the host's LaneCtl::tail only serves the exit handshake).  Warps 1..31 are workers: worker
 // w moves messages m with m % 31 == w as soon as the shared tail passes m,
 // independently of the others (no CTA barrier per batch, so messages
 // published while others are in flight start at once).  A worker's lanes read
@@ -655,31 +656,37 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_kernel(LaneCtl* ctl, Lan
     uint64_t pub = consumed;
     uint64_t idle_from = globaltimer_ns();
     for (;;) {
-      uint64_t t = 0;
-      if (lane == 0) t = ld_acquire_sys(&ctl->tail);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      __syncwarp();  // lane 0's acquire before the other lanes' descriptor reads
       // oldest message a worker may still read from the cache
       uint64_t oldest = lane < kLaneWorkers ? vq[lane] : ~0ull;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) oldest = min(oldest, __shfl_xor_sync(0xffffffffu, oldest, o));
-      t = min(t, oldest + kLaneCache);
-      if (t > pub) {
-        // descriptors [pub, t): lane l reads word l % 4 of descriptor pub + l / 4
-        for (uint64_t m0 = pub; m0 < t; m0 += 8) {
-          const uint64_t m = m0 + (lane >> 2);
-          const int wd = lane & 3;
-          uint64_t v = 0;
-          if (m < t && wd < 3) v = ld_volatile_u64(reinterpret_cast<const uint64_t*>(&ring[m % kLaneSlots]) + wd);
+      // the next 8 descriptors in one round trip: lane l reads word l % 4 of
+      // descriptor pub + l / 4 (the mark with acquire); a descriptor counts as
+      // published when its mark matches the fields read beside it
+      const uint64_t m = pub + (lane >> 2);
+      const int wd = lane & 3;
+      const uint64_t* dw = reinterpret_cast<const uint64_t*>(&ring[m % kLaneSlots]) + wd;
+      const uint64_t v = wd == 3 ? ld_acquire_sys(dw) : ld_volatile_u64(dw);
+      const int g0 = lane & ~3;
+      const uint64_t f_dst = __shfl_sync(0xffffffffu, v, g0);
+      const uint64_t f_src = __shfl_sync(0xffffffffu, v, g0 + 1);
+      const uint64_t f_n = __shfl_sync(0xffffffffu, v, g0 + 2);
+      const uint64_t f_pub = __shfl_sync(0xffffffffu, v, g0 + 3);
+      const bool ok = f_pub == lane_pub(f_dst, f_src, f_n, m) && m < oldest + kLaneCache;
+      const uint32_t okmask = __ballot_sync(0xffffffffu, ok && wd == 0);  // bit 4k: descriptor k
+      // published descriptors in order from pub: the run of set bits 0, 4, 8, ...
+      int count = 0;
+      while (count < 8 && (okmask >> (4 * count)) & 1u) ++count;
+      if (count > 0) {
+        if (wd == 0 && (lane >> 2) < count) {
           const int c = (int)(m % kLaneCache);
-          if (m < t) {
-            if (wd == 0) s_dst[c] = v;
-            else if (wd == 1) s_src[c] = v;
-            else if (wd == 2) s_n[c] = (uint32_t)v;
-          }
+          s_dst[c] = f_dst;
+          s_src[c] = f_src;
+          s_n[c] = (uint32_t)f_n;
         }
         __syncwarp();
         __threadfence_block();  // the cache entries before the tail the workers read
+        const uint64_t t = pub + (uint64_t)count;
         if (lane == 0) *vtail = t;
         pub = t;
         idle_from = globaltimer_ns();

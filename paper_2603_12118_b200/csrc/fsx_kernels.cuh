@@ -114,11 +114,25 @@ struct LaneDesc {                 // 64 B, mapped pinned host memory
   uint8_t* dst;                   // slab destination (device)
   const uint8_t* src;             // staged bytes (mapped pinned host memory)
   int64_t n;                      // bytes (<= FSX_SMALL_MAX)
+  uint64_t pub;                   // lane_pub(dst, src, n, seq), written last by the host
   uint64_t sent;                  // dg64 of the bytes read from src (kernel)
   uint64_t landed;                // dg64 of the bytes read back from dst (kernel)
   uint64_t done;                  // seq + 1 once sent/landed are written (kernel)
-  uint64_t _pad[2];
+  uint64_t _pad;
 };
+
+// Publication mark of descriptor `seq`: a mix of its three fields and its
+// sequence number.  The lane's poller reads a descriptor's first 32 bytes in
+// one round trip and takes it as published only if the mark matches what it
+// read -- a stale slot (an older sequence number) or a read torn by the
+// host's concurrent writes fails the check and is polled again.
+__host__ __device__ inline uint64_t lane_pub(uint64_t dst, uint64_t src, uint64_t n, uint64_t seq) {
+  uint64_t z = (seq + 1) * 0x9e3779b97f4a7c15ull ^ dst;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull ^ src;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull ^ n;
+  z = z ^ (z >> 31);
+  return z | 1;  // never 0 (a cleared slot)
+}
 struct LaneCtl {                  // mapped pinned host memory, one per device
   uint64_t tail;                  // descriptors published (host)
   uint64_t _p0[7];

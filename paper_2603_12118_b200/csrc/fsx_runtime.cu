@@ -1309,6 +1309,11 @@ int put_small_locked(fsx_fabric* f, int dst_gpu, int64_t dst_off, const void* sr
   d->src = device ? static_cast<const uint8_t*>(src) : f->mail + slot;
   d->n = n;
   vstore(&d->done, 0);
+  // the publication mark last: the lane's poller reads fields and mark in one
+  // round trip and trusts the fields only when the mark matches them
+  std::atomic_thread_fence(std::memory_order_release);
+  vstore(&d->pub, fsx::lane_pub(reinterpret_cast<uint64_t>(d->dst), reinterpret_cast<uint64_t>(d->src),
+                                (uint64_t)n, seq));
   // descriptor and bytes before the tail (x86 keeps stores in order; this
   // orders the compiler), then the exit handshake of lane_kernel: store tail,
   // full fence, load exit_epoch
