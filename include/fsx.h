@@ -166,6 +166,21 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * fence.sc.sys before the system-scope flag store, instead of a system-scope
  * acq_rel atomic per tile (the default).  No effect on local slabs. */
 #define FSX_FWD_PEER_GPU_COUNT 16u
+/* FSX_FWD_DMA: move each chunk with the copy engine (cudaMemcpyAsync) and
+ * publish the transfer's chunk flags with one tiny flag kernel behind the
+ * copies (stream order) instead of launching K1: a small isolated transfer
+ * then costs the copy engine's latency plus a one-thread launch (1.7-1.8 us
+ * for 64 KiB-1 MiB) instead of K1's tiles and per-tile completion protocol
+ * (2.6-2.8 us).  A transfer's flags turn together, after its last chunk.
+ * Chosen automatically for a batch of at most FSX_FWD_DMA_MAX_CHUNKS chunks
+ * and FSX_FWD_DMA_MAX_BYTES bytes in total, every destination local, no fused
+ * digest and no FSX_FWD_L2_KEEP (FSX_FWD_KERNEL or FSX_FWD_BULK force K1);
+ * with FSX_FWD_DMA it applies to any batch, peer destinations included.
+ * Ignored (K1 runs) when any transfer asks for a fused digest. */
+#define FSX_FWD_DMA 32u
+#define FSX_FWD_KERNEL 64u
+#define FSX_FWD_DMA_MAX_CHUNKS 4
+#define FSX_FWD_DMA_MAX_BYTES (16ll << 20)
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,
                    uint32_t options, void* stream);
@@ -438,6 +453,7 @@ typedef struct fsx_stats {
   int64_t segments_in_use; /* over all slabs */
   int64_t bytes_in_use;
   int64_t kernel_launches;
+  int64_t dma_forwards; /* transfers moved by the copy-engine form (FSX_FWD_DMA) */
 } fsx_stats;
 int fsx_get_stats(fsx_fabric* f, fsx_stats* out);
 

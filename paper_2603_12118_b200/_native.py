@@ -38,6 +38,9 @@ FWD_HOST_NOTIFY = 1
 FWD_L2_KEEP = 2
 FWD_BULK = 4
 FWD_PEER_GPU_COUNT = 16
+FWD_DMA = 32  # copy-engine form (cudaMemcpyAsync + cuStreamWriteValue64 flags)
+FWD_KERNEL = 64  # force K1 (no automatic copy-engine form)
+FWD_DMA_MAX_CHUNKS = 4
 FWD_MAX_BATCH = 64  # FSX_FWD_MAX_BATCH: transfers per K1 launch
 
 MERGE_FULL = 0
@@ -115,6 +118,7 @@ class Stats(C.Structure):
         ("segments_in_use", C.c_int64),
         ("bytes_in_use", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("dma_forwards", C.c_int64),
     ]
 
 

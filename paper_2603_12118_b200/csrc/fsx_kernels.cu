@@ -735,8 +735,13 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_kernel(LaneCtl* ctl, Lan
 
 __global__ void set_flags_kernel(FlagSetArgs a) {
   for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
-    st_release_sys(&a.dflags[i], a.token);
-    if (a.hflags) st_release_sys(&a.hflags[i], a.token);
+    if (a.gpu_scope) {
+      st_release_gpu(&a.dflags[i], a.token);
+      if (a.hflags) st_relaxed_sys(&a.hflags[i], a.token);
+    } else {
+      st_release_sys(&a.dflags[i], a.token);
+      if (a.hflags) st_release_sys(&a.hflags[i], a.token);
+    }
   }
 }
 

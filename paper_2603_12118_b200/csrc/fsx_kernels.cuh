@@ -76,6 +76,11 @@ struct FlagSetArgs {
   uint64_t* hflags;
   int32_t n;
   uint64_t token;
+  // 1: the bytes behind the flags were written on THIS device (a copy into a
+  // local slab): gpu-scope release of the device flag, relaxed host mirror,
+  // as K1 publishes a local chunk.  0: system-scope release (peer or host
+  // writers).
+  int32_t gpu_scope = 0;
 };
 
 // Streaming channels (config C): per-token rows pushed into a consumer ring.

@@ -430,7 +430,8 @@ struct fsx_fabric {
   std::vector<Ticket> tickets;
   std::vector<int64_t> free_tickets;
   std::atomic<uint64_t> next_token{1};
-  std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0};
+  std::atomic<int64_t> forwards{0}, bytes_forwarded{0}, merges{0}, merged_rows{0}, launches{0},
+      dma_forwards{0};
 };
 
 namespace {
@@ -886,6 +887,83 @@ int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, i
   return rc;
 }
 
+// The copy-engine form of a forward batch (FSX_FWD_DMA, fsx.h): per chunk one
+// cudaMemcpyAsync into the slab, then per transfer one set_flags_kernel (one
+// thread per chunk flag, release stores, + the host mirror) behind the copies
+// in stream order -- the same flags and tokens K1 publishes, so every consumer
+// (fsx_wait, early-start merges, fsx_stream_wait_flags) is unchanged; a
+// transfer's chunk flags turn together, after its last chunk.  The
+// fsx_forward_host pattern, device to device.  A stream memory operation
+// (cuStreamWriteValue64) for the flag measured 5.1 us per transfer against
+// 1.7 us for the flag kernel (profiles/k1_floor_dma_r02s.jsonl).  Returns
+// kNotDma when the batch is not eligible (a fused digest, FSX_FWD_KERNEL /
+// FSX_FWD_BULK, more than FSX_FWD_DMA_MAX_CHUNKS chunks or
+// FSX_FWD_DMA_MAX_BYTES bytes, L2_KEEP, or a peer destination, unless
+// FSX_FWD_DMA); the caller then launches K1.  Validation is K1's.
+constexpr int kNotDma = -1;
+int forward_dma(fsx_fabric* f, int src_dev, int32_t n, fsx_transfer* t, uint32_t options,
+                cudaStream_t st, bool graph) {
+  if (options & (FSX_FWD_KERNEL | FSX_FWD_BULK)) return kNotDma;
+  const bool forced = (options & FSX_FWD_DMA) != 0;
+  // automatic only in the latency regime, and not when the caller asked for
+  // K1's L2 residency hint (a same-GPU merge reads the slab right after)
+  if (!forced && (options & FSX_FWD_L2_KEEP)) return kNotDma;
+  int64_t batch_bytes = 0;
+  for (int32_t i = 0; i < n; ++i) batch_bytes += t[i].bytes;
+  if (!forced && batch_bytes > FSX_FWD_DMA_MAX_BYTES) return kNotDma;
+  struct Op {
+    uint8_t* dst;
+    const uint8_t* src;
+    int64_t bytes, chunk, n_chunks;
+    uint64_t* dflags;
+    uint64_t* hflags;
+    bool peer;
+  };
+  std::vector<Op> ops(n);
+  int64_t chunks = 0;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    for (int32_t i = 0; i < n; ++i) {
+      const fsx_transfer& x = t[i];
+      if (x.d_digest) return kNotDma;
+      int64_t chunk = x.chunk_bytes;
+      if (chunk <= 0 || chunk >= x.bytes) chunk = std::max<int64_t>(x.bytes, 1);
+      const int64_t n_chunks = x.bytes == 0 ? 1 : (x.bytes + chunk - 1) / chunk;
+      chunks += n_chunks;
+      if (!forced && chunks > FSX_FWD_DMA_MAX_CHUNKS) return kNotDma;
+      Slab* s = slab_of(f, x.dst_gpu);
+      if (!s) return kNotDma;  // K1's path reports it
+      if (!forced && (s->imported || s->device != src_dev)) return kNotDma;
+      if (x.dst_off < 0 || x.dst_off + x.bytes > s->capacity)
+        return fail(FSX_E_VALIDATION, "forward overruns the destination slab");
+      if (x.flag_base < 0 || x.flag_base + n_chunks > kFlagRing)
+        return fail(FSX_E_VALIDATION, "flag range out of the ring");
+      ops[i] = Op{s->base + x.dst_off, static_cast<const uint8_t*>(x.d_src), x.bytes, chunk, n_chunks,
+                  s->dflags + x.flag_base,
+                  (s->hflags && (options & FSX_FWD_HOST_NOTIFY)) ? s->hflags + x.flag_base : nullptr,
+                  s->imported || s->device != src_dev};
+    }
+    for (int32_t i = 0; i < n; ++i) {
+      if (graph) slab_of(f, t[i].dst_gpu)->flags.pin(t[i].flag_base, ops[i].n_chunks);
+      if (t[i].token == 0) t[i].token = f->next_token.fetch_add(1);
+    }
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    const Op& o = ops[i];
+    for (int64_t c = 0; c < o.n_chunks; ++c) {
+      const int64_t beg = c * o.chunk, len = std::min(o.chunk, o.bytes - beg);
+      if (len > 0) FSX_CUDA(cudaMemcpyAsync(o.dst + beg, o.src + beg, len, cudaMemcpyDefault, st));
+    }
+    fsx::FlagSetArgs fa{o.dflags, o.hflags, static_cast<int32_t>(o.n_chunks), t[i].token, o.peer ? 0 : 1};
+    FSX_CUDA(fsx::launch_set_flags(fa, st));
+    f->launches++;
+    f->bytes_forwarded += o.bytes;
+    f->forwards++;
+    f->dma_forwards++;
+  }
+  return FSX_OK;
+}
+
 int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t options, void* stream) {
   NvtxRange nvtx_range("fsx.forward");
   if (n <= 0) return n == 0 ? FSX_OK : fail(FSX_E_VALIDATION, "negative transfer count");
@@ -918,6 +996,8 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
   FSX_CUDA(cudaSetDevice(src_dev));
   cudaStream_t st = pick_stream(dev, stream);
   const bool graph = capturing(st);
+  rc = forward_dma(f, src_dev, n, t, options, st, graph);
+  if (rc != kNotDma) return rc;
   for (int32_t first = 0; first < n; first += fsx::kFwdMaxBatch) {
     const int32_t cnt = std::min<int32_t>(n - first, fsx::kFwdMaxBatch);
     fsx::FwdBatch b{};
@@ -1887,6 +1967,7 @@ int fsx_get_stats(fsx_fabric* f, fsx_stats* out) {
   out->merges = f->merges.load();
   out->merged_rows = f->merged_rows.load();
   out->kernel_launches = f->launches.load();
+  out->dma_forwards = f->dma_forwards.load();
   std::lock_guard<std::mutex> lk(f->mu);
   for (auto& [g, s] : f->slabs) {
     out->segments_in_use += s->blocks.segments();

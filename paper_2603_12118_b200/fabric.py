@@ -168,14 +168,19 @@ class DeviceFabric:
     # -- data movement ----------------------------------------------------------
     def forward(self, src_gpu: int, src_ptr: int, dst_gpu: int, dst_off: int, nbytes: int,
                 chunk_bytes: int, flag_base: int, stream=None, token: int = 0,
-                host_notify: bool = True, bulk: bool = False, peer_gpu_count: bool = False) -> int:
+                host_notify: bool = True, bulk: bool = False, peer_gpu_count: bool = False,
+                dma: bool | None = None) -> int:
         """K1.  host_notify mirrors chunk flags to host memory (fsx_wait);
         device-only consumers (stream order, early-start merge) skip it.
         bulk: the bulk-copy tile kernel (FSX_FWD_BULK); peer_gpu_count: peer
-        chunks counted at gpu scope, published once at system scope."""
+        chunks counted at gpu scope, published once at system scope.
+        dma: None = the library's choice (the copy-engine form for a local
+        transfer of at most FWD_DMA_MAX_CHUNKS chunks), True = the copy-engine
+        form (FSX_FWD_DMA), False = always the K1 kernel (FSX_FWD_KERNEL)."""
         tok = C.c_uint64(token)
         opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_BULK if bulk else 0) | \
-            (N.FWD_PEER_GPU_COUNT if peer_gpu_count else 0)
+            (N.FWD_PEER_GPU_COUNT if peer_gpu_count else 0) | \
+            (0 if dma is None else (N.FWD_DMA if dma else N.FWD_KERNEL))
         N.call("fsx_forward_ex", self._h, src_gpu, src_ptr, dst_gpu, dst_off, nbytes, chunk_bytes,
                flag_base, C.byref(tok), opts, _stream_ptr(stream))
         return tok.value

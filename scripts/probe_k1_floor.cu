@@ -27,6 +27,12 @@ __global__ void __launch_bounds__(256) lean_tiles(const uint4* __restrict__ s, u
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag), "l"(token) : "memory");
 }
 
+// one thread publishes a chunk flag behind a stream-ordered copy
+__global__ void flag_kernel(uint64_t* dflag, uint64_t* hflag, uint64_t token) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(dflag), "l"(token) : "memory");
+  if (hflag) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(hflag), "l"(token) : "memory");
+}
+
 int main() {
   const int reps = 200;
   uint8_t *s = nullptr, *d = nullptr;
@@ -44,6 +50,14 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   fsx::preload_kernels();
+  using WV = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+  void* wvp = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  cudaGetDriverEntryPoint("cuStreamWriteValue64", &wvp, cudaEnableDefault, &q);
+  const WV wv = reinterpret_cast<WV>(wvp);
+  if (!wv) return 1;
+  uint64_t* hf = nullptr;
+  cudaHostAlloc(&hf, 1 << 20, cudaHostAllocMapped);
   auto time_graph = [&](auto&& body) -> double {
     cudaGraph_t g;
     cudaGraphExec_t ge;
@@ -107,9 +121,30 @@ int main() {
     std::printf("{\"bytes\": %lld, \"lean_4k_same_counter_us\": %.3f, \"lean_4k_distinct_counters_us\": %.3f}\n",
                 (long long)n, lean_same, lean_distinct);
     const double mc = time_graph([&](int) { cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st); });
+    // the copy-engine form of K1 (FSX_FWD_DMA): the copy, then the chunk flag
+    // by a stream memory operation (device flag; + the mapped host mirror)
+    const double dma = time_graph([&](int i) {
+      cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st);
+      wv(st, reinterpret_cast<uintptr_t>(f + i), 1000 + i, 0);
+    });
+    const double dma_host = time_graph([&](int i) {
+      cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st);
+      wv(st, reinterpret_cast<uintptr_t>(f + i), 1000 + i, 0);
+      wv(st, reinterpret_cast<uintptr_t>(hf + i), 1000 + i, 0);
+    });
+    // the copy, then a one-thread flag kernel behind it (stream order)
+    const double dma_fk = time_graph([&](int i) {
+      cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st);
+      flag_kernel<<<1, 1, 0, st>>>(f + i, nullptr, 1000 + i);
+    });
+    const double dma_fk_host = time_graph([&](int i) {
+      cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, st);
+      flag_kernel<<<1, 1, 0, st>>>(f + i, hf + i, 1000 + i);
+    });
     std::printf("{\"bytes\": %lld, \"k1_tile_4k_us\": %.3f, \"k1_tile_32k_us\": %.3f, \"k1_bulk_4k_us\": %.3f, "
-                "\"k1_bulk_32k_us\": %.3f, \"memcpy_us\": %.3f}\n",
-                (long long)n, t4, t32, b4, b32, mc);
+                "\"k1_bulk_32k_us\": %.3f, \"dma_memop_flag_us\": %.3f, \"dma_memop_flag_host_us\": %.3f, "
+                "\"dma_flag_kernel_us\": %.3f, \"dma_flag_kernel_host_us\": %.3f, \"memcpy_us\": %.3f}\n",
+                (long long)n, t4, t32, b4, b32, dma, dma_host, dma_fk, dma_fk_host, mc);
   }
   return 0;
 }

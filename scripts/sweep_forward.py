@@ -28,6 +28,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--bulk", action="store_true", help="bulk-copy K1 tiles (FSX_FWD_BULK)")
+    ap.add_argument("--form", choices=["auto", "kernel", "dma"], default="auto",
+                    help="auto: the library's choice (copy-engine form for small local transfers); "
+                         "kernel: always K1 (FSX_FWD_KERNEL); dma: always the copy-engine form")
     ap.add_argument("--flush", action="store_true", help="L2 flush before every repetition (--graph)")
     ap.add_argument("--cpu-ref", action="store_true",
                     help="also time the reference CPU forward (oracle/_ref SidecarFabric, 1 thread) per size")
@@ -40,6 +43,7 @@ def main():
 
     from paper_2603_12118_b200.fabric import DeviceFabric
 
+    dma = {"auto": None, "kernel": False, "dma": True}[args.form]
     sizes = [64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20]
     fab = DeviceFabric({0: 0, 1: 0}, {0: 0, 1: 0})
     fab.slab_register(1, 1 << 30)
@@ -59,7 +63,7 @@ def main():
         nch = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
         with torch.cuda.stream(s):
             for _ in range(3):
-                fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+                fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s, dma=dma)
             torch.cuda.synchronize()
             if args.graph:
                 fb = fab.flags_alloc(1, nch)
@@ -69,7 +73,7 @@ def main():
                         if flush_buf is not None:
                             flush_buf.fill_(1)
                         fab.forward(0, src.data_ptr(), 1, off, n, chunk, fb, s, token=(1 << 40) + n,
-                                    host_notify=False, bulk=args.bulk)
+                                    host_notify=False, bulk=args.bulk, dma=dma)
                 with torch.cuda.graph(gc, stream=s):
                     for _ in range(reps):
                         if flush_buf is not None:
@@ -87,7 +91,7 @@ def main():
             else:
                 def fwd_run():
                     for _ in range(reps):
-                        fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s)
+                        fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s, dma=dma)
 
                 def cpy_run():
                     for _ in range(reps):
@@ -112,14 +116,18 @@ def main():
                 f1.synchronize()
                 fms = f0.elapsed_time(f1) / reps
                 ms, cms = ms - fms, cms - fms
-        fab.slab_free(1, off)
         cpu = {}
         if cref is not None and chunk == 0:
             iters = max(2, min(200, (256 << 20) // max(n, 1)))
             secs = cref.ref_forward_bench(n, iters, 1)
             cpu = {"cpu_ref_us": round(secs / iters * 1e6, 1),
                    "cpu_ref_payload_gbs": round(n * iters / secs / 1e9, 3), "cpu_ref_threads": 1}
-        print(json.dumps({"k1": "bulk" if args.bulk else "tile", "graph": args.graph,
+        d0 = fab.stats()["dma_forwards"]
+        fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s, bulk=args.bulk, dma=dma)
+        s.synchronize()
+        fab.slab_free(1, off)
+        form = "dma" if fab.stats()["dma_forwards"] > d0 else ("bulk" if args.bulk else "tile")
+        print(json.dumps({"k1": form, "form_arg": args.form, "graph": args.graph,
                           "l2_flush": bool(args.flush and args.graph), "bytes": n, **cpu, "chunk_bytes": chunk,
                           "chunks": nch, "us": round(ms * 1e3, 2),
                           "hbm_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),

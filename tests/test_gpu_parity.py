@@ -74,7 +74,7 @@ def test_synth_kat_appendix(fab, kat):
         assert h == case["sha256"], case["case"]
 
 
-def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1):
+def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1, dma=None):
     torch = _torch()
     seed = T.fnv1a64(f"req-x/r{n}")
     src = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
@@ -83,7 +83,12 @@ def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1):
     assert off is not None and off % 64 == 0
     nchunks = 1 if chunk <= 0 or chunk >= n else -(-n // chunk)
     fb = fab.flags_alloc(dst_gpu, nchunks)
-    tok = fab.forward(0, src.data_ptr() + src_shift, dst_gpu, off, n, chunk, fb)
+    d0 = fab.stats()["dma_forwards"]
+    tok = fab.forward(0, src.data_ptr() + src_shift, dst_gpu, off, n, chunk, fb, dma=dma)
+    # which form ran: FSX_FWD_DMA / FSX_FWD_KERNEL as asked, else the library's
+    # rule (copy engine for a local batch of <= 4 chunks and <= 16 MiB)
+    auto_dma = nchunks <= N.FWD_DMA_MAX_CHUNKS and n <= (16 << 20)
+    assert fab.stats()["dma_forwards"] - d0 == int(auto_dma if dma is None else dma)
     fab.wait(dst_gpu, fb, nchunks, tok, timeout_us=20_000_000)
     for c in range(nchunks):
         assert fab.chunk_ready(dst_gpu, fb + c, tok)
@@ -93,21 +98,61 @@ def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1):
     fab.slab_free(dst_gpu, off)
 
 
+# forms: None = the library's choice, False = K1 forced (FSX_FWD_KERNEL),
+# True = the copy-engine form forced (FSX_FWD_DMA)
+@pytest.mark.parametrize("dma", [None, False, True], ids=["auto", "kernel", "dma"])
 @pytest.mark.parametrize("n", [0, 1, 7, 256, 4096, 65536, 1 << 20, 8 << 20, 64 << 20, 256 << 20])
-def test_forward_single_shot_byte_exact(fab, oracle_mod, n):
+def test_forward_single_shot_byte_exact(fab, oracle_mod, n, dma):
     # tests/test_sidecar.cpp:60-87 sizes; single-shot = one chunk, one flag
-    _forward_check(fab, oracle_mod, n, 0)
+    _forward_check(fab, oracle_mod, n, 0, dma=dma)
 
 
+@pytest.mark.parametrize("dma", [None, False, True], ids=["auto", "kernel", "dma"])
 @pytest.mark.parametrize("n,chunk", [(1 << 20, 65536), (8 << 20, 1 << 20), (7_340_032 * 3 + 48, 7_340_032),
-                                     (300_017, 4096), (65536 * 7 + 5, 65536)])
-def test_forward_chunked_flags(fab, oracle_mod, n, chunk):
-    _forward_check(fab, oracle_mod, n, chunk)
+                                     (300_017, 4096), (65536 * 7 + 5, 65536), (4 << 20, 1 << 20)])
+def test_forward_chunked_flags(fab, oracle_mod, n, chunk, dma):
+    _forward_check(fab, oracle_mod, n, chunk, dma=dma)
 
 
-def test_forward_unaligned_source(fab, oracle_mod):
-    _forward_check(fab, oracle_mod, 100_003, 0, src_shift=3)
-    _forward_check(fab, oracle_mod, 100_003, 4096, src_shift=5)
+@pytest.mark.parametrize("dma", [None, False, True], ids=["auto", "kernel", "dma"])
+def test_forward_unaligned_source(fab, oracle_mod, dma):
+    _forward_check(fab, oracle_mod, 100_003, 0, src_shift=3, dma=dma)
+    _forward_check(fab, oracle_mod, 100_003, 4096, src_shift=5, dma=dma)
+
+
+def test_forward_dma_form_in_graph_publishes_flags(fab, oracle_mod):
+    """The copy-engine form captured in a CUDA graph (memcpy node + memory-op
+    flag nodes): every replay lands the bytes and sets each chunk flag to the
+    replay's token only after its bytes (an early-start merge / fsx_wait
+    consumer sees the same protocol as K1's)."""
+    torch = _torch()
+    n, chunk = 3 << 20, 1 << 20
+    seed = T.fnv1a64("req-dma/graph")
+    src = torch.empty(n, dtype=torch.uint8, device="cuda")
+    fab.synth(0, seed, src.data_ptr(), n)
+    off = fab.slab_alloc(1, n)
+    fb = fab.flags_alloc(1, 3)
+    s = torch.cuda.Stream()
+    tok = (1 << 41) + 7
+    g = torch.cuda.CUDAGraph()
+    d0 = fab.stats()["dma_forwards"]
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fab.forward(0, src.data_ptr(), 1, off, n, chunk, fb, s, token=tok, dma=True)
+    assert fab.stats()["dma_forwards"] - d0 == 1
+    want = oracle_mod.synth_payload(seed, n)
+    for r in range(3):
+        fab.synth(1, seed + 1 + r, fab.slab_ptr(1, off), n)  # scribble over the segment
+        torch.cuda.synchronize()
+        assert fab.slab_read(1, off, n) != want
+        g.replay()
+        if r == 0:  # fresh flags: the host mirror turns to tok only behind the bytes
+            fab.wait(1, fb, 3, tok, timeout_us=20_000_000)
+        else:
+            s.synchronize()
+        assert all(fab.chunk_ready(1, fb + c, tok) for c in range(3))
+        assert fab.slab_read(1, off, n) == want
+    fab.slab_free(1, off)
 
 
 def test_forward_rejects_bad_chunk_and_overrun(fab):
