@@ -20,6 +20,8 @@ done
 timeout 600 python scripts/sweep_forward.py --graph --cpu-ref > $O/k1_sweep_configE_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 python scripts/sweep_forward.py --graph --flush > $O/k1_sweep_flush_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 python scripts/sweep_forward.py --graph --flush --bulk > $O/k1_sweep_flush_bulk_$TAG.jsonl 2>> $O/bench_${TAG}.err
+timeout 600 python scripts/sweep_forward.py --graph --form kernel > $O/k1_sweep_graph_kernel_$TAG.jsonl 2>> $O/bench_${TAG}.err
+timeout 600 python scripts/sweep_forward.py --graph --form auto > $O/k1_sweep_graph_auto_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 600 build/bench_fabric 4 > $O/bench_fabric_dropin_$TAG.jsonl 2>> $O/bench_${TAG}.err
 timeout 120 build/probe_small_path 7168 > $O/small_path_phases_$TAG.jsonl 2>> $O/bench_${TAG}.err
 [ -x build/probe_k1_floor ] && timeout 120 build/probe_k1_floor > $O/k1_floor_$TAG.jsonl 2>> $O/bench_${TAG}.err
