@@ -85,6 +85,7 @@ def test_python_constants_match_header():
              "TRANSPORT_LOCAL_BUFFER": "LOCAL_BUFFER", "TRANSPORT_NETWORK_STREAM": "NETWORK_STREAM",
              "FWD_HOST_NOTIFY": "FWD_HOST_NOTIFY", "FWD_L2_KEEP": "FWD_L2_KEEP", "FWD_BULK": "FWD_BULK",
              "FWD_PEER_GPU_COUNT": "FWD_PEER_GPU_COUNT", "FWD_MAX_BATCH": "FWD_MAX_BATCH",
+             "FWD_DMA": "FWD_DMA", "FWD_KERNEL": "FWD_KERNEL", "FWD_DMA_MAX_CHUNKS": "FWD_DMA_MAX_CHUNKS",
              "MERGE_FULL": "MERGE_FULL", "MERGE_SCAN_ONLY": "MERGE_SCAN_ONLY",
              "MERGE_COPY_ONLY": "MERGE_COPY_ONLY", "MERGE_DISCARD": "MERGE_DISCARD",
              "MERGE_COLOCATED": "MERGE_COLOCATED"}
