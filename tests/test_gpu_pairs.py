@@ -39,11 +39,13 @@ def _run(args, timeout=400, launcher="torchrun", nproc=2):
 @pytest.mark.parametrize("config,requests,transfer,k1", [("B", 1, "slab", "auto"), ("A", 16, "slab", "tile"),
                                                          ("A", 16, "slab", "gpucount"),
                                                          ("A", 16, "slab", "bulk"),
+                                                         ("A", 16, "slab", "dma"),
                                                          ("B", 2, "direct", "auto"), ("A", 16, "direct", "auto")])
 def test_pairs_protocol_same_device(gpu, config, requests, transfer, k1):
     """The pair protocol for every peer K1 form (register tiles with a
     system-scope count per tile, gpu-scope count + one system-scope publish
-    per chunk, bulk-copy tiles; auto probes all three) and for direct
+    per chunk, bulk-copy tiles, the copy engine + a flag kernel; auto probes
+    all four) and for direct
     placement (fsx_forward_place into the consumer's IPC-mapped prompt + done
     flag): merged embeddings verified bit-exact on the consumer."""
     d = _run(["--gpus", "2", "--pin-device", "0", "--steps", "4", "--warmup", "2", "--config", config,
