@@ -119,11 +119,11 @@ def load_peaks():
 
 def load_traffic(config: str, kernel: str, alg_bytes: int):
     """DRAM bytes per launch of `kernel` on `config` from the committed
-    `ncu --set full` capture (profiles/traffic_r02q.json, written by
+    `ncu --set full` capture (profiles/traffic_r02s.json, written by
     scripts/profile_round.sh), only when that capture is of the same kernel on
     the same launch size; else (None, reason)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic_r02q.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "traffic_r02s.json")) as fh:
             rec = json.load(fh).get(f"{config}:{kernel}")
     except Exception:
         rec = None
