@@ -386,30 +386,54 @@ def run_config_c(args):
     s = torch.cuda.Stream()
 
     def step(st):
+        # the step's hidden rows and codes in ONE push launch and ONE pull
+        # launch (fsx_channel_push_groups / _pull_groups: 48 streams, two
+        # row sizes, two buffers)
+        fab.channel_push_groups([(hch, hrows.data_ptr(), row), (cch, codes.data_ptr(), 4)], st)
+        fab.channel_pull_groups([(hch, hout.data_ptr(), row), (cch, cout.data_ptr(), 4)], st)
+
+    def step_per_group(st):  # round-2 r02q form: push + pull per group (4 launches)
         fab.channel_push(hch, hrows.data_ptr(), row, st)
         fab.channel_pull(hch, hout.data_ptr(), row, st)
         fab.channel_push(cch, codes.data_ptr(), 4, st)
         fab.channel_pull(cch, cout.data_ptr(), 4, st)
 
-    with torch.cuda.stream(s):
-        for _ in range(max(3, args.warmup)):
-            step(s)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
-        step(s)
-    with torch.cuda.stream(s):
-        for _ in range(max(3, args.warmup)):
-            g.replay()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk, torch.cuda.stream(s):
-        e0.record(s)
-        for _ in range(args.steps):
-            g.replay()
-        e1.record(s)
-        e1.synchronize()
-    ms_step = e0.elapsed_time(e1) / args.steps
+    def graph_of(fn):
+        with torch.cuda.stream(s):
+            for _ in range(max(3, args.warmup)):
+                fn(s)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        l0 = fab.stats()["kernel_launches"]
+        with torch.cuda.graph(gr, stream=s):
+            fn(s)
+        nk = fab.stats()["kernel_launches"] - l0
+        with torch.cuda.stream(s):
+            for _ in range(max(3, args.warmup)):
+                gr.replay()
+        torch.cuda.synchronize()
+        return gr, nk
+
+    def time_graph(gr):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for _ in range(args.steps):
+                gr.replay()
+            e1.record(s)
+            e1.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    g4, k4 = graph_of(step_per_group)
+    hout.zero_()
+    cout.zero_()
+    ms_per_group = time_graph(g4)
+    assert torch.equal(hout, hrows) and torch.equal(cout, codes), "streamed rows differ (per group)"
+    hout.zero_()
+    cout.zero_()
+    g, kernels_per_step = graph_of(step)
+    with ClockSampler(0) as clk:
+        ms_step = time_graph(g)
     assert torch.equal(hout, hrows) and torch.equal(cout, codes), "streamed rows differ"
     # e2e: host rows through the drop-in's small-message path, host-timed
     hin = torch.empty(nh * row + nc * 4, dtype=torch.uint8, pin_memory=True)
@@ -472,17 +496,21 @@ def run_config_c(args):
         "msgs_per_s": round((nh + nc) / (ms_step * 1e-3), 1),
         "config": {"workload": cfg["workload"],
                    "placement": "thinker, talker and vocoder slabs on one B200 (intra-device channels)",
-                   "schedule": "one CUDA graph per decode step: push + pull of the hidden rows, then of "
-                               "the codes (4 kernels)",
+                   "schedule": "one CUDA graph per decode step: one push launch and one pull launch "
+                               "for the hidden rows and the codes together (channel groups)",
                    "parallelism": "1 GPU", "l2": "decode-step working set is L2-resident by nature"},
         "roofline": {"bound": "hbm", "kernel": "fsx::kern::chan_push_kernel + chan_pull_kernel",
                      "achieved": round(2 * step_bytes / (ms_step * 1e-3) / 1e9, 2), "peak": peak,
                      "peak_kind": f"{peak_kind} hbm_gbs (copy, burst)", "unit": "GB/s",
                      "frac": round(2 * step_bytes / (ms_step * 1e-3) / 1e9 / peak, 6), "traffic": None,
                      "traffic_note": "latency-bound: a decode step moves 229 KB; the step time is the "
-                                     "four kernel nodes' launch and flag round trips, not bandwidth",
+                                     "two kernel nodes' launch and flag round trips, not bandwidth",
                      "algorithmic_bytes_per_launch": 2 * step_bytes},
-        "gpu_launches": 4 * args.steps, "gpu_launches_per_step": 4,
+        "schedules": {"groups": {"what": "push + pull of both groups in one launch each",
+                                 "kernels_per_step": kernels_per_step, "us_per_step": round(ms_step * 1e3, 2)},
+                      "per_group": {"what": "push + pull per group (hidden rows, then codes)",
+                                    "kernels_per_step": k4, "us_per_step": round(ms_per_group * 1e3, 2)}},
+        "gpu_launches": kernels_per_step * args.steps, "gpu_launches_per_step": kernels_per_step,
         "clocks": clk.summary(),
         "e2e": {"value": round(step_bytes / (e2e_us * 1e-6) / 1e9, 4), "unit": "GB/s",
                 "h2d_bytes_per_step": step_bytes, "d2h_bytes_per_step": step_bytes,

@@ -395,6 +395,22 @@ int fsx_channel_push(fsx_fabric* f, int32_t n, const int32_t* channels, const vo
                      int64_t row_stride, void* stream);
 int fsx_channel_pull(fsx_fabric* f, int32_t n, const int32_t* channels, void* d_out,
                      int64_t out_stride, void* stream);
+/* Several groups of channels in one step -- e.g. a decode step's thinker
+ * hidden rows and talker codes, different row sizes from different buffers --
+ * moved by one push launch and one pull launch (up to 48 rows per launch)
+ * instead of one per group.  Group g: channels[0..n) with rows at
+ * d_rows + i * stride (push: the producer rows; pull: the output rows).  Same
+ * rules as fsx_channel_push / fsx_channel_pull per row. */
+typedef struct fsx_chan_group {
+  int32_t n;
+  const int32_t* channels;
+  void* d_rows;
+  int64_t stride;
+} fsx_chan_group;
+int fsx_channel_push_groups(fsx_fabric* f, int32_t n_groups, const fsx_chan_group* groups,
+                            void* stream);
+int fsx_channel_pull_groups(fsx_fabric* f, int32_t n_groups, const fsx_chan_group* groups,
+                            void* stream);
 int fsx_channel_progress(fsx_fabric* f, int32_t channel, uint64_t* produced, uint64_t* consumed);
 
 /* ---- synthesis (K0) ---------------------------------------------------------

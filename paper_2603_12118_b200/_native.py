@@ -109,6 +109,15 @@ def _transfer_dtype():
 TRANSFER_DTYPE = _transfer_dtype()
 
 
+class ChanGroup(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32),
+        ("channels", C.POINTER(C.c_int32)),
+        ("d_rows", C.c_void_p),
+        ("stride", C.c_int64),
+    ]
+
+
 class Stats(C.Structure):
     _fields_ = [
         ("forwards", C.c_int64),
@@ -180,6 +189,8 @@ _SIGS = {
     "fsx_channel_close": [C.c_void_p, C.c_int32],
     "fsx_channel_push": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_channel_pull": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "fsx_channel_push_groups": [C.c_void_p, C.c_int32, C.POINTER(ChanGroup), C.c_void_p],
+    "fsx_channel_pull_groups": [C.c_void_p, C.c_int32, C.POINTER(ChanGroup), C.c_void_p],
     "fsx_channel_progress": [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "fsx_synth_payload": [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p],
     "fsx_digest": [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],

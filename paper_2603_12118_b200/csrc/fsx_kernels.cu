@@ -1146,7 +1146,7 @@ __global__ void __launch_bounds__(32) chan_push_kernel(const __grid_constant__ C
   }
   __syncwarp();
   uint8_t* dst = c.ring + (seq % c.slots) * (uint64_t)c.row_bytes;
-  warp_copy_row(s.rows + blockIdx.x * s.stride, dst, c.row_bytes, lane);
+  warp_copy_row(c.io, dst, c.row_bytes, lane);
   __syncwarp();
   if (lane == 0) {
     const uint64_t tag = c.salt | (seq + 1);
@@ -1166,8 +1166,7 @@ __global__ void __launch_bounds__(32) chan_pull_kernel(const __grid_constant__ C
   const uint64_t slot = seq % c.slots;
   if (lane == 0) spin_until(&c.flags[slot], c.salt | (seq + 1));
   __syncwarp();
-  uint8_t* out = const_cast<uint8_t*>(s.rows) + blockIdx.x * s.stride;
-  warp_copy_row(c.ring + slot * (uint64_t)c.row_bytes, out, c.row_bytes, lane);
+  warp_copy_row(c.ring + slot * (uint64_t)c.row_bytes, c.io, c.row_bytes, lane);
   __syncwarp();
   if (lane == 0) st_release_sys(c.tail, seq + 1);  // slot free for the producer
 }

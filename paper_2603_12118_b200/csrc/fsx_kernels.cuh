@@ -94,13 +94,12 @@ struct ChanRow {
   uint32_t row_bytes;
   int32_t peer;         // ring is peer memory
   int32_t _pad;
+  uint8_t* io;          // this row's producer source (push) / consumer output (pull)
 };
 constexpr int kChanMaxRows = 48;
 struct ChanStep {
   int32_t n;
   int32_t _pad;
-  const uint8_t* rows;  // producer rows (push) / consumer output rows (pull)
-  int64_t stride;
   ChanRow c[kChanMaxRows];
 };
 

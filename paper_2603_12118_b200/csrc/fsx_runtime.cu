@@ -1828,19 +1828,24 @@ int state_slot(fsx_fabric* f, Device* d, uint64_t** out) {
   return FSX_OK;
 }
 
-int build_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, int64_t stride,
-               bool push, fsx::ChanStep* st, int* device) {
+// One launch's rows: channel + the row's producer source (push) or consumer
+// output (pull).
+struct ChanIo {
+  int32_t ch;
+  uint8_t* io;
+};
+
+int build_step(fsx_fabric* f, int32_t n, const ChanIo* rows, bool push, fsx::ChanStep* st,
+               int* device) {
   st->n = n;
-  st->rows = static_cast<const uint8_t*>(rows);
-  st->stride = stride;
   for (int32_t i = 0; i < n; ++i) {
-    if (chs[i] < 0 || chs[i] >= (int32_t)f->channels.size() || !f->channels[chs[i]].open)
-      return fail(FSX_E_NOT_FOUND, "unknown or closed channel " + std::to_string(chs[i]));
-    const Channel& c = f->channels[chs[i]];
+    const int32_t ch = rows[i].ch;
+    if (ch < 0 || ch >= (int32_t)f->channels.size() || !f->channels[ch].open)
+      return fail(FSX_E_NOT_FOUND, "unknown or closed channel " + std::to_string(ch));
+    const Channel& c = f->channels[ch];
     const int dev = push ? c.src_dev : c.dst_dev;
     if (i == 0) *device = dev;
     else if (dev != *device) return fail(FSX_E_VALIDATION, "channels of one step must share a device");
-    if (stride < (int64_t)c.row_bytes) return fail(FSX_E_VALIDATION, "row stride below row size");
     Slab* s = slab_of(f, c.dst_gpu);
     fsx::ChanRow& r = st->c[i];
     r.ring = s->base + c.ring_off;
@@ -1851,13 +1856,32 @@ int build_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, i
     r.slots = c.slots;
     r.row_bytes = c.row_bytes;
     r.peer = (s->imported || c.src_dev != c.dst_dev) ? 1 : 0;
+    r.io = rows[i].io;
   }
   return FSX_OK;
 }
 
-int chan_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, int64_t stride,
-              bool push, void* stream) {
-  if (n < 0) return fail(FSX_E_VALIDATION, "negative channel count");
+// Every group's rows in launches of up to kChanMaxRows rows (one launch for a
+// whole decode step of up to 48 streams, whatever their row sizes).
+int chan_step(fsx_fabric* f, int32_t n_groups, const fsx_chan_group* groups, bool push,
+              void* stream) {
+  if (n_groups < 0) return fail(FSX_E_VALIDATION, "negative group count");
+  std::vector<ChanIo> rows;
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    for (int32_t g = 0; g < n_groups; ++g) {
+      const fsx_chan_group& gr = groups[g];
+      if (gr.n < 0) return fail(FSX_E_VALIDATION, "negative channel count");
+      if (gr.n > 0 && !gr.channels) return fail(FSX_E_VALIDATION, "null channel list");
+      for (int32_t i = 0; i < gr.n; ++i) {
+        const int32_t ch = gr.channels[i];
+        if (ch >= 0 && ch < (int32_t)f->channels.size() && gr.stride < (int64_t)f->channels[ch].row_bytes)
+          return fail(FSX_E_VALIDATION, "row stride below row size");
+        rows.push_back({ch, static_cast<uint8_t*>(gr.d_rows) + i * gr.stride});
+      }
+    }
+  }
+  const int32_t n = (int32_t)rows.size();
   for (int32_t first = 0; first < n; first += fsx::kChanMaxRows) {
     const int32_t cnt = std::min<int32_t>(n - first, fsx::kChanMaxRows);
     fsx::ChanStep st{};
@@ -1865,8 +1889,7 @@ int chan_step(fsx_fabric* f, int32_t n, const int32_t* chs, const void* rows, in
     Device* dev = nullptr;
     {
       std::lock_guard<std::mutex> lk(f->mu);
-      int rc = build_step(f, cnt, chs + first, static_cast<const uint8_t*>(rows) + first * stride,
-                          stride, push, &st, &device);
+      int rc = build_step(f, cnt, rows.data() + first, push, &st, &device);
       if (rc) return rc;
       rc = device_state(f, device, &dev);
       if (rc) return rc;
@@ -1937,13 +1960,27 @@ int fsx_channel_close(fsx_fabric* f, int32_t channel) {
 int fsx_channel_push(fsx_fabric* f, int32_t n, const int32_t* channels, const void* d_rows,
                      int64_t row_stride, void* stream) {
   NvtxRange nvtx_range("fsx.channel_push");
-  return chan_step(f, n, channels, d_rows, row_stride, true, stream);
+  const fsx_chan_group g{n, channels, const_cast<void*>(d_rows), row_stride};
+  return chan_step(f, 1, &g, true, stream);
 }
 
 int fsx_channel_pull(fsx_fabric* f, int32_t n, const int32_t* channels, void* d_out,
                      int64_t out_stride, void* stream) {
   NvtxRange nvtx_range("fsx.channel_pull");
-  return chan_step(f, n, channels, d_out, out_stride, false, stream);
+  const fsx_chan_group g{n, channels, d_out, out_stride};
+  return chan_step(f, 1, &g, false, stream);
+}
+
+int fsx_channel_push_groups(fsx_fabric* f, int32_t n_groups, const fsx_chan_group* groups,
+                            void* stream) {
+  NvtxRange nvtx_range("fsx.channel_push");
+  return chan_step(f, n_groups, groups, true, stream);
+}
+
+int fsx_channel_pull_groups(fsx_fabric* f, int32_t n_groups, const fsx_chan_group* groups,
+                            void* stream) {
+  NvtxRange nvtx_range("fsx.channel_pull");
+  return chan_step(f, n_groups, groups, false, stream);
 }
 
 int fsx_channel_progress(fsx_fabric* f, int32_t channel, uint64_t* produced, uint64_t* consumed) {

@@ -243,6 +243,27 @@ class DeviceFabric:
         N.call("fsx_channel_pull", self._h, len(chs), self._chs(chs), out_ptr, stride,
                _stream_ptr(stream))
 
+    def _groups(self, groups):
+        """[(channels, rows_ptr, stride), ...] -> a ChanGroup array (the
+        channel arrays are kept alive on the array object)."""
+        arr = (N.ChanGroup * max(len(groups), 1))()
+        keep = []
+        for i, (chs, ptr, stride) in enumerate(groups):
+            a = self._chs(chs)
+            keep.append(a)
+            arr[i] = N.ChanGroup(len(chs), C.cast(a, C.POINTER(C.c_int32)), ptr, stride)
+        arr._keep = keep
+        return arr
+
+    def channel_push_groups(self, groups, stream=None) -> None:
+        """One push launch for several channel groups (fsx_channel_push_groups):
+        groups = [(channels, rows_ptr, stride), ...]."""
+        N.call("fsx_channel_push_groups", self._h, len(groups), self._groups(groups), _stream_ptr(stream))
+
+    def channel_pull_groups(self, groups, stream=None) -> None:
+        """One pull launch for several channel groups (fsx_channel_pull_groups)."""
+        N.call("fsx_channel_pull_groups", self._h, len(groups), self._groups(groups), _stream_ptr(stream))
+
     def channel_progress(self, ch: int):
         p, c = C.c_uint64(), C.c_uint64()
         N.call("fsx_channel_progress", self._h, ch, C.byref(p), C.byref(c))

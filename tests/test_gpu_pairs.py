@@ -129,4 +129,7 @@ def test_bench_config_c_line(gpu):
     assert d["config"]["workload"] == b.CONFIGS["C"]["workload"] and d["metric"] == b.METRIC
     assert d["value"] > 0 and 0 < d["us_per_step"] < 1000
     assert d["e2e"]["h2d_bytes_per_step"] == 32 * 7168 + 16 * 4 and d["e2e"]["value"] > 0
-    assert d["gpu_launches"] == 4 * 20
+    # one push + one pull launch per step (channel groups), against four per
+    # step when each group is pushed and pulled on its own
+    assert d["gpu_launches"] == 2 * 20 and d["gpu_launches_per_step"] == 2
+    assert d["schedules"]["per_group"]["kernels_per_step"] == 4

@@ -121,3 +121,54 @@ def test_channel_errors(fab):
     assert e.value.code == "validation"
     fab.channel_close(a)
     fab.channel_close(b)
+
+
+def test_channel_groups_one_launch_per_step(fab, oracle_mod):
+    """fsx_channel_push_groups / _pull_groups: a decode step's thinker hidden
+    rows (gpu 0 -> 1, 7 KiB) and talker codes (gpu 1 -> 2, 4 B) from two
+    buffers move in one push and one pull launch, in seq order, byte-exact;
+    more than 48 rows in one call split into several launches."""
+    import torch
+
+    for nh, nc in [(32, 16), (40, 20)]:  # 48 rows: one launch each way; 60: two
+        hb = 3584 * 2
+        hrefs = [f"req-{i:06d}/r0002" for i in range(nh)]
+        crefs = [f"req-{i:06d}/r0003" for i in range(nc)]
+        hch = [fab.channel_open(0, 1, hb, slots=4) for _ in hrefs]
+        cch = [fab.channel_open(1, 2, 4, slots=4) for _ in crefs]
+        hrows = torch.empty((nh, hb), dtype=torch.uint8, device="cuda")
+        crows = torch.empty((nc, 4), dtype=torch.uint8, device="cuda")
+        hout, cout = torch.empty_like(hrows), torch.empty_like(crows)
+        for step in range(6):
+            hw, cw = _rows(oracle_mod, hrefs, step, hb), _rows(oracle_mod, crefs, step, 4)
+            hrows.copy_(torch.from_numpy(hw))
+            crows.copy_(torch.from_numpy(cw))
+            hout.zero_()
+            cout.zero_()
+            l0 = fab.stats()["kernel_launches"]
+            fab.channel_push_groups([(hch, hrows.data_ptr(), hb), (cch, crows.data_ptr(), 4)])
+            fab.channel_pull_groups([(hch, hout.data_ptr(), hb), (cch, cout.data_ptr(), 4)])
+            assert fab.stats()["kernel_launches"] - l0 == 2 * -(-(nh + nc) // 48)
+            torch.cuda.synchronize()
+            assert np.array_equal(hout.cpu().numpy(), hw), step
+            assert np.array_equal(cout.cpu().numpy(), cw), step
+        for ch in hch + cch:
+            assert fab.channel_progress(ch) == (6, 6)
+            fab.channel_close(ch)
+
+
+def test_channel_groups_validation(fab):
+    import torch
+
+    from paper_2603_12118_b200 import _native as N
+
+    ch = fab.channel_open(0, 1, 64, slots=2)
+    rows = torch.empty((2, 64), dtype=torch.uint8, device="cuda")
+    with pytest.raises(N.FsxError) as e:  # stride below the row size
+        fab.channel_push_groups([([ch], rows.data_ptr(), 32)])
+    assert e.value.code == "validation"
+    with pytest.raises(N.FsxError) as e:
+        fab.channel_push_groups([([ch], rows.data_ptr(), 64), ([12345], rows.data_ptr(), 64)])
+    assert e.value.code == "not_found"
+    assert fab.channel_progress(ch) == (0, 0)  # nothing launched
+    fab.channel_close(ch)
