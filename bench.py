@@ -70,7 +70,7 @@ KERNELS = {
 
 
 # N>1: the K1 forms for peer (NVLink) destinations (fsx_forward_batch options)
-K1_FORMS = {"tile": 0,          # register tiles, system-scope acq_rel count per tile
+K1_FORMS = {"tile": 64,         # register tiles (FSX_FWD_KERNEL), system-scope acq_rel count per tile
             "gpucount": 16,     # register tiles, gpu-scope count, one fence.sc.sys + flag per chunk
             "bulk": 4,          # bulk-copy (cp.async.bulk) tiles into the peer slab
             "dma": 32}          # copy engine (cudaMemcpyAsync per chunk) + one flag kernel per transfer

@@ -178,6 +178,11 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * with FSX_FWD_DMA it applies to any batch, peer destinations included.
  * Ignored (K1 runs) when any transfer asks for a fused digest. */
 #define FSX_FWD_DMA 32u
+/* FSX_FWD_KERNEL: always the register-tile K1 (no copy-engine form, no
+ * automatic bulk-copy tiles).  Without FSX_FWD_KERNEL / FSX_FWD_BULK /
+ * FSX_FWD_L2_KEEP, a local batch above 2 MiB that is not taken by the
+ * copy-engine form runs the bulk-copy tiles (forward_tma_kernel) when every
+ * transfer is 16-byte aligned without a fused digest. */
 #define FSX_FWD_KERNEL 64u
 #define FSX_FWD_DMA_MAX_CHUNKS 4
 #define FSX_FWD_DMA_MAX_BYTES (16ll << 20)

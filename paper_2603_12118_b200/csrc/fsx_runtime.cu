@@ -1051,7 +1051,17 @@ int fsx_forward_batch(fsx_fabric* f, int32_t n, fsx_transfer* t, uint32_t option
       f->bytes_forwarded += x.bytes;
       f->forwards++;
     }
-    FSX_CUDA(fsx::launch_forward(b, (options & FSX_FWD_BULK) != 0, st));
+    // K1 form: FSX_FWD_BULK / FSX_FWD_KERNEL as asked; otherwise the bulk-copy
+    // tiles for a local batch above the small-batch size without the L2 hint
+    // (256 MiB alone: 81.5 us bulk vs 90.3 us register tiles, 64 MiB 24.0 vs
+    // 26.7, 4 MiB 4.8 vs 6.0 with an L2 flush, profiles/k1_sweep_flush_*_r02s);
+    // peer batches keep the register tiles unless asked (the N > 1 probe
+    // picks the peer form per run)
+    bool any_peer = false;
+    for (int32_t k = 0; k < cnt; ++k) any_peer = any_peer || b.t[k].peer;
+    const bool bulk = (options & FSX_FWD_BULK) != 0 ||
+                      (!(options & (FSX_FWD_KERNEL | FSX_FWD_L2_KEEP)) && !any_peer && !b.small);
+    FSX_CUDA(fsx::launch_forward(b, bulk, st));
     f->launches++;
     for (int32_t k = 0; k < cnt; ++k) {
       const fsx_transfer& x = t[first + k];

@@ -140,11 +140,13 @@ class DataPlaneBatch:
 
     def forward(self, stream=None, host_notify: bool = True, l2_keep: bool = False,
                 bulk: bool = False, flag_base0: Optional[int] = None,
-                tokens: Optional[np.ndarray] = None, peer_gpu_count: bool = False) -> int:
+                tokens: Optional[np.ndarray] = None, peer_gpu_count: bool = False,
+                tile: bool = False) -> int:
         """Push every item into its slab segment (one fsx_forward_batch call,
         one K1 launch per N.FWD_MAX_BATCH items); returns the launches.  host_notify=False
         when only device work (stream order / early-start merge) waits on the
-        chunk flags."""
+        chunk flags.  K1 form: bulk = the bulk-copy tiles, tile = the register
+        tiles (FSX_FWD_KERNEL), neither = the library's choice (fsx.h)."""
         assert self.slab_off is not None, "alloc() first"
         M = len(self.lay.items)
         if M == 0:
@@ -152,7 +154,8 @@ class DataPlaneBatch:
         self._prep_transfers(flag_base0, tokens)  # numpy view of the fsx_transfer array
         view = self._xview
         opts = (N.FWD_HOST_NOTIFY if host_notify else 0) | (N.FWD_L2_KEEP if l2_keep else 0) | \
-            (N.FWD_BULK if bulk else 0) | (N.FWD_PEER_GPU_COUNT if peer_gpu_count else 0)
+            (N.FWD_BULK if bulk else 0) | (N.FWD_PEER_GPU_COUNT if peer_gpu_count else 0) | \
+            (N.FWD_KERNEL if tile else 0)
         N.call("fsx_forward_batch", self.fab._h, M, self._xfers, opts, _stream_ptr(stream))
         self.tokens[:] = view["token"]
         return -(-M // N.FWD_MAX_BATCH)

@@ -44,7 +44,7 @@ def main(config: str) -> None:
         b.merge(s, mode=N.MERGE_COPY_ONLY)           # merge_copy_kernel
         b.release()
         assert b.alloc()
-        b.forward(s, host_notify=False)              # forward_tile_kernel
+        b.forward(s, host_notify=False, tile=True)   # forward_tile_kernel
         b.merge(s, early_start=True, mode=N.MERGE_COPY_ONLY)  # merge_follow_kernel (flags set)
         b.release()
 

@@ -126,7 +126,10 @@ def main():
         fab.forward(0, src.data_ptr(), 1, off, n, chunk, fab.flags_alloc(1, nch), s, bulk=args.bulk, dma=dma)
         s.synchronize()
         fab.slab_free(1, off)
-        form = "dma" if fab.stats()["dma_forwards"] > d0 else ("bulk" if args.bulk else "tile")
+        # the K1 form that ran: the copy engine (counted), else bulk when asked
+        # or when the library picks it (a local aligned batch above 2 MiB)
+        auto_bulk = args.form == "auto" and n > (2 << 20)
+        form = "dma" if fab.stats()["dma_forwards"] > d0 else ("bulk" if args.bulk or auto_bulk else "tile")
         print(json.dumps({"k1": form, "form_arg": args.form, "graph": args.graph,
                           "l2_flush": bool(args.flush and args.graph), "bytes": n, **cpu, "chunk_bytes": chunk,
                           "chunks": nch, "us": round(ms * 1e3, 2),
