@@ -172,7 +172,9 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * then costs the copy engine's latency plus a one-thread launch (1.7-1.8 us
  * for 64 KiB-1 MiB) instead of K1's tiles and per-tile completion protocol
  * (2.6-2.8 us).  A transfer's flags turn together, after its last chunk.
- * Chosen automatically for a batch of at most FSX_FWD_DMA_MAX_CHUNKS chunks
+ * Chosen automatically for a batch of at most FSX_FWD_DMA_MAX_CHUNKS chunks (one
+ * transfer of one chunk: a memcpy + flag launch per chunk or transfer would
+ * cost more than one K1 launch)
  * and FSX_FWD_DMA_MAX_BYTES bytes in total, every destination local, no fused
  * digest and no FSX_FWD_L2_KEEP (FSX_FWD_KERNEL or FSX_FWD_BULK force K1);
  * with FSX_FWD_DMA it applies to any batch, peer destinations included.
@@ -184,7 +186,7 @@ int fsx_forward(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int6
  * copy-engine form runs the bulk-copy tiles (forward_tma_kernel) when every
  * transfer is 16-byte aligned without a fused digest. */
 #define FSX_FWD_KERNEL 64u
-#define FSX_FWD_DMA_MAX_CHUNKS 4
+#define FSX_FWD_DMA_MAX_CHUNKS 1
 #define FSX_FWD_DMA_MAX_BYTES (16ll << 20)
 int fsx_forward_ex(fsx_fabric* f, int src_gpu, const void* d_src, int dst_gpu, int64_t dst_off,
                    int64_t bytes, int64_t chunk_bytes, int64_t flag_base, uint64_t* token,

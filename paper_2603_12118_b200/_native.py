@@ -40,7 +40,7 @@ FWD_BULK = 4
 FWD_PEER_GPU_COUNT = 16
 FWD_DMA = 32  # copy-engine form (cudaMemcpyAsync + cuStreamWriteValue64 flags)
 FWD_KERNEL = 64  # force K1 (no automatic copy-engine form)
-FWD_DMA_MAX_CHUNKS = 4
+FWD_DMA_MAX_CHUNKS = 1
 FWD_MAX_BATCH = 64  # FSX_FWD_MAX_BATCH: transfers per K1 launch
 
 MERGE_FULL = 0

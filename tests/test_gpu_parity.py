@@ -86,7 +86,7 @@ def _forward_check(fab, oracle_mod, n, chunk, src_shift=0, dst_gpu=1, dma=None):
     d0 = fab.stats()["dma_forwards"]
     tok = fab.forward(0, src.data_ptr() + src_shift, dst_gpu, off, n, chunk, fb, dma=dma)
     # which form ran: FSX_FWD_DMA / FSX_FWD_KERNEL as asked, else the library's
-    # rule (copy engine for a local batch of <= 4 chunks and <= 16 MiB)
+    # rule (copy engine for one local single-chunk transfer of <= 16 MiB)
     auto_dma = nchunks <= N.FWD_DMA_MAX_CHUNKS and n <= (16 << 20)
     assert fab.stats()["dma_forwards"] - d0 == int(auto_dma if dma is None else dma)
     fab.wait(dst_gpu, fb, nchunks, tok, timeout_us=20_000_000)
