@@ -1168,7 +1168,16 @@ __global__ void __launch_bounds__(32) chan_pull_kernel(const __grid_constant__ C
   __syncwarp();
   warp_copy_row(c.ring + slot * (uint64_t)c.row_bytes, c.io, c.row_bytes, lane);
   __syncwarp();
-  if (lane == 0) st_release_sys(c.tail, seq + 1);  // slot free for the producer
+  // slot free for the producer: its reads are ordered before the tail store
+  // (gpu scope when the producer shares this device -- a system-scope release
+  // here cost ~3 us per pull launch -- system scope for a peer producer)
+  if (lane == 0) {
+    if (c.peer) {
+      st_release_sys(c.tail, seq + 1);
+    } else {
+      st_release_gpu(c.tail, seq + 1);
+    }
+  }
 }
 
 }  // namespace kern
