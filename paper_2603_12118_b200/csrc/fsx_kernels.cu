@@ -1139,7 +1139,7 @@ __global__ void __launch_bounds__(32) chan_push_kernel(const __grid_constant__ C
   if (lane == 0) {  // backpressure: the slot's previous message was consumed
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
-    while (seq - ld_acquire_sys(c.tail) >= c.slots) {
+    while (seq - (c.peer ? ld_acquire_sys(c.tail) : ld_acquire_gpu(c.tail)) >= c.slots) {
       __nanosleep(64);
       if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > c_spin_timeout_ns) asm volatile("trap;");
     }
