@@ -109,6 +109,9 @@ int main(int argc, char** argv) {
     or_synth_payload_into(7, rowbuf.data(), row);
     for (int r = 0; r < batch && device; ++r)
       cudaMemcpy(static_cast<uint8_t*>(drow) + (size_t)r * row, rowbuf.data(), row, cudaMemcpyHostToDevice);
+    // a pageable-source cudaMemcpy may return before its DMA lands: the rows
+    // must be complete before a send hands them to the (unordered) lane kernel
+    if (device) cudaDeviceSynchronize();
     int64_t got = 0;
     for (int r = 0; r < batch; ++r) {
       if (device)

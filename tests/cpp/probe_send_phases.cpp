@@ -52,6 +52,7 @@ int main(int argc, char** argv) {
     if (cudaMalloc(&drow, (size_t)row * batch) != cudaSuccess) return 2;
     for (int r = 0; r < batch; ++r)
       cudaMemcpy(static_cast<uint8_t*>(drow) + (size_t)r * row, rowbuf.data(), row, cudaMemcpyHostToDevice);
+    cudaDeviceSynchronize();  // pageable-source copies may return before their DMA lands
   }
   int64_t got = 0;
   for (int r = 0; r < batch; ++r) {

@@ -129,6 +129,7 @@ TEST_CASE("device payloads land byte-exact (small ones on the lane, large ones b
     auto payload = synth(or_payload_seed(id.data(), id.size(), 0), n);
     DeviceBuffer d(n);
     REQUIRE(cudaMemcpy(d.p, payload.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
+    REQUIRE(cudaDeviceSynchronize() == cudaSuccess);  // pageable copy landed
     Got g;
     collect(f, 1, id, g);
     k.post("send", [&, id] {
@@ -156,6 +157,7 @@ TEST_CASE("local envelopes carry the dg64 digest of the payload") {
     auto payload = synth(seed_of(id), n);
     DeviceBuffer d(n);
     REQUIRE(cudaMemcpy(d.p, payload.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
+    REQUIRE(cudaDeviceSynchronize() == cudaSuccess);  // pageable copy landed
     Got g;
     collect(f, 2, id, g);
     const uint8_t* src = device ? static_cast<const uint8_t*>(d.p) : payload.data();
@@ -457,6 +459,7 @@ TEST_CASE("early-start interest gets the segment and its chunk flags at placemen
   auto want = synth(seed_of("req-e/r0"), n);
   DeviceBuffer src(n);
   REQUIRE(cudaMemcpy(src.p, want.data(), n, cudaMemcpyHostToDevice) == cudaSuccess);
+  REQUIRE(cudaDeviceSynchronize() == cudaSuccess);  // pageable copy landed
   int64_t off = -1;
   SidecarFabric::ChunkFlags flags;
   double handed_at = -1;
@@ -571,6 +574,10 @@ TEST_CASE("streamed device rows ride the small-message lane, in seq order, borro
           want[r].push_back(bytes);
           uint8_t* slot = static_cast<uint8_t*>(d.p) + row * (async_src ? (size_t)(s * reqs + r) : (size_t)r);
           REQUIRE(cudaMemcpy(slot, bytes.data(), row, cudaMemcpyHostToDevice) == cudaSuccess);
+          // a cudaMemcpy from pageable memory may return before its DMA lands;
+          // the send contract is that a device span is complete at the call
+          // (the lane kernel reads it unordered with the producer's stream)
+          REQUIRE(cudaDeviceSynchronize() == cudaSuccess);
           DataRef ref{id, 0, true};
           f.send("req-c" + std::to_string(r), ref, 0, 1, std::span<const uint8_t>(slot, row), s, s == steps - 1);
         }
